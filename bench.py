@@ -1,0 +1,369 @@
+#!/usr/bin/env python
+"""Benchmark: A/A^T projector pair throughput (BASELINE config 3) on B200.
+
+A step is one forward projection A x plus one backprojection A^T y of the
+config-3 workload (n x n grid, n angles in [0, pi), ceil(n sqrt 2) detectors,
+float32 data, x ~ U[0,1] seed 3000, y ~ U[0,1] seed 3001).  Default n = 4096
+(the largest config-3 size; 64 MB image + 95 MB sinogram per operand, larger
+than the 126 MB L2 together, so no explicit flush is needed; for n < 4096 an
+L2 flush is done between steps outside the timed events).
+
+Multi-GPU (torchrun, one process per GPU): angles are dealt round-robin to the
+ranks (angle k -> rank k mod N), each rank projects its angles and
+backprojects its sinogram rows, and the partial A^T y images are summed with an
+NCCL allreduce -- total work fixed ("strong" scaling).  Time = max over ranks of
+the CUDA-event time.
+
+Prints ONE JSON line (rank 0).  ``--impl reference`` times the reference
+algorithm on the host CPU instead (the pinned C oracle: the reference's CSR
+built exactly, then CSR SpMV pairs with all host threads, on a bounded angle
+sample of the same workload).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "A/AT pair GRays/s"
+UNIT = "GRays/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--n", type=int, default=4096)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-angles", type=int, default=4)
+    return ap.parse_args()
+
+
+def workload(n):
+    m = n
+    d = int(math.ceil(n * math.sqrt(2.0)))
+    return n, d, m
+
+
+def config_dict(n, d, m, world, extra=None):
+    c = {"workload": f"config3_pair_n{n}", "n": n, "n_angles": m, "n_detectors": d,
+         "dtype_data": "float32", "geometry": "fixed-point64", "angle_sharding": "round-robin",
+         "parallelism": f"angles{world}", "l2": ("inputs larger than L2" if n >= 4096
+                                                  else "L2 flushed between steps")}
+    if extra:
+        c.update(extra)
+    return c
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._th = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                     "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                    timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([s.strip() for s in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._th = threading.Thread(target=self._run, daemon=True)
+        self._th.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._th:
+            self._th.join(timeout=10)
+
+    def summary(self):
+        sm = []
+        mx = None
+        reasons = set()
+        for r in self.rows:
+            try:
+                sm.append(float(r[1]))
+                mx = float(r[2])
+            except (ValueError, IndexError):
+                continue
+            names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+            for nm, v in zip(names, r[5:9]):
+                if v.strip().lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return json.load(fh), "measured"
+    except OSError:
+        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+def ncu_traffic():
+    """Per-launch DRAM bytes of the dominant kernel from the committed ncu summary."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(p) as fh:
+            return json.load(fh)
+    except OSError:
+        return {}
+
+
+# ------------------------------------------------------------ CPU baseline
+def cpu_pair_rate(n, d, m, k_angles, target_seconds=10.0, max_reps=50):
+    """Reference algorithm on the host: exact CSR of W for k evenly spaced
+    angles (setup, untimed), then W x + W^T y by CSR SpMV with all threads."""
+    from oracle import cproj
+    idx = np.linspace(0, m - 1, k_angles).round().astype(int)
+    angles = (np.arange(m) * (np.pi / m))[idx]
+    w = cproj.build_csr(n, d, angles)
+    wt = w.T.tocsr()
+    rs = np.random.default_rng(3000)
+    x = rs.uniform(0.0, 1.0, n * n)
+    y = np.random.default_rng(3001).uniform(0.0, 1.0, w.shape[0])
+    cproj.csr_matvec(w, x)
+    cproj.csr_matvec(wt, y)
+    reps, t_tot = 0, 0.0
+    while t_tot < target_seconds and reps < max_reps:
+        t0 = time.perf_counter()
+        cproj.csr_matvec(w, x)
+        cproj.csr_matvec(wt, y)
+        t_tot += time.perf_counter() - t0
+        reps += 1
+    t_pair = t_tot / reps
+    rays = w.shape[0]
+    return {"value": rays / t_pair / 1e9, "unit": UNIT, "cores": cproj.num_threads(),
+            "kind": "port",
+            "sample": f"{k_angles} of {m} angles (exact reference CSR rows), {reps} pairs, "
+                      f"{t_pair * 1e3:.1f} ms/pair, nnz={w.nnz}; rate scales linearly in angles"}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    n, d, m = workload(args.n)
+    from oracle import cproj
+    idx = np.linspace(0, m - 1, args.cpu_angles).round().astype(int)
+    angles = (np.arange(m) * (np.pi / m))[idx]
+    w = cproj.build_csr(n, d, angles)
+    wt = w.T.tocsr()
+    x = np.random.default_rng(3000).uniform(0.0, 1.0, n * n)
+    y = np.random.default_rng(3001).uniform(0.0, 1.0, w.shape[0])
+    for _ in range(args.warmup):
+        cproj.csr_matvec(w, x)
+        cproj.csr_matvec(wt, y)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        cproj.csr_matvec(w, x)
+        cproj.csr_matvec(wt, y)
+    dt = (time.perf_counter() - t0) / args.steps
+    value = w.shape[0] / dt / 1e9
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": config_dict(n, d, m, 1, {"sample_angles": int(args.cpu_angles)}),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cproj.num_threads(),
+                             "kind": "port",
+                             "sample": f"{args.cpu_angles} of {m} angles per step, exact "
+                                       f"reference CSR (nnz={w.nnz}), CSR SpMV pair"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------- our arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    from paper_1310_0956_b200.geometry import Geometry, build_projector
+
+    n, d, m = workload(args.n)
+    all_angles = np.arange(m) * (np.pi / m)
+    mine = np.arange(rank, m, world)
+    g = Geometry(n, d, mine.size, angles=all_angles[mine])
+    w = build_projector(g, precision="float32", device=dev)
+    M_loc, Npix = w.shape
+
+    x_h = np.random.default_rng(3000).uniform(0.0, 1.0, n * n).astype(np.float32)
+    y_full = np.random.default_rng(3001).uniform(0.0, 1.0, m * d).astype(np.float32)
+    y_h = np.ascontiguousarray(y_full.reshape(m, d)[mine].reshape(-1))
+    x = torch.from_numpy(x_h).to(dev)
+    y = torch.from_numpy(y_h).to(dev)
+    sino = torch.empty(M_loc, dtype=torch.float32, device=dev)
+    img = torch.empty(Npix, dtype=torch.float32, device=dev)
+    flush = None if n >= 4096 else torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        w.forward_(x, sino)
+        w.backward_(y, img)
+        if world > 1:
+            dist.all_reduce(img)
+
+    for _ in range(max(args.warmup, 0)):
+        step()
+    torch.cuda.synchronize(dev)
+
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+           torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    with ClockSampler(local) as clocks:
+        for i in range(args.steps):
+            if flush is not None:
+                flush.fill_(i & 0xFF)
+            e0, e1, e2, e3 = ev[i]
+            e0.record(stream)
+            w.forward_(x, sino)
+            e1.record(stream)
+            w.backward_(y, img)
+            e2.record(stream)
+            if world > 1:
+                dist.all_reduce(img)
+            e3.record(stream)
+        torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    t_fwd = sum(a.elapsed_time(b) for a, b, _, _ in ev) / 1e3
+    t_bwd = sum(b.elapsed_time(c) for _, b, c, _ in ev) / 1e3
+    t_tot = sum(a.elapsed_time(dd) for a, _, _, dd in ev) / 1e3
+    tt = torch.tensor([t_tot, t_fwd, t_bwd], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    t_tot, t_fwd, t_bwd = [float(v) for v in tt.cpu()]
+    ms_step = t_tot / args.steps * 1e3
+    rays_total = m * d
+    value = rays_total * args.steps / t_tot / 1e9
+
+    # ---- end to end through the public API with host buffers -------------
+    pin_x = torch.from_numpy(x_h).pin_memory()
+    pin_y = torch.from_numpy(y_h).pin_memory()
+    out_s = torch.empty(M_loc, dtype=torch.float32).pin_memory()
+    out_i = torch.empty(Npix, dtype=torch.float32).pin_memory()
+
+    def e2e_step():
+        xd = pin_x.to(dev, non_blocking=True)
+        yd = pin_y.to(dev, non_blocking=True)
+        s_ = w.forward(xd)
+        i_ = w.backward(yd)
+        if world > 1:
+            dist.all_reduce(i_)
+        out_s.copy_(s_, non_blocking=True)
+        out_i.copy_(i_, non_blocking=True)
+
+    e2e_step()
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    s0 = torch.cuda.Event(enable_timing=True)
+    s1 = torch.cuda.Event(enable_timing=True)
+    s0.record(stream)
+    for _ in range(args.steps):
+        e2e_step()
+    s1.record(stream)
+    torch.cuda.synchronize(dev)
+    te = torch.tensor([s0.elapsed_time(s1) / 1e3], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    t_e2e = float(te.item())
+    e2e_value = rays_total * args.steps / t_e2e / 1e9
+
+    # ---- roofline ---------------------------------------------------------
+    peaks, peak_src = measured_peaks()
+    hbm = float(peaks.get("hbm_gbs", 6650.0))
+    clk = clocks.summary()
+    f_sm = (clk["sm_mhz"] or peaks.get("sm_max_mhz", 1965.0)) * 1e6
+    n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
+    nnz_total = int(round(4.0 / math.pi * m * n * n))    # (4/pi) m n^2, SURVEY A.1
+    fwd_avg, bwd_avg = t_fwd / args.steps, t_bwd / args.steps
+    dom = "backward" if bwd_avg >= fwd_avg else "forward"
+    t_dom = max(fwd_avg, bwd_avg)
+    bytes_dom = 4 * (Npix + M_loc)                       # read one operand, write the other
+    achieved = bytes_dom / t_dom / 1e9
+    upd_rate = (nnz_total / world) / t_dom               # intersection updates per second
+    gather_peak = n_sm * 32 * f_sm
+    traffic = ncu_traffic().get(f"{dom}_n{n}")
+    launches = args.steps * (3 if True else 2)           # transpose + forward + backward
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": config_dict(n, d, m, world),
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 4 * (Npix + M_loc),
+                "d2h_bytes_per_step": 4 * (Npix + M_loc)},
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm,
+                     "unit": "GB/s", "frac": achieved / hbm, "traffic": traffic,
+                     "peak_source": peak_src},
+        "roofline_gather": {"kernel": dom, "achieved": upd_rate / 1e9,
+                            "peak": gather_peak / 1e9, "unit": "Gupdates/s",
+                            "frac": upd_rate / gather_peak,
+                            "definition": "SURVEY s8(d): 148 SMs x 32 lanes x f_SM"},
+        "kernels_ms": {"forward": fwd_avg * 1e3, "backward": bwd_avg * 1e3},
+        "gpu_launches": launches,
+        "clocks": clk,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            line["cpu_baseline"] = cpu_pair_rate(n, d, m, args.cpu_angles)
+        except Exception as exc:  # pragma: no cover
+            line["cpu_baseline"] = {"error": repr(exc)}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

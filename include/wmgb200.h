@@ -1,0 +1,148 @@
+/*
+ * wmgb200.h -- C ABI of the B200-native WMG tomography hot path.
+ *
+ * Library: paper_1310_0956_b200/lib/libwmgb200.so (sm_100a).  Every entry point
+ * takes plain pointers and sizes; device buffers are CALLER-OWNED (no
+ * allocation inside kernels; the only internal allocation is the small
+ * per-angle table made by wmg_geometry_create and freed by
+ * wmg_geometry_destroy).  All work is asynchronous on the caller's CUDA stream
+ * (cudaStream_t passed as void*, NULL = legacy default stream).  Functions are
+ * reentrant; a geometry handle is immutable after creation and may be shared
+ * read-only across threads and streams.
+ *
+ * Return codes (mapped by the Python host layer the way the reference raises):
+ *   WMG_OK        0
+ *   WMG_EINVAL    1  invalid argument                -> ValueError
+ *   WMG_EDIM      2  dimension mismatch              -> DimensionMismatchError
+ *   WMG_ENOTSPD   3  not symmetric positive definite -> NotPositiveDefiniteError
+ *   WMG_ECUDA     4  CUDA launch / runtime error     -> RuntimeError
+ * wmg_last_error() returns a thread-local message for the last failure.
+ *
+ * Reference interfaces replaced (paths under /root/reference/pkg/src/wmgtomo):
+ *   geometry.py:68-74   build_geometry / Geometry   -> wmg_geometry_create
+ *   geometry.py:178-197 build_projector (CSR W)     -> (matrix-free) wmg_forward /
+ *                                                      wmg_backward; exact CSR export
+ *                                                      via wmg_csr_counts / wmg_csr_fill
+ *   geometry.py:200-206 apply        (W x)          -> wmg_forward
+ *   geometry.py:209-215 apply_transpose (W^T y)     -> wmg_backward
+ *   solvers.py:79-86    sirt_scaling (row/col sums) -> wmg_row_sums / wmg_col_sums
+ *   solvers.py:116-135  sirt_solve vector ops       -> wmg_sirt_update, wmg_det_reduce
+ *   solvers.py:140-156  normal_operator (+lambda v) -> wmg_add_scaled
+ *   solvers.py:195-241  bicgstab_solve vector ops   -> wmg_bicg_p, wmg_bicg_x, wmg_axpy,
+ *                                                      wmg_det_reduce
+ *   phantom.py:64-75    error_metrics               -> wmg_det_reduce(SQDIFF), wmg_maxabs
+ *   multilevel.py:36-79 haar_* / build_intergrid_set-> wmg_haar_restrict / wmg_haar_prolong
+ *   multilevel.py:123-130 leaf Gram assembly        -> wmg_leaf_factor (+ DGEMM)
+ */
+#ifndef WMGB200_H
+#define WMGB200_H
+
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define WMG_OK 0
+#define WMG_EINVAL 1
+#define WMG_EDIM 2
+#define WMG_ENOTSPD 3
+#define WMG_ECUDA 4
+
+/* projector modes */
+#define WMG_MODE_PARITY 0 /* float64, bit-exact reference weights and sum order */
+#define WMG_MODE_FAST 1   /* fixed-point geometry, any summation order */
+/* dtypes / precisions */
+#define WMG_F32 0
+#define WMG_F64 1
+
+/* deterministic reduction ops (wmg_det_reduce) */
+#define WMG_RED_DOT 0     /* sum a_i * b_i            */
+#define WMG_RED_SQDIFF 1  /* sum (a_i - b_i)^2        */
+#define WMG_RED_SUM 2     /* sum a_i                  */
+#define WMG_RED_DOTDIFF 3 /* sum a_i * (b_i - c_i)    */
+#define WMG_RED_SQ 4      /* sum a_i^2                */
+
+typedef struct wmg_geometry wmg_geometry;
+
+int wmg_version(void);
+const char *wmg_last_error(void);
+
+/* Geometry: n x n unit pixels, n_detectors rays per angle (spacing 1), and
+ * n_angles angles given by their SNAPPED cos/sin (host arrays, float64),
+ * i.e. geometry.py:77-85 evaluated on the host.  Angles must lie in [0, pi). */
+int wmg_geometry_create(int n, int n_detectors, int n_angles, const double *cos_h,
+                        const double *sin_h, wmg_geometry **out);
+int wmg_geometry_destroy(wmg_geometry *g);
+int wmg_geometry_shape(const wmg_geometry *g, long long *n_rows, long long *n_cols);
+
+/* bytes of caller workspace wmg_forward needs (transposed image) */
+int wmg_forward_workspace(const wmg_geometry *g, int dtype_in, size_t *bytes);
+
+/* y = W x (length m*d).  mode PARITY requires dtype_in = dtype_out = F64 and
+ * ignores precision/workspace; anomaly (device int*, may be NULL) counts
+ * segments whose midpoint pixel contradicts the walk (0 on all pinned sizes). */
+int wmg_forward(const wmg_geometry *g, int mode, int precision, int dtype_in, int dtype_out,
+                const void *x, void *y, void *workspace, int *anomaly, void *stream);
+
+/* x = W^T y (accumulate = 1: x += W^T y).  PARITY: y == NULL means y = 1. */
+int wmg_backward(const wmg_geometry *g, int mode, int precision, int dtype_in, int dtype_out,
+                 const void *y, void *x, int accumulate, int *anomaly, void *stream);
+
+/* exact reference row sums (np.add.reduceat) and column sums (ones @ W) */
+int wmg_row_sums(const wmg_geometry *g, double *out, void *stream);
+int wmg_col_sums(const wmg_geometry *g, double *out, void *stream);
+
+/* exact CSR export (entry for entry equal to build_projector): counts per ray,
+ * then fill at a caller-built indptr (int64) */
+int wmg_csr_counts(const wmg_geometry *g, long long *counts, int *anomaly, void *stream);
+int wmg_csr_fill(const wmg_geometry *g, const long long *indptr, long long *cols, double *vals,
+                 void *stream);
+
+/* deterministic float64 reductions: out[k] = DET_SUM over i of op_k(a_k, b_k, c_k)
+ * for k < K <= 8.  scratch: wmg_det_scratch_len(n, K) doubles of device memory. */
+long long wmg_det_scratch_len(long long n, int K);
+int wmg_det_reduce(long long n, int K, const int *ops, const double *const *a,
+                   const double *const *b, const double *const *c, double *scratch,
+                   double *out, void *stream);
+/* out[0] = max |a - b| (b may be NULL: max |a|) */
+int wmg_maxabs(long long n, const double *a, const double *b, double *out, void *stream);
+
+/* elementwise float64 ops (individually rounded, no FMA) */
+int wmg_axpy(long long n, double *out, const double *y, double alpha, int sgn, const double *x,
+             void *stream);
+int wmg_lincomb(long long n, double *out, double a, const double *x, double b, const double *y,
+                double c, const double *z, void *stream);
+int wmg_bicg_p(long long n, double *p, const double *r, double beta, double omega,
+               const double *v, void *stream);
+int wmg_bicg_x(long long n, double *x, double alpha, const double *ph, double omega,
+               const double *sh, void *stream);
+int wmg_scale(long long n, double *out, double a, const double *x, const double *y,
+              void *stream);
+int wmg_recip(long long n, double *out, const double *s, void *stream);
+int wmg_sirt_update(long long n, double *x, const double *c, const double *g, double lam,
+                    void *stream);
+int wmg_add_scaled(long long n, double *out, const double *g, double lam, int sgn,
+                   const double *v, void *stream);
+int wmg_cgs_update(long long n, int k, double *w, const double *V, long long ldv,
+                   const double *h, void *stream);
+int wmg_combo(long long n, int k, double *out, const double *V, long long ldv, const double *cf,
+              int accumulate, void *stream);
+int wmg_cast(long long n, int to_f32, void *out, const void *in, void *stream);
+
+/* Haar intergrid operators (side even).  band: 0 LL, 1 LH, 2 HL, 3 HH.
+ * restrict: out holds one (side/2)^2 block per band set in band_mask, in band
+ * order.  prolong: fine = (accumulate ? fine : 0) + R_band^T coarse. */
+int wmg_haar_restrict(int side, const double *fine, int band_mask, double *out, void *stream);
+int wmg_haar_prolong(int side, const double *coarse, int band, double *fine, int accumulate,
+                     void *stream);
+
+/* WMG leaf factor rows P_L[ray0 : ray0 + nrays, :] (row-major, caller zeroes P)
+ * for the leaf reached by bands[0..depth) from the root. */
+int wmg_leaf_factor(const wmg_geometry *g, int depth, const int *bands, long long ray0,
+                    long long nrays, double *P, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* WMGB200_H */

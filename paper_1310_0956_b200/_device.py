@@ -1,0 +1,160 @@
+"""Device-buffer plumbing shared by the operator and solver layers.
+
+PyTorch supplies HBM buffers and the current CUDA stream; every arithmetic op on
+the hot path is one of our sm_100a kernels called through the C ABI
+(``_native``).  Vectors arrive as numpy arrays (copied to HBM, results copied
+back -- the reference's calling convention) or as torch CUDA tensors (kept
+resident).
+"""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _native as N
+
+_scratch = {}
+
+
+def torch():
+    import torch as _t
+    return _t
+
+
+def require_cuda():
+    t = torch()
+    N.load(require_gpu=True)
+    return t
+
+
+def stream_handle():
+    t = torch()
+    return ctypes.c_void_p(t.cuda.current_stream().cuda_stream)
+
+
+def ptr(tensor):
+    return ctypes.c_void_p(tensor.data_ptr()) if tensor is not None else None
+
+
+def is_torch(v) -> bool:
+    try:
+        import torch as _t
+    except ImportError:  # pragma: no cover
+        return False
+    return isinstance(v, _t.Tensor)
+
+
+def to_device(v, dtype=None, device=None):
+    """Return (tensor on GPU, was_numpy)."""
+    t = require_cuda()
+    dtype = dtype or t.float64
+    if is_torch(v):
+        if v.is_cuda:
+            out = v
+            if out.dtype != dtype:
+                out = out.to(dtype)
+            return out.contiguous(), False
+        return v.to(device=device or "cuda", dtype=dtype).contiguous(), True
+    a = np.ascontiguousarray(np.asarray(v), dtype=np.float64 if dtype == t.float64 else np.float32)
+    return t.from_numpy(a).to(device or "cuda", non_blocking=False), True
+
+
+def to_caller(tensor, was_numpy):
+    if was_numpy:
+        return tensor.detach().cpu().numpy()
+    return tensor
+
+
+def scratch(n: int, K: int, device):
+    """Cached device scratch for wmg_det_reduce (+ K result slots)."""
+    t = torch()
+    L = N.load()
+    need = int(L.wmg_det_scratch_len(int(n), int(K))) + 16
+    key = (str(device), t.cuda.current_stream(device).cuda_stream)
+    buf = _scratch.get(key)
+    if buf is None or buf.numel() < need:
+        buf = t.empty(max(need, 4096), dtype=t.float64, device=device)
+        _scratch[key] = buf
+    return buf
+
+
+def det_reduce(specs, n=None):
+    """Deterministic float64 reductions (DET_SUM, see csrc/vecops.cu).
+
+    ``specs`` is a list of (op, a, b, c) tuples of CUDA float64 tensors of equal
+    length.  Returns a float64 CUDA tensor with one result per spec (no sync).
+    """
+    t = torch()
+    K = len(specs)
+    if not 1 <= K <= 8:
+        raise ValueError("det_reduce takes 1..8 reductions")
+    a0 = specs[0][1]
+    n = a0.numel() if n is None else n
+    dev = a0.device
+    sc = scratch(n, K, dev)
+    out = t.empty(K, dtype=t.float64, device=dev)
+    ops = (ctypes.c_int * K)(*[int(s[0]) for s in specs])
+    A = (ctypes.c_void_p * K)(*[s[1].data_ptr() for s in specs])
+    B = (ctypes.c_void_p * K)(*[(s[2].data_ptr() if s[2] is not None else 0) for s in specs])
+    C = (ctypes.c_void_p * K)(*[(s[3].data_ptr() if len(s) > 3 and s[3] is not None else 0)
+                                for s in specs])
+    N.call("wmg_det_reduce", int(n), K, ops, A, B, C, ptr(sc), ptr(out), stream_handle())
+    return out
+
+
+def det_dot(a, b):
+    return det_reduce([(N.RED_DOT, a, b, None)])
+
+
+def det_norm_sq(a):
+    return det_reduce([(N.RED_SQ, a, None, None)])
+
+
+def maxabs(a, b=None):
+    t = torch()
+    out = t.empty(1, dtype=t.float64, device=a.device)
+    N.call("wmg_maxabs", a.numel(), ptr(a), ptr(b), ptr(out), stream_handle())
+    return out
+
+
+def axpy(out, y, alpha, sgn, x):
+    N.call("wmg_axpy", out.numel(), ptr(out), ptr(y), float(alpha), int(sgn), ptr(x),
+           stream_handle())
+    return out
+
+
+def lincomb(out, a, x, b, y, c=0.0, z=None):
+    N.call("wmg_lincomb", out.numel(), ptr(out), float(a), ptr(x), float(b), ptr(y), float(c),
+           ptr(z), stream_handle())
+    return out
+
+
+def add_scaled(out, g, lam, sgn, v):
+    N.call("wmg_add_scaled", out.numel(), ptr(out), ptr(g), float(lam), int(sgn), ptr(v),
+           stream_handle())
+    return out
+
+
+def hadamard(out, x, y):
+    N.call("wmg_scale", out.numel(), ptr(out), 1.0, ptr(x), ptr(y), stream_handle())
+    return out
+
+
+def scale(out, a, x):
+    N.call("wmg_scale", out.numel(), ptr(out), float(a), ptr(x), None, stream_handle())
+    return out
+
+
+def recip(out, s):
+    N.call("wmg_recip", out.numel(), ptr(out), ptr(s), stream_handle())
+    return out
+
+
+def error_metrics_dev(x, x_ex, ex_norm2=None, ex_inf=None):
+    """Device-side rel-L2 / rel-Linf (phantom.py:64-75); returns a CUDA tensor
+    [sum (x-x_ex)^2, max|x-x_ex|] plus the precomputed exact-image norms."""
+    t = torch()
+    r = det_reduce([(N.RED_SQDIFF, x, x_ex, None)])
+    m = maxabs(x, x_ex)
+    return t.cat([r, m])

@@ -1,0 +1,339 @@
+// capi.cu -- extern "C" boundary (include/wmgb200.h).  Argument validation and
+// error mapping live here; the kernels live in projector_*.cu, vecops.cu and
+// multilevel.cu.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <new>
+#include <vector>
+
+#include "../../include/wmgb200.h"
+#include "common.cuh"
+
+namespace wmg {
+cudaError_t parity_forward(const GeomDev&, const double*, double*, int*, cudaStream_t);
+cudaError_t parity_backward(const GeomDev&, const double*, double*, bool, int*, cudaStream_t);
+cudaError_t parity_row_sums(const GeomDev&, double*, cudaStream_t);
+cudaError_t parity_csr(const GeomDev&, int, long long*, const long long*, long long*, double*,
+                       int*, cudaStream_t);
+cudaError_t fast_forward(const GeomDev&, int, int, int, const void*, void*, void*, cudaStream_t);
+cudaError_t fast_backward(const GeomDev&, int, int, int, const void*, void*, bool, cudaStream_t);
+cudaError_t det_reduce(long long, int, const int*, const double* const*, const double* const*,
+                       const double* const*, double*, double*, cudaStream_t);
+long long det_scratch_len(long long, int);
+cudaError_t maxabs(long long, const double*, const double*, double*, cudaStream_t);
+cudaError_t ew_axpy(long long, double*, const double*, double, int, const double*, cudaStream_t);
+cudaError_t ew_lincomb(long long, double*, double, const double*, double, const double*, double,
+                       const double*, cudaStream_t);
+cudaError_t ew_bicg_p(long long, double*, const double*, double, double, const double*,
+                      cudaStream_t);
+cudaError_t ew_bicg_x(long long, double*, double, const double*, double, const double*,
+                      cudaStream_t);
+cudaError_t ew_scale(long long, double*, double, const double*, const double*, cudaStream_t);
+cudaError_t ew_recip(long long, double*, const double*, cudaStream_t);
+cudaError_t ew_sirt_update(long long, double*, const double*, const double*, double,
+                           cudaStream_t);
+cudaError_t ew_add_scaled(long long, double*, const double*, double, int, const double*,
+                          cudaStream_t);
+cudaError_t ew_cgs_update(long long, int, double*, const double*, long long, const double*,
+                          cudaStream_t);
+cudaError_t ew_combo(long long, int, double*, const double*, long long, const double*, int,
+                     cudaStream_t);
+cudaError_t ew_cast(long long, int, void*, const void*, cudaStream_t);
+cudaError_t haar_restrict(int, const double*, int, double*, cudaStream_t);
+cudaError_t haar_prolong(int, const double*, int, double*, int, cudaStream_t);
+cudaError_t leaf_factor(const GeomDev&, int, const int*, long long, long long, double*,
+                        cudaStream_t);
+}  // namespace wmg
+
+struct wmg_geometry {
+  wmg::GeomDev dev;
+  wmg::AngleParams* d_ang;
+};
+
+static thread_local char g_err[512] = "";
+
+static int fail(int code, const char* fmt, const char* detail = "") {
+  snprintf(g_err, sizeof(g_err), fmt, detail);
+  return code;
+}
+
+static int cuda_rc(cudaError_t e) {
+  if (e == cudaSuccess) return WMG_OK;
+  return fail(WMG_ECUDA, "CUDA error: %s", cudaGetErrorString(e));
+}
+
+#define STREAM(s) (reinterpret_cast<cudaStream_t>(s))
+
+extern "C" {
+
+int wmg_version(void) { return 1; }
+const char* wmg_last_error(void) { return g_err; }
+
+int wmg_geometry_create(int n, int n_detectors, int n_angles, const double* cos_h,
+                        const double* sin_h, wmg_geometry** out) {
+  if (!out) return fail(WMG_EINVAL, "out is NULL");
+  *out = nullptr;
+  if (n < 1 || n_detectors < 1 || n_angles < 1)
+    return fail(WMG_EINVAL, "geometry dimensions must be positive");
+  if (n > 16384) return fail(WMG_EINVAL, "n > 16384 is not supported");
+  if (!cos_h || !sin_h) return fail(WMG_EINVAL, "cos/sin tables are NULL");
+  std::vector<wmg::AngleParams> P((size_t)n_angles);
+  const double half = 0.5 * n;
+  for (int a = 0; a < n_angles; ++a) {
+    const double c = cos_h[a], s = sin_h[a];
+    if (!std::isfinite(c) || !std::isfinite(s) || s < 0.0)
+      return fail(WMG_EINVAL, "angles must lie in [0, pi) (sin >= 0)");
+    wmg::AngleParams& q = P[(size_t)a];
+    memset(&q, 0, sizeof(q));
+    q.c = c;
+    q.s = s;
+    const double ac = std::fabs(c), as = std::fabs(s);
+    const double inf = std::numeric_limits<double>::infinity();
+    if (ac >= as) {   // y-major: slabs are rows (top -> bottom), minor = column
+      const double t = s / c;
+      q.major = 0;
+      q.u0 = half * (1.0 - t);
+      q.du = 1.0 / c;
+      q.slope = t;
+      q.mirror = t < 0.0;
+      q.L = (float)(1.0 / ac);
+      q.Ls = (float)(as == 0.0 ? inf : 1.0 / as);
+    } else {          // x-major: slabs are columns (left -> right), minor = row
+      const double ct = c / s;
+      q.major = 1;
+      q.u0 = half * (1.0 - ct);
+      q.du = -1.0 / s;
+      q.slope = ct;
+      q.mirror = ct <= 0.0;   // theta = pi/2: ties go to the upper row
+      q.L = (float)(1.0 / as);
+      q.Ls = (float)(ac == 0.0 ? inf : 1.0 / ac);
+    }
+    if (q.mirror) {
+      q.u0 = (double)n - q.u0;
+      q.du = -q.du;
+      q.slope = -q.slope;
+    }
+    q.axis = (c == 0.0 || s == 0.0) ? 1 : 0;
+    q.hw = (float)(0.5 * (ac + as));
+    q.inv_cs = q.axis ? 0.0f : (float)(1.0 / (ac * as));
+  }
+  wmg_geometry* g = new (std::nothrow) wmg_geometry;
+  if (!g) return fail(WMG_EINVAL, "out of host memory");
+  g->d_ang = nullptr;
+  cudaError_t e = cudaMalloc(&g->d_ang, sizeof(wmg::AngleParams) * (size_t)n_angles);
+  if (e == cudaSuccess)
+    e = cudaMemcpy(g->d_ang, P.data(), sizeof(wmg::AngleParams) * (size_t)n_angles,
+                   cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    if (g->d_ang) cudaFree(g->d_ang);
+    delete g;
+    return cuda_rc(e);
+  }
+  g->dev.n = n;
+  g->dev.d = n_detectors;
+  g->dev.m = n_angles;
+  g->dev.ang = g->d_ang;
+  *out = g;
+  return WMG_OK;
+}
+
+int wmg_geometry_destroy(wmg_geometry* g) {
+  if (!g) return WMG_OK;
+  cudaError_t e = cudaFree(g->d_ang);
+  delete g;
+  return cuda_rc(e);
+}
+
+int wmg_geometry_shape(const wmg_geometry* g, long long* n_rows, long long* n_cols) {
+  if (!g) return fail(WMG_EINVAL, "geometry is NULL");
+  if (n_rows) *n_rows = (long long)g->dev.m * g->dev.d;
+  if (n_cols) *n_cols = (long long)g->dev.n * g->dev.n;
+  return WMG_OK;
+}
+
+int wmg_forward_workspace(const wmg_geometry* g, int dtype_in, size_t* bytes) {
+  if (!g || !bytes) return fail(WMG_EINVAL, "NULL argument");
+  const size_t es = dtype_in == WMG_F32 ? 4 : 8;
+  *bytes = es * (size_t)g->dev.n * (size_t)g->dev.n;
+  return WMG_OK;
+}
+
+static int check_types(int mode, int precision, int tin, int tout) {
+  if (mode == WMG_MODE_PARITY) {
+    if (tin != WMG_F64 || tout != WMG_F64)
+      return fail(WMG_EINVAL, "parity mode is float64 only");
+    return WMG_OK;
+  }
+  if (mode != WMG_MODE_FAST) return fail(WMG_EINVAL, "unknown projector mode");
+  if ((tin != WMG_F32 && tin != WMG_F64) || (tout != WMG_F32 && tout != WMG_F64))
+    return fail(WMG_EINVAL, "unknown dtype");
+  if (precision != WMG_F32 && precision != WMG_F64) return fail(WMG_EINVAL, "unknown precision");
+  if (precision == WMG_F64 && tin != tout)
+    return fail(WMG_EINVAL, "fast float64 arithmetic needs equal in/out dtypes");
+  return WMG_OK;
+}
+
+int wmg_forward(const wmg_geometry* g, int mode, int precision, int dtype_in, int dtype_out,
+                const void* x, void* y, void* workspace, int* anomaly, void* stream) {
+  if (!g || !x || !y) return fail(WMG_EINVAL, "NULL argument");
+  int rc = check_types(mode, precision, dtype_in, dtype_out);
+  if (rc) return rc;
+  if (mode == WMG_MODE_PARITY)
+    return cuda_rc(wmg::parity_forward(g->dev, (const double*)x, (double*)y, anomaly,
+                                       STREAM(stream)));
+  if (!workspace) return fail(WMG_EINVAL, "fast forward needs a workspace");
+  return cuda_rc(wmg::fast_forward(g->dev, precision, dtype_in, dtype_out, x, workspace, y,
+                                   STREAM(stream)));
+}
+
+int wmg_backward(const wmg_geometry* g, int mode, int precision, int dtype_in, int dtype_out,
+                 const void* y, void* x, int accumulate, int* anomaly, void* stream) {
+  if (!g || !x) return fail(WMG_EINVAL, "NULL argument");
+  int rc = check_types(mode, precision, dtype_in, dtype_out);
+  if (rc) return rc;
+  if (mode == WMG_MODE_PARITY)
+    return cuda_rc(wmg::parity_backward(g->dev, (const double*)y, (double*)x, accumulate != 0,
+                                        anomaly, STREAM(stream)));
+  if (!y) return fail(WMG_EINVAL, "y is NULL");
+  return cuda_rc(wmg::fast_backward(g->dev, precision, dtype_in, dtype_out, y, x,
+                                    accumulate != 0, STREAM(stream)));
+}
+
+int wmg_row_sums(const wmg_geometry* g, double* out, void* stream) {
+  if (!g || !out) return fail(WMG_EINVAL, "NULL argument");
+  return cuda_rc(wmg::parity_row_sums(g->dev, out, STREAM(stream)));
+}
+
+int wmg_col_sums(const wmg_geometry* g, double* out, void* stream) {
+  if (!g || !out) return fail(WMG_EINVAL, "NULL argument");
+  return cuda_rc(wmg::parity_backward(g->dev, nullptr, out, false, nullptr, STREAM(stream)));
+}
+
+int wmg_csr_counts(const wmg_geometry* g, long long* counts, int* anomaly, void* stream) {
+  if (!g || !counts) return fail(WMG_EINVAL, "NULL argument");
+  return cuda_rc(wmg::parity_csr(g->dev, 0, counts, nullptr, nullptr, nullptr, anomaly,
+                                 STREAM(stream)));
+}
+
+int wmg_csr_fill(const wmg_geometry* g, const long long* indptr, long long* cols, double* vals,
+                 void* stream) {
+  if (!g || !indptr || !cols || !vals) return fail(WMG_EINVAL, "NULL argument");
+  return cuda_rc(wmg::parity_csr(g->dev, 1, nullptr, indptr, cols, vals, nullptr,
+                                 STREAM(stream)));
+}
+
+long long wmg_det_scratch_len(long long n, int K) { return wmg::det_scratch_len(n, K); }
+
+int wmg_det_reduce(long long n, int K, const int* ops, const double* const* a,
+                   const double* const* b, const double* const* c, double* scratch, double* out,
+                   void* stream) {
+  if (K < 1 || K > 8 || !ops || !a || !scratch || !out)
+    return fail(WMG_EINVAL, "bad det_reduce arguments");
+  if (n > 1024LL * 1024LL * 1024LL) return fail(WMG_EINVAL, "vector longer than 2^30");
+  for (int k = 0; k < K; ++k) {
+    if (ops[k] < 0 || ops[k] > 4) return fail(WMG_EINVAL, "unknown reduction op");
+    if (!a[k]) return fail(WMG_EINVAL, "NULL operand");
+    if ((ops[k] == WMG_RED_DOT || ops[k] == WMG_RED_SQDIFF || ops[k] == WMG_RED_DOTDIFF) &&
+        (!b || !b[k]))
+      return fail(WMG_EINVAL, "NULL operand");
+    if (ops[k] == WMG_RED_DOTDIFF && (!c || !c[k])) return fail(WMG_EINVAL, "NULL operand");
+  }
+  return cuda_rc(wmg::det_reduce(n, K, ops, a, b, c, scratch, out, STREAM(stream)));
+}
+
+int wmg_maxabs(long long n, const double* a, const double* b, double* out, void* stream) {
+  if (!a || !out) return fail(WMG_EINVAL, "NULL argument");
+  return cuda_rc(wmg::maxabs(n, a, b, out, STREAM(stream)));
+}
+
+#define REQ(p) \
+  if (!(p)) return fail(WMG_EINVAL, "NULL argument")
+
+int wmg_axpy(long long n, double* out, const double* y, double alpha, int sgn, const double* x,
+             void* stream) {
+  REQ(out && y && x);
+  return cuda_rc(wmg::ew_axpy(n, out, y, alpha, sgn, x, STREAM(stream)));
+}
+int wmg_lincomb(long long n, double* out, double a, const double* x, double b, const double* y,
+                double c, const double* z, void* stream) {
+  REQ(out && x && y);
+  return cuda_rc(wmg::ew_lincomb(n, out, a, x, b, y, c, z, STREAM(stream)));
+}
+int wmg_bicg_p(long long n, double* p, const double* r, double beta, double omega,
+               const double* v, void* stream) {
+  REQ(p && r && v);
+  return cuda_rc(wmg::ew_bicg_p(n, p, r, beta, omega, v, STREAM(stream)));
+}
+int wmg_bicg_x(long long n, double* x, double alpha, const double* ph, double omega,
+               const double* sh, void* stream) {
+  REQ(x && ph && sh);
+  return cuda_rc(wmg::ew_bicg_x(n, x, alpha, ph, omega, sh, STREAM(stream)));
+}
+int wmg_scale(long long n, double* out, double a, const double* x, const double* y,
+              void* stream) {
+  REQ(out && x);
+  return cuda_rc(wmg::ew_scale(n, out, a, x, y, STREAM(stream)));
+}
+int wmg_recip(long long n, double* out, const double* s, void* stream) {
+  REQ(out && s);
+  return cuda_rc(wmg::ew_recip(n, out, s, STREAM(stream)));
+}
+int wmg_sirt_update(long long n, double* x, const double* c, const double* g, double lam,
+                    void* stream) {
+  REQ(x && c && g);
+  return cuda_rc(wmg::ew_sirt_update(n, x, c, g, lam, STREAM(stream)));
+}
+int wmg_add_scaled(long long n, double* out, const double* g, double lam, int sgn,
+                   const double* v, void* stream) {
+  REQ(out && g && v);
+  return cuda_rc(wmg::ew_add_scaled(n, out, g, lam, sgn, v, STREAM(stream)));
+}
+int wmg_cgs_update(long long n, int k, double* w, const double* V, long long ldv,
+                   const double* h, void* stream) {
+  REQ(w && V && h);
+  if (k < 0) return fail(WMG_EINVAL, "k < 0");
+  return cuda_rc(wmg::ew_cgs_update(n, k, w, V, ldv, h, STREAM(stream)));
+}
+int wmg_combo(long long n, int k, double* out, const double* V, long long ldv, const double* cf,
+              int accumulate, void* stream) {
+  REQ(out && V && cf);
+  if (k < 0) return fail(WMG_EINVAL, "k < 0");
+  return cuda_rc(wmg::ew_combo(n, k, out, V, ldv, cf, accumulate, STREAM(stream)));
+}
+int wmg_cast(long long n, int to_f32, void* out, const void* in, void* stream) {
+  REQ(out && in);
+  return cuda_rc(wmg::ew_cast(n, to_f32, out, in, STREAM(stream)));
+}
+
+int wmg_haar_restrict(int side, const double* fine, int band_mask, double* out, void* stream) {
+  REQ(fine && out);
+  if (side < 2 || side % 2) return fail(WMG_EINVAL, "grid side must be even and >= 2");
+  if (band_mask < 1 || band_mask > 15) return fail(WMG_EINVAL, "bad band mask");
+  return cuda_rc(wmg::haar_restrict(side, fine, band_mask, out, STREAM(stream)));
+}
+
+int wmg_haar_prolong(int side, const double* coarse, int band, double* fine, int accumulate,
+                     void* stream) {
+  REQ(coarse && fine);
+  if (side < 2 || side % 2) return fail(WMG_EINVAL, "grid side must be even and >= 2");
+  if (band < 0 || band > 3) return fail(WMG_EINVAL, "bad band");
+  return cuda_rc(wmg::haar_prolong(side, coarse, band, fine, accumulate, STREAM(stream)));
+}
+
+int wmg_leaf_factor(const wmg_geometry* g, int depth, const int* bands, long long ray0,
+                    long long nrays, double* P, void* stream) {
+  REQ(g && bands && P);
+  if (depth < 1 || depth > 12) return fail(WMG_EINVAL, "bad depth");
+  if ((g->dev.n >> depth) << depth != g->dev.n)
+    return fail(WMG_EINVAL, "n is not divisible by 2^depth");
+  const long long rays = (long long)g->dev.m * g->dev.d;
+  if (ray0 < 0 || nrays < 0 || ray0 + nrays > rays) return fail(WMG_EDIM, "ray range");
+  for (int i = 0; i < depth; ++i)
+    if (bands[i] < 0 || bands[i] > 3) return fail(WMG_EINVAL, "bad band");
+  if (nrays == 0) return WMG_OK;
+  return cuda_rc(wmg::leaf_factor(g->dev, depth, bands, ray0, nrays, P, STREAM(stream)));
+}
+
+}  // extern "C"

@@ -1,0 +1,49 @@
+// common.cuh -- shared types for the sm_100a projector / solver kernels.
+//
+// Conventions follow the reference geometry (/root/reference/pkg/src/wmgtomo/
+// geometry.py:1-21): n x n unit pixels centred at the origin, image vectors
+// row-major with row 0 at the top (largest y), sinograms angle-major m x d,
+// ray point = o*(c, s) + t*(-s, c), detector offsets o_j = j - (d-1)/2.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace wmg {
+
+// Per-angle parameters.  (c, s) are the reference's snapped trig values
+// (geometry.py:77-85), computed on the host with numpy so the device never
+// evaluates cos/sin itself.  The remaining fields drive the fast kernels'
+// slab walk and are derived on the host in float64.
+struct AngleParams {
+  double c, s;        // snapped cos / sin
+  // ---- fast slab-walk parameters -------------------------------------
+  // The ray is walked slab by slab along its major axis (image rows when
+  // |c| >= |s|, columns otherwise).  u is the minor-axis grid coordinate in
+  // [0, n]; after the optional mirror u -> n - u the slope per slab is >= 0.
+  double u0;          // u at slab 0 for detector offset o = 0 (after mirror)
+  double du;          // du / do (per unit detector offset, after mirror)
+  double slope;       // du per slab, >= 0
+  float L;            // ray length per full slab = 1 / |major component|
+  float Ls;           // ray length per unit u = 1 / |minor component| (inf if 0)
+  // ---- pixel-driven (backprojection) trapezoid -------------------------
+  float hw;           // (|c| + |s|) / 2 : half support in detector units
+  float inv_cs;       // 1 / (|c| |s|) (unused when axis aligned)
+  int major;          // 0: slabs are rows (y-major), 1: slabs are columns
+  int mirror;         // 1 when the minor axis is mirrored
+  int axis;           // 1 when s == 0 or c == 0 (exact axis-aligned angle)
+  int pad_;
+};
+
+struct GeomDev {
+  int n;              // pixels per side
+  int d;              // detectors per angle
+  int m;              // angles
+  const AngleParams* ang;   // device table, length m
+};
+
+// Fixed-point minor coordinate used by the fast kernels: 64-bit signed with
+// 40 fractional bits (|u| < 2^22 is ample for n <= 8192).
+constexpr int kFixFrac = 40;
+constexpr double kFixScale = 1099511627776.0;  // 2^40
+
+}  // namespace wmg

@@ -1,0 +1,217 @@
+// projector_fast.cu -- throughput line-intersection projector pair.
+//
+// Same system matrix as the reference (/root/reference/pkg/src/wmgtomo/
+// geometry.py:88-128: exact ray/pixel intersection lengths, axis-aligned rays
+// on a grid line belong to the higher-x / higher-y pixel) but evaluated in the
+// form that is cheapest on sm_100a, with arbitrary summation order:
+//
+//  forward  (ray-driven): the ray is walked slab by slab along its major axis
+//    (rows for |cos| >= |sin|, columns otherwise; columns are read from a
+//    transposed copy of the image so every slab is a contiguous line).  In a
+//    slab the ray covers the minor interval [u, u + slope] (slope in [0,1]
+//    after an optional mirror), i.e. at most two pixels:
+//        w(k_hi) = min(frac(u + slope) * Ls, L),  w(k_hi - 1) = L - w(k_hi)
+//    u is carried in 64-bit fixed point (40 fractional bits) so the geometry is
+//    exact to ~1e-9 px at every n while the data path is fp32.
+//  backward (pixel-driven gather, no atomics): for each angle the pixel's
+//    chord function is the trapezoid T(delta) = clamp((hw - |delta|)/(|c||s|),
+//    0, 1/max(|c|,|s|)) of the detector offset delta = j - p; at most two
+//    detectors are in its support.  p is evaluated in float64.
+//
+// Tolerance vs the float64 reference: 1e-5 relative (fp32 data), see
+// tests/test_gpu_projector.py.
+#include "common.cuh"
+
+namespace wmg {
+namespace fast {
+
+template <typename T>
+__device__ __forceinline__ float to_f(T v) { return (float)v; }
+
+template <typename R>
+__device__ __forceinline__ R frac_of(long long U);
+
+template <>
+__device__ __forceinline__ float frac_of<float>(long long U) {
+  // 23 high fractional bits -> [1,2) mantissa -> subtract 1
+  const unsigned bits = (unsigned)((unsigned long long)U >> (kFixFrac - 23)) & 0x7FFFFFu;
+  return __int_as_float(0x3F800000u | bits) - 1.0f;
+}
+template <>
+__device__ __forceinline__ double frac_of<double>(long long U) {
+  const long long m = U & ((1LL << kFixFrac) - 1);
+  return (double)m * (1.0 / kFixScale);
+}
+
+template <typename TIn, typename R>
+__device__ __forceinline__ R load_px(const TIn* __restrict__ src, long long rowbase, int k, int n,
+                                     int mirror) {
+  if (k < 0 || k >= n) return R(0);
+  const int kk = mirror ? (n - 1 - k) : k;
+  return (R)__ldg(src + rowbase + kk);
+}
+
+// One thread per ray, block = consecutive detectors of one angle (blockIdx.y).
+template <typename TIn, typename TOut, typename R>
+__global__ void __launch_bounds__(128) fwd_kernel(GeomDev G, const TIn* __restrict__ img,
+                                                  const TIn* __restrict__ imgT,
+                                                  TOut* __restrict__ sino) {
+  const int a = blockIdx.y;
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= G.d) return;
+  const AngleParams& P = G.ang[a];
+  const int n = G.n;
+  const TIn* __restrict__ src = P.major ? imgT : img;
+  const double off = (double)j - (double)(G.d - 1) * 0.5;
+  const double u0 = P.u0 + off * P.du;   // minor coordinate at the start of slab 0
+  const double slope = P.slope;
+  int r0 = 0, r1 = n - 1;
+  if (slope > 0.0) {
+    const double ra = floor((-1.0 - u0) / slope) - 1.0;
+    const double rb = ceil(((double)n + 1.0 - u0) / slope) + 1.0;
+    r0 = (int)fmax(ra, 0.0);
+    r1 = (int)fmin(rb, (double)(n - 1));
+  } else if (u0 < -1.0 || u0 > (double)n + 1.0) {
+    r1 = -1;
+  }
+  const long long S = llrint(slope * kFixScale);
+  long long U = llrint(u0 * kFixScale) + (long long)r0 * S;
+  const R L = (R)P.L, Ls = (R)P.Ls;
+  R acc = R(0);
+  for (int r = r0; r <= r1; ++r) {
+    const long long Uh = U + S;
+    const int k = (int)(Uh >> kFixFrac);
+    const R f = frac_of<R>(Uh);
+    R wh = f * Ls;
+    wh = (wh < L) ? wh : L;              // NaN (0*inf, ray on a grid line) -> L
+    const R wl = L - wh;
+    const long long rowbase = (long long)r * n;
+    acc += wh * load_px<TIn, R>(src, rowbase, k, n, P.mirror);
+    acc += wl * load_px<TIn, R>(src, rowbase, k - 1, n, P.mirror);
+    U = Uh;
+  }
+  sino[(long long)a * G.d + j] = (TOut)acc;
+}
+
+// One thread per pixel; all threads walk the angles in the same order.
+template <typename TIn, typename TOut, typename R, bool kAccumulate>
+__global__ void __launch_bounds__(256) bwd_kernel(GeomDev G, const TIn* __restrict__ sino,
+                                                  TOut* __restrict__ img) {
+  const int n = G.n;
+  const int ix = blockIdx.x * 32 + (threadIdx.x & 31);
+  const int row = blockIdx.y * 8 + (threadIdx.x >> 5);
+  if (ix >= n || row >= n) return;
+  const double xc = (double)ix - (double)n * 0.5 + 0.5;
+  const double yc = (double)n * 0.5 - (double)row - 0.5;
+  const double dc = (double)(G.d - 1) * 0.5;
+  R acc = R(0);
+  for (int a = 0; a < G.m; ++a) {
+    const AngleParams& P = G.ang[a];
+    const double p = xc * P.c + yc * P.s + dc;   // detector-index coordinate
+    const TIn* __restrict__ yrow = sino + (long long)a * G.d;
+    if (P.axis) {
+      const int j = (int)ceil(p - 0.5);
+      if (j >= 0 && j < G.d) acc += (R)__ldg(yrow + j);
+      continue;
+    }
+    const double fl = floor(p - (double)P.hw);
+    const int j0 = (int)fl + 1;
+    const R d0 = (R)(fl + 1.0 - p);
+    const R d1 = d0 + R(1);
+    const R hw = (R)P.hw, ic = (R)P.inv_cs, L = (R)P.L;
+    R w0 = (hw - fabs(d0)) * ic;
+    R w1 = (hw - fabs(d1)) * ic;
+    w0 = w0 < R(0) ? R(0) : (w0 > L ? L : w0);
+    w1 = w1 < R(0) ? R(0) : (w1 > L ? L : w1);
+    if (j0 >= 0 && j0 < G.d) acc += w0 * (R)__ldg(yrow + j0);
+    if (j0 + 1 >= 0 && j0 + 1 < G.d) acc += w1 * (R)__ldg(yrow + j0 + 1);
+  }
+  const long long p = (long long)row * n + ix;
+  if (kAccumulate)
+    img[p] = (TOut)((R)img[p] + acc);
+  else
+    img[p] = (TOut)acc;
+}
+
+template <typename T>
+__global__ void transpose_kernel(const T* __restrict__ in, T* __restrict__ out, int n) {
+  __shared__ T tile[32][33];
+  const int bx = blockIdx.x * 32, by = blockIdx.y * 32;
+  for (int i = threadIdx.y; i < 32; i += 8) {
+    const int r = by + i, c = bx + threadIdx.x;
+    if (r < n && c < n) tile[i][threadIdx.x] = in[(long long)r * n + c];
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += 8) {
+    const int r = bx + i, c = by + threadIdx.x;
+    if (r < n && c < n) out[(long long)r * n + c] = tile[threadIdx.x][i];
+  }
+}
+
+}  // namespace fast
+
+// ---------------------------------------------------------------------------
+// host launchers.  dtype codes: 0 = float32, 1 = float64.
+// ---------------------------------------------------------------------------
+template <typename TIn>
+static cudaError_t launch_transpose(const TIn* in, TIn* out, int n, cudaStream_t st) {
+  dim3 grid((n + 31) / 32, (n + 31) / 32), block(32, 8);
+  fast::transpose_kernel<TIn><<<grid, block, 0, st>>>(in, out, n);
+  return cudaGetLastError();
+}
+
+template <typename TIn, typename TOut, typename R>
+static cudaError_t fwd_impl(const GeomDev& G, const void* x, void* xT_ws, void* y,
+                            cudaStream_t st) {
+  const TIn* img = (const TIn*)x;
+  TIn* imgT = (TIn*)xT_ws;
+  cudaError_t e = launch_transpose<TIn>(img, imgT, G.n, st);
+  if (e != cudaSuccess) return e;
+  dim3 grid((G.d + 127) / 128, G.m);
+  fast::fwd_kernel<TIn, TOut, R><<<grid, 128, 0, st>>>(G, img, imgT, (TOut*)y);
+  return cudaGetLastError();
+}
+
+template <typename TIn, typename TOut, typename R>
+static cudaError_t bwd_impl(const GeomDev& G, const void* y, void* x, bool accumulate,
+                            cudaStream_t st) {
+  dim3 grid((G.n + 31) / 32, (G.n + 7) / 8);
+  if (accumulate)
+    fast::bwd_kernel<TIn, TOut, R, true><<<grid, 256, 0, st>>>(G, (const TIn*)y, (TOut*)x);
+  else
+    fast::bwd_kernel<TIn, TOut, R, false><<<grid, 256, 0, st>>>(G, (const TIn*)y, (TOut*)x);
+  return cudaGetLastError();
+}
+
+// precision: 0 = fp32 arithmetic, 1 = fp64 arithmetic
+cudaError_t fast_forward(const GeomDev& G, int precision, int tin, int tout, const void* x,
+                         void* xT_ws, void* y, cudaStream_t st) {
+  if (G.m == 0 || G.d == 0) return cudaSuccess;
+  if (precision == 0) {
+    if (tin == 0 && tout == 0) return fwd_impl<float, float, float>(G, x, xT_ws, y, st);
+    if (tin == 1 && tout == 1) return fwd_impl<double, double, float>(G, x, xT_ws, y, st);
+    if (tin == 1 && tout == 0) return fwd_impl<double, float, float>(G, x, xT_ws, y, st);
+    if (tin == 0 && tout == 1) return fwd_impl<float, double, float>(G, x, xT_ws, y, st);
+  } else {
+    if (tin == 1 && tout == 1) return fwd_impl<double, double, double>(G, x, xT_ws, y, st);
+    if (tin == 0 && tout == 0) return fwd_impl<float, float, double>(G, x, xT_ws, y, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t fast_backward(const GeomDev& G, int precision, int tin, int tout, const void* y,
+                          void* x, bool accumulate, cudaStream_t st) {
+  if (G.n == 0) return cudaSuccess;
+  if (precision == 0) {
+    if (tin == 0 && tout == 0) return bwd_impl<float, float, float>(G, y, x, accumulate, st);
+    if (tin == 1 && tout == 1) return bwd_impl<double, double, float>(G, y, x, accumulate, st);
+    if (tin == 1 && tout == 0) return bwd_impl<double, float, float>(G, y, x, accumulate, st);
+    if (tin == 0 && tout == 1) return bwd_impl<float, double, float>(G, y, x, accumulate, st);
+  } else {
+    if (tin == 1 && tout == 1) return bwd_impl<double, double, double>(G, y, x, accumulate, st);
+    if (tin == 0 && tout == 0) return bwd_impl<float, float, double>(G, y, x, accumulate, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace wmg

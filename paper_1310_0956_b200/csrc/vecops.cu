@@ -1,0 +1,403 @@
+// vecops.cu -- Krylov vector kernels (float64) and Haar intergrid kernels.
+//
+// Deterministic reduction ("DET_SUM"), shared bit for bit with the CPU
+// restatement in oracle/solvers.py (det_sum):
+//   * element values v_i are formed with individually rounded ops (no FMA),
+//   * the vector is cut into 1024-element chunks (zero padded); in chunk c,
+//     lane l of a warp sums v[c*1024 + k*32 + l] for k = 0..31 sequentially,
+//     then the 32 lane sums are combined by the fixed tree
+//     s[l] += s[l + off], off = 16, 8, 4, 2, 1 (lane 0 holds the chunk sum),
+//   * the chunk sums are reduced by the same procedure until one value is left.
+// Every Krylov dot/norm in the GPU solvers uses it, so GPU and oracle residual
+// histories agree to the last bit (SURVEY.md s8(c) "parity protocol").
+//
+// Haar kernels follow /root/reference/pkg/src/wmgtomo/multilevel.py:36-79
+// (coefficients +-fl(fl(1/sqrt 2)^2) = +-0.4999999999999999, 2x2 block in the
+// order (2i,2k), (2i,2k+1), (2i+1,2k), (2i+1,2k+1); csr_matvec summation from
+// 0.0) and the band accumulation of wtg_apply (multilevel.py:175-198).
+#include "common.cuh"
+
+namespace wmg {
+namespace vec {
+
+__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+
+enum RedOp : int { kDot = 0, kSqDiff = 1, kSum = 2, kDotDiff = 3, kSq = 4 };
+
+struct RedArgs {
+  const double* a[8];
+  const double* b[8];
+  const double* c[8];
+  int op[8];
+};
+
+__device__ __forceinline__ double elem(const RedArgs& A, int k, long long i) {
+  const int op = A.op[k];
+  const double a = A.a[k][i];
+  if (op == kSum) return a;
+  if (op == kSq) return dmul(a, a);
+  const double b = A.b[k][i];
+  if (op == kDot) return dmul(a, b);
+  if (op == kSqDiff) {
+    const double t = dsub(a, b);
+    return dmul(t, t);
+  }
+  return dmul(a, dsub(b, A.c[k][i]));   // kDotDiff
+}
+
+// level 1: 8 warps per block, one chunk of 1024 elements per warp
+__global__ void __launch_bounds__(256) det_level1(long long n, RedArgs A, double* partials,
+                                                  long long C) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long chunk = (long long)blockIdx.x * 8 + warp;
+  const int k = blockIdx.y;
+  if (chunk >= C) return;
+  const long long base = chunk * 1024;
+  double s = 0.0;
+#pragma unroll 4
+  for (int r = 0; r < 32; ++r) {
+    const long long i = base + r * 32 + lane;
+    const double v = (i < n) ? elem(A, k, i) : 0.0;
+    s = (r == 0) ? v : dadd(s, v);
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) s = dadd(s, __shfl_down_sync(0xffffffffu, s, off));
+  if (lane == 0) partials[(long long)k * C + chunk] = s;
+}
+
+// chunk reduce of one warp over buf[0..len) (zero padded), chunk index c
+__device__ __forceinline__ double warp_chunk(const double* buf, long long len, long long c,
+                                             int lane) {
+  const long long base = c * 1024;
+  double s = 0.0;
+  for (int r = 0; r < 32; ++r) {
+    const long long i = base + r * 32 + lane;
+    const double v = (i < len) ? buf[i] : 0.0;
+    s = (r == 0) ? v : dadd(s, v);
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) s = dadd(s, __shfl_down_sync(0xffffffffu, s, off));
+  return s;
+}
+
+// finish: one block (32 warps) per reduction; level 2 (C <= 2^20 chunk sums,
+// i.e. n <= 2^30) into shared memory, level 3 by warp 0.
+__global__ void __launch_bounds__(1024) det_finish(const double* partials, long long C,
+                                                   double* out) {
+  __shared__ double lvl[1024];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int k = blockIdx.x;
+  const double* buf = partials + (long long)k * C;
+  if (C == 1) {
+    if (threadIdx.x == 0) out[k] = buf[0];
+    return;
+  }
+  const long long C2 = (C + 1023) / 1024;
+  for (long long c = warp; c < C2; c += 32) {
+    const double s = warp_chunk(buf, C, c, lane);
+    if (lane == 0) lvl[c] = s;
+  }
+  __syncthreads();
+  if (C2 == 1) {
+    if (threadIdx.x == 0) out[k] = lvl[0];
+    return;
+  }
+  if (warp == 0) {
+    const double s = warp_chunk(lvl, C2, 0, lane);
+    if (lane == 0) out[k] = s;
+  }
+}
+
+// max |a - b| (or max |a| when b == nullptr); order independent
+__global__ void maxabs_kernel(long long n, const double* a, const double* b,
+                              unsigned long long* out) {
+  double m = 0.0;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const double v = b ? fabs(dsub(a[i], b[i])) : fabs(a[i]);
+    m = fmax(m, v);
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) m = fmax(m, __shfl_down_sync(0xffffffffu, m, off));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, (unsigned long long)__double_as_longlong(m));
+}
+
+// ---------------------------------------------------------------------------
+// elementwise kernels; every op individually rounded, same as numpy
+// ---------------------------------------------------------------------------
+#define GRID_LOOP(i, n)                                                            \
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < (n); \
+       i += (long long)gridDim.x * blockDim.x)
+
+// out = y + s * (alpha * x), s = +1 / -1   (numpy: y + alpha*x, y - alpha*x)
+__global__ void axpy_kernel(long long n, double* out, const double* y, double alpha, int sgn,
+                            const double* x) {
+  GRID_LOOP(i, n) {
+    const double t = dmul(alpha, x[i]);
+    out[i] = sgn > 0 ? dadd(y[i], t) : dsub(y[i], t);
+  }
+}
+
+// out = a*x + b*y (+ c*z)  evaluated as ((a*x + b*y) + c*z)
+__global__ void lincomb_kernel(long long n, double* out, double a, const double* x, double b,
+                               const double* y, double c, const double* z) {
+  GRID_LOOP(i, n) {
+    double t = dadd(dmul(a, x[i]), dmul(b, y[i]));
+    if (z) t = dadd(t, dmul(c, z[i]));
+    out[i] = t;
+  }
+}
+
+// BiCGStab direction: p = r + beta * (p - omega * v)   (solvers.py:207)
+__global__ void bicg_p_kernel(long long n, double* p, const double* r, double beta, double omega,
+                              const double* v) {
+  GRID_LOOP(i, n) { p[i] = dadd(r[i], dmul(beta, dsub(p[i], dmul(omega, v[i])))); }
+}
+
+// x = x + alpha*ph + omega*sh   (solvers.py:229)
+__global__ void bicg_x_kernel(long long n, double* x, double alpha, const double* ph,
+                              double omega, const double* sh) {
+  GRID_LOOP(i, n) { x[i] = dadd(dadd(x[i], dmul(alpha, ph[i])), dmul(omega, sh[i])); }
+}
+
+// out = a * x (scale), or out = x * y elementwise when y != nullptr
+__global__ void scale_kernel(long long n, double* out, double a, const double* x,
+                             const double* y) {
+  GRID_LOOP(i, n) { out[i] = y ? dmul(x[i], y[i]) : dmul(a, x[i]); }
+}
+
+// inverse with the SIRT zero convention: out = s > 0 ? 1/s : 0 (solvers.py:84-85)
+__global__ void recip_kernel(long long n, double* out, const double* s) {
+  GRID_LOOP(i, n) { out[i] = s[i] > 0.0 ? __drcp_rn(s[i]) : 0.0; }
+}
+
+// SIRT update (solvers.py:125-128): upd = c*g; if lam>0: upd -= lam*(c*x); x += upd
+__global__ void sirt_update_kernel(long long n, double* x, const double* c, const double* g,
+                                   double lam) {
+  GRID_LOOP(i, n) {
+    double upd = dmul(c[i], g[i]);
+    if (lam > 0.0) upd = dsub(upd, dmul(lam, dmul(c[i], x[i])));
+    x[i] = dadd(x[i], upd);
+  }
+}
+
+// out = g + lam*v  (normal_operator, solvers.py:151-153; only when lam != 0)
+// out = g - lam*v  (sgn < 0, CGLS gradient W^T r - lam x)
+__global__ void add_scaled_kernel(long long n, double* out, const double* g, double lam, int sgn,
+                                  const double* v) {
+  GRID_LOOP(i, n) {
+    const double t = dmul(lam, v[i]);
+    out[i] = sgn > 0 ? dadd(g[i], t) : dsub(g[i], t);
+  }
+}
+
+// w = w - sum_i h_i v_i, i ascending (classical Gram-Schmidt update, GMRES)
+__global__ void cgs_update_kernel(long long n, int k, double* w, const double* V, long long ldv,
+                                  const double* h) {
+  GRID_LOOP(i, n) {
+    double t = w[i];
+    for (int q = 0; q < k; ++q) t = dsub(t, dmul(h[q], V[(long long)q * ldv + i]));
+    w[i] = t;
+  }
+}
+
+// out = sum_i c_i v_i, i ascending starting from c_0 v_0 (GMRES solution update)
+__global__ void combo_kernel(long long n, int k, double* out, const double* V, long long ldv,
+                             const double* cf, int accumulate) {
+  GRID_LOOP(i, n) {
+    double t = accumulate ? out[i] : 0.0;
+    for (int q = 0; q < k; ++q) {
+      const double pr = dmul(cf[q], V[(long long)q * ldv + i]);
+      t = (q == 0 && !accumulate) ? pr : dadd(t, pr);
+    }
+    out[i] = t;
+  }
+}
+
+// dtype casts for the fp32-projector / fp64-Krylov configurations
+__global__ void cast_f64_f32(long long n, float* out, const double* in) {
+  GRID_LOOP(i, n) { out[i] = (float)in[i]; }
+}
+__global__ void cast_f32_f64(long long n, double* out, const float* in) {
+  GRID_LOOP(i, n) { out[i] = (double)in[i]; }
+}
+
+// ---------------------------------------------------------------------------
+// Haar intergrid operators on a side x side row-major grid
+// band: 0 LL, 1 LH, 2 HL, 3 HH.  kron(row factor, col factor) with the row
+// factor acting along y (multilevel.py:61-79): LH = kron(J, S), HL = kron(S, J).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void band_signs(int band, double& s00, double& s01, double& s10,
+                                           double& s11) {
+  const double h = 0.4999999999999999;   // fl(fl(1/sqrt(2))^2), multilevel.py:43,53
+  const bool wy = (band == 1 || band == 3);   // wavelet along rows (y)
+  const bool wx = (band == 2 || band == 3);   // wavelet along columns (x)
+  s00 = h;
+  s01 = wx ? -h : h;
+  s10 = wy ? -h : h;
+  s11 = (wx != wy) ? -h : h;
+}
+
+// coarse[b][(i,k)] = R_b fine, for the bands in mask (bit b); out laid out as
+// out + b_slot * side^2/4 where b_slot counts the selected bands in order
+__global__ void haar_restrict_kernel(int side, const double* __restrict__ fine, int band_mask,
+                                     double* __restrict__ out) {
+  const int hs = side / 2;
+  const long long nc = (long long)hs * hs;
+  GRID_LOOP(q, nc) {
+    const int i = (int)(q / hs), k = (int)(q % hs);
+    const long long f0 = (long long)(2 * i) * side + 2 * k;
+    const double x00 = fine[f0], x01 = fine[f0 + 1];
+    const double x10 = fine[f0 + side], x11 = fine[f0 + side + 1];
+    int slot = 0;
+    for (int b = 0; b < 4; ++b) {
+      if (!((band_mask >> b) & 1)) continue;
+      double s00, s01, s10, s11;
+      band_signs(b, s00, s01, s10, s11);
+      double acc = 0.0;
+      acc = dadd(acc, dmul(s00, x00));
+      acc = dadd(acc, dmul(s01, x01));
+      acc = dadd(acc, dmul(s10, x10));
+      acc = dadd(acc, dmul(s11, x11));
+      out[(long long)slot * nc + q] = acc;
+      ++slot;
+    }
+  }
+}
+
+// fine = (accumulate ? fine : 0) + R_b^T coarse  (one product per fine pixel)
+__global__ void haar_prolong_kernel(int side, const double* __restrict__ coarse, int band,
+                                    double* __restrict__ fine, int accumulate) {
+  const long long nf = (long long)side * side;
+  const int hs = side / 2;
+  double s[4];
+  band_signs(band, s[0], s[1], s[2], s[3]);
+  GRID_LOOP(f, nf) {
+    const int r = (int)(f / side), col = (int)(f % side);
+    const int q = (r >> 1) * hs + (col >> 1);
+    const double v = dmul(s[((r & 1) << 1) | (col & 1)], coarse[q]);
+    fine[f] = accumulate ? dadd(fine[f], v) : v;
+  }
+}
+
+}  // namespace vec
+
+// ---------------------------------------------------------------------------
+// host launchers
+// ---------------------------------------------------------------------------
+static inline unsigned grid_for(long long n, int tpb) {
+  long long g = (n + tpb - 1) / tpb;
+  if (g > 148LL * 32) g = 148LL * 32;
+  if (g < 1) g = 1;
+  return (unsigned)g;
+}
+
+cudaError_t det_reduce(long long n, int K, const int* ops, const double* const* a,
+                       const double* const* b, const double* const* c, double* scratch,
+                       double* out, cudaStream_t st) {
+  if (K < 1 || K > 8) return cudaErrorInvalidValue;
+  vec::RedArgs A;
+  for (int k = 0; k < 8; ++k) {
+    A.a[k] = k < K ? a[k] : nullptr;
+    A.b[k] = (k < K && b) ? b[k] : nullptr;
+    A.c[k] = (k < K && c) ? c[k] : nullptr;
+    A.op[k] = k < K ? ops[k] : 0;
+  }
+  if (n <= 0) {
+    return cudaMemsetAsync(out, 0, sizeof(double) * K, st);
+  }
+  const long long C = (n + 1023) / 1024;
+  if (C > 1024LL * 1024LL) return cudaErrorInvalidValue;
+  dim3 grid((unsigned)((C + 7) / 8), K);
+  vec::det_level1<<<grid, 256, 0, st>>>(n, A, scratch, C);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  vec::det_finish<<<K, 1024, 0, st>>>(scratch, C, out);
+  return cudaGetLastError();
+}
+
+long long det_scratch_len(long long n, int K) { return ((n + 1023) / 1024 + 1) * (long long)K; }
+
+cudaError_t maxabs(long long n, const double* a, const double* b, double* out_bits,
+                   cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(out_bits, 0, sizeof(double), st);
+  if (e != cudaSuccess) return e;
+  if (n <= 0) return cudaSuccess;
+  vec::maxabs_kernel<<<grid_for(n, 256), 256, 0, st>>>(n, a, b, (unsigned long long*)out_bits);
+  return cudaGetLastError();
+}
+
+#define LAUNCH_EW(kernel, n, ...)                                        \
+  do {                                                                   \
+    if ((n) <= 0) return cudaSuccess;                                    \
+    kernel<<<grid_for((n), 256), 256, 0, st>>>((n), __VA_ARGS__);        \
+    return cudaGetLastError();                                           \
+  } while (0)
+
+cudaError_t ew_axpy(long long n, double* out, const double* y, double alpha, int sgn,
+                    const double* x, cudaStream_t st) {
+  LAUNCH_EW(vec::axpy_kernel, n, out, y, alpha, sgn, x);
+}
+cudaError_t ew_lincomb(long long n, double* out, double a, const double* x, double b,
+                       const double* y, double c, const double* z, cudaStream_t st) {
+  LAUNCH_EW(vec::lincomb_kernel, n, out, a, x, b, y, c, z);
+}
+cudaError_t ew_bicg_p(long long n, double* p, const double* r, double beta, double omega,
+                      const double* v, cudaStream_t st) {
+  LAUNCH_EW(vec::bicg_p_kernel, n, p, r, beta, omega, v);
+}
+cudaError_t ew_bicg_x(long long n, double* x, double alpha, const double* ph, double omega,
+                      const double* sh, cudaStream_t st) {
+  LAUNCH_EW(vec::bicg_x_kernel, n, x, alpha, ph, omega, sh);
+}
+cudaError_t ew_scale(long long n, double* out, double a, const double* x, const double* y,
+                     cudaStream_t st) {
+  LAUNCH_EW(vec::scale_kernel, n, out, a, x, y);
+}
+cudaError_t ew_recip(long long n, double* out, const double* s, cudaStream_t st) {
+  LAUNCH_EW(vec::recip_kernel, n, out, s);
+}
+cudaError_t ew_sirt_update(long long n, double* x, const double* c, const double* g, double lam,
+                           cudaStream_t st) {
+  LAUNCH_EW(vec::sirt_update_kernel, n, x, c, g, lam);
+}
+cudaError_t ew_add_scaled(long long n, double* out, const double* g, double lam, int sgn,
+                          const double* v, cudaStream_t st) {
+  LAUNCH_EW(vec::add_scaled_kernel, n, out, g, lam, sgn, v);
+}
+cudaError_t ew_cgs_update(long long n, int k, double* w, const double* V, long long ldv,
+                          const double* h, cudaStream_t st) {
+  LAUNCH_EW(vec::cgs_update_kernel, n, k, w, V, ldv, h);
+}
+cudaError_t ew_combo(long long n, int k, double* out, const double* V, long long ldv,
+                     const double* cf, int accumulate, cudaStream_t st) {
+  LAUNCH_EW(vec::combo_kernel, n, k, out, V, ldv, cf, accumulate);
+}
+cudaError_t ew_cast(long long n, int to_f32, void* out, const void* in, cudaStream_t st) {
+  if (to_f32) {
+    LAUNCH_EW(vec::cast_f64_f32, n, (float*)out, (const double*)in);
+  } else {
+    LAUNCH_EW(vec::cast_f32_f64, n, (double*)out, (const float*)in);
+  }
+}
+
+cudaError_t haar_restrict(int side, const double* fine, int band_mask, double* out,
+                          cudaStream_t st) {
+  const long long nc = (long long)(side / 2) * (side / 2);
+  if (nc <= 0) return cudaSuccess;
+  vec::haar_restrict_kernel<<<grid_for(nc, 256), 256, 0, st>>>(side, fine, band_mask, out);
+  return cudaGetLastError();
+}
+
+cudaError_t haar_prolong(int side, const double* coarse, int band, double* fine, int accumulate,
+                         cudaStream_t st) {
+  const long long nf = (long long)side * side;
+  if (nf <= 0) return cudaSuccess;
+  vec::haar_prolong_kernel<<<grid_for(nf, 256), 256, 0, st>>>(side, coarse, band, fine,
+                                                              accumulate);
+  return cudaGetLastError();
+}
+
+}  // namespace wmg

@@ -1,0 +1,360 @@
+"""Parallel-beam geometry and the matrix-free line-intersection projector on B200.
+
+Drop-in for /root/reference/pkg/src/wmgtomo/geometry.py:
+  * ``Geometry`` / ``build_geometry`` (:34-74) -- identical validation and
+    angle grid ``arange(m) * (pi / m)``;
+  * ``build_projector(g, kernel="line")`` (:178-197) returns a ``LineProjector``
+    instead of a scipy CSR.  It implements the subset of the scipy protocol the
+    reference solvers use: ``shape``, ``@``, ``.T``,
+    ``.tocsr()``, ``.sum(axis)``; W is never materialised -- the weights are
+    recomputed by the sm_100a kernels on every application;
+  * ``apply`` / ``apply_transpose`` (:200-215) with the same
+    ``DimensionMismatchError`` contract.
+
+Numerics.  ``precision="float64"`` (default) runs the PARITY kernels: weights,
+pixel assignment and summation orders are bit-identical to the reference CSR and
+scipy's csr_matvec / csc_matvec.  ``precision="float32"`` runs the FAST kernels
+(fp32 data and accumulation, 64-bit fixed-point geometry), within 1e-5 relative
+of the float64 reference.  ``mode="fast"`` with float64 selects the fast kernels
+in float64 arithmetic.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _device as D
+from . import _native as N
+from .sparse_kernels import DimensionMismatchError
+
+
+@dataclass(frozen=True)
+class Geometry:
+    """Parallel-beam scan description: n-by-n grid, m angles, rays per angle."""
+
+    n_pixels_per_side: int
+    n_detectors: int
+    n_angles: int
+    angles: np.ndarray = field(repr=False)
+    pixel_size: float = 1.0
+    detector_spacing: float = 1.0
+
+    def __post_init__(self):
+        if self.n_pixels_per_side < 1 or self.n_detectors < 1 or self.n_angles < 1:
+            raise ValueError("geometry dimensions must be positive")
+        a = np.asarray(self.angles, dtype=np.float64)
+        if a.shape != (self.n_angles,):
+            raise ValueError("angles length must equal n_angles")
+        if np.any(a < 0.0) or np.any(a >= np.pi):
+            raise ValueError("angles must lie in [0, pi)")
+        if np.any(np.diff(a) <= 0.0):
+            raise ValueError("angles must be strictly increasing")
+        if self.pixel_size != 1.0 or self.detector_spacing != 1.0:
+            # the reference hard-wires unit pixels (geometry.py:92-95)
+            raise ValueError("only unit pixel size and detector spacing are supported")
+        object.__setattr__(self, "angles", a)
+
+    @property
+    def n_image(self) -> int:
+        return self.n_pixels_per_side ** 2
+
+    @property
+    def n_data(self) -> int:
+        return self.n_angles * self.n_detectors
+
+    def subset(self, index) -> "Geometry":
+        """Geometry restricted to a subset of the angles (rows of W)."""
+        a = self.angles[np.asarray(index)]
+        return Geometry(self.n_pixels_per_side, self.n_detectors, a.size, angles=a)
+
+
+def build_geometry(n: int, n_detectors: int, n_angles: int) -> Geometry:
+    """Equiangular geometry over the half-turn [0, pi) (geometry.py:68-74)."""
+    if n < 1 or n_detectors < 1 or n_angles < 1:
+        raise ValueError("all geometry arguments must be >= 1")
+    angles = np.arange(n_angles) * (np.pi / n_angles)
+    return Geometry(n_pixels_per_side=n, n_detectors=n_detectors,
+                    n_angles=n_angles, angles=angles)
+
+
+def snapped_trig(angles):
+    """geometry.py:77-85, evaluated on the host with numpy for every angle."""
+    a = np.asarray(angles, dtype=np.float64)
+    c = np.cos(a)
+    s = np.sin(a)
+    for i in range(a.size):
+        ci, si = float(np.cos(a[i])), float(np.sin(a[i]))
+        if abs(ci) < 1e-15:
+            ci, si = 0.0, float(np.sign(si))
+        elif abs(si) < 1e-15:
+            ci, si = float(np.sign(ci)), 0.0
+        c[i], s[i] = ci, si
+    return np.ascontiguousarray(c), np.ascontiguousarray(s)
+
+
+_PRECISIONS = {"float64": N.F64, "fp64": N.F64, "double": N.F64,
+               "float32": N.F32, "fp32": N.F32, "float": N.F32}
+
+
+class LineProjector:
+    """Matrix-free W (M x N) with the reference line-intersection weights."""
+
+    format = "matrix-free"
+
+    def __init__(self, g: Geometry, precision: str = "float64", mode: str | None = None,
+                 device=None):
+        t = D.require_cuda()
+        if precision not in _PRECISIONS:
+            raise ValueError(f"unknown precision '{precision}'")
+        self.geometry = g
+        self.precision = _PRECISIONS[precision]
+        if mode is None:
+            mode = "parity" if self.precision == N.F64 else "fast"
+        if mode not in ("parity", "fast"):
+            raise ValueError(f"unknown mode '{mode}'")
+        if mode == "parity" and self.precision != N.F64:
+            raise ValueError("parity mode is float64 only")
+        self.mode = mode
+        self._mode_code = N.MODE_PARITY if mode == "parity" else N.MODE_FAST
+        self.device = t.device(device) if device is not None else t.device("cuda",
+                                                                        t.cuda.current_device())
+        self.n = g.n_pixels_per_side
+        self.shape = (g.n_data, g.n_image)
+        self.dtype = np.float64
+        c, s = snapped_trig(g.angles)
+        self._cos, self._sin = c, s
+        handle = N.ctypes.c_void_p()
+        with t.cuda.device(self.device):
+            N.call("wmg_geometry_create", self.n, g.n_detectors, g.n_angles,
+                   c.ctypes.data_as(N.ctypes.POINTER(N.ctypes.c_double)),
+                   s.ctypes.data_as(N.ctypes.POINTER(N.ctypes.c_double)),
+                   N.ctypes.byref(handle))
+        self._h = handle
+        self._ws = {}
+        self._anomaly = t.zeros(1, dtype=t.int32, device=self.device)
+        self._sums = {}
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            try:
+                N.load().wmg_geometry_destroy(h)
+            except Exception:  # pragma: no cover - interpreter shutdown
+                pass
+            self._h = None
+
+    # ---------------------------------------------------------------- helpers
+    @property
+    def handle(self):
+        return self._h
+
+    @property
+    def T(self):
+        return _Transposed(self)
+
+    def tocsr(self):
+        return self
+
+    def _workspace(self, tin_code):
+        t = D.torch()
+        ws = self._ws.get(tin_code)
+        if ws is None:
+            dt = t.float32 if tin_code == N.F32 else t.float64
+            ws = t.empty(self.n * self.n, dtype=dt, device=self.device)
+            self._ws[tin_code] = ws
+        return ws
+
+    @staticmethod
+    def _code(tensor):
+        t = D.torch()
+        if tensor.dtype == t.float64:
+            return N.F64
+        if tensor.dtype == t.float32:
+            return N.F32
+        raise TypeError(f"unsupported dtype {tensor.dtype}")
+
+    def _io_dtype(self, v):
+        t = D.torch()
+        if D.is_torch(v) and v.is_cuda and v.dtype == t.float32 and self.precision == N.F32:
+            return t.float32
+        return t.float64 if (self.precision == N.F64 or not D.is_torch(v)) else v.dtype
+
+    # ------------------------------------------------------------ operators
+    def forward_(self, x, out, anomaly=None):
+        """out = W x on device tensors (float32/float64 as the mode allows)."""
+        tin, tout = self._code(x), self._code(out)
+        if x.numel() != self.shape[1]:
+            raise DimensionMismatchError(
+                f"apply: vector length {x.numel()} != n_cols {self.shape[1]}")
+        if out.numel() != self.shape[0]:
+            raise DimensionMismatchError("apply: output length mismatch")
+        ws = self._workspace(tin) if self._mode_code == N.MODE_FAST else None
+        N.call("wmg_forward", self._h, self._mode_code, self.precision, tin, tout,
+               D.ptr(x), D.ptr(out), D.ptr(ws), D.ptr(anomaly), D.stream_handle())
+        return out
+
+    def backward_(self, y, out, accumulate=False, anomaly=None):
+        """out (+)= W^T y on device tensors."""
+        tin, tout = self._code(y), self._code(out)
+        if y.numel() != self.shape[0]:
+            raise DimensionMismatchError(
+                f"apply_transpose: vector length {y.numel()} != n_rows {self.shape[0]}")
+        if out.numel() != self.shape[1]:
+            raise DimensionMismatchError("apply_transpose: output length mismatch")
+        N.call("wmg_backward", self._h, self._mode_code, self.precision, tin, tout, D.ptr(y),
+               D.ptr(out), int(bool(accumulate)), D.ptr(anomaly), D.stream_handle())
+        return out
+
+    def forward(self, x):
+        t = D.torch()
+        dt = self._io_dtype(x)
+        xd, was_np = D.to_device(x, dt, self.device)
+        if xd.dim() != 1:
+            xd = xd.reshape(-1)
+        if xd.numel() != self.shape[1]:
+            raise DimensionMismatchError(
+                f"apply: vector length {xd.numel()} != n_cols {self.shape[1]}")
+        out = t.empty(self.shape[0], dtype=dt, device=self.device)
+        self.forward_(xd, out)
+        return D.to_caller(out, was_np)
+
+    def backward(self, y):
+        t = D.torch()
+        dt = self._io_dtype(y)
+        yd, was_np = D.to_device(y, dt, self.device)
+        if yd.dim() != 1:
+            yd = yd.reshape(-1)
+        if yd.numel() != self.shape[0]:
+            raise DimensionMismatchError(
+                f"apply_transpose: vector length {yd.numel()} != n_rows {self.shape[0]}")
+        out = t.empty(self.shape[1], dtype=dt, device=self.device)
+        self.backward_(yd, out)
+        return D.to_caller(out, was_np)
+
+    def __matmul__(self, v):
+        return self.forward(v)
+
+    def dot(self, v):
+        return self.forward(v)
+
+    # ------------------------------------------------------------ scalings
+    def row_sums_dev(self):
+        """Row sums with the reference's np.add.reduceat semantics (device)."""
+        t = D.torch()
+        r = self._sums.get("rows")
+        if r is None:
+            r = t.empty(self.shape[0], dtype=t.float64, device=self.device)
+            N.call("wmg_row_sums", self._h, D.ptr(r), D.stream_handle())
+            self._sums["rows"] = r
+        return r
+
+    def col_sums_dev(self):
+        """Column sums = ones @ W (device)."""
+        t = D.torch()
+        c = self._sums.get("cols")
+        if c is None:
+            c = t.empty(self.shape[1], dtype=t.float64, device=self.device)
+            N.call("wmg_col_sums", self._h, D.ptr(c), D.stream_handle())
+            self._sums["cols"] = c
+        return c
+
+    def sum(self, axis=None):
+        if axis in (1, -1):
+            return self.row_sums_dev().cpu().numpy()
+        if axis in (0, -2):
+            return self.col_sums_dev().cpu().numpy()
+        if axis is None:
+            return float(self.row_sums_dev().sum().item())
+        raise ValueError(f"bad axis {axis}")
+
+    # ------------------------------------------------------------ exports
+    def csr_device(self):
+        """Exact CSR of W assembled on the GPU: (indptr, indices, data) tensors."""
+        t = D.torch()
+        M = self.shape[0]
+        counts = t.empty(M, dtype=t.int64, device=self.device)
+        anomaly = t.zeros(1, dtype=t.int32, device=self.device)
+        N.call("wmg_csr_counts", self._h, D.ptr(counts), D.ptr(anomaly), D.stream_handle())
+        indptr = t.zeros(M + 1, dtype=t.int64, device=self.device)
+        t.cumsum(counts, 0, out=indptr[1:])
+        nnz = int(indptr[-1].item())
+        cols = t.empty(max(nnz, 1), dtype=t.int64, device=self.device)
+        vals = t.empty(max(nnz, 1), dtype=t.float64, device=self.device)
+        N.call("wmg_csr_fill", self._h, D.ptr(indptr), D.ptr(cols), D.ptr(vals),
+               D.stream_handle())
+        return indptr, cols[:nnz], vals[:nnz], int(anomaly.item())
+
+    def to_scipy(self):
+        """Exact scipy CSR (small n only; for oracle comparisons)."""
+        import scipy.sparse as sp
+        indptr, cols, vals, _ = self.csr_device()
+        return sp.csr_matrix((vals.cpu().numpy(), cols.cpu().numpy(), indptr.cpu().numpy()),
+                             shape=self.shape)
+
+    def anomaly_count(self):
+        """Parity-walk consistency counter over one forward + backward pass."""
+        t = D.torch()
+        a = t.zeros(1, dtype=t.int32, device=self.device)
+        x = t.zeros(self.shape[1], dtype=t.float64, device=self.device)
+        y = t.zeros(self.shape[0], dtype=t.float64, device=self.device)
+        if self.mode == "parity":
+            self.forward_(x, y, anomaly=a)
+            self.backward_(y, x, anomaly=a)
+        return int(a.item())
+
+
+class _Transposed:
+    """W^T view (geometry.py:215 ``w.T``; solvers.py:111 ``w.T.tocsr()``)."""
+
+    def __init__(self, w: LineProjector):
+        self._w = w
+        self.shape = (w.shape[1], w.shape[0])
+
+    @property
+    def T(self):
+        return self._w
+
+    def tocsr(self):
+        return self
+
+    def __matmul__(self, v):
+        return self._w.backward(v)
+
+    def dot(self, v):
+        return self._w.backward(v)
+
+    def sum(self, axis=None):
+        if axis in (0, -2):
+            return self._w.sum(axis=1)
+        if axis in (1, -1):
+            return self._w.sum(axis=0)
+        return self._w.sum(axis)
+
+
+def build_projector(g: Geometry, kernel: str = "line", precision: str = "float64",
+                    mode: str | None = None, device=None) -> LineProjector:
+    """Matrix-free projector with the reference's line-intersection weights."""
+    if kernel == "joseph":
+        raise NotImplementedError(
+            "kernel='joseph' is outside the B200 hot path (SURVEY.md s8(f) row f4)")
+    if kernel != "line":
+        raise ValueError(f"unknown kernel '{kernel}'")
+    return LineProjector(g, precision=precision, mode=mode, device=device)
+
+
+def apply(w, x):
+    """Forward projection W x (geometry.py:200-206)."""
+    n = x.numel() if D.is_torch(x) else np.asarray(x).shape[0]
+    if n != w.shape[1]:
+        raise DimensionMismatchError(f"apply: vector length {n} != n_cols {w.shape[1]}")
+    return w @ x
+
+
+def apply_transpose(w, y):
+    """Backprojection W^T y (geometry.py:209-215)."""
+    n = y.numel() if D.is_torch(y) else np.asarray(y).shape[0]
+    if n != w.shape[0]:
+        raise DimensionMismatchError(
+            f"apply_transpose: vector length {n} != n_rows {w.shape[0]}")
+    return w.T @ y

@@ -1,0 +1,442 @@
+"""Haar intergrid operators, the WMG hierarchy and the WTG V-cycle on B200.
+
+Drop-in for /root/reference/pkg/src/wmgtomo/multilevel.py:
+  * ``BAND_IDS``, ``haar_scaling_1d``, ``haar_wavelet_1d``, ``IntergridSet``,
+    ``build_intergrid_set`` (:28-79) -- host descriptors (scipy CSR, small),
+    identical to the reference; the device applies them with the
+    ``wmg_haar_restrict`` / ``wmg_haar_prolong`` kernels (same coefficients
+    +-0.4999999999999999 and summation order);
+  * ``WmgNode`` / ``WmgHierarchy`` / ``build_wmg_hierarchy`` (:82-166): the
+    internal-node systems P^T P + lam I with P = W R_path^T are applied
+    MATRIX-FREE (prolong along the path -> projector pair -> restrict); only
+    the coarsest (leaf) Grams are assembled -- directly from the exact ray walk
+    (wmg_leaf_factor) and a float64 GEMM -- and Cholesky-factored in HBM;
+  * ``wtg_apply`` (:175-198, hybrid and multiplicative), ``wmg_preconditioner``
+    (:201-208).
+
+Extension (BASELINE configs 1/2/4: "2 pre- and 2 post-smoothing SIRT sweeps per
+level"; not defined by the reference, SURVEY.md s8 a16 option (ii)): with
+``nu_pre``/``nu_post`` > 0 every internal node applies
+    z <- z + omega_p C_p (v - A_p z),
+    C_p = 1 / (2^-k * sum of W's column sums over each coarse pixel block),
+    omega_p = 0.95 / lambda_max(C_p A_p)   (10 power iterations at setup)
+before and after its wavelet two-grid correction.  nu_pre = nu_post = 0 (the
+default) is exactly the reference's smoother-free cycle.
+``classical_tg_preconditioner`` is out of scope.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from typing import Callable, Optional
+
+import numpy as np
+import scipy.sparse as sp
+
+from . import _device as D
+from . import _native as N
+from .sparse_kernels import (DenseFactorization, DimensionMismatchError,
+                             NotPositiveDefiniteError)
+
+BAND_IDS = ("LL", "LH", "HL", "HH")
+BAND_CODE = {"LL": 0, "LH": 1, "HL": 2, "HH": 3}
+
+
+def _check_even(n: int):
+    if n < 2 or n % 2 != 0:
+        raise ValueError(f"grid side must be even and >= 2, got {n}")
+
+
+def haar_scaling_1d(n: int) -> sp.csr_matrix:
+    """(n/2)-by-n averaging operator: row k = 1/sqrt(2) at columns 2k, 2k+1."""
+    _check_even(n)
+    h = n // 2
+    return sp.csr_matrix((np.full(n, 1.0 / np.sqrt(2.0)), (np.repeat(np.arange(h), 2),
+                                                           np.arange(n))), shape=(h, n))
+
+
+def haar_wavelet_1d(n: int) -> sp.csr_matrix:
+    """(n/2)-by-n differencing operator: row k = (1, -1)/sqrt(2) at 2k, 2k+1."""
+    _check_even(n)
+    h = n // 2
+    vals = np.tile([1.0, -1.0], h) / np.sqrt(2.0)
+    return sp.csr_matrix((vals, (np.repeat(np.arange(h), 2), np.arange(n))), shape=(h, n))
+
+
+@dataclass(frozen=True)
+class IntergridSet:
+    """The four orthonormal restrictions for one coarsening step of an n-grid."""
+
+    n: int
+    restrictions: dict
+
+    def __getitem__(self, band: str) -> sp.csr_matrix:
+        return self.restrictions[band]
+
+
+def build_intergrid_set(n: int) -> IntergridSet:
+    """kron(row factor, col factor); the row factor acts along y (rows)."""
+    _check_even(n)
+    s = haar_scaling_1d(n)
+    j = haar_wavelet_1d(n)
+    return IntergridSet(n=n, restrictions={
+        "LL": sp.kron(s, s, format="csr"),
+        "LH": sp.kron(j, s, format="csr"),
+        "HL": sp.kron(s, j, format="csr"),
+        "HH": sp.kron(j, j, format="csr"),
+    })
+
+
+# ------------------------------------------------------------ device kernels
+def restrict(side: int, fine, bands, out=None):
+    """R_band fine for each band in ``bands`` -> tensor (len(bands), (side/2)^2)."""
+    t = D.torch()
+    mask = 0
+    for b in bands:
+        mask |= 1 << BAND_CODE[b]
+    order = [b for b in BAND_IDS if (mask >> BAND_CODE[b]) & 1]
+    if order != list(bands):
+        raise ValueError("bands must be given in LL, LH, HL, HH order")
+    nc = (side // 2) ** 2
+    if out is None:
+        out = t.empty((len(bands), nc), dtype=t.float64, device=fine.device)
+    N.call("wmg_haar_restrict", side, D.ptr(fine), mask, D.ptr(out), D.stream_handle())
+    return out
+
+
+def prolong(side: int, coarse, band: str, fine, accumulate: bool):
+    """fine = (fine if accumulate else 0) + R_band^T coarse."""
+    N.call("wmg_haar_prolong", side, D.ptr(coarse), BAND_CODE[band], D.ptr(fine),
+           int(bool(accumulate)), D.stream_handle())
+    return fine
+
+
+# ------------------------------------------------------------------ nodes
+@dataclass
+class WmgNode:
+    """One subproblem; its system is v -> P^T (P v) + lam v with P = W R_path^T."""
+
+    side: int
+    level: int
+    path: str
+    factor: Optional[object]           # the shared projector (matrix-free P)
+    lam: float
+    intergrid: Optional[IntergridSet] = None
+    children: dict = field(default_factory=dict)
+    coarse_solve: Optional[DenseFactorization] = None
+    bands: tuple = ()
+    hierarchy: Optional["WmgHierarchy"] = field(default=None, repr=False)
+    smooth_c: Optional[object] = field(default=None, repr=False)
+    smooth_omega: float = 0.0
+
+    @property
+    def dim(self) -> int:
+        return self.side * self.side
+
+    @property
+    def is_coarsest(self) -> bool:
+        return self.coarse_solve is not None
+
+    def apply_system_(self, v, out):
+        """Device: out = P^T (P v) + lam v (matrix-free)."""
+        h = self.hierarchy
+        w = h.projector
+        k = len(self.bands)
+        t = D.torch()
+        # prolong to the fine grid (coarsest factor first, as R_path^T does)
+        cur = v
+        for lv in range(k - 1, -1, -1):
+            side_f = h.n >> lv
+            buf = h.buf(("pf", lv), side_f * side_f)
+            prolong(side_f, cur, self.bands[lv], buf, accumulate=False)
+            cur = buf
+        sino = h.buf(("sino",), w.shape[0])
+        w.forward_(cur, sino)
+        img = h.buf(("img",), w.shape[1]) if k else out
+        w.backward_(sino, img)
+        cur = img
+        for lv in range(k):
+            side_f = h.n >> lv
+            dst = out if lv == k - 1 else h.buf(("rs", lv), (side_f // 2) ** 2)
+            restrict(side_f, cur, (self.bands[lv],), out=dst.view(1, -1))
+            cur = dst
+        if self.lam != 0:
+            D.add_scaled(out, out, self.lam, +1, v)
+        return out
+
+    def apply_system(self, v):
+        t = D.torch()
+        vd, was_np = D.to_device(v)
+        if vd.numel() != self.dim:
+            raise DimensionMismatchError(f"apply_system: length {vd.numel()} != {self.dim}")
+        out = t.empty(self.dim, dtype=t.float64, device=vd.device)
+        self.apply_system_(vd, out)
+        return D.to_caller(out, was_np)
+
+
+@dataclass(frozen=True)
+class WmgHierarchy:
+    levels: int
+    lam: float
+    root: WmgNode
+    projector: object = field(default=None, repr=False, compare=False)
+    n: int = 0
+    nu_pre: int = 0
+    nu_post: int = 0
+    leaf_factors: object = field(default=None, repr=False, compare=False)
+    _bufs: dict = field(default_factory=dict, repr=False, compare=False)
+
+    def buf(self, key, numel):
+        t = D.torch()
+        b = self._bufs.get(key)
+        if b is None or b.numel() < numel:
+            b = t.empty(numel, dtype=t.float64, device=self.projector.device)
+            self._bufs[key] = b
+        return b[:numel]
+
+    def nodes(self):
+        out = []
+
+        def rec(nd):
+            out.append(nd)
+            for b in BAND_IDS:
+                if b in nd.children:
+                    rec(nd.children[b])
+        rec(self.root)
+        return out
+
+
+def _leaf_paths(levels):
+    paths = [()]
+    for _ in range(levels - 1):
+        paths = [p + (b,) for p in paths for b in BAND_IDS]
+    return paths
+
+
+def _assemble_leaf_grams(w, n, lam, levels, ray_chunk=None):
+    """Dense Gram P_L^T P_L + lam I for every leaf, batched in HBM."""
+    t = D.torch()
+    depth = levels - 1
+    side_c = n >> depth
+    p = side_c * side_c
+    M = w.shape[0]
+    paths = _leaf_paths(levels)
+    grams = t.zeros((len(paths), p, p), dtype=t.float64, device=w.device)
+    if ray_chunk is None:
+        # keep the factor slab around 512 MB
+        ray_chunk = max(256, min(M, (512 << 20) // (8 * p)))
+    P = t.empty((min(ray_chunk, M), p), dtype=t.float64, device=w.device)
+    for li, path in enumerate(paths):
+        bands = (N.ctypes.c_int * depth)(*[BAND_CODE[b] for b in path])
+        for r0 in range(0, M, ray_chunk):
+            nr = min(ray_chunk, M - r0)
+            Pc = P[:nr]
+            Pc.zero_()
+            N.call("wmg_leaf_factor", w.handle, depth, bands, r0, nr, D.ptr(Pc),
+                   D.stream_handle())
+            grams[li].addmm_(Pc.T, Pc)
+        if lam != 0:
+            grams[li].diagonal().add_(lam)
+    # symmetrise the GEMM result exactly (P^T P is symmetric in exact arithmetic)
+    grams = 0.5 * (grams + grams.transpose(1, 2))
+    return paths, grams
+
+
+def build_wmg_hierarchy(w, n: int, lam: float, levels: int, nu_pre: int = 0,
+                        nu_post: int = 0) -> WmgHierarchy:
+    """Recursive 4-way splitting of W (multilevel.py:151-166), matrix-free."""
+    if levels < 2:
+        raise ValueError("levels must be >= 2")
+    if lam < 0:
+        raise ValueError("lambda must be nonnegative")
+    if n % (2 ** (levels - 1)) != 0:
+        raise ValueError(f"n={n} is not divisible by 2^(levels-1)={2 ** (levels - 1)}")
+    if nu_pre < 0 or nu_post < 0:
+        raise ValueError("smoothing counts must be nonnegative")
+    if w.shape[1] != n * n:
+        raise DimensionMismatchError(f"projector has {w.shape[1]} columns, expected {n * n}")
+    if not hasattr(w, "handle"):
+        raise TypeError("build_wmg_hierarchy needs a LineProjector (build_projector)")
+    t = D.require_cuda()
+    paths, grams = _assemble_leaf_grams(w, n, lam, levels)
+    lower, info = t.linalg.cholesky_ex(grams)
+    bad = info.cpu().numpy()
+    for li, code in enumerate(bad):
+        if code > 0:
+            name = "/".join(paths[li]) or "root"
+            raise NotPositiveDefiniteError(
+                f"coarsest subproblem '{name}' is singular (lambda={lam}): "
+                f"leading minor of order {int(code)} is not positive definite")
+    leaf_index = {path: i for i, path in enumerate(paths)}
+    p = grams.shape[-1]
+    del grams
+
+    def make(bands, level):
+        side = n >> (level - 1)
+        path = "/".join(bands)
+        if level == levels:
+            li = leaf_index[bands]
+            return WmgNode(side=side, level=level, path=path, factor=None, lam=lam,
+                           coarse_solve=DenseFactorization(dimension=p, lower=lower[li]),
+                           bands=bands)
+        node = WmgNode(side=side, level=level, path=path, factor=w, lam=lam,
+                       intergrid=None, bands=bands)
+        for b in BAND_IDS:
+            node.children[b] = make(bands + (b,), level + 1)
+        return node
+
+    root = make((), 1)
+    h = WmgHierarchy(levels=levels, lam=lam, root=root, projector=w, n=n, nu_pre=nu_pre,
+                     nu_post=nu_post, leaf_factors=lower)
+    for nd in h.nodes():
+        nd.hierarchy = h
+        if not nd.is_coarsest:
+            nd.intergrid = _LazyIntergrid(nd.side)
+    if nu_pre or nu_post:
+        _setup_smoothers(h)
+    return h
+
+
+class _LazyIntergrid:
+    """Host CSR intergrid set built on first access (API compatibility only)."""
+
+    def __init__(self, side):
+        self.n = side
+        self._set = None
+
+    def __getitem__(self, band):
+        if self._set is None:
+            self._set = build_intergrid_set(self.n)
+        return self._set[band]
+
+
+def _setup_smoothers(h: WmgHierarchy, power_iterations: int = 10):
+    """C_p and omega_p for the SIRT-type node smoother (see module docstring)."""
+    t = D.torch()
+    w = h.projector
+    colsum = w.col_sums_dev().view(h.n, h.n)
+    gen = t.Generator(device=w.device)
+    gen.manual_seed(1234)
+    for nd in h.nodes():
+        if nd.is_coarsest:
+            continue
+        k = len(nd.bands)
+        B = 1 << k
+        blk = colsum.view(h.n // B, B, h.n // B, B).sum(dim=(1, 3)).reshape(-1)
+        blk = blk * (0.5 ** k)
+        c = t.where(blk > 0, 1.0 / blk, t.zeros_like(blk))
+        nd.smooth_c = c.contiguous()
+        v = t.rand(nd.dim, dtype=t.float64, device=w.device, generator=gen)
+        out = t.empty_like(v)
+        lam_max = 1.0
+        for _ in range(power_iterations):
+            v = v / v.norm()
+            nd.apply_system_(v, out)
+            out.mul_(c)
+            lam_max = float(v.dot(out))
+            v = out.clone()
+        nd.smooth_omega = 0.95 / lam_max if lam_max > 0 else 0.0
+
+
+# ------------------------------------------------------------------ V-cycle
+def _node_solve_(node: WmgNode, r, multiplicative: bool):
+    """Approximate solve of the node system (device tensors)."""
+    if node.is_coarsest:
+        from .sparse_kernels import cholesky_solve
+        return cholesky_solve(node.coarse_solve, r)
+    h = node.hierarchy
+    if h is None or (h.nu_pre == 0 and h.nu_post == 0):
+        return _wtg_(node, r, multiplicative)
+    t = D.torch()
+    z = t.zeros_like(r)
+    az = t.empty_like(r)
+    res = t.empty_like(r)
+    upd = t.empty_like(r)
+
+    def sweep(z_is_zero):
+        if z_is_zero:
+            res.copy_(r)
+        else:
+            node.apply_system_(z, az)
+            D.axpy(res, r, 1.0, -1, az)
+        D.hadamard(upd, node.smooth_c, res)
+        D.axpy(z, z, node.smooth_omega, +1, upd)
+
+    zero = True
+    for _ in range(h.nu_pre):
+        sweep(zero)
+        zero = False
+    if zero:
+        e = _wtg_(node, r, multiplicative)
+        z.copy_(e)
+    else:
+        node.apply_system_(z, az)
+        D.axpy(res, r, 1.0, -1, az)
+        e = _wtg_(node, res, multiplicative)
+        D.axpy(z, z, 1.0, +1, e)
+    for _ in range(h.nu_post):
+        sweep(False)
+    return z
+
+
+def _wtg_(node: WmgNode, r, multiplicative: bool):
+    """One wavelet two-grid correction, zero initial guess (multilevel.py:175-198)."""
+    t = D.torch()
+    side = node.side
+    r_ll = restrict(side, r, ("LL",))[0]
+    e = t.empty_like(r)
+    prolong(side, _node_solve_(node.children["LL"], r_ll, multiplicative), "LL", e,
+            accumulate=False)
+    ae = t.empty_like(r)
+    r_work = t.empty_like(r)
+    node.apply_system_(e, ae)
+    D.axpy(r_work, r, 1.0, -1, ae)
+    if not multiplicative:
+        rb = restrict(side, r_work, ("LH", "HL", "HH"))
+        for i, band in enumerate(("LH", "HL", "HH")):
+            zb = _node_solve_(node.children[band], rb[i].contiguous(), multiplicative)
+            prolong(side, zb, band, e, accumulate=True)
+        return e
+    for band in ("LH", "HL", "HH"):
+        r_band = restrict(side, r_work, (band,))[0]
+        zb = _node_solve_(node.children[band], r_band, multiplicative)
+        prolong(side, zb, band, e, accumulate=True)
+        if band != "HH":
+            node.apply_system_(e, ae)
+            D.axpy(r_work, r, 1.0, -1, ae)
+    return e
+
+
+def wtg_apply(node: WmgNode, r, multiplicative: bool = False):
+    """One wavelet two-grid correction for the node's system, zero initial guess."""
+    rd, was_np = D.to_device(r)
+    if rd.numel() != node.dim:
+        raise DimensionMismatchError(f"wtg_apply: residual length {rd.numel()} != {node.dim}")
+    if node.is_coarsest:
+        raise ValueError("wtg_apply needs an internal node")
+    return D.to_caller(_wtg_(node, rd, multiplicative), was_np)
+
+
+class WmgPreconditioner:
+    """One V-cycle as an approximate solve of (W^T W + lam I) z = v."""
+
+    _wmg_device = True
+
+    def __init__(self, h: WmgHierarchy, multiplicative: bool = False):
+        self.h = h
+        self.multiplicative = multiplicative
+
+    def apply_(self, v, out):
+        z = _node_solve_(self.h.root, v, self.multiplicative)
+        out.copy_(z)
+        return out
+
+    def __call__(self, v):
+        vd, was_np = D.to_device(v)
+        if vd.numel() != self.h.root.dim:
+            raise DimensionMismatchError(
+                f"wmg_preconditioner: length {vd.numel()} != {self.h.root.dim}")
+        return D.to_caller(_node_solve_(self.h.root, vd, self.multiplicative), was_np)
+
+
+def wmg_preconditioner(h: WmgHierarchy, multiplicative: bool = False) -> Callable:
+    return WmgPreconditioner(h, multiplicative)
