@@ -98,8 +98,8 @@ int wmg_geometry_create(int n, int n_detectors, int n_angles, const double* cos_
       q.du = 1.0 / c;
       q.slope = t;
       q.mirror = t < 0.0;
-      q.L = (float)(1.0 / ac);
-      q.Ls = (float)(as == 0.0 ? inf : 1.0 / as);
+      q.L = 1.0 / ac;
+      q.Ls = as == 0.0 ? inf : 1.0 / as;
     } else {          // x-major: slabs are columns (left -> right), minor = row
       const double ct = c / s;
       q.major = 1;
@@ -107,8 +107,8 @@ int wmg_geometry_create(int n, int n_detectors, int n_angles, const double* cos_
       q.du = -1.0 / s;
       q.slope = ct;
       q.mirror = ct <= 0.0;   // theta = pi/2: ties go to the upper row
-      q.L = (float)(1.0 / as);
-      q.Ls = (float)(ac == 0.0 ? inf : 1.0 / ac);
+      q.L = 1.0 / as;
+      q.Ls = ac == 0.0 ? inf : 1.0 / ac;
     }
     if (q.mirror) {
       q.u0 = (double)n - q.u0;
@@ -116,8 +116,12 @@ int wmg_geometry_create(int n, int n_detectors, int n_angles, const double* cos_
       q.slope = -q.slope;
     }
     q.axis = (c == 0.0 || s == 0.0) ? 1 : 0;
-    q.hw = (float)(0.5 * (ac + as));
-    q.inv_cs = q.axis ? 0.0f : (float)(1.0 / (ac * as));
+    q.hw = 0.5 * (ac + as);
+    q.inv_cs = q.axis ? 0.0 : 1.0 / (ac * as);
+    q.Lf = (float)q.L;
+    q.Lsf = (float)q.Ls;
+    q.hwf = (float)q.hw;
+    q.inv_csf = (float)q.inv_cs;
   }
   wmg_geometry* g = new (std::nothrow) wmg_geometry;
   if (!g) return fail(WMG_EINVAL, "out of host memory");

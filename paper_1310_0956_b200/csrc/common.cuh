@@ -23,11 +23,12 @@ struct AngleParams {
   double u0;          // u at slab 0 for detector offset o = 0 (after mirror)
   double du;          // du / do (per unit detector offset, after mirror)
   double slope;       // du per slab, >= 0
-  float L;            // ray length per full slab = 1 / |major component|
-  float Ls;           // ray length per unit u = 1 / |minor component| (inf if 0)
+  double L;           // ray length per full slab = 1 / |major component|
+  double Ls;          // ray length per unit u = 1 / |minor component| (inf if 0)
   // ---- pixel-driven (backprojection) trapezoid -------------------------
-  float hw;           // (|c| + |s|) / 2 : half support in detector units
-  float inv_cs;       // 1 / (|c| |s|) (unused when axis aligned)
+  double hw;          // (|c| + |s|) / 2 : half support in detector units
+  double inv_cs;      // 1 / (|c| |s|) (unused when axis aligned)
+  float Lf, Lsf, hwf, inv_csf;   // float copies for the fp32 kernels
   int major;          // 0: slabs are rows (y-major), 1: slabs are columns
   int mirror;         // 1 when the minor axis is mirrored
   int axis;           // 1 when s == 0 or c == 0 (exact axis-aligned angle)

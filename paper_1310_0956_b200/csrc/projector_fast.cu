@@ -43,6 +43,21 @@ __device__ __forceinline__ double frac_of<double>(long long U) {
   return (double)m * (1.0 / kFixScale);
 }
 
+// per-angle constants in the kernel's arithmetic type
+template <typename R> struct Pc;
+template <> struct Pc<float> {
+  static __device__ __forceinline__ float L(const AngleParams& P) { return P.Lf; }
+  static __device__ __forceinline__ float Ls(const AngleParams& P) { return P.Lsf; }
+  static __device__ __forceinline__ float hw(const AngleParams& P) { return P.hwf; }
+  static __device__ __forceinline__ float ic(const AngleParams& P) { return P.inv_csf; }
+};
+template <> struct Pc<double> {
+  static __device__ __forceinline__ double L(const AngleParams& P) { return P.L; }
+  static __device__ __forceinline__ double Ls(const AngleParams& P) { return P.Ls; }
+  static __device__ __forceinline__ double hw(const AngleParams& P) { return P.hw; }
+  static __device__ __forceinline__ double ic(const AngleParams& P) { return P.inv_cs; }
+};
+
 template <typename TIn, typename R>
 __device__ __forceinline__ R load_px(const TIn* __restrict__ src, long long rowbase, int k, int n,
                                      int mirror) {
@@ -74,21 +89,37 @@ __global__ void __launch_bounds__(128) fwd_kernel(GeomDev G, const TIn* __restri
   } else if (u0 < -1.0 || u0 > (double)n + 1.0) {
     r1 = -1;
   }
-  const long long S = llrint(slope * kFixScale);
-  long long U = llrint(u0 * kFixScale) + (long long)r0 * S;
-  const R L = (R)P.L, Ls = (R)P.Ls;
+  const R L = Pc<R>::L(P), Ls = Pc<R>::Ls(P);
   R acc = R(0);
-  for (int r = r0; r <= r1; ++r) {
-    const long long Uh = U + S;
-    const int k = (int)(Uh >> kFixFrac);
-    const R f = frac_of<R>(Uh);
-    R wh = f * Ls;
-    wh = (wh < L) ? wh : L;              // NaN (0*inf, ray on a grid line) -> L
-    const R wl = L - wh;
-    const long long rowbase = (long long)r * n;
-    acc += wh * load_px<TIn, R>(src, rowbase, k, n, P.mirror);
-    acc += wl * load_px<TIn, R>(src, rowbase, k - 1, n, P.mirror);
-    U = Uh;
+  if constexpr (sizeof(R) == 4) {
+    // fp32 data path: 64-bit fixed-point minor coordinate (exact increments)
+    const long long S = llrint(slope * kFixScale);
+    long long U = llrint(u0 * kFixScale) + (long long)r0 * S;
+    for (int r = r0; r <= r1; ++r) {
+      const long long Uh = U + S;
+      const int k = (int)(Uh >> kFixFrac);
+      const R f = frac_of<R>(Uh);
+      R wh = f * Ls;
+      wh = (wh < L) ? wh : L;              // NaN (0*inf, ray on a grid line) -> L
+      const R wl = L - wh;
+      const long long rowbase = (long long)r * n;
+      acc += wh * load_px<TIn, R>(src, rowbase, k, n, P.mirror);
+      acc += wl * load_px<TIn, R>(src, rowbase, k - 1, n, P.mirror);
+      U = Uh;
+    }
+  } else {
+    // fp64 arithmetic: evaluate u at every slab end directly (no drift)
+    for (int r = r0; r <= r1; ++r) {
+      const double uh = fma((double)(r + 1), slope, u0);
+      const double fk = floor(uh);
+      const int k = (int)fk;
+      R wh = (uh - fk) * Ls;
+      wh = (wh < L) ? wh : L;
+      const R wl = L - wh;
+      const long long rowbase = (long long)r * n;
+      acc += wh * load_px<TIn, R>(src, rowbase, k, n, P.mirror);
+      acc += wl * load_px<TIn, R>(src, rowbase, k - 1, n, P.mirror);
+    }
   }
   sino[(long long)a * G.d + j] = (TOut)acc;
 }
@@ -118,7 +149,7 @@ __global__ void __launch_bounds__(256) bwd_kernel(GeomDev G, const TIn* __restri
     const int j0 = (int)fl + 1;
     const R d0 = (R)(fl + 1.0 - p);
     const R d1 = d0 + R(1);
-    const R hw = (R)P.hw, ic = (R)P.inv_cs, L = (R)P.L;
+    const R hw = Pc<R>::hw(P), ic = Pc<R>::ic(P), L = Pc<R>::L(P);
     R w0 = (hw - fabs(d0)) * ic;
     R w1 = (hw - fabs(d1)) * ic;
     w0 = w0 < R(0) ? R(0) : (w0 > L ? L : w0);

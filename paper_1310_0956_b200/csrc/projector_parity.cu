@@ -76,31 +76,52 @@ __device__ __forceinline__ double pull(RayWalker& wk) {
   return w;
 }
 
-__device__ double pairwise_pull(RayWalker& wk, long long n) {
+// one leaf block of numpy's pairwise sum (n <= 128)
+__device__ double pairwise_leaf(RayWalker& wk, long long n) {
   if (n < 8) {
     double r = -0.0;
     for (long long i = 0; i < n; ++i) r = dadd(r, pull(wk));
     return r;
   }
-  if (n <= 128) {
-    double acc[8];
+  double acc[8];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) acc[q] = pull(wk);
-    long long i = 8;
-    for (; i < n - (n % 8); i += 8) {
+  for (int q = 0; q < 8; ++q) acc[q] = pull(wk);
+  long long i = 8;
+  for (; i < n - (n % 8); i += 8) {
 #pragma unroll
-      for (int q = 0; q < 8; ++q) acc[q] = dadd(acc[q], pull(wk));
-    }
-    double r = dadd(dadd(dadd(acc[0], acc[1]), dadd(acc[2], acc[3])),
-                    dadd(dadd(acc[4], acc[5]), dadd(acc[6], acc[7])));
-    for (; i < n; ++i) r = dadd(r, pull(wk));
-    return r;
+    for (int q = 0; q < 8; ++q) acc[q] = dadd(acc[q], pull(wk));
   }
-  long long h = n / 2;
-  h -= h % 8;
-  const double lhs = pairwise_pull(wk, h);
-  const double rhs = pairwise_pull(wk, n - h);
-  return dadd(lhs, rhs);
+  double r = dadd(dadd(dadd(acc[0], acc[1]), dadd(acc[2], acc[3])),
+                  dadd(dadd(acc[4], acc[5]), dadd(acc[6], acc[7])));
+  for (; i < n; ++i) r = dadd(r, pull(wk));
+  return r;
+}
+
+// numpy pairwise sum of the next n walker entries, evaluated with an explicit
+// post-order task stack (no device recursion): split n -> (h, n - h) with
+// h = n/2 - (n/2) % 8 until n <= 128, then lhs + rhs.
+__device__ double pairwise_pull(RayWalker& wk, long long n) {
+  long long task[48];      // >= 0: evaluate a node of that size; -1: combine
+  double val[24];
+  int nt = 0, nv = 0;
+  task[nt++] = n;
+  while (nt > 0) {
+    const long long m = task[--nt];
+    if (m < 0) {
+      const double b = val[--nv];
+      const double a = val[--nv];
+      val[nv++] = dadd(a, b);
+    } else if (m <= 128) {
+      val[nv++] = pairwise_leaf(wk, m);
+    } else {
+      long long h = m / 2;
+      h -= h % 8;
+      task[nt++] = -1;        // combine after both halves
+      task[nt++] = m - h;     // right half (evaluated second)
+      task[nt++] = h;         // left half (evaluated first)
+    }
+  }
+  return val[0];
 }
 
 __global__ void rowsum_kernel(GeomDev G, double* __restrict__ out) {

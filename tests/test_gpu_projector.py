@@ -123,9 +123,12 @@ def test_adjoint_identity_fast(gpu):
     x = torch.from_numpy(rs.standard_normal(w.shape[1])).cuda()
     y = torch.from_numpy(rs.standard_normal(w.shape[0])).cuda()
     wf = build_projector(build_geometry(300, 425, 301), precision="float64", mode="fast")
-    lhs = float(wf.forward(x).dot(y))
+    wx = wf.forward(x)
+    lhs = float(wx.dot(y))
     rhs = float(x.dot(wf.backward(y)))
-    assert abs(lhs - rhs) <= 1e-12 * abs(lhs)
+    # forward (slab walk) and backward (pixel trapezoid) are independent
+    # evaluations of the same weights: adjoint to rounding
+    assert abs(lhs - rhs) <= 1e-13 * float(wx.norm() * y.norm())
 
 
 def test_dimension_checks(gpu):
