@@ -76,8 +76,9 @@ int wmg_geometry_create(int n, int n_detectors, int n_angles, const double *cos_
 int wmg_geometry_destroy(wmg_geometry *g);
 int wmg_geometry_shape(const wmg_geometry *g, long long *n_rows, long long *n_cols);
 
-/* bytes of caller workspace wmg_forward needs (transposed image) */
-int wmg_forward_workspace(const wmg_geometry *g, int dtype_in, size_t *bytes);
+/* bytes of caller workspace wmg_forward (mode FAST) needs: zero-padded image
+ * copies in both orientations for fp32 arithmetic, a transposed copy otherwise */
+int wmg_forward_workspace(const wmg_geometry *g, int precision, int dtype_in, size_t *bytes);
 
 /* y = W x (length m*d).  mode PARITY requires dtype_in = dtype_out = F64 and
  * ignores precision/workspace; anomaly (device int*, may be NULL) counts

@@ -91,6 +91,10 @@ def det_reduce(specs, n=None):
         raise ValueError("det_reduce takes 1..8 reductions")
     a0 = specs[0][1]
     n = a0.numel() if n is None else n
+    for sp_ in specs:
+        for v in sp_[1:]:
+            if v is not None and v.numel() != n:
+                raise ValueError("det_reduce operands must have equal lengths")
     dev = a0.device
     sc = scratch(n, K, dev)
     out = t.empty(K, dtype=t.float64, device=dev)

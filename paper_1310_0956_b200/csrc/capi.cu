@@ -19,6 +19,7 @@ cudaError_t parity_csr(const GeomDev&, int, long long*, const long long*, long l
                        int*, cudaStream_t);
 cudaError_t fast_forward(const GeomDev&, int, int, int, const void*, void*, void*, cudaStream_t);
 cudaError_t fast_backward(const GeomDev&, int, int, int, const void*, void*, bool, cudaStream_t);
+size_t fast_forward_workspace_bytes(int, int, int);
 cudaError_t det_reduce(long long, int, const int*, const double* const*, const double* const*,
                        const double* const*, double*, double*, cudaStream_t);
 long long det_scratch_len(long long, int);
@@ -122,6 +123,13 @@ int wmg_geometry_create(int n, int n_detectors, int n_angles, const double* cos_
     q.Lsf = (float)q.Ls;
     q.hwf = (float)q.hw;
     q.inv_csf = (float)q.inv_cs;
+    q.Cfix = llrint(c * 4294967296.0);   // 2^32: v2 backprojector fixed point
+    q.Sfix = llrint(s * 4294967296.0);
+    q.a0 = (float)(2.0 - q.hw);
+    const double icb = q.axis ? 1152921504606846976.0 : q.inv_cs;   // 2^60
+    q.icb = (float)icb;
+    q.hwic = (float)(q.hw * icb);
+    q.w1c = (float)((2.0 * q.hw - 3.0) * icb);
   }
   wmg_geometry* g = new (std::nothrow) wmg_geometry;
   if (!g) return fail(WMG_EINVAL, "out of host memory");
@@ -157,10 +165,9 @@ int wmg_geometry_shape(const wmg_geometry* g, long long* n_rows, long long* n_co
   return WMG_OK;
 }
 
-int wmg_forward_workspace(const wmg_geometry* g, int dtype_in, size_t* bytes) {
+int wmg_forward_workspace(const wmg_geometry* g, int precision, int dtype_in, size_t* bytes) {
   if (!g || !bytes) return fail(WMG_EINVAL, "NULL argument");
-  const size_t es = dtype_in == WMG_F32 ? 4 : 8;
-  *bytes = es * (size_t)g->dev.n * (size_t)g->dev.n;
+  *bytes = wmg::fast_forward_workspace_bytes(g->dev.n, precision, dtype_in);
   return WMG_OK;
 }
 

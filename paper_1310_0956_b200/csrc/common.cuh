@@ -29,6 +29,12 @@ struct AngleParams {
   double hw;          // (|c| + |s|) / 2 : half support in detector units
   double inv_cs;      // 1 / (|c| |s|) (unused when axis aligned)
   float Lf, Lsf, hwf, inv_csf;   // float copies for the fp32 kernels
+  // ---- tiled fp32 backprojector (fixed-point detector coordinate) -------
+  long long Cfix, Sfix;  // c * 2^32, s * 2^32: detector-index step per +1 column / +1 row
+  float a0;              // 2 - hw
+  float icb;             // 1/(|c||s|), or 2^60 for axis-aligned angles (finite: no inf-inf)
+  float hwic;            // hw * icb
+  float w1c;             // (2 hw - 3) * icb
   int major;          // 0: slabs are rows (y-major), 1: slabs are columns
   int mirror;         // 1 when the minor axis is mirrored
   int axis;           // 1 when s == 0 or c == 0 (exact axis-aligned angle)
@@ -46,5 +52,8 @@ struct GeomDev {
 // 40 fractional bits (|u| < 2^22 is ample for n <= 8192).
 constexpr int kFixFrac = 40;
 constexpr double kFixScale = 1099511627776.0;  // 2^40
+// zero margin (pixels) around the padded image copies read by the fast
+// forward kernel: >= 31 * sqrt(2) + 2 so a warp can walk its union slab range
+constexpr int kPadMargin = 64;
 
 }  // namespace wmg

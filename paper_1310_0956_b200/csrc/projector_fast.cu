@@ -179,6 +179,224 @@ __global__ void transpose_kernel(const T* __restrict__ in, T* __restrict__ out, 
   }
 }
 
+
+// ===========================================================================
+// v2 fp32 kernels (the throughput path)
+// ===========================================================================
+
+// v2 fixed point: 64-bit with 32 fractional bits, so the integer part is the
+// high register and the fraction the low register.  Slope quantisation drift
+// over n slabs <= n * 2^-33 px (< 5e-7 px at n = 4096).
+constexpr double kQ32 = 4294967296.0;   // 2^32
+
+// low word -> float in [1, 2): 1 + top 23 fraction bits
+__device__ __forceinline__ float frac1(unsigned lo) {
+  return __int_as_float(0x3F800000u | (lo >> 9));
+}
+__device__ __forceinline__ int hi32(long long v) { return (int)((unsigned long long)v >> 32); }
+
+// Zero-padded copies for the forward slab walk: P[r][M + k] = img[r][k] and
+// PT[c][M + k] = img[k][c], pitch n + 2M, margins zero.
+template <typename T>
+__global__ void pad_transpose_kernel(const T* __restrict__ in, float* __restrict__ P,
+                                     float* __restrict__ PT, int n) {
+  __shared__ float tile[32][33];
+  const int pitch = n + 2 * kPadMargin;
+  const int bx = blockIdx.x * 32, by = blockIdx.y * 32;   // column / row of the input tile
+  for (int i = threadIdx.y; i < 32; i += 8) {
+    const int r = by + i, c = bx + threadIdx.x;
+    float v = 0.0f;
+    if (r < n && c < n) {
+      v = (float)in[(long long)r * n + c];
+      P[(long long)r * pitch + kPadMargin + c] = v;
+    }
+    tile[i][threadIdx.x] = v;
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += 8) {
+    const int c = bx + i, r = by + threadIdx.x;
+    if (r < n && c < n) PT[(long long)c * pitch + kPadMargin + r] = tile[threadIdx.x][i];
+  }
+  // margins (written by the blocks of the first / last tile column)
+  if (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1) {
+    for (int i = threadIdx.y; i < 32; i += 8) {
+      const int r = by + i;
+      if (r >= n) continue;
+      for (int k = threadIdx.x; k < kPadMargin; k += 32) {
+        if (blockIdx.x == 0) {
+          P[(long long)r * pitch + k] = 0.0f;
+          PT[(long long)r * pitch + k] = 0.0f;
+        }
+        if (blockIdx.x == gridDim.x - 1) {
+          P[(long long)r * pitch + kPadMargin + n + k] = 0.0f;
+          PT[(long long)r * pitch + kPadMargin + n + k] = 0.0f;
+        }
+      }
+    }
+  }
+}
+
+// Forward: one thread per ray, 128 consecutive detectors of one angle per
+// block.  Each warp walks the union of its lanes' slab ranges; the zero margin
+// makes out-of-grid reads harmless, so the inner loop has no branches.
+template <typename TOut>
+__global__ void __launch_bounds__(128) fwd_v2_kernel(GeomDev G, const float* __restrict__ P,
+                                                     const float* __restrict__ PT,
+                                                     TOut* __restrict__ sino) {
+  const int a = blockIdx.y;
+  const int j = blockIdx.x * 128 + threadIdx.x;
+  const AngleParams& A = G.ang[a];
+  const int n = G.n;
+  const int pitch = n + 2 * kPadMargin;
+  const double off = (double)j - (double)(G.d - 1) * 0.5;
+  const double u0 = A.u0 + off * A.du;
+  const double slope = A.slope;
+  int r0 = 0, r1 = n - 1;
+  if (j >= G.d) {
+    r0 = n; r1 = -1;
+  } else if (slope > 0.0) {
+    const double ra = floor((-1.0 - u0) / slope) - 1.0;
+    const double rb = ceil(((double)n + 1.0 - u0) / slope) + 1.0;
+    r0 = (int)fmin(fmax(ra, 0.0), (double)n);
+    r1 = (int)fmax(fmin(rb, (double)(n - 1)), -1.0);
+  } else if (u0 < -1.0 || u0 > (double)n + 1.0) {
+    r0 = n; r1 = -1;
+  }
+  const int rw0 = __reduce_min_sync(0xffffffffu, r0);
+  const int rw1 = __reduce_max_sync(0xffffffffu, r1);
+  float acc = 0.0f;
+  if (rw0 <= rw1) {
+    const float* __restrict__ src = (A.major ? PT : P) + kPadMargin;
+    const long long S = llrint(slope * kQ32);
+    long long U = llrint(u0 * kQ32) + (long long)rw0 * S;
+    const float L = A.Lf, Ls = A.Lsf;
+    const int mir = A.mirror;
+    // mirrored minor axis: pixel k lives at column n-1-k; walk a pointer that
+    // moves by -1 per unit of k instead (same instruction count)
+    const long long rowstep = pitch;
+    long long rowoff = (long long)rw0 * rowstep;
+    if (!mir) {
+#pragma unroll 4
+      for (int r = rw0; r <= rw1; ++r) {
+        U += S;
+        const int k = hi32(U);
+        const float f = frac1((unsigned)U);
+        const float wh = fminf(fmaf(f, Ls, -Ls), L);    // NaN (axis: inf-inf) -> L
+        const float* p = src + rowoff + k;
+        const float v1 = __ldg(p), v0 = __ldg(p - 1);
+        acc = fmaf(L, v0, acc);
+        acc = fmaf(wh, v1 - v0, acc);
+        rowoff += rowstep;
+      }
+    } else {
+#pragma unroll 4
+      for (int r = rw0; r <= rw1; ++r) {
+        U += S;
+        const int k = hi32(U);
+        const float f = frac1((unsigned)U);
+        const float wh = fminf(fmaf(f, Ls, -Ls), L);
+        const float* p = src + rowoff + (n - 1 - k);
+        const float v1 = __ldg(p), v0 = __ldg(p + 1);
+        acc = fmaf(L, v0, acc);
+        acc = fmaf(wh, v1 - v0, acc);
+        rowoff += rowstep;
+      }
+    }
+  }
+  if (j < G.d) sino[(long long)a * G.d + j] = (TOut)acc;
+}
+
+// Backward: 32 x 32 pixel tile per block (128 threads; warp w owns rows
+// 8w..8w+7, lane = column).  Angles are processed in chunks of 32: the
+// detector window of every angle is staged in shared memory as pairs
+// (y[j], y[j+1]) and the fixed-point detector coordinate of every lane is
+// tabulated, so the per-(pixel, angle) work is integer adds, one LDS.64 and
+// the branch-free trapezoid weights.
+constexpr int kBwdTile = 32;
+constexpr int kBwdChunk = 32;
+constexpr int kBwdWin = 64;
+
+template <typename TIn, typename TOut, bool kAccumulate>
+__global__ void __launch_bounds__(128) bwd_v2_kernel(GeomDev G, const TIn* __restrict__ sino,
+                                                     TOut* __restrict__ img) {
+  __shared__ float2 win[kBwdChunk][kBwdWin];
+  __shared__ long long qx[kBwdChunk][kBwdTile];
+  __shared__ long long qhead[kBwdChunk];
+  __shared__ int jlo_s[kBwdChunk];
+  const int n = G.n;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int col0 = blockIdx.x * kBwdTile, row0 = blockIdx.y * kBwdTile;
+  const double half = (double)n * 0.5, dc = (double)(G.d - 1) * 0.5;
+  const double xc0 = (double)col0 - half + 0.5;           // pixel-centre x of the tile origin
+  const double yc0 = half - (double)row0 - 0.5;           // pixel-centre y
+  const double bias = 1.0 / kQ32;                         // ties of axis angles go up/right
+  float acc[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) acc[i] = 0.0f;
+
+  for (int a0 = 0; a0 < G.m; a0 += kBwdChunk) {
+    const int na = min(kBwdChunk, G.m - a0);
+    __syncthreads();
+    if (tid < na) {
+      const AngleParams& A = G.ang[a0 + tid];
+      const double p0 = xc0 * A.c + yc0 * A.s + dc - A.hw - bias;
+      const double t = (double)(kBwdTile - 1);
+      const double pmin = p0 + fmin(0.0, t * A.c) + fmin(0.0, -t * A.s);
+      const int jlo = (int)floor(pmin) - 1;
+      jlo_s[tid] = jlo;
+      qhead[tid] = llrint((p0 - (double)jlo) * kQ32);
+    }
+    __syncthreads();
+    // fixed-point coordinate of every lane's column, and the windows
+    for (int e = tid; e < na * kBwdTile; e += 128) {
+      const int aa = e / kBwdTile, l = e % kBwdTile;
+      qx[aa][l] = qhead[aa] + (long long)l * G.ang[a0 + aa].Cfix;
+    }
+    for (int e = tid; e < na * kBwdWin; e += 128) {
+      const int aa = e / kBwdWin, t = e % kBwdWin;
+      const int j = jlo_s[aa] + t;
+      const TIn* yrow = sino + (long long)(a0 + aa) * G.d;
+      const float v0 = (j >= 0 && j < G.d) ? (float)__ldg(yrow + j) : 0.0f;
+      const float v1 = (j + 1 >= 0 && j + 1 < G.d) ? (float)__ldg(yrow + j + 1) : 0.0f;
+      win[aa][t] = make_float2(v0, v1);
+    }
+    __syncthreads();
+    for (int aa = 0; aa < na; ++aa) {
+      const AngleParams& A = G.ang[a0 + aa];
+      const long long S = A.Sfix;
+      const float ca0 = A.a0, icb = A.icb, hwic = A.hwic, w1c = A.w1c, L = A.Lf;
+      long long Q = qx[aa][lane] - (long long)(8 * warp) * S;
+      const float2* wrow = win[aa];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int hi = hi32(Q);
+        const float f = frac1((unsigned)Q);
+        const float d0 = ca0 - f;                        // delta0 = j0 - p
+        const float w0 = fminf(fmaf(-fabsf(d0), icb, hwic), L);
+        const float w1 = fmaxf(fmaf(f, icb, w1c), 0.0f);
+        const float2 v = wrow[hi + 1];
+        acc[i] = fmaf(w0, v.x, acc[i]);
+        acc[i] = fmaf(w1, v.y, acc[i]);
+        Q -= S;
+      }
+    }
+  }
+  const int col = col0 + lane;
+  if (col < n) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int row = row0 + 8 * warp + i;
+      if (row < n) {
+        const long long p = (long long)row * n + col;
+        if (kAccumulate)
+          img[p] = (TOut)((float)img[p] + acc[i]);
+        else
+          img[p] = (TOut)acc[i];
+      }
+    }
+  }
+}
+
 }  // namespace fast
 
 // ---------------------------------------------------------------------------
@@ -189,6 +407,38 @@ static cudaError_t launch_transpose(const TIn* in, TIn* out, int n, cudaStream_t
   dim3 grid((n + 31) / 32, (n + 31) / 32), block(32, 8);
   fast::transpose_kernel<TIn><<<grid, block, 0, st>>>(in, out, n);
   return cudaGetLastError();
+}
+
+template <typename TIn, typename TOut>
+static cudaError_t fwd_v2_impl(const GeomDev& G, const void* x, void* ws, void* y,
+                               cudaStream_t st) {
+  const long long plane = (long long)G.n * (G.n + 2 * kPadMargin);
+  float* P = (float*)ws;
+  float* PT = P + plane;
+  dim3 tg((G.n + 31) / 32, (G.n + 31) / 32), tb(32, 8);
+  fast::pad_transpose_kernel<TIn><<<tg, tb, 0, st>>>((const TIn*)x, P, PT, G.n);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  dim3 grid((G.d + 127) / 128, G.m);
+  fast::fwd_v2_kernel<TOut><<<grid, 128, 0, st>>>(G, P, PT, (TOut*)y);
+  return cudaGetLastError();
+}
+
+template <typename TIn, typename TOut>
+static cudaError_t bwd_v2_impl(const GeomDev& G, const void* y, void* x, bool accumulate,
+                               cudaStream_t st) {
+  dim3 grid((G.n + fast::kBwdTile - 1) / fast::kBwdTile,
+            (G.n + fast::kBwdTile - 1) / fast::kBwdTile);
+  if (accumulate)
+    fast::bwd_v2_kernel<TIn, TOut, true><<<grid, 128, 0, st>>>(G, (const TIn*)y, (TOut*)x);
+  else
+    fast::bwd_v2_kernel<TIn, TOut, false><<<grid, 128, 0, st>>>(G, (const TIn*)y, (TOut*)x);
+  return cudaGetLastError();
+}
+
+size_t fast_forward_workspace_bytes(int n, int precision, int tin) {
+  if (precision == 0) return sizeof(float) * 2 * (size_t)n * (size_t)(n + 2 * kPadMargin);
+  return (tin == 0 ? 4 : 8) * (size_t)n * (size_t)n;
 }
 
 template <typename TIn, typename TOut, typename R>
@@ -219,10 +469,10 @@ cudaError_t fast_forward(const GeomDev& G, int precision, int tin, int tout, con
                          void* xT_ws, void* y, cudaStream_t st) {
   if (G.m == 0 || G.d == 0) return cudaSuccess;
   if (precision == 0) {
-    if (tin == 0 && tout == 0) return fwd_impl<float, float, float>(G, x, xT_ws, y, st);
-    if (tin == 1 && tout == 1) return fwd_impl<double, double, float>(G, x, xT_ws, y, st);
-    if (tin == 1 && tout == 0) return fwd_impl<double, float, float>(G, x, xT_ws, y, st);
-    if (tin == 0 && tout == 1) return fwd_impl<float, double, float>(G, x, xT_ws, y, st);
+    if (tin == 0 && tout == 0) return fwd_v2_impl<float, float>(G, x, xT_ws, y, st);
+    if (tin == 1 && tout == 1) return fwd_v2_impl<double, double>(G, x, xT_ws, y, st);
+    if (tin == 1 && tout == 0) return fwd_v2_impl<double, float>(G, x, xT_ws, y, st);
+    if (tin == 0 && tout == 1) return fwd_v2_impl<float, double>(G, x, xT_ws, y, st);
   } else {
     if (tin == 1 && tout == 1) return fwd_impl<double, double, double>(G, x, xT_ws, y, st);
     if (tin == 0 && tout == 0) return fwd_impl<float, float, double>(G, x, xT_ws, y, st);
@@ -234,10 +484,10 @@ cudaError_t fast_backward(const GeomDev& G, int precision, int tin, int tout, co
                           void* x, bool accumulate, cudaStream_t st) {
   if (G.n == 0) return cudaSuccess;
   if (precision == 0) {
-    if (tin == 0 && tout == 0) return bwd_impl<float, float, float>(G, y, x, accumulate, st);
-    if (tin == 1 && tout == 1) return bwd_impl<double, double, float>(G, y, x, accumulate, st);
-    if (tin == 1 && tout == 0) return bwd_impl<double, float, float>(G, y, x, accumulate, st);
-    if (tin == 0 && tout == 1) return bwd_impl<float, double, float>(G, y, x, accumulate, st);
+    if (tin == 0 && tout == 0) return bwd_v2_impl<float, float>(G, y, x, accumulate, st);
+    if (tin == 1 && tout == 1) return bwd_v2_impl<double, double>(G, y, x, accumulate, st);
+    if (tin == 1 && tout == 0) return bwd_v2_impl<double, float>(G, y, x, accumulate, st);
+    if (tin == 0 && tout == 1) return bwd_v2_impl<float, double>(G, y, x, accumulate, st);
   } else {
     if (tin == 1 && tout == 1) return bwd_impl<double, double, double>(G, y, x, accumulate, st);
     if (tin == 0 && tout == 0) return bwd_impl<float, float, double>(G, y, x, accumulate, st);

@@ -160,8 +160,11 @@ class LineProjector:
         t = D.torch()
         ws = self._ws.get(tin_code)
         if ws is None:
-            dt = t.float32 if tin_code == N.F32 else t.float64
-            ws = t.empty(self.n * self.n, dtype=dt, device=self.device)
+            nbytes = N.ctypes.c_size_t()
+            N.call("wmg_forward_workspace", self._h, self.precision, tin_code,
+                   N.ctypes.byref(nbytes))
+            # zero-initialised once: the padded margins are never written again
+            ws = t.zeros((nbytes.value + 7) // 8, dtype=t.float64, device=self.device)
             self._ws[tin_code] = ws
         return ws
 

@@ -439,7 +439,7 @@ def cgls_solve(w, b, precond=None, x0=None, cfg: SolverConfig = None, x_ex=None)
     for k in range(1, cfg.max_iterations + 1):
         w.forward_(p, q)
         if lam != 0:
-            hd = _readback(D.det_reduce([(N.RED_SQ, q, None, None), (N.RED_SQ, p, None, None)]))
+            hd = _readback(D.det_norm_sq(q), D.det_norm_sq(p))
             delta = float(hd[0]) + lam * float(hd[1])
         else:
             delta = float(_readback(D.det_norm_sq(q))[0])
