@@ -217,13 +217,18 @@ def run_ours(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
 
-    from paper_1310_0956_b200.geometry import Geometry, build_projector
+    from paper_1310_0956_b200.geometry import build_geometry, build_projector
+    from paper_1310_0956_b200.sharding import AngleShardedProjector
 
     n, d, m = workload(args.n)
-    all_angles = np.arange(m) * (np.pi / m)
-    mine = np.arange(rank, m, world)
-    g = Geometry(n, d, mine.size, angles=all_angles[mine])
-    w = build_projector(g, precision="float32", device=dev)
+    g_full = build_geometry(n, d, m)
+    if world > 1:
+        # angle k -> rank k mod world; A^T y partials summed by one NCCL allreduce
+        w = AngleShardedProjector(g_full, precision="float32", device=dev)
+        mine = w.index
+    else:
+        w = build_projector(g_full, precision="float32", device=dev)
+        mine = np.arange(m)
     M_loc, Npix = w.shape
 
     x_h = np.random.default_rng(3000).uniform(0.0, 1.0, n * n).astype(np.float32)
@@ -238,9 +243,7 @@ def run_ours(args):
 
     def step():
         w.forward_(x, sino)
-        w.backward_(y, img)
-        if world > 1:
-            dist.all_reduce(img)
+        w.backward_(y, img)          # includes the allreduce when sharded
 
     for _ in range(max(args.warmup, 0)):
         step()
@@ -260,10 +263,8 @@ def run_ours(args):
             e0.record(stream)
             w.forward_(x, sino)
             e1.record(stream)
-            w.backward_(y, img)
+            w.backward_(y, img)      # local backprojection (+ NCCL allreduce if N > 1)
             e2.record(stream)
-            if world > 1:
-                dist.all_reduce(img)
             e3.record(stream)
         torch.cuda.synchronize(dev)
     if world > 1:
@@ -285,15 +286,16 @@ def run_ours(args):
     out_s = torch.empty(M_loc, dtype=torch.float32).pin_memory()
     out_i = torch.empty(Npix, dtype=torch.float32).pin_memory()
 
+    e2e_s = torch.empty(M_loc, dtype=torch.float32, device=dev)
+    e2e_i = torch.empty(Npix, dtype=torch.float32, device=dev)
+
     def e2e_step():
         xd = pin_x.to(dev, non_blocking=True)
         yd = pin_y.to(dev, non_blocking=True)
-        s_ = w.forward(xd)
-        i_ = w.backward(yd)
-        if world > 1:
-            dist.all_reduce(i_)
-        out_s.copy_(s_, non_blocking=True)
-        out_i.copy_(i_, non_blocking=True)
+        w.forward_(xd, e2e_s)
+        w.backward_(yd, e2e_i)
+        out_s.copy_(e2e_s, non_blocking=True)
+        out_i.copy_(e2e_i, non_blocking=True)
 
     e2e_step()
     torch.cuda.synchronize(dev)

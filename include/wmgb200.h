@@ -75,6 +75,12 @@ int wmg_geometry_create(int n, int n_detectors, int n_angles, const double *cos_
                         const double *sin_h, wmg_geometry **out);
 int wmg_geometry_destroy(wmg_geometry *g);
 int wmg_geometry_shape(const wmg_geometry *g, long long *n_rows, long long *n_cols);
+/* Mirror-symmetry acceleration of the FAST kernels.  Available when the angle set
+ * satisfies theta_{m-a} = pi - theta_a (to 1e-12) with exact axis angles at a = 0
+ * and m/2 and n % 64 == 0 (e.g. build_geometry grids); then one weight evaluation
+ * serves four (pixel, angle) pairs.  set = 0 / 1 disables / enables it (1 is a
+ * no-op when unavailable), set = -1 only queries; *enabled receives the state. */
+int wmg_geometry_symmetry(wmg_geometry *g, int set, int *enabled);
 
 /* bytes of caller workspace wmg_forward (mode FAST) needs: zero-padded image
  * copies in both orientations for fp32 arithmetic, a transposed copy otherwise */

@@ -17,8 +17,10 @@ cudaError_t parity_backward(const GeomDev&, const double*, double*, bool, int*, 
 cudaError_t parity_row_sums(const GeomDev&, double*, cudaStream_t);
 cudaError_t parity_csr(const GeomDev&, int, long long*, const long long*, long long*, double*,
                        int*, cudaStream_t);
-cudaError_t fast_forward(const GeomDev&, int, int, int, const void*, void*, void*, cudaStream_t);
-cudaError_t fast_backward(const GeomDev&, int, int, int, const void*, void*, bool, cudaStream_t);
+cudaError_t fast_forward(const GeomDev&, int, int, int, const void*, void*, void*, cudaStream_t,
+                         const GeomDev*);
+cudaError_t fast_backward(const GeomDev&, int, int, int, const void*, void*, bool, cudaStream_t,
+                          const GeomDev*);
 size_t fast_forward_workspace_bytes(int, int, int);
 cudaError_t det_reduce(long long, int, const int*, const double* const*, const double* const*,
                        const double* const*, double*, double*, cudaStream_t);
@@ -51,6 +53,11 @@ cudaError_t leaf_factor(const GeomDev&, int, const int*, long long, long long, d
 struct wmg_geometry {
   wmg::GeomDev dev;
   wmg::AngleParams* d_ang;
+  // symmetric angle sets: the two axis-aligned angles as their own geometry
+  wmg::GeomDev axis;
+  wmg::AngleParams* d_axis;
+  int* d_rowmap;
+  int sym_capable;
 };
 
 static thread_local char g_err[512] = "";
@@ -131,15 +138,39 @@ int wmg_geometry_create(int n, int n_detectors, int n_angles, const double* cos_
     q.hwic = (float)(q.hw * icb);
     q.w1c = (float)((2.0 * q.hw - 3.0) * icb);
   }
+  // mirror symmetry theta_{m-a} = pi - theta_a with exact axis angles at 0, m/2
+  bool sym = (n_angles % 2 == 0) && n_angles >= 4 && (n % 64 == 0);
+  if (sym) {
+    const int h = n_angles / 2;
+    sym = cos_h[0] == 1.0 && sin_h[0] == 0.0 && cos_h[h] == 0.0 && sin_h[h] == 1.0;
+    for (int a = 1; sym && a < n_angles; ++a) {
+      const int b = n_angles - a;
+      if (std::fabs(cos_h[b] + cos_h[a]) > 1e-12 || std::fabs(sin_h[b] - sin_h[a]) > 1e-12)
+        sym = false;
+      if (a != h && (cos_h[a] == 0.0 || sin_h[a] == 0.0)) sym = false;
+    }
+  }
   wmg_geometry* g = new (std::nothrow) wmg_geometry;
   if (!g) return fail(WMG_EINVAL, "out of host memory");
   g->d_ang = nullptr;
+  g->d_axis = nullptr;
+  g->d_rowmap = nullptr;
   cudaError_t e = cudaMalloc(&g->d_ang, sizeof(wmg::AngleParams) * (size_t)n_angles);
   if (e == cudaSuccess)
     e = cudaMemcpy(g->d_ang, P.data(), sizeof(wmg::AngleParams) * (size_t)n_angles,
                    cudaMemcpyHostToDevice);
+  if (e == cudaSuccess && sym) {
+    wmg::AngleParams ax[2] = {P[0], P[(size_t)(n_angles / 2)]};
+    int rows[2] = {0, n_angles / 2};
+    e = cudaMalloc(&g->d_axis, sizeof(ax));
+    if (e == cudaSuccess) e = cudaMemcpy(g->d_axis, ax, sizeof(ax), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMalloc(&g->d_rowmap, sizeof(rows));
+    if (e == cudaSuccess) e = cudaMemcpy(g->d_rowmap, rows, sizeof(rows), cudaMemcpyHostToDevice);
+  }
   if (e != cudaSuccess) {
     if (g->d_ang) cudaFree(g->d_ang);
+    if (g->d_axis) cudaFree(g->d_axis);
+    if (g->d_rowmap) cudaFree(g->d_rowmap);
     delete g;
     return cuda_rc(e);
   }
@@ -147,6 +178,14 @@ int wmg_geometry_create(int n, int n_detectors, int n_angles, const double* cos_
   g->dev.d = n_detectors;
   g->dev.m = n_angles;
   g->dev.ang = g->d_ang;
+  g->dev.rowmap = nullptr;
+  g->dev.sym = sym ? 1 : 0;
+  g->sym_capable = sym ? 1 : 0;
+  g->axis = g->dev;
+  g->axis.m = 2;
+  g->axis.ang = g->d_axis;
+  g->axis.rowmap = g->d_rowmap;
+  g->axis.sym = 0;
   *out = g;
   return WMG_OK;
 }
@@ -154,8 +193,17 @@ int wmg_geometry_create(int n, int n_detectors, int n_angles, const double* cos_
 int wmg_geometry_destroy(wmg_geometry* g) {
   if (!g) return WMG_OK;
   cudaError_t e = cudaFree(g->d_ang);
+  if (g->d_axis) cudaFree(g->d_axis);
+  if (g->d_rowmap) cudaFree(g->d_rowmap);
   delete g;
   return cuda_rc(e);
+}
+
+int wmg_geometry_symmetry(wmg_geometry* g, int set, int* enabled) {
+  if (!g) return fail(WMG_EINVAL, "geometry is NULL");
+  if (set == 0 || set == 1) g->dev.sym = (set && g->sym_capable) ? 1 : 0;
+  if (enabled) *enabled = g->dev.sym;
+  return WMG_OK;
 }
 
 int wmg_geometry_shape(const wmg_geometry* g, long long* n_rows, long long* n_cols) {
@@ -196,7 +244,7 @@ int wmg_forward(const wmg_geometry* g, int mode, int precision, int dtype_in, in
                                        STREAM(stream)));
   if (!workspace) return fail(WMG_EINVAL, "fast forward needs a workspace");
   return cuda_rc(wmg::fast_forward(g->dev, precision, dtype_in, dtype_out, x, workspace, y,
-                                   STREAM(stream)));
+                                   STREAM(stream), g->dev.sym ? &g->axis : nullptr));
 }
 
 int wmg_backward(const wmg_geometry* g, int mode, int precision, int dtype_in, int dtype_out,
@@ -209,7 +257,8 @@ int wmg_backward(const wmg_geometry* g, int mode, int precision, int dtype_in, i
                                         anomaly, STREAM(stream)));
   if (!y) return fail(WMG_EINVAL, "y is NULL");
   return cuda_rc(wmg::fast_backward(g->dev, precision, dtype_in, dtype_out, y, x,
-                                    accumulate != 0, STREAM(stream)));
+                                    accumulate != 0, STREAM(stream),
+                                    g->dev.sym ? &g->axis : nullptr));
 }
 
 int wmg_row_sums(const wmg_geometry* g, double* out, void* stream) {

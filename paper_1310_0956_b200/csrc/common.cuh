@@ -46,6 +46,9 @@ struct GeomDev {
   int d;              // detectors per angle
   int m;              // angles
   const AngleParams* ang;   // device table, length m
+  const int* rowmap;  // optional: sinogram row of local angle a (nullptr = a)
+  int sym;            // 1: angle set symmetric under theta -> pi - theta (fast kernels
+                      //    may share weights across mirror images), n % 64 == 0
 };
 
 // Fixed-point minor coordinate used by the fast kernels: 64-bit signed with

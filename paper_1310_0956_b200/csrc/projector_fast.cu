@@ -303,7 +303,7 @@ __global__ void __launch_bounds__(128) fwd_v2_kernel(GeomDev G, const float* __r
       }
     }
   }
-  if (j < G.d) sino[(long long)a * G.d + j] = (TOut)acc;
+  if (j < G.d) sino[(long long)(G.rowmap ? G.rowmap[a] : a) * G.d + j] = (TOut)acc;
 }
 
 // Backward: 32 x 32 pixel tile per block (128 threads; warp w owns rows
@@ -355,7 +355,8 @@ __global__ void __launch_bounds__(128) bwd_v2_kernel(GeomDev G, const TIn* __res
     for (int e = tid; e < na * kBwdWin; e += 128) {
       const int aa = e / kBwdWin, t = e % kBwdWin;
       const int j = jlo_s[aa] + t;
-      const TIn* yrow = sino + (long long)(a0 + aa) * G.d;
+      const int srow = G.rowmap ? G.rowmap[a0 + aa] : a0 + aa;
+      const TIn* yrow = sino + (long long)srow * G.d;
       const float v0 = (j >= 0 && j < G.d) ? (float)__ldg(yrow + j) : 0.0f;
       const float v1 = (j + 1 >= 0 && j + 1 < G.d) ? (float)__ldg(yrow + j + 1) : 0.0f;
       win[aa][t] = make_float2(v0, v1);
@@ -397,6 +398,205 @@ __global__ void __launch_bounds__(128) bwd_v2_kernel(GeomDev G, const TIn* __res
   }
 }
 
+
+// Symmetric backprojector.  For an equiangular angle set (theta_{m-a} = pi -
+// theta_a) on a square grid, the trapezoid weights of pixel p at angle a equal
+// those of (i) the x-mirrored pixel at angle m-a (same detectors), (ii) the
+// 180-degree rotated pixel at angle a (detectors reversed) and (iii) the
+// y-mirrored pixel at angle m-a (detectors reversed).  One block owns a 32x32
+// tile of the top-left quadrant and its three images; every weight evaluation
+// feeds four accumulators (two packed FFMA2 per detector).  Axis-aligned
+// angles (0, pi/2) are excluded: the reference's tie rule for rays on grid
+// lines is not mirror symmetric, so they run through bwd_v2 afterwards.
+constexpr int kSymChunk = 16;
+
+template <typename TIn, typename TOut, bool kAccumulate>
+__global__ void __launch_bounds__(256) bwd_sym_kernel(GeomDev G, const TIn* __restrict__ sino,
+                                                      TOut* __restrict__ img) {
+  __shared__ float4 winA[kSymChunk][kBwdWin];   // (y_a[t], y_b[t], y_a[t+1], y_b[t+1])
+  __shared__ float4 winB[kSymChunk][kBwdWin];   // same with detectors reversed
+  __shared__ long long qx[kSymChunk][kBwdTile];
+  __shared__ long long qhead[kSymChunk];
+  __shared__ int jlo_s[kSymChunk];
+  __shared__ int ang_s[kSymChunk];
+  const int n = G.n, m = G.m, d = G.d;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int col0 = blockIdx.x * kBwdTile, row0 = blockIdx.y * kBwdTile;
+  const double half = (double)n * 0.5, dc = (double)(d - 1) * 0.5;
+  const double xc0 = (double)col0 - half + 0.5;
+  const double yc0 = half - (double)row0 - 0.5;
+  const double bias = 1.0 / kQ32;
+  const int half_m = m / 2;
+  float2 accA[4], accB[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    accA[i] = make_float2(0.0f, 0.0f);
+    accB[i] = make_float2(0.0f, 0.0f);
+  }
+  // primary angles: 1 .. m-1 except m/2 (m - 2 of them)
+  const int n_prim = m - 2;
+  for (int c0 = 0; c0 < n_prim; c0 += kSymChunk) {
+    const int na = min(kSymChunk, n_prim - c0);
+    __syncthreads();
+    if (tid < na) {
+      const int q = c0 + tid;                       // 0 .. m-3
+      const int a = q + 1 + (q + 1 >= half_m ? 1 : 0);
+      ang_s[tid] = a;
+      const AngleParams& A = G.ang[a];
+      const double p0 = xc0 * A.c + yc0 * A.s + dc - A.hw - bias;
+      const double t = (double)(kBwdTile - 1);
+      const double pmin = p0 + fmin(0.0, t * A.c) + fmin(0.0, -t * A.s);
+      const int jlo = (int)floor(pmin) - 1;
+      jlo_s[tid] = jlo;
+      qhead[tid] = llrint((p0 - (double)jlo) * kQ32);
+    }
+    __syncthreads();
+    for (int e = tid; e < na * kBwdTile; e += 256) {
+      const int aa = e / kBwdTile, l = e % kBwdTile;
+      qx[aa][l] = qhead[aa] + (long long)l * G.ang[ang_s[aa]].Cfix;
+    }
+    for (int e = tid; e < na * kBwdWin; e += 256) {
+      const int aa = e / kBwdWin, t = e % kBwdWin;
+      const int a = ang_s[aa], b = m - a;
+      const int j = jlo_s[aa] + t;
+      const TIn* ya = sino + (long long)a * d;
+      const TIn* yb = sino + (long long)b * d;
+      auto ld = [&](const TIn* y, int jj) -> float {
+        return (jj >= 0 && jj < d) ? (float)__ldg(y + jj) : 0.0f;
+      };
+      winA[aa][t] = make_float4(ld(ya, j), ld(yb, j), ld(ya, j + 1), ld(yb, j + 1));
+      const int r0 = d - 1 - j, r1 = d - 2 - j;
+      winB[aa][t] = make_float4(ld(ya, r0), ld(yb, r0), ld(ya, r1), ld(yb, r1));
+    }
+    __syncthreads();
+    for (int aa = 0; aa < na; ++aa) {
+      const AngleParams& A = G.ang[ang_s[aa]];
+      const long long S = A.Sfix;
+      const float ca0 = A.a0, icb = A.icb, hwic = A.hwic, w1c = A.w1c, L = A.Lf;
+      long long Q = qx[aa][lane] - (long long)(4 * warp) * S;
+      const float4* wa = winA[aa];
+      const float4* wb = winB[aa];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int hi = hi32(Q);
+        const float f = frac1((unsigned)Q);
+        const float d0 = ca0 - f;
+        const float w0 = fminf(fmaf(-fabsf(d0), icb, hwic), L);
+        const float w1 = fmaxf(fmaf(f, icb, w1c), 0.0f);
+        const float2 W0 = make_float2(w0, w0), W1 = make_float2(w1, w1);
+        const float4 va = wa[hi + 1];
+        const float4 vb = wb[hi + 1];
+        accA[i] = __ffma2_rn(W0, make_float2(va.x, va.y), accA[i]);
+        accA[i] = __ffma2_rn(W1, make_float2(va.z, va.w), accA[i]);
+        accB[i] = __ffma2_rn(W0, make_float2(vb.x, vb.y), accB[i]);
+        accB[i] = __ffma2_rn(W1, make_float2(vb.z, vb.w), accB[i]);
+        Q -= S;
+      }
+    }
+  }
+  const int col = col0 + lane;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int row = row0 + 4 * warp + i;
+    const long long p1 = (long long)row * n + col;                       // (p, a)
+    const long long p2 = (long long)row * n + (n - 1 - col);             // x-mirror, m-a
+    const long long p3 = (long long)(n - 1 - row) * n + (n - 1 - col);   // rotation, a rev
+    const long long p4 = (long long)(n - 1 - row) * n + col;             // y-mirror, m-a rev
+    if (kAccumulate) {
+      img[p1] = (TOut)((float)img[p1] + accA[i].x);
+      img[p2] = (TOut)((float)img[p2] + accA[i].y);
+      img[p3] = (TOut)((float)img[p3] + accB[i].x);
+      img[p4] = (TOut)((float)img[p4] + accB[i].y);
+    } else {
+      img[p1] = (TOut)accA[i].x;
+      img[p2] = (TOut)accA[i].y;
+      img[p3] = (TOut)accB[i].x;
+      img[p4] = (TOut)accB[i].y;
+    }
+  }
+}
+
+
+// Symmetric forward.  Rays (a, j), (m-a, j), (a, d-1-j), (m-a, d-1-j) see the
+// same weights on the slab-coordinate images (s, q), (s, n-1-q), (n-1-s, n-1-q),
+// (n-1-s, q) of one walk (x-mirror / 180-degree rotation of the grid), so one
+// thread walks a representative ray a in [1, m/2), j < ceil(d/2) and
+// accumulates all four.  Representative angles are never mirrored (slope > 0).
+template <typename TOut>
+__global__ void __launch_bounds__(128) fwd_sym_kernel(GeomDev G, const float* __restrict__ P,
+                                                      const float* __restrict__ PT,
+                                                      TOut* __restrict__ sino) {
+  const int a = blockIdx.y + 1;
+  const int d = G.d, m = G.m, n = G.n;
+  const int jh = (d + 1) / 2;
+  const int j = blockIdx.x * 128 + threadIdx.x;
+  const AngleParams& A = G.ang[a];
+  const int pitch = n + 2 * kPadMargin;
+  const double off = (double)j - (double)(d - 1) * 0.5;
+  const double u0 = A.u0 + off * A.du;
+  const double slope = A.slope;
+  int r0 = 0, r1 = n - 1;
+  if (j >= jh) {
+    r0 = n; r1 = -1;
+  } else if (slope > 0.0) {
+    const double ra = floor((-1.0 - u0) / slope) - 1.0;
+    const double rb = ceil(((double)n + 1.0 - u0) / slope) + 1.0;
+    r0 = (int)fmin(fmax(ra, 0.0), (double)n);
+    r1 = (int)fmax(fmin(rb, (double)(n - 1)), -1.0);
+  } else if (u0 < -1.0 || u0 > (double)n + 1.0) {
+    r0 = n; r1 = -1;
+  }
+  const int rw0 = __reduce_min_sync(0xffffffffu, r0);
+  const int rw1 = __reduce_max_sync(0xffffffffu, r1);
+  float2 accA = make_float2(0.0f, 0.0f);   // (s, q), (s, n-1-q)
+  float2 accB = make_float2(0.0f, 0.0f);   // (n-1-s, n-1-q), (n-1-s, q)
+  if (rw0 <= rw1) {
+    const float* __restrict__ src = (A.major ? PT : P) + kPadMargin;
+    const long long S = llrint(slope * kQ32);
+    long long U = llrint(u0 * kQ32) + (long long)rw0 * S;
+    const float L = A.Lf, Ls = A.Lsf;
+    const float2 LL = make_float2(L, L);
+    // 32-bit unsigned element offsets from one base (margin keeps them >= 0)
+    unsigned rowA = (unsigned)(rw0 * pitch + kPadMargin);
+    unsigned rowB = (unsigned)((n - 1 - rw0) * pitch + kPadMargin);
+    const float* __restrict__ base = src - kPadMargin;
+#pragma unroll 2
+    for (int r = rw0; r <= rw1; ++r) {
+      U += S;
+      const int k = hi32(U);
+      const float f = frac1((unsigned)U);
+      const float wh = fminf(fmaf(f, Ls, -Ls), L);
+      const float2 W = make_float2(wh, wh);
+      const int km = n - 1 - k;
+      const float* pa1 = base + (rowA + (unsigned)k);
+      const float* pa2 = base + (rowA + (unsigned)km);
+      const float* pb1 = base + (rowB + (unsigned)km);
+      const float* pb2 = base + (rowB + (unsigned)k);
+      const float2 v1A = make_float2(__ldg(pa1), __ldg(pa2));
+      const float2 v0A = make_float2(__ldg(pa1 - 1), __ldg(pa2 + 1));
+      const float2 v1B = make_float2(__ldg(pb1), __ldg(pb2));
+      const float2 v0B = make_float2(__ldg(pb1 + 1), __ldg(pb2 - 1));
+      accA = __ffma2_rn(LL, v0A, accA);
+      accA = __ffma2_rn(W, __fadd2_rn(v1A, make_float2(-v0A.x, -v0A.y)), accA);
+      accB = __ffma2_rn(LL, v0B, accB);
+      accB = __ffma2_rn(W, __fadd2_rn(v1B, make_float2(-v0B.x, -v0B.y)), accB);
+      rowA += (unsigned)pitch;
+      rowB -= (unsigned)pitch;
+    }
+  }
+  if (j < jh) {
+    // slab-coordinate images -> rays; x-major swaps which image is the x-mirror
+    const float r_m = A.major ? accB.y : accA.y;    // (m-a, j)
+    const float r_mr = A.major ? accA.y : accB.y;   // (m-a, d-1-j)
+    sino[(long long)a * d + j] = (TOut)accA.x;
+    sino[(long long)(m - a) * d + j] = (TOut)r_m;
+    if (d - 1 - j != j) {
+      sino[(long long)a * d + (d - 1 - j)] = (TOut)accB.x;
+      sino[(long long)(m - a) * d + (d - 1 - j)] = (TOut)r_mr;
+    }
+  }
+}
+
 }  // namespace fast
 
 // ---------------------------------------------------------------------------
@@ -411,7 +611,7 @@ static cudaError_t launch_transpose(const TIn* in, TIn* out, int n, cudaStream_t
 
 template <typename TIn, typename TOut>
 static cudaError_t fwd_v2_impl(const GeomDev& G, const void* x, void* ws, void* y,
-                               cudaStream_t st) {
+                               cudaStream_t st, const GeomDev* Gx = nullptr) {
   const long long plane = (long long)G.n * (G.n + 2 * kPadMargin);
   float* P = (float*)ws;
   float* PT = P + plane;
@@ -419,14 +619,43 @@ static cudaError_t fwd_v2_impl(const GeomDev& G, const void* x, void* ws, void* 
   fast::pad_transpose_kernel<TIn><<<tg, tb, 0, st>>>((const TIn*)x, P, PT, G.n);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
+  if (G.sym && Gx) {
+    dim3 sgrid(((G.d + 1) / 2 + 127) / 128, G.m / 2 - 1);
+    fast::fwd_sym_kernel<TOut><<<sgrid, 128, 0, st>>>(G, P, PT, (TOut*)y);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    dim3 xgrid((G.d + 127) / 128, Gx->m);   // the two axis-aligned angles
+    fast::fwd_v2_kernel<TOut><<<xgrid, 128, 0, st>>>(*Gx, P, PT, (TOut*)y);
+    return cudaGetLastError();
+  }
   dim3 grid((G.d + 127) / 128, G.m);
   fast::fwd_v2_kernel<TOut><<<grid, 128, 0, st>>>(G, P, PT, (TOut*)y);
   return cudaGetLastError();
 }
 
+// G_axis: the two axis-aligned angles of a symmetric geometry (rowmap -> their
+// sinogram rows), or nullptr
 template <typename TIn, typename TOut>
 static cudaError_t bwd_v2_impl(const GeomDev& G, const void* y, void* x, bool accumulate,
-                               cudaStream_t st) {
+                               cudaStream_t st, const GeomDev* G_axis = nullptr);
+
+template <typename TIn, typename TOut>
+static cudaError_t bwd_sym_impl(const GeomDev& G, const GeomDev& Gx, const void* y, void* x,
+                                bool accumulate, cudaStream_t st) {
+  dim3 grid(G.n / 64, G.n / 64);
+  if (accumulate)
+    fast::bwd_sym_kernel<TIn, TOut, true><<<grid, 256, 0, st>>>(G, (const TIn*)y, (TOut*)x);
+  else
+    fast::bwd_sym_kernel<TIn, TOut, false><<<grid, 256, 0, st>>>(G, (const TIn*)y, (TOut*)x);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  return bwd_v2_impl<TIn, TOut>(Gx, y, x, true, st);   // axis angles, accumulate
+}
+
+template <typename TIn, typename TOut>
+static cudaError_t bwd_v2_impl(const GeomDev& G, const void* y, void* x, bool accumulate,
+                               cudaStream_t st, const GeomDev* G_axis) {
+  if (G.sym && G_axis) return bwd_sym_impl<TIn, TOut>(G, *G_axis, y, x, accumulate, st);
   dim3 grid((G.n + fast::kBwdTile - 1) / fast::kBwdTile,
             (G.n + fast::kBwdTile - 1) / fast::kBwdTile);
   if (accumulate)
@@ -466,13 +695,13 @@ static cudaError_t bwd_impl(const GeomDev& G, const void* y, void* x, bool accum
 
 // precision: 0 = fp32 arithmetic, 1 = fp64 arithmetic
 cudaError_t fast_forward(const GeomDev& G, int precision, int tin, int tout, const void* x,
-                         void* xT_ws, void* y, cudaStream_t st) {
+                         void* xT_ws, void* y, cudaStream_t st, const GeomDev* Gx) {
   if (G.m == 0 || G.d == 0) return cudaSuccess;
   if (precision == 0) {
-    if (tin == 0 && tout == 0) return fwd_v2_impl<float, float>(G, x, xT_ws, y, st);
-    if (tin == 1 && tout == 1) return fwd_v2_impl<double, double>(G, x, xT_ws, y, st);
-    if (tin == 1 && tout == 0) return fwd_v2_impl<double, float>(G, x, xT_ws, y, st);
-    if (tin == 0 && tout == 1) return fwd_v2_impl<float, double>(G, x, xT_ws, y, st);
+    if (tin == 0 && tout == 0) return fwd_v2_impl<float, float>(G, x, xT_ws, y, st, Gx);
+    if (tin == 1 && tout == 1) return fwd_v2_impl<double, double>(G, x, xT_ws, y, st, Gx);
+    if (tin == 1 && tout == 0) return fwd_v2_impl<double, float>(G, x, xT_ws, y, st, Gx);
+    if (tin == 0 && tout == 1) return fwd_v2_impl<float, double>(G, x, xT_ws, y, st, Gx);
   } else {
     if (tin == 1 && tout == 1) return fwd_impl<double, double, double>(G, x, xT_ws, y, st);
     if (tin == 0 && tout == 0) return fwd_impl<float, float, double>(G, x, xT_ws, y, st);
@@ -481,13 +710,13 @@ cudaError_t fast_forward(const GeomDev& G, int precision, int tin, int tout, con
 }
 
 cudaError_t fast_backward(const GeomDev& G, int precision, int tin, int tout, const void* y,
-                          void* x, bool accumulate, cudaStream_t st) {
+                          void* x, bool accumulate, cudaStream_t st, const GeomDev* Gx) {
   if (G.n == 0) return cudaSuccess;
   if (precision == 0) {
-    if (tin == 0 && tout == 0) return bwd_v2_impl<float, float>(G, y, x, accumulate, st);
-    if (tin == 1 && tout == 1) return bwd_v2_impl<double, double>(G, y, x, accumulate, st);
-    if (tin == 1 && tout == 0) return bwd_v2_impl<double, float>(G, y, x, accumulate, st);
-    if (tin == 0 && tout == 1) return bwd_v2_impl<float, double>(G, y, x, accumulate, st);
+    if (tin == 0 && tout == 0) return bwd_v2_impl<float, float>(G, y, x, accumulate, st, Gx);
+    if (tin == 1 && tout == 1) return bwd_v2_impl<double, double>(G, y, x, accumulate, st, Gx);
+    if (tin == 1 && tout == 0) return bwd_v2_impl<double, float>(G, y, x, accumulate, st, Gx);
+    if (tin == 0 && tout == 1) return bwd_v2_impl<float, double>(G, y, x, accumulate, st, Gx);
   } else {
     if (tin == 1 && tout == 1) return bwd_impl<double, double, double>(G, y, x, accumulate, st);
     if (tin == 0 && tout == 0) return bwd_impl<float, float, double>(G, y, x, accumulate, st);

@@ -153,6 +153,20 @@ class LineProjector:
     def T(self):
         return _Transposed(self)
 
+    @property
+    def symmetric(self) -> bool:
+        """Whether the fast kernels share weights across mirror images."""
+        st = N.ctypes.c_int()
+        N.call("wmg_geometry_symmetry", self._h, -1, N.ctypes.byref(st))
+        return bool(st.value)
+
+    def set_symmetry(self, enable: bool) -> bool:
+        """Enable/disable the mirror-symmetry path (no-op if the angle set is not
+        symmetric); returns the resulting state."""
+        st = N.ctypes.c_int()
+        N.call("wmg_geometry_symmetry", self._h, int(bool(enable)), N.ctypes.byref(st))
+        return bool(st.value)
+
     def tocsr(self):
         return self
 

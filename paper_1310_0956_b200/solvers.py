@@ -153,6 +153,12 @@ class _ErrorTracker:
                 float(host_terms[1] / self.norminf))
 
 
+def _sino(w, t):
+    """Sinogram-space reduction hook: allreduce partials when W is angle-sharded."""
+    red = getattr(w, "reduce_sino_", None)
+    return red(t) if red is not None else t
+
+
 def _readback(*tensors):
     """One D2H copy for several small device tensors -> numpy float64."""
     t = D.torch()
@@ -189,7 +195,7 @@ def sirt_solve(w, b, x0, cfg: SolverConfig, x_ex=None, scaling: Optional[SirtSca
     g = t.empty(Nn, dtype=t.float64, device=bd.device)
     w.forward_(x, wx)
     D.axpy(res, bd, 1.0, -1, wx)                      # res = b - W x
-    h = _readback(D.det_norm_sq(res), errs.device_terms(x))
+    h = _readback(_sino(w, D.det_norm_sq(res)), errs.device_terms(x))
     res_norm0 = float(np.sqrt(h[0]))
     e2, einf = errs.finish(h[1:3]) if errs.active else (None, None)
     record.log(0, 1.0, e2, einf, time.perf_counter() - t0)
@@ -204,7 +210,7 @@ def sirt_solve(w, b, x0, cfg: SolverConfig, x_ex=None, scaling: Optional[SirtSca
                D.stream_handle())
         w.forward_(x, wx)
         D.axpy(res, bd, 1.0, -1, wx)
-        h = _readback(D.det_norm_sq(res), errs.device_terms(x))
+        h = _readback(_sino(w, D.det_norm_sq(res)), errs.device_terms(x))
         rel = float(np.sqrt(h[0])) / res_norm0
         e2, einf = errs.finish(h[1:3]) if errs.active else (None, None)
         record.log(k, rel, e2, einf, time.perf_counter() - t0)
@@ -439,10 +445,10 @@ def cgls_solve(w, b, precond=None, x0=None, cfg: SolverConfig = None, x_ex=None)
     for k in range(1, cfg.max_iterations + 1):
         w.forward_(p, q)
         if lam != 0:
-            hd = _readback(D.det_norm_sq(q), D.det_norm_sq(p))
+            hd = _readback(_sino(w, D.det_norm_sq(q)), D.det_norm_sq(p))
             delta = float(hd[0]) + lam * float(hd[1])
         else:
-            delta = float(_readback(D.det_norm_sq(q))[0])
+            delta = float(_readback(_sino(w, D.det_norm_sq(q)))[0])
         if delta <= 0.0 or not np.isfinite(delta):
             record.status = STATUS_BREAKDOWN
             return D.to_caller(x, was_np), record

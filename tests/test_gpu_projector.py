@@ -139,3 +139,37 @@ def test_dimension_checks(gpu):
         apply(w, np.ones(7))
     with pytest.raises(DimensionMismatchError):
         apply_transpose(w, np.ones(7))
+
+
+@pytest.mark.parametrize("n,d,m", [(256, 363, 180), (512, 725, 512), (320, 453, 64)])
+def test_symmetric_fast_paths(gpu, oracle_proj, n, d, m):
+    """Full equiangular grids take the mirror-symmetric kernels: same result as
+    the plain fast kernels (1e-6) and within 1e-5 of the float64 reference."""
+    torch = gpu
+    from paper_1310_0956_b200.geometry import build_geometry, build_projector
+    g = build_geometry(n, d, m)
+    w = build_projector(g, precision="float32")
+    assert w.symmetric
+    rs = np.random.default_rng(n)
+    x = rs.uniform(0.0, 1.0, n * n)
+    y = rs.uniform(0.0, 1.0, m * d)
+    xd = torch.from_numpy(x.astype(np.float32)).cuda()
+    yd = torch.from_numpy(y.astype(np.float32)).cuda()
+    fs, bs = w.forward(xd).double(), w.backward(yd).double()
+    assert not w.set_symmetry(False)
+    fp, bp = w.forward(xd).double(), w.backward(yd).double()
+    assert w.set_symmetry(True)
+    assert float((fs - fp).norm()) <= 1e-6 * float(fp.norm())
+    assert float((bs - bp).norm()) <= 1e-6 * float(bp.norm())
+    ref_f = oracle_proj.forward(n, d, g.angles, x)
+    ref_b = oracle_proj.backward(n, d, g.angles, y)
+    assert np.linalg.norm(fs.cpu().numpy() - ref_f) <= 1e-5 * np.linalg.norm(ref_f)
+    assert np.linalg.norm(bs.cpu().numpy() - ref_b) <= 1e-5 * np.linalg.norm(ref_b)
+
+
+def test_symmetry_not_used_for_asymmetric_sets(gpu):
+    from paper_1310_0956_b200.geometry import Geometry, build_geometry, build_projector
+    assert not build_projector(build_geometry(100, 145, 64), precision="float32").symmetric
+    assert not build_projector(build_geometry(128, 181, 63), precision="float32").symmetric
+    a = np.sort(np.random.default_rng(0).uniform(0, np.pi, 64))
+    assert not build_projector(Geometry(128, 181, 64, angles=a), precision="float32").symmetric
