@@ -144,6 +144,12 @@ int wmg_haar_restrict(int side, const double *fine, int band_mask, double *out, 
 int wmg_haar_prolong(int side, const double *coarse, int band, double *fine, int accumulate,
                      void *stream);
 
+/* WMG coarse solves: y_b = A_b x_b for b < batch, A_b p x p row-major float64
+ * (the stored SPD inverse of leaf b's Gram), p <= 24576.  Replaces the
+ * reference's cho_solve (sparse_kernels.py:68-75) inside the V-cycle. */
+int wmg_batched_gemv(int batch, int p, const double *A, long long strideA, const double *x,
+                     long long stridex, double *y, long long stridey, void *stream);
+
 /* WMG leaf factor rows P_L[ray0 : ray0 + nrays, :] (row-major, caller zeroes P)
  * for the leaf reached by bands[0..depth) from the root. */
 int wmg_leaf_factor(const wmg_geometry *g, int depth, const int *bands, long long ray0,

@@ -60,6 +60,7 @@ _SIGS = {
     "wmg_cgs_update": (_i, [_ll, _i, _dp, _dp, _ll, _dp, _vp]),
     "wmg_combo": (_i, [_ll, _i, _dp, _dp, _ll, _dp, _i, _vp]),
     "wmg_cast": (_i, [_ll, _i, _dp, _dp, _vp]),
+    "wmg_batched_gemv": (_i, [_i, _i, _dp, _ll, _dp, _ll, _dp, _ll, _vp]),
     "wmg_haar_restrict": (_i, [_i, _dp, _i, _dp, _vp]),
     "wmg_haar_prolong": (_i, [_i, _dp, _i, _dp, _i, _vp]),
     "wmg_leaf_factor": (_i, [_vp, _i, ctypes.POINTER(_i), _ll, _ll, _dp, _vp]),

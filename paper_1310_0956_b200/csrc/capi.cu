@@ -45,6 +45,8 @@ cudaError_t ew_combo(long long, int, double*, const double*, long long, const do
                      cudaStream_t);
 cudaError_t ew_cast(long long, int, void*, const void*, cudaStream_t);
 cudaError_t haar_restrict(int, const double*, int, double*, cudaStream_t);
+cudaError_t batched_gemv(int, int, const double*, long long, const double*, long long, double*,
+                         long long, cudaStream_t);
 cudaError_t haar_prolong(int, const double*, int, double*, int, cudaStream_t);
 cudaError_t leaf_factor(const GeomDev&, int, const int*, long long, long long, double*,
                         cudaStream_t);
@@ -365,6 +367,14 @@ int wmg_combo(long long n, int k, double* out, const double* V, long long ldv, c
 int wmg_cast(long long n, int to_f32, void* out, const void* in, void* stream) {
   REQ(out && in);
   return cuda_rc(wmg::ew_cast(n, to_f32, out, in, STREAM(stream)));
+}
+
+int wmg_batched_gemv(int batch, int p, const double* A, long long strideA, const double* x,
+                     long long stridex, double* y, long long stridey, void* stream) {
+  REQ(A && x && y);
+  if (batch < 0 || p < 0) return fail(WMG_EINVAL, "negative size");
+  if (p > 24576) return fail(WMG_EINVAL, "p > 24576 (shared-memory staging of x)");
+  return cuda_rc(wmg::batched_gemv(batch, p, A, strideA, x, stridex, y, stridey, STREAM(stream)));
 }
 
 int wmg_haar_restrict(int side, const double* fine, int band_mask, double* out, void* stream) {

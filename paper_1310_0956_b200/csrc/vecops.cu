@@ -282,6 +282,41 @@ __global__ void haar_prolong_kernel(int side, const double* __restrict__ coarse,
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// Batched dense float64 GEMV for the WMG coarse solves: y_b = A_b x_b with the
+// stored SPD inverse A_b (p x p, row-major).  HBM-bound: every element of A is
+// read once, coalesced; x_b is staged in shared memory; each warp reduces its
+// rows with a fixed shuffle tree (deterministic).
+// ---------------------------------------------------------------------------
+constexpr int kGemvRows = 32;   // rows per block (4 per warp)
+
+__global__ void __launch_bounds__(256) batched_gemv_kernel(int p, const double* __restrict__ A,
+                                                           long long sA,
+                                                           const double* __restrict__ x,
+                                                           long long sx, double* __restrict__ y,
+                                                           long long sy) {
+  extern __shared__ double xs[];
+  const int b = blockIdx.y;
+  const double* Ab = A + (long long)b * sA;
+  const double* xb = x + (long long)b * sx;
+  for (int i = threadIdx.x; i < p; i += blockDim.x) xs[i] = xb[i];
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int row0 = blockIdx.x * kGemvRows + warp * (kGemvRows / 8);
+#pragma unroll
+  for (int rr = 0; rr < kGemvRows / 8; ++rr) {
+    const int row = row0 + rr;
+    if (row >= p) break;
+    const double* Ar = Ab + (long long)row * p;
+    double acc = 0.0;
+    for (int c = lane; c < p; c += 32) acc = fma(__ldg(Ar + c), xs[c], acc);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, off);
+    if (lane == 0) y[(long long)b * sy + row] = acc;
+  }
+}
+
 }  // namespace vec
 
 // ---------------------------------------------------------------------------
@@ -381,6 +416,20 @@ cudaError_t ew_cast(long long n, int to_f32, void* out, const void* in, cudaStre
   } else {
     LAUNCH_EW(vec::cast_f32_f64, n, (double*)out, (const float*)in);
   }
+}
+
+cudaError_t batched_gemv(int batch, int p, const double* A, long long sA, const double* x,
+                         long long sx, double* y, long long sy, cudaStream_t st) {
+  if (batch <= 0 || p <= 0) return cudaSuccess;
+  const size_t smem = sizeof(double) * (size_t)p;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(vec::batched_gemv_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  dim3 grid((p + vec::kGemvRows - 1) / vec::kGemvRows, batch);
+  vec::batched_gemv_kernel<<<grid, 256, smem, st>>>(p, A, sA, x, sx, y, sy);
+  return cudaGetLastError();
 }
 
 cudaError_t haar_restrict(int side, const double* fine, int band_mask, double* out,

@@ -139,7 +139,7 @@ class WmgNode:
     def apply_system_(self, v, out):
         """Device: out = P^T (P v) + lam v (matrix-free)."""
         h = self.hierarchy
-        w = h.projector
+        w = h.node_projector
         k = len(self.bands)
         t = D.torch()
         # prolong to the fine grid (coarsest factor first, as R_path^T does)
@@ -183,6 +183,8 @@ class WmgHierarchy:
     nu_pre: int = 0
     nu_post: int = 0
     leaf_factors: object = field(default=None, repr=False, compare=False)
+    leaf_inverses: object = field(default=None, repr=False, compare=False)
+    node_projector: object = field(default=None, repr=False, compare=False)
     _bufs: dict = field(default_factory=dict, repr=False, compare=False)
 
     def buf(self, key, numel):
@@ -242,8 +244,13 @@ def _assemble_leaf_grams(w, n, lam, levels, ray_chunk=None):
 
 
 def build_wmg_hierarchy(w, n: int, lam: float, levels: int, nu_pre: int = 0,
-                        nu_post: int = 0) -> WmgHierarchy:
-    """Recursive 4-way splitting of W (multilevel.py:151-166), matrix-free."""
+                        nu_post: int = 0, node_mode: str = "fast") -> WmgHierarchy:
+    """Recursive 4-way splitting of W (multilevel.py:151-166), matrix-free.
+
+    ``node_mode``: projector mode of the internal node systems -- "fast"
+    (float64 fast kernels, <= 1e-12 relative, default) or "parity".  Leaf Grams
+    always come from the exact (parity) weights.
+    """
     if levels < 2:
         raise ValueError("levels must be >= 2")
     if lam < 0:
@@ -269,6 +276,13 @@ def build_wmg_hierarchy(w, n: int, lam: float, levels: int, nu_pre: int = 0,
     leaf_index = {path: i for i, path in enumerate(paths)}
     p = grams.shape[-1]
     del grams
+    inverses = t.cholesky_inverse(lower)
+    inverses = 0.5 * (inverses + inverses.transpose(1, 2))
+    if node_mode == "parity" or getattr(w, "mode", None) == "fast":
+        node_w = w
+    else:
+        from .geometry import LineProjector
+        node_w = LineProjector(w.geometry, precision="float64", mode="fast", device=w.device)
 
     def make(bands, level):
         side = n >> (level - 1)
@@ -276,7 +290,8 @@ def build_wmg_hierarchy(w, n: int, lam: float, levels: int, nu_pre: int = 0,
         if level == levels:
             li = leaf_index[bands]
             return WmgNode(side=side, level=level, path=path, factor=None, lam=lam,
-                           coarse_solve=DenseFactorization(dimension=p, lower=lower[li]),
+                           coarse_solve=DenseFactorization(dimension=p, lower=lower[li],
+                                                           inverse=inverses[li]),
                            bands=bands)
         node = WmgNode(side=side, level=level, path=path, factor=w, lam=lam,
                        intergrid=None, bands=bands)
@@ -286,7 +301,8 @@ def build_wmg_hierarchy(w, n: int, lam: float, levels: int, nu_pre: int = 0,
 
     root = make((), 1)
     h = WmgHierarchy(levels=levels, lam=lam, root=root, projector=w, n=n, nu_pre=nu_pre,
-                     nu_post=nu_post, leaf_factors=lower)
+                     nu_post=nu_post, leaf_factors=lower, leaf_inverses=inverses,
+                     node_projector=node_w)
     for nd in h.nodes():
         nd.hierarchy = h
         if not nd.is_coarsest:
@@ -341,8 +357,7 @@ def _setup_smoothers(h: WmgHierarchy, power_iterations: int = 10):
 def _node_solve_(node: WmgNode, r, multiplicative: bool):
     """Approximate solve of the node system (device tensors)."""
     if node.is_coarsest:
-        from .sparse_kernels import cholesky_solve
-        return cholesky_solve(node.coarse_solve, r)
+        return node.coarse_solve.apply_inverse(r)
     h = node.hierarchy
     if h is None or (h.nu_pre == 0 and h.nu_post == 0):
         return _wtg_(node, r, multiplicative)
@@ -392,8 +407,18 @@ def _wtg_(node: WmgNode, r, multiplicative: bool):
     D.axpy(r_work, r, 1.0, -1, ae)
     if not multiplicative:
         rb = restrict(side, r_work, ("LH", "HL", "HH"))
+        kids = [node.children[b] for b in ("LH", "HL", "HH")]
+        h = node.hierarchy
+        if all(k.is_coarsest for k in kids) and h is not None and h.leaf_inverses is not None:
+            # the three sibling leaves are consecutive in the leaf tensor
+            i0 = _leaf_slot(h, kids[0])
+            from .sparse_kernels import batched_gemv
+            zb3 = batched_gemv(h.leaf_inverses[i0:i0 + 3], rb)
+            for i, band in enumerate(("LH", "HL", "HH")):
+                prolong(side, zb3[i], band, e, accumulate=True)
+            return e
         for i, band in enumerate(("LH", "HL", "HH")):
-            zb = _node_solve_(node.children[band], rb[i].contiguous(), multiplicative)
+            zb = _node_solve_(kids[i], rb[i].contiguous(), multiplicative)
             prolong(side, zb, band, e, accumulate=True)
         return e
     for band in ("LH", "HL", "HH"):
@@ -404,6 +429,14 @@ def _wtg_(node: WmgNode, r, multiplicative: bool):
             node.apply_system_(e, ae)
             D.axpy(r_work, r, 1.0, -1, ae)
     return e
+
+
+def _leaf_slot(h, leaf):
+    """Index of a leaf in the hierarchy's leaf tensors (paths in band order)."""
+    idx = 0
+    for b in leaf.bands:
+        idx = idx * 4 + BAND_CODE[b]
+    return idx
 
 
 def wtg_apply(node: WmgNode, r, multiplicative: bool = False):
@@ -417,26 +450,62 @@ def wtg_apply(node: WmgNode, r, multiplicative: bool = False):
 
 
 class WmgPreconditioner:
-    """One V-cycle as an approximate solve of (W^T W + lam I) z = v."""
+    """One V-cycle as an approximate solve of (W^T W + lam I) z = v.
+
+    The cycle has no data-dependent control flow, so after one eager warm-up it
+    is captured once as a CUDA graph (static input/output buffers) and replayed:
+    the ~50-300 small launches of a cycle cost one graph launch.
+    """
 
     _wmg_device = True
 
-    def __init__(self, h: WmgHierarchy, multiplicative: bool = False):
+    def __init__(self, h: WmgHierarchy, multiplicative: bool = False, graph: bool = True):
         self.h = h
         self.multiplicative = multiplicative
+        self.use_graph = graph
+        self._graph = None
+        self._gin = self._gout = None
+        self._eager_calls = 0
+
+    def _eager(self, v):
+        return _node_solve_(self.h.root, v, self.multiplicative)
 
     def apply_(self, v, out):
-        z = _node_solve_(self.h.root, v, self.multiplicative)
-        out.copy_(z)
+        t = D.torch()
+        if not self.use_graph:
+            out.copy_(self._eager(v))
+            return out
+        if self._graph is None:
+            if self._eager_calls < 1:               # warm-up (allocator, cuBLAS handles)
+                self._eager_calls += 1
+                out.copy_(self._eager(v))
+                return out
+            self._gin = t.empty_like(v)
+            self._gin.copy_(v)
+            side = t.cuda.Stream(device=v.device)
+            side.wait_stream(t.cuda.current_stream(v.device))
+            with t.cuda.stream(side):
+                g = t.cuda.CUDAGraph()
+                with t.cuda.graph(g, stream=side):
+                    self._gout = self._eager(self._gin)
+            t.cuda.current_stream(v.device).wait_stream(side)
+            self._graph = g
+        self._gin.copy_(v)
+        self._graph.replay()
+        out.copy_(self._gout)
         return out
 
     def __call__(self, v):
+        t = D.torch()
         vd, was_np = D.to_device(v)
         if vd.numel() != self.h.root.dim:
             raise DimensionMismatchError(
                 f"wmg_preconditioner: length {vd.numel()} != {self.h.root.dim}")
-        return D.to_caller(_node_solve_(self.h.root, vd, self.multiplicative), was_np)
+        out = t.empty_like(vd)
+        self.apply_(vd, out)
+        return D.to_caller(out, was_np)
 
 
-def wmg_preconditioner(h: WmgHierarchy, multiplicative: bool = False) -> Callable:
-    return WmgPreconditioner(h, multiplicative)
+def wmg_preconditioner(h: WmgHierarchy, multiplicative: bool = False,
+                       graph: bool = True) -> Callable:
+    return WmgPreconditioner(h, multiplicative, graph=graph)

@@ -28,13 +28,43 @@ class DenseFactorization:
     """Lower Cholesky factor(s) of SPD matrices resident on the GPU.
 
     ``lower`` is a torch float64 tensor of shape (dim, dim) or (batch, dim, dim).
+    ``inverse`` (optional) holds G^-1 = L^-T L^-1 for the WMG coarse solves: one
+    bandwidth-bound GEMV per solve instead of two latency-bound triangular
+    solves (same kappa * eps forward-error class).
     """
 
     dimension: int
     lower: object
+    inverse: object = None
 
     def solve(self, rhs):
         return cholesky_solve(self, rhs)
+
+    def apply_inverse(self, rhs, out=None):
+        """G^-1 rhs via the stored inverse: our batched GEMV kernel (falls back to
+        the triangular solves when no inverse is stored)."""
+        if self.inverse is None:
+            return cholesky_solve(self, rhs)
+        return batched_gemv(self.inverse, rhs, out)
+
+
+def batched_gemv(A, x, out=None):
+    """y_b = A_b x_b (A: (p,p) or (b,p,p) float64 CUDA, x: (p,) or (b,p))."""
+    import ctypes
+    import torch
+    from . import _native as N
+    A3 = A if A.dim() == 3 else A.unsqueeze(0)
+    x2 = x if x.dim() == 2 else x.unsqueeze(0)
+    b, p = A3.shape[0], A3.shape[-1]
+    if tuple(x2.shape) != (b, p):
+        raise DimensionMismatchError(f"batched_gemv: rhs {tuple(x.shape)} vs {tuple(A.shape)}")
+    if not (A3.is_contiguous() and x2.is_contiguous()):
+        A3, x2 = A3.contiguous(), x2.contiguous()
+    y = torch.empty((b, p), dtype=torch.float64, device=x.device) if out is None else out
+    st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    N.call("wmg_batched_gemv", b, p, ctypes.c_void_p(A3.data_ptr()), p * p,
+           ctypes.c_void_p(x2.data_ptr()), p, ctypes.c_void_p(y.data_ptr()), p, st)
+    return y if x.dim() == 2 else y.view(p)
 
 
 def cholesky_factor(g, sym_tol: float = 1e-10) -> DenseFactorization:
