@@ -245,6 +245,17 @@ def run_wmg_cgls(dev, reps=3):
     _, rec_c = cgls_solve(wf, bd, cfg=SolverConfig(max_iterations=500, residual_tolerance=1e-4))
     torch.cuda.synchronize(dev)
     t_cgls = time.perf_counter() - t0
+    # the reference's smoother-free cycle (nu = 0), for the like-for-like CPU comparison
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    h0 = build_wmg_hierarchy(w, n, 0.0, 3)
+    M0 = wmg_preconditioner(h0)
+    torch.cuda.synchronize(dev)
+    t1 = time.perf_counter()
+    _, rec0 = cgls_solve(wf, bd, precond=M0, cfg=cfg)
+    torch.cuda.synchronize(dev)
+    t2 = time.perf_counter()
+    nu0 = {"seconds": t2 - t1, "setup_seconds": t1 - t0, "iterations": rec0.iterations[-1]}
     return {"metric": "WMG-CGLS seconds to rel. residual 1e-4", "config": "config1_256_180x363",
             "seconds": min(solves), "setup_seconds": min(setups),
             "seconds_incl_setup": min(s + u for s, u in zip(solves, setups)),
@@ -252,7 +263,32 @@ def run_wmg_cgls(dev, reps=3):
             "levels": 3, "nu_pre": 2, "nu_post": 2, "lambda": 0.0,
             "projector": "float64 fast (<=1e-12 of the reference W); leaf Grams from exact W",
             "cgls_seconds": t_cgls, "cgls_iterations": rec_c.iterations[-1],
+            "nu0": nu0, "b": b, "x_ex": x_ex,
             "timing": "torch.cuda.synchronize + perf_counter, best of %d" % reps}
+
+
+def cpu_wmg_cgls(b):
+    """CPU baseline for config 1: the reference algorithm (exact W, hierarchy of
+    stored sparse factors, smoother-free hybrid V-cycle, dense Cholesky leaves)
+    restated in oracle/multilevel.py, inside the oracle's flexible PCG-NE, on the
+    box's host cores (scipy SpMV single-threaded, LAPACK multi-threaded)."""
+    from oracle import cproj
+    from oracle import multilevel as oml
+    from oracle import solvers as osol
+    n, d, m = 256, 363, 180
+    w = cproj.build_csr(n, d, np.arange(m) * (np.pi / m))
+    t0 = time.perf_counter()
+    root = oml.build_hierarchy(w, n, 0.0, 3)
+    t1 = time.perf_counter()
+    _, rec = osol.cgls_solve(w, b, precond=oml.preconditioner(root), max_iterations=100,
+                             tol=1e-4)
+    t2 = time.perf_counter()
+    _, rec_c = osol.cgls_solve(w, b, max_iterations=500, tol=1e-4)
+    t3 = time.perf_counter()
+    return {"seconds": t2 - t1, "setup_seconds": t1 - t0, "iterations": rec.iterations[-1],
+            "cgls_seconds": t3 - t2, "cgls_iterations": rec_c.iterations[-1],
+            "cores": cproj.num_threads(), "kind": "port",
+            "sample": "full config-1 problem, reference smoother-free V-cycle (nu = 0)"}
 
 
 # ---------------------------------------------------------------- our arm
@@ -401,7 +437,12 @@ def run_ours(args):
     }
     if rank == 0 and world == 1 and not args.no_wmg:
         try:
-            line["wmg_cgls"] = run_wmg_cgls(dev)
+            wmg = run_wmg_cgls(dev)
+            b1 = wmg.pop("b")
+            wmg.pop("x_ex")
+            if not args.no_cpu_baseline:
+                wmg["cpu_baseline"] = cpu_wmg_cgls(b1)
+            line["wmg_cgls"] = wmg
         except Exception as exc:  # pragma: no cover
             line["wmg_cgls"] = {"error": repr(exc)}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

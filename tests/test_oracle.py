@@ -99,3 +99,16 @@ def test_det_sum_definition():
     # the tree on one chunk: lane sums then s[l] + s[l+16] ... order
     v = np.arange(1024, dtype=np.float64)
     assert det_sum(v) == float(v.sum())
+
+
+@pytest.mark.parametrize("levels", [2, 3])
+def test_oracle_wtg_matches_reference(golden, oracle_proj, levels):
+    from oracle import multilevel as oml
+    meta, g = golden
+    n, d, angles = case_geometry(meta["projector"]["w16"])
+    w = oracle_proj.build_csr(n, d, angles)
+    root = oml.build_hierarchy(w, 16, 1.0, levels)
+    r = g[f"wtg_w16_l{levels}_r"]
+    for mult, key in ((False, "hyb"), (True, "mul")):
+        got = oml.wtg_apply(root, r, mult)
+        assert np.abs(got - g[f"wtg_w16_l{levels}_{key}"]).max() <= 1e-12
