@@ -277,7 +277,8 @@ def build_wmg_hierarchy(w, n: int, lam: float, levels: int, nu_pre: int = 0,
     p = grams.shape[-1]
     del grams
     inverses = t.cholesky_inverse(lower)
-    inverses = 0.5 * (inverses + inverses.transpose(1, 2))
+    # symmetrise and force row-major storage (the GEMV streams rows)
+    inverses = (0.5 * (inverses + inverses.transpose(1, 2))).contiguous()
     if node_mode == "parity" or getattr(w, "mode", None) == "fast":
         node_w = w
     else:

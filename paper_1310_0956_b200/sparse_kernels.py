@@ -58,8 +58,9 @@ def batched_gemv(A, x, out=None):
     b, p = A3.shape[0], A3.shape[-1]
     if tuple(x2.shape) != (b, p):
         raise DimensionMismatchError(f"batched_gemv: rhs {tuple(x.shape)} vs {tuple(A.shape)}")
-    if not (A3.is_contiguous() and x2.is_contiguous()):
-        A3, x2 = A3.contiguous(), x2.contiguous()
+    if not A3.is_contiguous():
+        raise ValueError("batched_gemv: matrices must be row-major contiguous")
+    x2 = x2.contiguous()
     y = torch.empty((b, p), dtype=torch.float64, device=x.device) if out is None else out
     st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
     N.call("wmg_batched_gemv", b, p, ctypes.c_void_p(A3.data_ptr()), p * p,
