@@ -70,7 +70,7 @@ __device__ __forceinline__ R load_px(const TIn* __restrict__ src, long long rowb
 template <typename TIn, typename TOut, typename R>
 __global__ void __launch_bounds__(128) fwd_kernel(GeomDev G, const TIn* __restrict__ img,
                                                   const TIn* __restrict__ imgT,
-                                                  TOut* __restrict__ sino) {
+                                                  TOut* __restrict__ sino, int pitch) {
   const int a = blockIdx.y;
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= G.d) return;
@@ -102,7 +102,7 @@ __global__ void __launch_bounds__(128) fwd_kernel(GeomDev G, const TIn* __restri
       R wh = f * Ls;
       wh = (wh < L) ? wh : L;              // NaN (0*inf, ray on a grid line) -> L
       const R wl = L - wh;
-      const long long rowbase = (long long)r * n;
+      const long long rowbase = (long long)r * pitch;
       acc += wh * load_px<TIn, R>(src, rowbase, k, n, P.mirror);
       acc += wl * load_px<TIn, R>(src, rowbase, k - 1, n, P.mirror);
       U = Uh;
@@ -116,12 +116,12 @@ __global__ void __launch_bounds__(128) fwd_kernel(GeomDev G, const TIn* __restri
       R wh = (uh - fk) * Ls;
       wh = (wh < L) ? wh : L;
       const R wl = L - wh;
-      const long long rowbase = (long long)r * n;
+      const long long rowbase = (long long)r * pitch;
       acc += wh * load_px<TIn, R>(src, rowbase, k, n, P.mirror);
       acc += wl * load_px<TIn, R>(src, rowbase, k - 1, n, P.mirror);
     }
   }
-  sino[(long long)a * G.d + j] = (TOut)acc;
+  sino[(long long)(G.rowmap ? G.rowmap[a] : a) * G.d + j] = (TOut)acc;
 }
 
 // One thread per pixel; all threads walk the angles in the same order.
@@ -139,7 +139,7 @@ __global__ void __launch_bounds__(256) bwd_kernel(GeomDev G, const TIn* __restri
   for (int a = 0; a < G.m; ++a) {
     const AngleParams& P = G.ang[a];
     const double p = xc * P.c + yc * P.s + dc;   // detector-index coordinate
-    const TIn* __restrict__ yrow = sino + (long long)a * G.d;
+    const TIn* __restrict__ yrow = sino + (long long)(G.rowmap ? G.rowmap[a] : a) * G.d;
     if (P.axis) {
       const int j = (int)ceil(p - 0.5);
       if (j >= 0 && j < G.d) acc += (R)__ldg(yrow + j);
@@ -408,10 +408,10 @@ __global__ void __launch_bounds__(128) bwd_v2_kernel(GeomDev G, const TIn* __res
 // feeds four accumulators (two packed FFMA2 per detector).  Axis-aligned
 // angles (0, pi/2) are excluded: the reference's tie rule for rays on grid
 // lines is not mirror symmetric, so they run through bwd_v2 afterwards.
-constexpr int kSymChunk = 16;
+constexpr int kSymChunk = 8;
 
 template <typename TIn, typename TOut, bool kAccumulate>
-__global__ void __launch_bounds__(256) bwd_sym_kernel(GeomDev G, const TIn* __restrict__ sino,
+__global__ void __launch_bounds__(256, 6) bwd_sym_kernel(GeomDev G, const TIn* __restrict__ sino,
                                                       TOut* __restrict__ img) {
   __shared__ float4 winA[kSymChunk][kBwdWin];   // (y_a[t], y_b[t], y_a[t+1], y_b[t+1])
   __shared__ float4 winB[kSymChunk][kBwdWin];   // same with detectors reversed
@@ -560,8 +560,40 @@ __global__ void __launch_bounds__(128) fwd_sym_kernel(GeomDev G, const float* __
     unsigned rowA = (unsigned)(rw0 * pitch + kPadMargin);
     unsigned rowB = (unsigned)((n - 1 - rw0) * pitch + kPadMargin);
     const float* __restrict__ base = src - kPadMargin;
-#pragma unroll 2
-    for (int r = rw0; r <= rw1; ++r) {
+    const unsigned up = (unsigned)pitch;
+    int r = rw0;
+    // batches of 4 slabs: all 32 loads are issued before any is consumed
+    for (; r + 3 <= rw1; r += 4) {
+      float2 v1A[4], v0A[4], v1B[4], v0B[4];
+      float wh[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        U += S;
+        const int k = hi32(U);
+        const float f = frac1((unsigned)U);
+        wh[q] = fminf(fmaf(f, Ls, -Ls), L);
+        const int km = n - 1 - k;
+        const float* pa1 = base + (rowA + (unsigned)k);
+        const float* pa2 = base + (rowA + (unsigned)km);
+        const float* pb1 = base + (rowB + (unsigned)km);
+        const float* pb2 = base + (rowB + (unsigned)k);
+        v1A[q] = make_float2(__ldg(pa1), __ldg(pa2));
+        v0A[q] = make_float2(__ldg(pa1 - 1), __ldg(pa2 + 1));
+        v1B[q] = make_float2(__ldg(pb1), __ldg(pb2));
+        v0B[q] = make_float2(__ldg(pb1 + 1), __ldg(pb2 - 1));
+        rowA += up;
+        rowB -= up;
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float2 W = make_float2(wh[q], wh[q]);
+        accA = __ffma2_rn(LL, v0A[q], accA);
+        accA = __ffma2_rn(W, __fadd2_rn(v1A[q], make_float2(-v0A[q].x, -v0A[q].y)), accA);
+        accB = __ffma2_rn(LL, v0B[q], accB);
+        accB = __ffma2_rn(W, __fadd2_rn(v1B[q], make_float2(-v0B[q].x, -v0B[q].y)), accB);
+      }
+    }
+    for (; r <= rw1; ++r) {
       U += S;
       const int k = hi32(U);
       const float f = frac1((unsigned)U);
@@ -580,8 +612,8 @@ __global__ void __launch_bounds__(128) fwd_sym_kernel(GeomDev G, const float* __
       accA = __ffma2_rn(W, __fadd2_rn(v1A, make_float2(-v0A.x, -v0A.y)), accA);
       accB = __ffma2_rn(LL, v0B, accB);
       accB = __ffma2_rn(W, __fadd2_rn(v1B, make_float2(-v0B.x, -v0B.y)), accB);
-      rowA += (unsigned)pitch;
-      rowB -= (unsigned)pitch;
+      rowA += up;
+      rowB -= up;
     }
   }
   if (j < jh) {
@@ -597,11 +629,221 @@ __global__ void __launch_bounds__(128) fwd_sym_kernel(GeomDev G, const float* __
   }
 }
 
+
+// ===========================================================================
+// float64 fast kernels (same algorithms, float64 arithmetic; <= 1e-12)
+// ===========================================================================
+template <typename T>
+__global__ void pad_transpose64_kernel(const T* __restrict__ in, double* __restrict__ P,
+                                       double* __restrict__ PT, int n) {
+  __shared__ double tile[32][33];
+  const int pitch = n + 2 * kPadMargin;
+  const int bx = blockIdx.x * 32, by = blockIdx.y * 32;
+  for (int i = threadIdx.y; i < 32; i += 8) {
+    const int r = by + i, c = bx + threadIdx.x;
+    double v = 0.0;
+    if (r < n && c < n) {
+      v = (double)in[(long long)r * n + c];
+      P[(long long)r * pitch + kPadMargin + c] = v;
+    }
+    tile[i][threadIdx.x] = v;
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += 8) {
+    const int c = bx + i, r = by + threadIdx.x;
+    if (r < n && c < n) PT[(long long)c * pitch + kPadMargin + r] = tile[threadIdx.x][i];
+  }
+}
+
+// symmetric forward in float64: u evaluated directly at every slab end
+template <typename TOut>
+__global__ void __launch_bounds__(128) fwd_sym64_kernel(GeomDev G, const double* __restrict__ P,
+                                                        const double* __restrict__ PT,
+                                                        TOut* __restrict__ sino) {
+  const int a = blockIdx.y + 1;
+  const int d = G.d, m = G.m, n = G.n;
+  const int jh = (d + 1) / 2;
+  const int j = blockIdx.x * 128 + threadIdx.x;
+  const AngleParams& A = G.ang[a];
+  const int pitch = n + 2 * kPadMargin;
+  const double off = (double)j - (double)(d - 1) * 0.5;
+  const double u0 = A.u0 + off * A.du;
+  const double slope = A.slope;
+  int r0 = 0, r1 = n - 1;
+  if (j >= jh) {
+    r0 = n; r1 = -1;
+  } else if (slope > 0.0) {
+    const double ra = floor((-1.0 - u0) / slope) - 1.0;
+    const double rb = ceil(((double)n + 1.0 - u0) / slope) + 1.0;
+    r0 = (int)fmin(fmax(ra, 0.0), (double)n);
+    r1 = (int)fmax(fmin(rb, (double)(n - 1)), -1.0);
+  } else if (u0 < -1.0 || u0 > (double)n + 1.0) {
+    r0 = n; r1 = -1;
+  }
+  const int rw0 = __reduce_min_sync(0xffffffffu, r0);
+  const int rw1 = __reduce_max_sync(0xffffffffu, r1);
+  double a1 = 0.0, a2 = 0.0, a3 = 0.0, a4 = 0.0;
+  if (rw0 <= rw1) {
+    const double* __restrict__ base = (A.major ? PT : P);
+    const double L = A.L, Ls = A.Ls;
+    unsigned rowA = (unsigned)(rw0 * pitch + kPadMargin);
+    unsigned rowB = (unsigned)((n - 1 - rw0) * pitch + kPadMargin);
+    const unsigned up = (unsigned)pitch;
+#pragma unroll 2
+    for (int r = rw0; r <= rw1; ++r) {
+      const double uh = fma((double)(r + 1), slope, u0);
+      const double fk = floor(uh);
+      const int k = (int)fk;
+      const double wh = fmin((uh - fk) * Ls, L);
+      const int km = n - 1 - k;
+      const double* pa1 = base + (rowA + (unsigned)k);
+      const double* pa2 = base + (rowA + (unsigned)km);
+      const double* pb1 = base + (rowB + (unsigned)km);
+      const double* pb2 = base + (rowB + (unsigned)k);
+      const double u1 = __ldg(pa1), v1 = __ldg(pa1 - 1);
+      const double u2 = __ldg(pa2), v2 = __ldg(pa2 + 1);
+      const double u3 = __ldg(pb1), v3 = __ldg(pb1 + 1);
+      const double u4 = __ldg(pb2), v4 = __ldg(pb2 - 1);
+      a1 = fma(wh, u1 - v1, fma(L, v1, a1));
+      a2 = fma(wh, u2 - v2, fma(L, v2, a2));
+      a3 = fma(wh, u3 - v3, fma(L, v3, a3));
+      a4 = fma(wh, u4 - v4, fma(L, v4, a4));
+      rowA += up;
+      rowB -= up;
+    }
+  }
+  if (j < jh) {
+    const double r_m = A.major ? a4 : a2;
+    const double r_mr = A.major ? a2 : a4;
+    sino[(long long)a * d + j] = (TOut)a1;
+    sino[(long long)(m - a) * d + j] = (TOut)r_m;
+    if (d - 1 - j != j) {
+      sino[(long long)a * d + (d - 1 - j)] = (TOut)a3;
+      sino[(long long)(m - a) * d + (d - 1 - j)] = (TOut)r_mr;
+    }
+  }
+}
+
+// symmetric backprojector in float64: 52-fractional-bit fixed point
+constexpr double kQ52 = 4503599627370496.0;   // 2^52
+constexpr int kSym64Chunk = 8;
+
+template <typename TIn, typename TOut, bool kAccumulate>
+__global__ void __launch_bounds__(256) bwd_sym64_kernel(GeomDev G, const TIn* __restrict__ sino,
+                                                        TOut* __restrict__ img) {
+  __shared__ double4 winA[kSym64Chunk][kBwdWin];
+  __shared__ double4 winB[kSym64Chunk][kBwdWin];
+  __shared__ long long qx[kSym64Chunk][kBwdTile];
+  __shared__ long long qhead[kSym64Chunk];
+  __shared__ int jlo_s[kSym64Chunk];
+  __shared__ int ang_s[kSym64Chunk];
+  const int n = G.n, m = G.m, d = G.d;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int col0 = blockIdx.x * kBwdTile, row0 = blockIdx.y * kBwdTile;
+  const double half = (double)n * 0.5, dc = (double)(d - 1) * 0.5;
+  const double xc0 = (double)col0 - half + 0.5;
+  const double yc0 = half - (double)row0 - 0.5;
+  const int half_m = m / 2;
+  double acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc[i][q] = 0.0;
+  const int n_prim = m - 2;
+  for (int c0 = 0; c0 < n_prim; c0 += kSym64Chunk) {
+    const int na = min(kSym64Chunk, n_prim - c0);
+    __syncthreads();
+    if (tid < na) {
+      const int q = c0 + tid;
+      const int a = q + 1 + (q + 1 >= half_m ? 1 : 0);
+      ang_s[tid] = a;
+      const AngleParams& A = G.ang[a];
+      const double p0 = xc0 * A.c + yc0 * A.s + dc - A.hw;
+      const double t = (double)(kBwdTile - 1);
+      const double pmin = p0 + fmin(0.0, t * A.c) + fmin(0.0, -t * A.s);
+      const int jlo = (int)floor(pmin) - 1;
+      jlo_s[tid] = jlo;
+      qhead[tid] = llrint((p0 - (double)jlo) * kQ52);
+    }
+    __syncthreads();
+    for (int e = tid; e < na * kBwdTile; e += 256) {
+      const int aa = e / kBwdTile, l = e % kBwdTile;
+      qx[aa][l] = qhead[aa] + (long long)l * llrint(G.ang[ang_s[aa]].c * kQ52);
+    }
+    for (int e = tid; e < na * kBwdWin; e += 256) {
+      const int aa = e / kBwdWin, t = e % kBwdWin;
+      const int a = ang_s[aa], b = m - a;
+      const int jj = jlo_s[aa] + t;
+      const TIn* ya = sino + (long long)a * d;
+      const TIn* yb = sino + (long long)b * d;
+      auto ld = [&](const TIn* y, int q) -> double {
+        return (q >= 0 && q < d) ? (double)__ldg(y + q) : 0.0;
+      };
+      winA[aa][t] = make_double4(ld(ya, jj), ld(yb, jj), ld(ya, jj + 1), ld(yb, jj + 1));
+      const int q0 = d - 1 - jj, q1 = d - 2 - jj;
+      winB[aa][t] = make_double4(ld(ya, q0), ld(yb, q0), ld(ya, q1), ld(yb, q1));
+    }
+    __syncthreads();
+    for (int aa = 0; aa < na; ++aa) {
+      const AngleParams& A = G.ang[ang_s[aa]];
+      const long long S = llrint(A.s * kQ52);
+      const double hw = A.hw, ic = A.inv_cs, L = A.L;
+      const double ca0 = 2.0 - hw, hwic = hw * ic, w1c = (2.0 * hw - 3.0) * ic;
+      long long Q = qx[aa][lane] - (long long)(4 * warp) * S;
+      const double4* wa = winA[aa];
+      const double4* wb = winB[aa];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int hi = (int)(Q >> 52);
+        const double f = __longlong_as_double(0x3FF0000000000000LL | (Q & 0xFFFFFFFFFFFFFLL));
+        const double d0 = ca0 - f;
+        const double w0 = fmin(fma(-fabs(d0), ic, hwic), L);
+        const double w1 = fmax(fma(f, ic, w1c), 0.0);
+        const double4 va = wa[hi + 1];
+        const double4 vb = wb[hi + 1];
+        acc[i][0] = fma(w0, va.x, fma(w1, va.z, acc[i][0]));
+        acc[i][1] = fma(w0, va.y, fma(w1, va.w, acc[i][1]));
+        acc[i][2] = fma(w0, vb.x, fma(w1, vb.z, acc[i][2]));
+        acc[i][3] = fma(w0, vb.y, fma(w1, vb.w, acc[i][3]));
+        Q -= S;
+      }
+    }
+  }
+  const int col = col0 + lane;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int row = row0 + 4 * warp + i;
+    const long long p[4] = {(long long)row * n + col, (long long)row * n + (n - 1 - col),
+                            (long long)(n - 1 - row) * n + (n - 1 - col),
+                            (long long)(n - 1 - row) * n + col};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (kAccumulate)
+        img[p[q]] = (TOut)((double)img[p[q]] + acc[i][q]);
+      else
+        img[p[q]] = (TOut)acc[i][q];
+    }
+  }
+}
+
 }  // namespace fast
 
 // ---------------------------------------------------------------------------
 // host launchers.  dtype codes: 0 = float32, 1 = float64.
 // ---------------------------------------------------------------------------
+// Path selection.  The symmetric kernels do a quarter of the weight work but
+// expose 4x less parallelism (blocks own four tile/ray images), so they only
+// pay off once the grid still fills the 148 SMs several times over.
+// G.sym: 0 off, 1 on when profitable, 2 forced (tests)
+static inline bool use_sym_bwd(const GeomDev& G) {
+  return G.sym == 2 || (G.sym == 1 && G.n >= 1024);
+}
+static inline bool use_sym_fwd(const GeomDev& G) {
+  const long long blocks = (long long)(((G.d + 1) / 2 + 127) / 128) * (G.m / 2 - 1);
+  return G.sym == 2 || (G.sym == 1 && blocks >= 4LL * 148);
+}
+static inline bool use_tiled_bwd(const GeomDev& G) { return G.n >= 768; }
+
 template <typename TIn>
 static cudaError_t launch_transpose(const TIn* in, TIn* out, int n, cudaStream_t st) {
   dim3 grid((n + 31) / 32, (n + 31) / 32), block(32, 8);
@@ -619,7 +861,7 @@ static cudaError_t fwd_v2_impl(const GeomDev& G, const void* x, void* ws, void* 
   fast::pad_transpose_kernel<TIn><<<tg, tb, 0, st>>>((const TIn*)x, P, PT, G.n);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  if (G.sym && Gx) {
+  if (use_sym_fwd(G) && Gx) {
     dim3 sgrid(((G.d + 1) / 2 + 127) / 128, G.m / 2 - 1);
     fast::fwd_sym_kernel<TOut><<<sgrid, 128, 0, st>>>(G, P, PT, (TOut*)y);
     e = cudaGetLastError();
@@ -632,6 +874,7 @@ static cudaError_t fwd_v2_impl(const GeomDev& G, const void* x, void* ws, void* 
   fast::fwd_v2_kernel<TOut><<<grid, 128, 0, st>>>(G, P, PT, (TOut*)y);
   return cudaGetLastError();
 }
+
 
 // G_axis: the two axis-aligned angles of a symmetric geometry (rowmap -> their
 // sinogram rows), or nullptr
@@ -655,7 +898,16 @@ static cudaError_t bwd_sym_impl(const GeomDev& G, const GeomDev& Gx, const void*
 template <typename TIn, typename TOut>
 static cudaError_t bwd_v2_impl(const GeomDev& G, const void* y, void* x, bool accumulate,
                                cudaStream_t st, const GeomDev* G_axis) {
-  if (G.sym && G_axis) return bwd_sym_impl<TIn, TOut>(G, *G_axis, y, x, accumulate, st);
+  if (use_sym_bwd(G) && G_axis)
+    return bwd_sym_impl<TIn, TOut>(G, *G_axis, y, x, accumulate, st);
+  if (!use_tiled_bwd(G)) {   // small grids: one thread per pixel
+    dim3 g1((G.n + 31) / 32, (G.n + 7) / 8);
+    if (accumulate)
+      fast::bwd_kernel<TIn, TOut, float, true><<<g1, 256, 0, st>>>(G, (const TIn*)y, (TOut*)x);
+    else
+      fast::bwd_kernel<TIn, TOut, float, false><<<g1, 256, 0, st>>>(G, (const TIn*)y, (TOut*)x);
+    return cudaGetLastError();
+  }
   dim3 grid((G.n + fast::kBwdTile - 1) / fast::kBwdTile,
             (G.n + fast::kBwdTile - 1) / fast::kBwdTile);
   if (accumulate)
@@ -667,7 +919,47 @@ static cudaError_t bwd_v2_impl(const GeomDev& G, const void* y, void* x, bool ac
 
 size_t fast_forward_workspace_bytes(int n, int precision, int tin) {
   if (precision == 0) return sizeof(float) * 2 * (size_t)n * (size_t)(n + 2 * kPadMargin);
-  return (tin == 0 ? 4 : 8) * (size_t)n * (size_t)n;
+  // float64: padded double planes (symmetric path) -- also holds the transposed
+  // copy of the generic path
+  return sizeof(double) * 2 * (size_t)n * (size_t)(n + 2 * kPadMargin);
+}
+
+template <typename TIn, typename TOut>
+static cudaError_t fwd64_impl(const GeomDev& G, const void* x, void* ws, void* y,
+                              cudaStream_t st, const GeomDev* Gx) {
+  if (!(G.sym && Gx)) return cudaErrorNotSupported;
+  const long long plane = (long long)G.n * (G.n + 2 * kPadMargin);
+  double* P = (double*)ws;
+  double* PT = P + plane;
+  dim3 tg((G.n + 31) / 32, (G.n + 31) / 32), tb(32, 8);
+  fast::pad_transpose64_kernel<TIn><<<tg, tb, 0, st>>>((const TIn*)x, P, PT, G.n);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  dim3 sgrid(((G.d + 1) / 2 + 127) / 128, G.m / 2 - 1);
+  fast::fwd_sym64_kernel<TOut><<<sgrid, 128, 0, st>>>(G, P, PT, (TOut*)y);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  // the two axis-aligned angles: generic walk on the padded planes
+  dim3 xgrid((G.d + 127) / 128, Gx->m);
+  fast::fwd_kernel<double, TOut, double><<<xgrid, 128, 0, st>>>(
+      *Gx, P + kPadMargin, PT + kPadMargin, (TOut*)y, G.n + 2 * kPadMargin);
+  return cudaGetLastError();
+}
+
+template <typename TIn, typename TOut>
+static cudaError_t bwd64_impl(const GeomDev& G, const void* y, void* x, bool accumulate,
+                              cudaStream_t st, const GeomDev* Gx) {
+  if (!(G.sym && Gx)) return cudaErrorNotSupported;
+  dim3 grid(G.n / 64, G.n / 64);
+  if (accumulate)
+    fast::bwd_sym64_kernel<TIn, TOut, true><<<grid, 256, 0, st>>>(G, (const TIn*)y, (TOut*)x);
+  else
+    fast::bwd_sym64_kernel<TIn, TOut, false><<<grid, 256, 0, st>>>(G, (const TIn*)y, (TOut*)x);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  dim3 g2((G.n + 31) / 32, (G.n + 7) / 8);
+  fast::bwd_kernel<TIn, TOut, double, true><<<g2, 256, 0, st>>>(*Gx, (const TIn*)y, (TOut*)x);
+  return cudaGetLastError();
 }
 
 template <typename TIn, typename TOut, typename R>
@@ -678,7 +970,7 @@ static cudaError_t fwd_impl(const GeomDev& G, const void* x, void* xT_ws, void* 
   cudaError_t e = launch_transpose<TIn>(img, imgT, G.n, st);
   if (e != cudaSuccess) return e;
   dim3 grid((G.d + 127) / 128, G.m);
-  fast::fwd_kernel<TIn, TOut, R><<<grid, 128, 0, st>>>(G, img, imgT, (TOut*)y);
+  fast::fwd_kernel<TIn, TOut, R><<<grid, 128, 0, st>>>(G, img, imgT, (TOut*)y, G.n);
   return cudaGetLastError();
 }
 
@@ -703,6 +995,8 @@ cudaError_t fast_forward(const GeomDev& G, int precision, int tin, int tout, con
     if (tin == 1 && tout == 0) return fwd_v2_impl<double, float>(G, x, xT_ws, y, st, Gx);
     if (tin == 0 && tout == 1) return fwd_v2_impl<float, double>(G, x, xT_ws, y, st, Gx);
   } else {
+    if (use_sym_fwd(G) && Gx && tin == 1 && tout == 1)
+      return fwd64_impl<double, double>(G, x, xT_ws, y, st, Gx);
     if (tin == 1 && tout == 1) return fwd_impl<double, double, double>(G, x, xT_ws, y, st);
     if (tin == 0 && tout == 0) return fwd_impl<float, float, double>(G, x, xT_ws, y, st);
   }
@@ -718,6 +1012,8 @@ cudaError_t fast_backward(const GeomDev& G, int precision, int tin, int tout, co
     if (tin == 1 && tout == 0) return bwd_v2_impl<double, float>(G, y, x, accumulate, st, Gx);
     if (tin == 0 && tout == 1) return bwd_v2_impl<float, double>(G, y, x, accumulate, st, Gx);
   } else {
+    if (use_sym_bwd(G) && Gx && tin == 1 && tout == 1)
+      return bwd64_impl<double, double>(G, y, x, accumulate, st, Gx);
     if (tin == 1 && tout == 1) return bwd_impl<double, double, double>(G, y, x, accumulate, st);
     if (tin == 0 && tout == 0) return bwd_impl<float, float, double>(G, y, x, accumulate, st);
   }

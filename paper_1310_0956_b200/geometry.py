@@ -160,11 +160,13 @@ class LineProjector:
         N.call("wmg_geometry_symmetry", self._h, -1, N.ctypes.byref(st))
         return bool(st.value)
 
-    def set_symmetry(self, enable: bool) -> bool:
-        """Enable/disable the mirror-symmetry path (no-op if the angle set is not
-        symmetric); returns the resulting state."""
+    def set_symmetry(self, enable) -> bool:
+        """Enable (True: where profitable), force ("force": at every size) or
+        disable (False) the mirror-symmetry kernels; no-op if the angle set is not
+        symmetric.  Returns whether it is enabled."""
+        code = 2 if enable == "force" else int(bool(enable))
         st = N.ctypes.c_int()
-        N.call("wmg_geometry_symmetry", self._h, int(bool(enable)), N.ctypes.byref(st))
+        N.call("wmg_geometry_symmetry", self._h, code, N.ctypes.byref(st))
         return bool(st.value)
 
     def tocsr(self):

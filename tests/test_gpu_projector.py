@@ -150,6 +150,7 @@ def test_symmetric_fast_paths(gpu, oracle_proj, n, d, m):
     g = build_geometry(n, d, m)
     w = build_projector(g, precision="float32")
     assert w.symmetric
+    assert w.set_symmetry("force")
     rs = np.random.default_rng(n)
     x = rs.uniform(0.0, 1.0, n * n)
     y = rs.uniform(0.0, 1.0, m * d)
@@ -158,7 +159,7 @@ def test_symmetric_fast_paths(gpu, oracle_proj, n, d, m):
     fs, bs = w.forward(xd).double(), w.backward(yd).double()
     assert not w.set_symmetry(False)
     fp, bp = w.forward(xd).double(), w.backward(yd).double()
-    assert w.set_symmetry(True)
+    assert w.set_symmetry("force")
     assert float((fs - fp).norm()) <= 1e-6 * float(fp.norm())
     assert float((bs - bp).norm()) <= 1e-6 * float(bp.norm())
     ref_f = oracle_proj.forward(n, d, g.angles, x)
@@ -173,3 +174,39 @@ def test_symmetry_not_used_for_asymmetric_sets(gpu):
     assert not build_projector(build_geometry(128, 181, 63), precision="float32").symmetric
     a = np.sort(np.random.default_rng(0).uniform(0, np.pi, 64))
     assert not build_projector(Geometry(128, 181, 64, angles=a), precision="float32").symmetric
+
+
+@pytest.mark.parametrize("n,d,m", [(256, 363, 180), (512, 725, 512)])
+def test_symmetric_fast_fp64(gpu, n, d, m):
+    """float64 symmetric kernels (forced) against the bit-exact parity kernels."""
+    torch = gpu
+    from paper_1310_0956_b200.geometry import build_geometry, build_projector
+    g = build_geometry(n, d, m)
+    wp = build_projector(g)
+    wf = build_projector(g, precision="float64", mode="fast")
+    assert wf.set_symmetry("force")
+    rs = np.random.default_rng(n + 1)
+    x = torch.from_numpy(rs.uniform(0.0, 1.0, n * n)).cuda()
+    y = torch.from_numpy(rs.uniform(0.0, 1.0, m * d)).cuda()
+    for a, b in ((wf.forward(x), wp.forward(x)), (wf.backward(y), wp.backward(y))):
+        assert float((a - b).norm()) <= 1e-12 * float(b.norm())
+
+
+def test_symmetric_fast_n1024_default_dispatch(gpu):
+    """At n = 1024 the default dispatch takes the symmetric kernels; compare with
+    the parity kernels (bit-identical to the reference)."""
+    torch = gpu
+    from paper_1310_0956_b200.geometry import build_geometry, build_projector
+    n, d, m = 1024, 1449, 1024
+    g = build_geometry(n, d, m)
+    wp = build_projector(g)
+    wf = build_projector(g, precision="float32")
+    rs = np.random.default_rng(7)
+    x = rs.uniform(0.0, 1.0, n * n)
+    y = rs.uniform(0.0, 1.0, m * d)
+    ff = wf.forward(torch.from_numpy(x.astype(np.float32)).cuda()).double()
+    bb = wf.backward(torch.from_numpy(y.astype(np.float32)).cuda()).double()
+    fr = wp.forward(torch.from_numpy(x).cuda())
+    br = wp.backward(torch.from_numpy(y).cuda())
+    assert float((ff - fr).norm()) <= 1e-5 * float(fr.norm())
+    assert float((bb - br).norm()) <= 1e-5 * float(br.norm())
