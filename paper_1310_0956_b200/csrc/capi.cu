@@ -50,6 +50,7 @@ cudaError_t batched_gemv(int, int, const double*, long long, const double*, long
 cudaError_t haar_prolong(int, const double*, int, double*, int, cudaStream_t);
 cudaError_t leaf_factor(const GeomDev&, int, const int*, long long, long long, double*,
                         cudaStream_t);
+bool tma_window_fits(const AngleParams*, int, int, int);
 }  // namespace wmg
 
 struct wmg_geometry {
@@ -182,12 +183,14 @@ int wmg_geometry_create(int n, int n_detectors, int n_angles, const double* cos_
   g->dev.ang = g->d_ang;
   g->dev.rowmap = nullptr;
   g->dev.sym = sym ? 1 : 0;
+  g->dev.tma_ok = (sym && wmg::tma_window_fits(P.data(), n, n_detectors, n_angles)) ? 1 : 0;
   g->sym_capable = sym ? 1 : 0;
   g->axis = g->dev;
   g->axis.m = 2;
   g->axis.ang = g->d_axis;
   g->axis.rowmap = g->d_rowmap;
   g->axis.sym = 0;
+  g->axis.tma_ok = 0;
   *out = g;
   return WMG_OK;
 }

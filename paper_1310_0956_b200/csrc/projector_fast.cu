@@ -831,6 +831,11 @@ __global__ void __launch_bounds__(256) bwd_sym64_kernel(GeomDev G, const TIn* __
 // ---------------------------------------------------------------------------
 // host launchers.  dtype codes: 0 = float32, 1 = float64.
 // ---------------------------------------------------------------------------
+bool tma_forward_supported(const GeomDev& G);
+template <typename TOut>
+cudaError_t tma_forward(const GeomDev& G, float* P, float* PT, TOut* sino, int* overflow,
+                        cudaStream_t st);
+
 // Path selection.  The symmetric kernels do a quarter of the weight work but
 // expose 4x less parallelism (blocks own four tile/ray images), so they only
 // pay off once the grid still fills the 148 SMs several times over.
@@ -862,9 +867,13 @@ static cudaError_t fwd_v2_impl(const GeomDev& G, const void* x, void* ws, void* 
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   if (use_sym_fwd(G) && Gx) {
-    dim3 sgrid(((G.d + 1) / 2 + 127) / 128, G.m / 2 - 1);
-    fast::fwd_sym_kernel<TOut><<<sgrid, 128, 0, st>>>(G, P, PT, (TOut*)y);
-    e = cudaGetLastError();
+    if (G.sym != 3 && tma_forward_supported(G)) {
+      e = tma_forward<TOut>(G, P, PT, (TOut*)y, nullptr, st);
+    } else {
+      dim3 sgrid(((G.d + 1) / 2 + 127) / 128, G.m / 2 - 1);
+      fast::fwd_sym_kernel<TOut><<<sgrid, 128, 0, st>>>(G, P, PT, (TOut*)y);
+      e = cudaGetLastError();
+    }
     if (e != cudaSuccess) return e;
     dim3 xgrid((G.d + 127) / 128, Gx->m);   // the two axis-aligned angles
     fast::fwd_v2_kernel<TOut><<<xgrid, 128, 0, st>>>(*Gx, P, PT, (TOut*)y);
