@@ -80,7 +80,8 @@ int wmg_geometry_shape(const wmg_geometry *g, long long *n_rows, long long *n_co
  * and m/2 and n % 64 == 0 (e.g. build_geometry grids); then one weight evaluation
  * serves four (pixel, angle) pairs.  set = 0 disables it, 1 enables it where
  * profitable (large grids; the default when available), 2 forces it at every
- * size (testing), -1 only queries; *enabled receives the state. */
+ * size (testing), 4 forces it with the experimental TMA-staged forward, -1 only
+ * queries; *enabled receives the state. */
 int wmg_geometry_symmetry(wmg_geometry *g, int set, int *enabled);
 
 /* bytes of caller workspace wmg_forward (mode FAST) needs: zero-padded image

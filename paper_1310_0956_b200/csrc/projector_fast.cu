@@ -839,13 +839,14 @@ cudaError_t tma_forward(const GeomDev& G, float* P, float* PT, TOut* sino, int* 
 // Path selection.  The symmetric kernels do a quarter of the weight work but
 // expose 4x less parallelism (blocks own four tile/ray images), so they only
 // pay off once the grid still fills the 148 SMs several times over.
-// G.sym: 0 off, 1 on when profitable, 2 forced (tests)
+// G.sym: 0 off, 1 on when profitable, 2 forced (tests), 4 forced + TMA-staged
+// forward (experimental: slower than the L2 gather on B200)
 static inline bool use_sym_bwd(const GeomDev& G) {
-  return G.sym == 2 || (G.sym == 1 && G.n >= 1024);
+  return G.sym >= 2 || (G.sym == 1 && G.n >= 1024);
 }
 static inline bool use_sym_fwd(const GeomDev& G) {
   const long long blocks = (long long)(((G.d + 1) / 2 + 127) / 128) * (G.m / 2 - 1);
-  return G.sym == 2 || (G.sym == 1 && blocks >= 4LL * 148);
+  return G.sym >= 2 || (G.sym == 1 && blocks >= 4LL * 148);
 }
 static inline bool use_tiled_bwd(const GeomDev& G) { return G.n >= 768; }
 
@@ -867,7 +868,7 @@ static cudaError_t fwd_v2_impl(const GeomDev& G, const void* x, void* ws, void* 
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   if (use_sym_fwd(G) && Gx) {
-    if (G.sym != 3 && tma_forward_supported(G)) {
+    if (G.sym == 4 && tma_forward_supported(G)) {   // opt-in: TMA-staged forward
       e = tma_forward<TOut>(G, P, PT, (TOut*)y, nullptr, st);
     } else {
       dim3 sgrid(((G.d + 1) / 2 + 127) / 128, G.m / 2 - 1);

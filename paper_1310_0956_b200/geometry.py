@@ -161,10 +161,13 @@ class LineProjector:
         return bool(st.value)
 
     def set_symmetry(self, enable) -> bool:
-        """Enable (True: where profitable), force ("force": at every size) or
-        disable (False) the mirror-symmetry kernels; no-op if the angle set is not
-        symmetric.  Returns whether it is enabled."""
-        code = 2 if enable == "force" else int(bool(enable))
+        """Enable (True: where profitable), force ("force": at every size; "tma":
+        forced with the experimental TMA-staged forward) or disable (False) the
+        mirror-symmetry kernels; no-op if the angle set is not symmetric.
+        Returns whether it is enabled."""
+        code = {"force": 2, "tma": 4}.get(enable, None)
+        if code is None:
+            code = int(bool(enable))
         st = N.ctypes.c_int()
         N.call("wmg_geometry_symmetry", self._h, code, N.ctypes.byref(st))
         return bool(st.value)

@@ -141,8 +141,9 @@ def test_dimension_checks(gpu):
         apply_transpose(w, np.ones(7))
 
 
+@pytest.mark.parametrize("mode", ["force", "tma"])
 @pytest.mark.parametrize("n,d,m", [(256, 363, 180), (512, 725, 512), (320, 453, 64)])
-def test_symmetric_fast_paths(gpu, oracle_proj, n, d, m):
+def test_symmetric_fast_paths(gpu, oracle_proj, n, d, m, mode):
     """Full equiangular grids take the mirror-symmetric kernels: same result as
     the plain fast kernels (1e-6) and within 1e-5 of the float64 reference."""
     torch = gpu
@@ -150,7 +151,7 @@ def test_symmetric_fast_paths(gpu, oracle_proj, n, d, m):
     g = build_geometry(n, d, m)
     w = build_projector(g, precision="float32")
     assert w.symmetric
-    assert w.set_symmetry("force")
+    assert w.set_symmetry(mode)
     rs = np.random.default_rng(n)
     x = rs.uniform(0.0, 1.0, n * n)
     y = rs.uniform(0.0, 1.0, m * d)
@@ -159,7 +160,7 @@ def test_symmetric_fast_paths(gpu, oracle_proj, n, d, m):
     fs, bs = w.forward(xd).double(), w.backward(yd).double()
     assert not w.set_symmetry(False)
     fp, bp = w.forward(xd).double(), w.backward(yd).double()
-    assert w.set_symmetry("force")
+    assert w.set_symmetry(mode)
     assert float((fs - fp).norm()) <= 1e-6 * float(fp.norm())
     assert float((bs - bp).norm()) <= 1e-6 * float(bp.norm())
     ref_f = oracle_proj.forward(n, d, g.angles, x)
