@@ -620,11 +620,11 @@ __global__ void __launch_bounds__(128) fwd_sym_kernel(GeomDev G, const float* __
     // slab-coordinate images -> rays; x-major swaps which image is the x-mirror
     const float r_m = A.major ? accB.y : accA.y;    // (m-a, j)
     const float r_mr = A.major ? accA.y : accB.y;   // (m-a, d-1-j)
-    sino[(long long)a * d + j] = (TOut)accA.x;
-    sino[(long long)(m - a) * d + j] = (TOut)r_m;
+    __stcs(sino + (long long)a * d + j, (TOut)accA.x);   // streaming: keep L2 for the planes
+    __stcs(sino + (long long)(m - a) * d + j, (TOut)r_m);
     if (d - 1 - j != j) {
-      sino[(long long)a * d + (d - 1 - j)] = (TOut)accB.x;
-      sino[(long long)(m - a) * d + (d - 1 - j)] = (TOut)r_mr;
+      __stcs(sino + (long long)a * d + (d - 1 - j), (TOut)accB.x);
+      __stcs(sino + (long long)(m - a) * d + (d - 1 - j), (TOut)r_mr);
     }
   }
 }
