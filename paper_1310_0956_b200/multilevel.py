@@ -247,9 +247,11 @@ def build_wmg_hierarchy(w, n: int, lam: float, levels: int, nu_pre: int = 0,
                         nu_post: int = 0, node_mode: str = "fast") -> WmgHierarchy:
     """Recursive 4-way splitting of W (multilevel.py:151-166), matrix-free.
 
-    ``node_mode``: projector mode of the internal node systems -- "fast"
-    (float64 fast kernels, <= 1e-12 relative, default) or "parity".  Leaf Grams
-    always come from the exact (parity) weights.
+    ``node_mode``: projector of the internal node systems -- "fast" (float64
+    fast kernels, <= 1e-12 relative, default), "fast32" (float32 arithmetic on
+    float64 vectors, <= 1e-5 relative: a cheaper, slightly inexact V-cycle for
+    flexible outer solvers) or "parity".  Leaf Grams always come from the exact
+    (parity) weights.
     """
     if levels < 2:
         raise ValueError("levels must be >= 2")
@@ -279,11 +281,16 @@ def build_wmg_hierarchy(w, n: int, lam: float, levels: int, nu_pre: int = 0,
     inverses = t.cholesky_inverse(lower)
     # symmetrise and force row-major storage (the GEMV streams rows)
     inverses = (0.5 * (inverses + inverses.transpose(1, 2))).contiguous()
-    if node_mode == "parity" or getattr(w, "mode", None) == "fast":
+    if node_mode not in ("fast", "fast32", "parity"):
+        raise ValueError(f"unknown node_mode '{node_mode}'")
+    from .geometry import LineProjector
+    if node_mode == "parity" or (node_mode == "fast" and getattr(w, "mode", None) == "fast"
+                                 and getattr(w, "precision", None) == N.F64):
         node_w = w
-    else:
-        from .geometry import LineProjector
+    elif node_mode == "fast":
         node_w = LineProjector(w.geometry, precision="float64", mode="fast", device=w.device)
+    else:
+        node_w = LineProjector(w.geometry, precision="float32", mode="fast", device=w.device)
 
     def make(bands, level):
         side = n >> (level - 1)
