@@ -51,6 +51,10 @@ def parse():
     ap.add_argument("--cpu-angles", type=int, default=4)
     ap.add_argument("--no-wmg", action="store_true",
                     help="skip the config-1 WMG-CGLS time-to-tolerance measurement")
+    ap.add_argument("--workload", choices=["pair", "config2"], default="pair",
+                    help="pair: config-3 projector pair (the default bench line); "
+                         "config2: CGLS vs WMG-GMRES on config 2 (separate JSON line)")
+    ap.add_argument("--levels", type=int, default=5)
     return ap.parse_args()
 
 
@@ -457,10 +461,68 @@ def run_ours(args):
     return 0
 
 
+# ------------------------------------------------------------ config 2
+def run_config2(args):
+    """BASELINE config 2: 1024^2, 720 angles, 1449 detectors; float32 projector
+    with float64 Krylov vectors; seeded 50-ellipse phantom (seed 2000, values
+    U[0,1]); Poisson data, I0 = 1e5, mu = 2/n, log transform (seed 2500).
+    Unpreconditioned CGLS vs WMG-preconditioned GMRES on the normal equations
+    (levels = 5, reference smoother-free cycle), each to normal-equations
+    residual 1e-4.  ``--n`` rescales the grid (detectors = ceil(n sqrt 2),
+    angles = 720 n / 1024) for quick checks."""
+    import torch
+    from paper_1310_0956_b200 import (SolverConfig, build_geometry, build_projector,
+                                      build_wmg_hierarchy, cgls_solve, gmres_solve,
+                                      normal_operator, poisson_log_data, random_ellipses,
+                                      wmg_preconditioner)
+    dev = torch.device("cuda", 0)
+    n = args.n if args.n != 4096 else 1024
+    m = int(round(720 * n / 1024))
+    m += m % 2
+    d = int(math.ceil(n * math.sqrt(2.0)))
+    g = build_geometry(n, d, m)
+    w32 = build_projector(g, precision="float32", device=dev)
+    x_ex = random_ellipses(n, 50, seed=2000, value_range=(0.0, 1.0))
+    b = poisson_log_data(w32 @ x_ex, 1e5, 2.0 / n, seed=2500)
+    bd = torch.from_numpy(b).to(dev)
+    out = {"metric": "config2 seconds to rel. residual 1e-4", "n": n, "n_angles": m,
+           "n_detectors": d, "projector": "float32 arithmetic, float64 Krylov vectors",
+           "data": "synthetic: 50-ellipse phantom, Poisson I0=1e5, mu=2/n"}
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    _, rec = cgls_solve(w32, bd, x_ex=x_ex,
+                        cfg=SolverConfig(max_iterations=3000, residual_tolerance=1e-4))
+    torch.cuda.synchronize(dev)
+    out["cgls"] = {"seconds": time.perf_counter() - t0, "iterations": rec.iterations[-1],
+                   "status": rec.status, "rel_err_l2": rec.rel_err_l2[-1]}
+    op = normal_operator(w32, 0.0)
+    f = w32.T @ bd
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    wexact = build_projector(g, device=dev)      # leaf Grams from the exact weights
+    h = build_wmg_hierarchy(wexact, n, 0.0, args.levels, node_mode="fast32")
+    M = wmg_preconditioner(h)
+    torch.cuda.synchronize(dev)
+    t_setup = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    _, rec = gmres_solve(op, f, precond=M, x_ex=x_ex, restart=100,
+                         cfg=SolverConfig(max_iterations=300, residual_tolerance=1e-4))
+    torch.cuda.synchronize(dev)
+    out["wmg_gmres"] = {"seconds": time.perf_counter() - t0, "setup_seconds": t_setup,
+                        "iterations": rec.iterations[-1], "status": rec.status,
+                        "rel_err_l2": rec.rel_err_l2[-1], "levels": args.levels,
+                        "leaves": 4 ** (args.levels - 1),
+                        "leaf_dim": (n >> (args.levels - 1)) ** 2}
+    print(json.dumps(out), flush=True)
+    return 0
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
+    if args.workload == "config2":
+        return run_config2(args)
     return run_ours(args)
 
 

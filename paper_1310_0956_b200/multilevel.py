@@ -224,8 +224,8 @@ def _assemble_leaf_grams(w, n, lam, levels, ray_chunk=None):
     paths = _leaf_paths(levels)
     grams = t.zeros((len(paths), p, p), dtype=t.float64, device=w.device)
     if ray_chunk is None:
-        # keep the factor slab around 512 MB
-        ray_chunk = max(256, min(M, (512 << 20) // (8 * p)))
+        # keep the factor slab around 1 GB
+        ray_chunk = max(256, min(M, (1 << 30) // (8 * p)))
     P = t.empty((min(ray_chunk, M), p), dtype=t.float64, device=w.device)
     for li, path in enumerate(paths):
         bands = (N.ctypes.c_int * depth)(*[BAND_CODE[b] for b in path])
@@ -238,8 +238,7 @@ def _assemble_leaf_grams(w, n, lam, levels, ray_chunk=None):
             grams[li].addmm_(Pc.T, Pc)
         if lam != 0:
             grams[li].diagonal().add_(lam)
-    # symmetrise the GEMM result exactly (P^T P is symmetric in exact arithmetic)
-    grams = 0.5 * (grams + grams.transpose(1, 2))
+    # (the Cholesky reads the lower triangle only; no symmetrisation copy needed)
     return paths, grams
 
 
@@ -267,20 +266,31 @@ def build_wmg_hierarchy(w, n: int, lam: float, levels: int, nu_pre: int = 0,
         raise TypeError("build_wmg_hierarchy needs a LineProjector (build_projector)")
     t = D.require_cuda()
     paths, grams = _assemble_leaf_grams(w, n, lam, levels)
-    lower, info = t.linalg.cholesky_ex(grams)
-    bad = info.cpu().numpy()
-    for li, code in enumerate(bad):
-        if code > 0:
-            name = "/".join(paths[li]) or "root"
-            raise NotPositiveDefiniteError(
-                f"coarsest subproblem '{name}' is singular (lambda={lam}): "
-                f"leading minor of order {int(code)} is not positive definite")
+    n_leaf, p = grams.shape[0], grams.shape[-1]
+    # keep the Cholesky factors (API: coarse_solve.lower) only when they are
+    # small; the V-cycle itself only needs the inverses
+    keep_lower = grams.numel() * 8 <= (8 << 30)
+    lower_all = t.empty_like(grams) if keep_lower else None
+    batch = max(1, min(n_leaf, (4 << 30) // max(1, p * p * 8)))
+    for b0 in range(0, n_leaf, batch):
+        g = grams[b0:b0 + batch]
+        low, info = t.linalg.cholesky_ex(g)
+        bad = info.cpu().numpy()
+        for li, code in enumerate(bad):
+            if code > 0:
+                name = "/".join(paths[b0 + li]) or "root"
+                raise NotPositiveDefiniteError(
+                    f"coarsest subproblem '{name}' is singular (lambda={lam}): "
+                    f"leading minor of order {int(code)} is not positive definite")
+        if keep_lower:
+            lower_all[b0:b0 + batch].copy_(low)
+        inv = t.cholesky_inverse(low)
+        # symmetrise into the (now consumed) Gram storage, row-major for the GEMV
+        g.copy_(inv)
+        g.add_(inv.transpose(1, 2)).mul_(0.5)
+        del low, inv
+    inverses = grams
     leaf_index = {path: i for i, path in enumerate(paths)}
-    p = grams.shape[-1]
-    del grams
-    inverses = t.cholesky_inverse(lower)
-    # symmetrise and force row-major storage (the GEMV streams rows)
-    inverses = (0.5 * (inverses + inverses.transpose(1, 2))).contiguous()
     if node_mode not in ("fast", "fast32", "parity"):
         raise ValueError(f"unknown node_mode '{node_mode}'")
     from .geometry import LineProjector
@@ -298,8 +308,9 @@ def build_wmg_hierarchy(w, n: int, lam: float, levels: int, nu_pre: int = 0,
         if level == levels:
             li = leaf_index[bands]
             return WmgNode(side=side, level=level, path=path, factor=None, lam=lam,
-                           coarse_solve=DenseFactorization(dimension=p, lower=lower[li],
-                                                           inverse=inverses[li]),
+                           coarse_solve=DenseFactorization(
+                               dimension=p, lower=None if lower_all is None else lower_all[li],
+                               inverse=inverses[li]),
                            bands=bands)
         node = WmgNode(side=side, level=level, path=path, factor=w, lam=lam,
                        intergrid=None, bands=bands)
@@ -309,7 +320,7 @@ def build_wmg_hierarchy(w, n: int, lam: float, levels: int, nu_pre: int = 0,
 
     root = make((), 1)
     h = WmgHierarchy(levels=levels, lam=lam, root=root, projector=w, n=n, nu_pre=nu_pre,
-                     nu_post=nu_post, leaf_factors=lower, leaf_inverses=inverses,
+                     nu_post=nu_post, leaf_factors=lower_all, leaf_inverses=inverses,
                      node_projector=node_w)
     for nd in h.nodes():
         nd.hierarchy = h
