@@ -138,6 +138,16 @@ int wmg_cgs_update(long long n, int k, double *w, const double *V, long long ldv
 int wmg_combo(long long n, int k, double *out, const double *V, long long ldv, const double *cf,
               int accumulate, void *stream);
 int wmg_cast(long long n, int to_f32, void *out, const void *in, void *stream);
+/* device-coefficient variants (coefficient read from device memory, so solver
+ * iterations can be captured in a CUDA graph): out = y + sgn*(coef[0]*x);
+ * out = a*x + coef[0]*y */
+int wmg_axpy_dev(long long n, double *out, const double *y, const double *coef, int sgn,
+                 const double *x, void *stream);
+int wmg_lincomb_dev(long long n, double *out, double a, const double *x, const double *coef,
+                    const double *y, void *stream);
+/* CGLS / flexible PCG-NE scalar recurrences on device slots (see vecops.cu):
+ * op 0 alpha = gamma/(qq + lam pp); op 1 beta = ss/gamma; op 2 beta = pr/gamma */
+int wmg_cgls_scalars(double *S, double lam, int op, void *stream);
 
 /* Haar intergrid operators (side even).  band: 0 LL, 1 LH, 2 HL, 3 HH.
  * restrict: out holds one (side/2)^2 block per band set in band_mask, in band

@@ -12,7 +12,8 @@ __version__ = "0.1.0"
 from .geometry import (Geometry, LineProjector, apply, apply_transpose,  # noqa: F401
                        build_geometry, build_projector)
 from .multilevel import (BAND_IDS, IntergridSet, WmgHierarchy, WmgNode,  # noqa: F401
-                         build_intergrid_set, build_wmg_hierarchy, haar_scaling_1d,
+                         build_intergrid_set, build_wmg_hierarchy,
+                         classical_tg_preconditioner, haar_scaling_1d,
                          haar_wavelet_1d, wmg_preconditioner, wtg_apply)
 from .phantom import (add_gaussian_noise, add_noise, error_metrics,  # noqa: F401
                       poisson_log_data, random_ellipses, seeded_uniform, shepp_logan)

@@ -79,7 +79,7 @@ def scratch(n: int, K: int, device):
     return buf
 
 
-def det_reduce(specs, n=None):
+def det_reduce(specs, n=None, out=None):
     """Deterministic float64 reductions (DET_SUM, see csrc/vecops.cu).
 
     ``specs`` is a list of (op, a, b, c) tuples of CUDA float64 tensors of equal
@@ -97,7 +97,8 @@ def det_reduce(specs, n=None):
                 raise ValueError("det_reduce operands must have equal lengths")
     dev = a0.device
     sc = scratch(n, K, dev)
-    out = t.empty(K, dtype=t.float64, device=dev)
+    if out is None:
+        out = t.empty(K, dtype=t.float64, device=dev)
     ops = (ctypes.c_int * K)(*[int(s[0]) for s in specs])
     A = (ctypes.c_void_p * K)(*[s[1].data_ptr() for s in specs])
     B = (ctypes.c_void_p * K)(*[(s[2].data_ptr() if s[2] is not None else 0) for s in specs])

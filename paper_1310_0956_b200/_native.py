@@ -60,6 +60,9 @@ _SIGS = {
     "wmg_cgs_update": (_i, [_ll, _i, _dp, _dp, _ll, _dp, _vp]),
     "wmg_combo": (_i, [_ll, _i, _dp, _dp, _ll, _dp, _i, _vp]),
     "wmg_cast": (_i, [_ll, _i, _dp, _dp, _vp]),
+    "wmg_axpy_dev": (_i, [_ll, _dp, _dp, _dp, _i, _dp, _vp]),
+    "wmg_lincomb_dev": (_i, [_ll, _dp, _d, _dp, _dp, _dp, _vp]),
+    "wmg_cgls_scalars": (_i, [_dp, _d, _i, _vp]),
     "wmg_batched_gemv": (_i, [_i, _i, _dp, _ll, _dp, _ll, _dp, _ll, _vp]),
     "wmg_haar_restrict": (_i, [_i, _dp, _i, _dp, _vp]),
     "wmg_haar_prolong": (_i, [_i, _dp, _i, _dp, _i, _vp]),

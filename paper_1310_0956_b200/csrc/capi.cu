@@ -45,6 +45,11 @@ cudaError_t ew_combo(long long, int, double*, const double*, long long, const do
                      cudaStream_t);
 cudaError_t ew_cast(long long, int, void*, const void*, cudaStream_t);
 cudaError_t haar_restrict(int, const double*, int, double*, cudaStream_t);
+cudaError_t ew_axpy_dev(long long, double*, const double*, const double*, int, const double*,
+                        cudaStream_t);
+cudaError_t ew_lincomb_dev(long long, double*, double, const double*, const double*,
+                           const double*, cudaStream_t);
+cudaError_t cgls_scalars(double*, double, int, cudaStream_t);
 cudaError_t batched_gemv(int, int, const double*, long long, const double*, long long, double*,
                          long long, cudaStream_t);
 cudaError_t haar_prolong(int, const double*, int, double*, int, cudaStream_t);
@@ -366,6 +371,21 @@ int wmg_combo(long long n, int k, double* out, const double* V, long long ldv, c
   REQ(out && V && cf);
   if (k < 0) return fail(WMG_EINVAL, "k < 0");
   return cuda_rc(wmg::ew_combo(n, k, out, V, ldv, cf, accumulate, STREAM(stream)));
+}
+int wmg_axpy_dev(long long n, double* out, const double* y, const double* coef, int sgn,
+                 const double* x, void* stream) {
+  REQ(out && y && coef && x);
+  return cuda_rc(wmg::ew_axpy_dev(n, out, y, coef, sgn, x, STREAM(stream)));
+}
+int wmg_lincomb_dev(long long n, double* out, double a, const double* x, const double* coef,
+                    const double* y, void* stream) {
+  REQ(out && x && coef && y);
+  return cuda_rc(wmg::ew_lincomb_dev(n, out, a, x, coef, y, STREAM(stream)));
+}
+int wmg_cgls_scalars(double* S, double lam, int op, void* stream) {
+  REQ(S);
+  if (op < 0 || op > 2) return fail(WMG_EINVAL, "bad scalar op");
+  return cuda_rc(wmg::cgls_scalars(S, lam, op, STREAM(stream)));
 }
 int wmg_cast(long long n, int to_f32, void* out, const void* in, void* stream) {
   REQ(out && in);

@@ -317,6 +317,48 @@ __global__ void __launch_bounds__(256) batched_gemv_kernel(int p, const double* 
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// device-resident Krylov scalars (graph-capturable solver iterations)
+// ---------------------------------------------------------------------------
+// out = y + sgn * (coef[0] * x)
+__global__ void axpy_dev_kernel(long long n, double* out, const double* y,
+                                const double* __restrict__ coef, int sgn, const double* x) {
+  const double alpha = coef[0];
+  GRID_LOOP(i, n) {
+    const double t = dmul(alpha, x[i]);
+    out[i] = sgn > 0 ? dadd(y[i], t) : dsub(y[i], t);
+  }
+}
+// out = a * x + coef[0] * y
+__global__ void lincomb_dev_kernel(long long n, double* out, double a, const double* x,
+                                   const double* __restrict__ coef, const double* y) {
+  const double b = coef[0];
+  GRID_LOOP(i, n) { out[i] = dadd(dmul(a, x[i]), dmul(b, y[i])); }
+}
+
+// CGLS / flexible PCG-NE scalar recurrences on the slot vector S:
+//  S[0] gamma, S[1] <q,q>, S[2] <p,p>, S[3] alpha, S[4] beta, S[5] <s,s>,
+//  S[6] <z,s>, S[7] <z,s-s_old>, S[8] breakdown flag
+// op 0: delta = qq (+ lam pp); alpha = gamma / delta (0 and flag on breakdown)
+// op 1: beta = ss / gamma; gamma = ss           (CGLS)
+// op 2: beta = pr / gamma; gamma = zs           (flexible PCG-NE)
+__global__ void cgls_scalars_kernel(double* S, double lam, int op) {
+  if (threadIdx.x || blockIdx.x) return;
+  if (op == 0) {
+    const double delta = lam != 0.0 ? dadd(S[1], dmul(lam, S[2])) : S[1];
+    const bool ok = delta > 0.0 && isfinite(delta);
+    S[3] = ok ? S[0] / delta : 0.0;
+    if (!ok) S[8] = 1.0;
+  } else if (op == 1) {
+    S[4] = S[5] / S[0];
+    S[0] = S[5];
+  } else {
+    S[4] = S[7] / S[0];
+    S[0] = S[6];
+  }
+}
+
 }  // namespace vec
 
 // ---------------------------------------------------------------------------
@@ -429,6 +471,19 @@ cudaError_t batched_gemv(int batch, int p, const double* A, long long sA, const 
   }
   dim3 grid((p + vec::kGemvRows - 1) / vec::kGemvRows, batch);
   vec::batched_gemv_kernel<<<grid, 256, smem, st>>>(p, A, sA, x, sx, y, sy);
+  return cudaGetLastError();
+}
+
+cudaError_t ew_axpy_dev(long long n, double* out, const double* y, const double* coef, int sgn,
+                        const double* x, cudaStream_t st) {
+  LAUNCH_EW(vec::axpy_dev_kernel, n, out, y, coef, sgn, x);
+}
+cudaError_t ew_lincomb_dev(long long n, double* out, double a, const double* x,
+                           const double* coef, const double* y, cudaStream_t st) {
+  LAUNCH_EW(vec::lincomb_dev_kernel, n, out, a, x, coef, y);
+}
+cudaError_t cgls_scalars(double* S, double lam, int op, cudaStream_t st) {
+  vec::cgls_scalars_kernel<<<1, 32, 0, st>>>(S, lam, op);
   return cudaGetLastError();
 }
 

@@ -22,7 +22,7 @@ level"; not defined by the reference, SURVEY.md s8 a16 option (ii)): with
     omega_p = 0.95 / lambda_max(C_p A_p)   (10 power iterations at setup)
 before and after its wavelet two-grid correction.  nu_pre = nu_post = 0 (the
 default) is exactly the reference's smoother-free cycle.
-``classical_tg_preconditioner`` is out of scope.
+``classical_tg_preconditioner`` is provided as well.
 """
 from __future__ import annotations
 
@@ -214,14 +214,15 @@ def _leaf_paths(levels):
     return paths
 
 
-def _assemble_leaf_grams(w, n, lam, levels, ray_chunk=None):
-    """Dense Gram P_L^T P_L + lam I for every leaf, batched in HBM."""
+def _assemble_leaf_grams(w, n, lam, levels, ray_chunk=None, paths=None):
+    """Dense Gram P_L^T P_L + lam I for every leaf (or the given band paths of
+    depth levels-1), batched in HBM."""
     t = D.torch()
     depth = levels - 1
     side_c = n >> depth
     p = side_c * side_c
     M = w.shape[0]
-    paths = _leaf_paths(levels)
+    paths = _leaf_paths(levels) if paths is None else [tuple(q) for q in paths]
     grams = t.zeros((len(paths), p, p), dtype=t.float64, device=w.device)
     if ray_chunk is None:
         # keep the factor slab around 1 GB
@@ -468,26 +469,22 @@ def wtg_apply(node: WmgNode, r, multiplicative: bool = False):
     return D.to_caller(_wtg_(node, rd, multiplicative), was_np)
 
 
-class WmgPreconditioner:
-    """One V-cycle as an approximate solve of (W^T W + lam I) z = v.
-
-    The cycle has no data-dependent control flow, so after one eager warm-up it
-    is captured once as a CUDA graph (static input/output buffers) and replayed:
-    the ~50-300 small launches of a cycle cost one graph launch.
-    """
+class _GraphedOperator:
+    """Device operator whose eager body has no data-dependent control flow: after
+    one eager warm-up it is captured once as a CUDA graph (static input/output
+    buffers) and replayed, so its ~50-300 small launches cost one graph launch."""
 
     _wmg_device = True
+    dim = 0
 
-    def __init__(self, h: WmgHierarchy, multiplicative: bool = False, graph: bool = True):
-        self.h = h
-        self.multiplicative = multiplicative
+    def _init_graph(self, graph: bool):
         self.use_graph = graph
         self._graph = None
         self._gin = self._gout = None
         self._eager_calls = 0
 
-    def _eager(self, v):
-        return _node_solve_(self.h.root, v, self.multiplicative)
+    def _eager(self, v):  # pragma: no cover - abstract
+        raise NotImplementedError
 
     def apply_(self, v, out):
         t = D.torch()
@@ -495,7 +492,7 @@ class WmgPreconditioner:
             out.copy_(self._eager(v))
             return out
         if self._graph is None:
-            if self._eager_calls < 1:               # warm-up (allocator, cuBLAS handles)
+            if self._eager_calls < 1:               # warm-up (allocator, buffers)
                 self._eager_calls += 1
                 out.copy_(self._eager(v))
                 return out
@@ -517,14 +514,114 @@ class WmgPreconditioner:
     def __call__(self, v):
         t = D.torch()
         vd, was_np = D.to_device(v)
-        if vd.numel() != self.h.root.dim:
+        if vd.numel() != self.dim:
             raise DimensionMismatchError(
-                f"wmg_preconditioner: length {vd.numel()} != {self.h.root.dim}")
+                f"{type(self).__name__}: length {vd.numel()} != {self.dim}")
         out = t.empty_like(vd)
         self.apply_(vd, out)
         return D.to_caller(out, was_np)
 
 
+class WmgPreconditioner(_GraphedOperator):
+    """One V-cycle as an approximate solve of (W^T W + lam I) z = v."""
+
+    def __init__(self, h: WmgHierarchy, multiplicative: bool = False, graph: bool = True):
+        self.h = h
+        self.multiplicative = multiplicative
+        self.dim = h.root.dim
+        self._init_graph(graph)
+
+    def _eager(self, v):
+        return _node_solve_(self.h.root, v, self.multiplicative)
+
+
 def wmg_preconditioner(h: WmgHierarchy, multiplicative: bool = False,
                        graph: bool = True) -> Callable:
     return WmgPreconditioner(h, multiplicative, graph=graph)
+
+
+# --------------------------------------------- classical two-grid (SURVEY f2)
+class ClassicalTGPreconditioner(_GraphedOperator):
+    """One classical two-grid cycle on the normal equations, LL coarsening only
+    (multilevel.py:211-258).  Smoother (the reference's, applied verbatim):
+    z <- z + C (v - (W^T R W + lam) z); coarse correction with the dense
+    Galerkin operator of W^T W + lam I under the LL restriction (exact weights,
+    stored inverse, our batched GEMV)."""
+
+    _wmg_device = True
+
+    def __init__(self, w, n: int, lam: float, smoother_steps=(1, 1), graph: bool = True):
+        _check_even(n)
+        nu1, nu2 = smoother_steps
+        if nu1 < 0 or nu2 < 0:
+            raise ValueError("smoothing counts must be nonnegative")
+        if w.shape[1] != n * n:
+            raise DimensionMismatchError(
+                f"projector has {w.shape[1]} columns, expected {n * n}")
+        if not hasattr(w, "handle"):
+            raise TypeError("classical_tg_preconditioner needs a LineProjector")
+        t = D.require_cuda()
+        from .solvers import sirt_scaling
+        self.w, self.n, self.lam = w, n, float(lam)
+        self.nu1, self.nu2 = int(nu1), int(nu2)
+        sc = sirt_scaling(w)
+        self.c, self.r = sc.c_dev, sc.r_dev
+        _, grams = _assemble_leaf_grams(w, n, lam, 2, paths=[("LL",)])
+        low, info = t.linalg.cholesky_ex(grams)
+        if int(info.max()) > 0:
+            raise NotPositiveDefiniteError(
+                f"coarse LL Galerkin operator is singular (lambda={lam})")
+        inv = t.cholesky_inverse(low)
+        self.coarse = DenseFactorization(dimension=grams.shape[-1], lower=low[0],
+                                         inverse=(0.5 * (inv + inv.transpose(1, 2)))[0]
+                                         .contiguous())
+        M, N_ = w.shape
+        dev = w.device
+        self._sino = t.empty(M, dtype=t.float64, device=dev)
+        self._img = t.empty(N_, dtype=t.float64, device=dev)
+        self.dim = n * n
+        self._init_graph(graph)
+
+    def _apply_a(self, v, out):
+        self.w.forward_(v, self._sino)
+        self.w.backward_(self._sino, out)
+        if self.lam != 0:
+            D.add_scaled(out, out, self.lam, +1, v)
+        return out
+
+    def _smooth(self, z, v):
+        t = D.torch()
+        self.w.forward_(z, self._sino)
+        D.hadamard(self._sino, self.r, self._sino)          # r * (W z)
+        self.w.backward_(self._sino, self._img)             # W^T (r * W z)
+        D.add_scaled(self._img, self._img, self.lam, +1, z)  # + lam z
+        u = t.empty_like(v)
+        D.axpy(u, v, 1.0, -1, self._img)                    # v - (...)
+        D.hadamard(u, self.c, u)                            # C (...)
+        D.axpy(z, z, 1.0, +1, u)                            # z + C(...)
+        return z
+
+    def _eager(self, v):
+        t = D.torch()
+        z = t.zeros_like(v)
+        for _ in range(self.nu1):
+            self._smooth(z, v)
+        if self.nu1 > 0:
+            az = t.empty_like(v)
+            self._apply_a(z, az)
+            res = t.empty_like(v)
+            D.axpy(res, v, 1.0, -1, az)
+        else:
+            res = v
+        rc = restrict(self.n, res, ("LL",))[0]
+        zc = self.coarse.apply_inverse(rc)
+        prolong(self.n, zc, "LL", z, accumulate=True)
+        for _ in range(self.nu2):
+            self._smooth(z, v)
+        return z
+
+
+
+def classical_tg_preconditioner(w, n: int, lam: float, smoother_steps=(1, 1),
+                                graph: bool = True) -> Callable:
+    return ClassicalTGPreconditioner(w, n, lam, smoother_steps, graph=graph)

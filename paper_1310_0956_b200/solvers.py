@@ -381,8 +381,137 @@ def bicgstab_solve(op, f, precond=None, x0=None, cfg: SolverConfig = None, x_ex=
     return D.to_caller(x, was_np), record
 
 
+class _GraphedLoop:
+    """Runs a device-only loop body: eagerly once (warm-up), then captured once
+    as a CUDA graph and replayed for every further iteration."""
+
+    def __init__(self, body):
+        self.body = body
+        self.calls = 0
+        self.graph = None
+
+    def step(self):
+        t = D.torch()
+        self.calls += 1
+        if self.calls == 1:
+            self.body()
+            return
+        if self.graph is None:
+            dev = t.cuda.current_device()
+            side = t.cuda.Stream(device=dev)
+            side.wait_stream(t.cuda.current_stream(dev))
+            with t.cuda.stream(side):
+                g = t.cuda.CUDAGraph()
+                with t.cuda.graph(g, stream=side):
+                    self.body()
+            t.cuda.current_stream(dev).wait_stream(side)
+            self.graph = g
+        self.graph.replay()
+
+
+def _graphable(w, precond):
+    if getattr(w, "world", 1) > 1:        # sharded: NCCL inside the loop, stay eager
+        return False
+    if not (hasattr(w, "forward_") and hasattr(w, "backward_")):
+        return False
+    return precond is None or hasattr(precond, "_eager")
+
+
+def _cgls_graphed(w, bd, x, lam, precond, cfg, errs, was_np, record, t0):
+    """CGLS / flexible PCG-NE with device-resident scalars: one graph replay and
+    one 12-double D2H per iteration; same arithmetic as the eager path (see
+    cgls_solve), hence bit-identical iterates and records."""
+    t = D.torch()
+    dev = bd.device
+    M_, Nn = w.shape
+    r = t.empty(M_, dtype=t.float64, device=dev)
+    q = t.empty(M_, dtype=t.float64, device=dev)
+    s = t.empty(Nn, dtype=t.float64, device=dev)
+    s_old = t.empty(Nn, dtype=t.float64, device=dev)
+    S = t.zeros(16, dtype=t.float64, device=dev)
+    S_host = t.zeros(16, dtype=t.float64).pin_memory()
+    st = D.stream_handle
+    w.forward_(x, q)
+    D.axpy(r, bd, 1.0, -1, q)
+    w.backward_(r, s)
+    if lam != 0:
+        D.add_scaled(s, s, lam, -1, x)
+    if precond is None:
+        z = s
+        D.det_reduce([(N.RED_SQ, s, None, None)], out=S[0:1])
+        D.det_reduce([(N.RED_SQ, s, None, None)], out=S[5:6])
+    else:
+        z = precond._eager(s)
+        D.det_reduce([(N.RED_SQ, s, None, None), (N.RED_DOT, z, s, None)], out=S[5:7])
+        S[0:1].copy_(S[6:7])
+    p = z.clone()
+    if errs.active:
+        S[9:11].copy_(errs.device_terms(x))
+    S_host.copy_(S, non_blocking=True)
+    t.cuda.current_stream(dev).synchronize()
+    h = S_host.numpy()
+    s0 = float(np.sqrt(h[5]))
+    e2, einf = errs.finish(h[9:11]) if errs.active else (None, None)
+    record.log(0, 1.0, e2, einf, time.perf_counter() - t0)
+    if s0 == 0.0:
+        record.status = STATUS_CONVERGED
+        return D.to_caller(x, was_np), record
+
+    n_img, n_sino = Nn, M_
+
+    def body():
+        w.forward_(p, q)
+        D.det_reduce([(N.RED_SQ, q, None, None)], out=S[1:2])
+        if lam != 0:
+            D.det_reduce([(N.RED_SQ, p, None, None)], out=S[2:3])
+        N.call("wmg_cgls_scalars", D.ptr(S), float(lam), 0, st())
+        N.call("wmg_axpy_dev", n_img, D.ptr(x), D.ptr(x), D.ptr(S[3:4]), 1, D.ptr(p), st())
+        N.call("wmg_axpy_dev", n_sino, D.ptr(r), D.ptr(r), D.ptr(S[3:4]), -1, D.ptr(q), st())
+        if precond is not None:
+            s_old.copy_(s)
+        w.backward_(r, s)
+        if lam != 0:
+            D.add_scaled(s, s, lam, -1, x)
+        if precond is None:
+            D.det_reduce([(N.RED_SQ, s, None, None)], out=S[5:6])
+            N.call("wmg_cgls_scalars", D.ptr(S), float(lam), 1, st())
+            N.call("wmg_lincomb_dev", n_img, D.ptr(p), 1.0, D.ptr(s), D.ptr(S[4:5]), D.ptr(p),
+                   st())
+        else:
+            zz = precond._eager(s)
+            D.det_reduce([(N.RED_SQ, s, None, None), (N.RED_DOT, zz, s, None),
+                          (N.RED_DOTDIFF, zz, s, s_old)], out=S[5:8])
+            N.call("wmg_cgls_scalars", D.ptr(S), float(lam), 2, st())
+            N.call("wmg_lincomb_dev", n_img, D.ptr(p), 1.0, D.ptr(zz), D.ptr(S[4:5]),
+                   D.ptr(p), st())
+        if errs.active:
+            S[9:11].copy_(errs.device_terms(x))
+        S_host.copy_(S, non_blocking=True)
+
+    loop = _GraphedLoop(body)
+    for k in range(1, cfg.max_iterations + 1):
+        loop.step()
+        t.cuda.current_stream(dev).synchronize()
+        h = S_host.numpy()
+        if h[8] != 0.0:
+            record.status = STATUS_BREAKDOWN
+            return D.to_caller(x, was_np), record
+        rel = float(np.sqrt(h[5])) / s0
+        e2, einf = errs.finish(h[9:11]) if errs.active else (None, None)
+        record.log(k, rel, e2, einf, time.perf_counter() - t0)
+        if cfg.residual_tolerance > 0 and rel < cfg.residual_tolerance:
+            record.status = STATUS_CONVERGED
+            return D.to_caller(x, was_np), record
+        if h[0] == 0.0:
+            record.status = STATUS_CONVERGED
+            return D.to_caller(x, was_np), record
+    record.status = STATUS_MAX_ITERATIONS
+    return D.to_caller(x, was_np), record
+
+
 # --------------------------------------------------------------- CGLS family
-def cgls_solve(w, b, precond=None, x0=None, cfg: SolverConfig = None, x_ex=None):
+def cgls_solve(w, b, precond=None, x0=None, cfg: SolverConfig = None, x_ex=None,
+               graph: bool = True):
     """CGLS on min ||W x - b||^2 + lam ||x||^2; with ``precond`` (an operator
     approximating (W^T W + lam I)^-1, e.g. ``wmg_preconditioner``) the flexible
     Polak-Ribiere PCG on the normal equations ("WMG-CGLS").
@@ -393,6 +522,10 @@ def cgls_solve(w, b, precond=None, x0=None, cfg: SolverConfig = None, x_ex=None)
             z = M s_new;  beta = <z, s_new - s> / gamma   (M = I: <s,s>/gamma)
             gamma = <z, s_new>;  p = z + beta p
     Logged residual: ||s_k|| / ||s_0|| (normal-equations recurrence residual).
+
+    With ``graph=True`` (default, when W and the preconditioner are our device
+    operators) the scalars stay on the device and each iteration is one CUDA
+    graph replay; results are bit-identical to the eager path.
     """
     t = D.require_cuda()
     if cfg is None:
@@ -408,10 +541,12 @@ def cgls_solve(w, b, precond=None, x0=None, cfg: SolverConfig = None, x_ex=None)
         if x.numel() != Nn:
             raise DimensionMismatchError("cgls_solve: x0 length mismatch")
     lam = float(cfg.regularization_lambda)
-    minv = _as_device_op(precond)
     errs = _ErrorTracker(x_ex, Nn, bd.device)
     record = ConvergenceRecord()
     t0 = time.perf_counter()
+    if graph and _graphable(w, precond):
+        return _cgls_graphed(w, bd, x, lam, precond, cfg, errs, was_np, record, t0)
+    minv = _as_device_op(precond)
 
     dev = bd.device
     r = t.empty(M_, dtype=t.float64, device=dev)

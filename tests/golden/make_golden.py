@@ -119,6 +119,16 @@ def main():
         arrays[f"wmgbicg_w16_l{lv}_x"] = xw
         arrays[f"wmgbicg_w16_l{lv}_res"] = np.array(rec.rel_residual)
         meta["solvers"][f"wmgbicg_w16_l{lv}_status"] = rec.status
+    from wmgtomo.multilevel import classical_tg_preconditioner
+    for steps in ((0, 0), (1, 1), (2, 1)):
+        tg = classical_tg_preconditioner(w16, 16, 1.0, smoother_steps=steps)
+        rr = np.random.default_rng(40 + sum(steps)).standard_normal(256)
+        arrays[f"tg_w16_{steps[0]}{steps[1]}_r"] = rr
+        arrays[f"tg_w16_{steps[0]}{steps[1]}_z"] = tg(rr)
+    tg = classical_tg_preconditioner(w16, 16, 1.0)
+    xt, rec = bicgstab_solve(op, f16, precond=tg,
+                             cfg=SolverConfig(max_iterations=200, residual_tolerance=1e-10))
+    arrays["tgbicg_w16_res"] = np.array(rec.rel_residual)
     print("solvers done", flush=True)
 
     np.savez_compressed(os.path.join(HERE, "golden.npz"), **arrays)
