@@ -164,6 +164,132 @@ __global__ void __launch_bounds__(256) bwd_kernel(GeomDev G, const TIn* __restri
     img[p] = (TOut)acc;
 }
 
+// Small grids (n <= 512, e.g. config 1 and the WMG node applies) expose too
+// little parallelism for one thread per ray / pixel: 65k rays of 256 serial
+// slabs leave the SMs latency-bound.  The split kernels give each ray (pixel)
+// kSplit threads -- consecutive slab (angle) segments -- and reduce the
+// partial sums in shared memory in segment order (deterministic).
+constexpr int kSplit = 8;
+
+// block (32 rays, kSplit slab segments); grid (ceil(d/32), m)
+template <typename TIn, typename TOut, typename R>
+__global__ void __launch_bounds__(32 * kSplit) fwd_split_kernel(GeomDev G,
+                                                                const TIn* __restrict__ img,
+                                                                const TIn* __restrict__ imgT,
+                                                                TOut* __restrict__ sino) {
+  __shared__ R part[kSplit][33];
+  const int a = blockIdx.y;
+  const int lane = threadIdx.x, seg = threadIdx.y;
+  const int j = blockIdx.x * 32 + lane;
+  const int n = G.n;
+  R acc = R(0);
+  if (j < G.d) {
+    const AngleParams& P = G.ang[a];
+    const TIn* __restrict__ src = P.major ? imgT : img;
+    const double off = (double)j - (double)(G.d - 1) * 0.5;
+    const double u0 = P.u0 + off * P.du;
+    const double slope = P.slope;
+    int r0 = 0, r1 = n - 1;
+    if (slope > 0.0) {
+      const double ra = floor((-1.0 - u0) / slope) - 1.0;
+      const double rb = ceil(((double)n + 1.0 - u0) / slope) + 1.0;
+      r0 = (int)fmax(ra, 0.0);
+      r1 = (int)fmin(rb, (double)(n - 1));
+    } else if (u0 < -1.0 || u0 > (double)n + 1.0) {
+      r1 = -1;
+    }
+    const int len = r1 - r0 + 1;
+    const int rs = r0 + (len > 0 ? (len * seg) / kSplit : 0);
+    const int re = r0 + (len > 0 ? (len * (seg + 1)) / kSplit : 0) - 1;
+    const R L = Pc<R>::L(P), Ls = Pc<R>::Ls(P);
+    if constexpr (sizeof(R) == 4) {
+      const long long S = llrint(slope * kFixScale);
+      long long U = llrint(u0 * kFixScale) + (long long)rs * S;
+      for (int r = rs; r <= re; ++r) {
+        const long long Uh = U + S;
+        const int k = (int)(Uh >> kFixFrac);
+        R wh = frac_of<R>(Uh) * Ls;
+        wh = (wh < L) ? wh : L;
+        const long long rowbase = (long long)r * n;
+        acc += wh * load_px<TIn, R>(src, rowbase, k, n, P.mirror);
+        acc += (L - wh) * load_px<TIn, R>(src, rowbase, k - 1, n, P.mirror);
+        U = Uh;
+      }
+    } else {
+      for (int r = rs; r <= re; ++r) {
+        const double uh = fma((double)(r + 1), slope, u0);
+        const double fk = floor(uh);
+        const int k = (int)fk;
+        R wh = (uh - fk) * Ls;
+        wh = (wh < L) ? wh : L;
+        const long long rowbase = (long long)r * n;
+        acc += wh * load_px<TIn, R>(src, rowbase, k, n, P.mirror);
+        acc += (L - wh) * load_px<TIn, R>(src, rowbase, k - 1, n, P.mirror);
+      }
+    }
+  }
+  part[seg][lane] = acc;
+  __syncthreads();
+  if (seg == 0 && j < G.d) {
+    R s = part[0][lane];
+#pragma unroll
+    for (int q = 1; q < kSplit; ++q) s += part[q][lane];
+    sino[(long long)(G.rowmap ? G.rowmap[a] : a) * G.d + j] = (TOut)s;
+  }
+}
+
+// block (32 pixels of one row, kSplit angle chunks); grid (ceil(n/32), n)
+template <typename TIn, typename TOut, typename R, bool kAccumulate>
+__global__ void __launch_bounds__(32 * kSplit) bwd_split_kernel(GeomDev G,
+                                                                const TIn* __restrict__ sino,
+                                                                TOut* __restrict__ img) {
+  __shared__ R part[kSplit][33];
+  const int n = G.n;
+  const int lane = threadIdx.x, seg = threadIdx.y;
+  const int ix = blockIdx.x * 32 + lane;
+  const int row = blockIdx.y;
+  const double xc = (double)ix - (double)n * 0.5 + 0.5;
+  const double yc = (double)n * 0.5 - (double)row - 0.5;
+  const double dc = (double)(G.d - 1) * 0.5;
+  const int a0 = (G.m * seg) / kSplit, a1 = (G.m * (seg + 1)) / kSplit;
+  R acc = R(0);
+  if (ix < n) {
+    for (int a = a0; a < a1; ++a) {
+      const AngleParams& P = G.ang[a];
+      const double p = xc * P.c + yc * P.s + dc;
+      const TIn* __restrict__ yrow = sino + (long long)(G.rowmap ? G.rowmap[a] : a) * G.d;
+      if (P.axis) {
+        const int j = (int)ceil(p - 0.5);
+        if (j >= 0 && j < G.d) acc += (R)__ldg(yrow + j);
+        continue;
+      }
+      const double fl = floor(p - (double)P.hw);
+      const int j0 = (int)fl + 1;
+      const R d0 = (R)(fl + 1.0 - p);
+      const R d1 = d0 + R(1);
+      const R hw = Pc<R>::hw(P), ic = Pc<R>::ic(P), L = Pc<R>::L(P);
+      R w0 = (hw - fabs(d0)) * ic;
+      R w1 = (hw - fabs(d1)) * ic;
+      w0 = w0 < R(0) ? R(0) : (w0 > L ? L : w0);
+      w1 = w1 < R(0) ? R(0) : (w1 > L ? L : w1);
+      if (j0 >= 0 && j0 < G.d) acc += w0 * (R)__ldg(yrow + j0);
+      if (j0 + 1 >= 0 && j0 + 1 < G.d) acc += w1 * (R)__ldg(yrow + j0 + 1);
+    }
+  }
+  part[seg][lane] = acc;
+  __syncthreads();
+  if (seg == 0 && ix < n) {
+    R s = part[0][lane];
+#pragma unroll
+    for (int q = 1; q < kSplit; ++q) s += part[q][lane];
+    const long long p = (long long)row * n + ix;
+    if (kAccumulate)
+      img[p] = (TOut)((R)img[p] + s);
+    else
+      img[p] = (TOut)s;
+  }
+}
+
 template <typename T>
 __global__ void transpose_kernel(const T* __restrict__ in, T* __restrict__ out, int n) {
   __shared__ T tile[32][33];
@@ -849,6 +975,21 @@ static inline bool use_sym_fwd(const GeomDev& G) {
   return G.sym >= 2 || (G.sym == 1 && blocks >= 4LL * 148);
 }
 static inline bool use_tiled_bwd(const GeomDev& G) { return G.n >= 768; }
+// one thread per ray / pixel fills the SMs only beyond ~512 px
+static inline bool use_split(const GeomDev& G) { return G.n <= 512; }
+
+template <typename TIn, typename TOut, typename R>
+static cudaError_t bwd_split_launch(const GeomDev& G, const void* y, void* x, bool accumulate,
+                                    cudaStream_t st) {
+  dim3 grid((G.n + 31) / 32, G.n), block(32, fast::kSplit);
+  if (accumulate)
+    fast::bwd_split_kernel<TIn, TOut, R, true><<<grid, block, 0, st>>>(G, (const TIn*)y,
+                                                                       (TOut*)x);
+  else
+    fast::bwd_split_kernel<TIn, TOut, R, false><<<grid, block, 0, st>>>(G, (const TIn*)y,
+                                                                        (TOut*)x);
+  return cudaGetLastError();
+}
 
 template <typename TIn>
 static cudaError_t launch_transpose(const TIn* in, TIn* out, int n, cudaStream_t st) {
@@ -910,6 +1051,7 @@ static cudaError_t bwd_v2_impl(const GeomDev& G, const void* y, void* x, bool ac
                                cudaStream_t st, const GeomDev* G_axis) {
   if (use_sym_bwd(G) && G_axis)
     return bwd_sym_impl<TIn, TOut>(G, *G_axis, y, x, accumulate, st);
+  if (use_split(G)) return bwd_split_launch<TIn, TOut, float>(G, y, x, accumulate, st);
   if (!use_tiled_bwd(G)) {   // small grids: one thread per pixel
     dim3 g1((G.n + 31) / 32, (G.n + 7) / 8);
     if (accumulate)
@@ -979,6 +1121,11 @@ static cudaError_t fwd_impl(const GeomDev& G, const void* x, void* xT_ws, void* 
   TIn* imgT = (TIn*)xT_ws;
   cudaError_t e = launch_transpose<TIn>(img, imgT, G.n, st);
   if (e != cudaSuccess) return e;
+  if (use_split(G)) {
+    dim3 sg((G.d + 31) / 32, G.m), sb(32, fast::kSplit);
+    fast::fwd_split_kernel<TIn, TOut, R><<<sg, sb, 0, st>>>(G, img, imgT, (TOut*)y);
+    return cudaGetLastError();
+  }
   dim3 grid((G.d + 127) / 128, G.m);
   fast::fwd_kernel<TIn, TOut, R><<<grid, 128, 0, st>>>(G, img, imgT, (TOut*)y, G.n);
   return cudaGetLastError();
@@ -987,6 +1134,7 @@ static cudaError_t fwd_impl(const GeomDev& G, const void* x, void* xT_ws, void* 
 template <typename TIn, typename TOut, typename R>
 static cudaError_t bwd_impl(const GeomDev& G, const void* y, void* x, bool accumulate,
                             cudaStream_t st) {
+  if (use_split(G)) return bwd_split_launch<TIn, TOut, R>(G, y, x, accumulate, st);
   dim3 grid((G.n + 31) / 32, (G.n + 7) / 8);
   if (accumulate)
     fast::bwd_kernel<TIn, TOut, R, true><<<grid, 256, 0, st>>>(G, (const TIn*)y, (TOut*)x);

@@ -97,6 +97,28 @@ _PRECISIONS = {"float64": N.F64, "fp64": N.F64, "double": N.F64,
                "float32": N.F32, "fp32": N.F32, "float": N.F32}
 
 
+_PENDING_DESTROY = []
+
+
+def _destroy_geometry(h):
+    """Free a device geometry, unless a CUDA graph capture is running on this
+    thread (the garbage collector may finalise a projector mid-capture, and a
+    cudaFree would invalidate the capture): then defer to the next call."""
+    t = D.torch()
+    try:
+        capturing = t.cuda.is_current_stream_capturing()
+    except Exception:  # pragma: no cover
+        capturing = False
+    if capturing:
+        _PENDING_DESTROY.append(h)
+        return
+    lib = N.load()
+    while _PENDING_DESTROY:
+        lib.wmg_geometry_destroy(_PENDING_DESTROY.pop())
+    if h is not None:
+        lib.wmg_geometry_destroy(h)
+
+
 class LineProjector:
     """Matrix-free W (M x N) with the reference line-intersection weights."""
 
@@ -125,6 +147,8 @@ class LineProjector:
         c, s = snapped_trig(g.angles)
         self._cos, self._sin = c, s
         handle = N.ctypes.c_void_p()
+        if _PENDING_DESTROY:
+            _destroy_geometry(None)
         with t.cuda.device(self.device):
             N.call("wmg_geometry_create", self.n, g.n_detectors, g.n_angles,
                    c.ctypes.data_as(N.ctypes.POINTER(N.ctypes.c_double)),
@@ -139,7 +163,7 @@ class LineProjector:
         h = getattr(self, "_h", None)
         if h is not None and h.value:
             try:
-                N.load().wmg_geometry_destroy(h)
+                _destroy_geometry(h)
             except Exception:  # pragma: no cover - interpreter shutdown
                 pass
             self._h = None

@@ -24,6 +24,7 @@ normal-equations residual ||W^T(b - W x) - lam x|| / ||W^T b - ...||.
 from __future__ import annotations
 
 import time
+import weakref
 from dataclasses import dataclass, field
 from typing import Callable, Optional
 
@@ -424,12 +425,31 @@ def _cgls_graphed(w, bd, x, lam, precond, cfg, errs, was_np, record, t0):
     t = D.torch()
     dev = bd.device
     M_, Nn = w.shape
-    r = t.empty(M_, dtype=t.float64, device=dev)
-    q = t.empty(M_, dtype=t.float64, device=dev)
-    s = t.empty(Nn, dtype=t.float64, device=dev)
-    s_old = t.empty(Nn, dtype=t.float64, device=dev)
-    S = t.zeros(16, dtype=t.float64, device=dev)
-    S_host = t.zeros(16, dtype=t.float64).pin_memory()
+    # The captured iteration (with the whole V-cycle inside) is cached on the
+    # projector per (preconditioner, lambda) together with its static buffers,
+    # so repeated solves replay it instead of re-capturing (no x_ex tracking:
+    # the error terms read a per-solve buffer).
+    owner = precond if precond is not None else w
+    key = (id(w), lam, str(dev))
+    cache = None if errs.active else owner.__dict__.setdefault("_cgls_graph_cache", {})
+    ctx = cache.get(key) if cache is not None else None
+    if ctx is not None and ctx["wref"]() is not w:
+        ctx = None
+    if ctx is None:
+        ctx = {"r": t.empty(M_, dtype=t.float64, device=dev),
+               "q": t.empty(M_, dtype=t.float64, device=dev),
+               "s": t.empty(Nn, dtype=t.float64, device=dev),
+               "s_old": t.empty(Nn, dtype=t.float64, device=dev),
+               "p": t.empty(Nn, dtype=t.float64, device=dev),
+               "x": t.empty(Nn, dtype=t.float64, device=dev),
+               "S": t.zeros(16, dtype=t.float64, device=dev),
+               "S_host": t.zeros(16, dtype=t.float64).pin_memory(),
+               "loop": None, "wref": weakref.ref(w)}
+        if cache is not None:
+            cache[key] = ctx
+    r, q, s, s_old, S, S_host = (ctx[k] for k in ("r", "q", "s", "s_old", "S", "S_host"))
+    ctx["x"].copy_(x)
+    x = ctx["x"]
     st = D.stream_handle
     w.forward_(x, q)
     D.axpy(r, bd, 1.0, -1, q)
@@ -444,7 +464,8 @@ def _cgls_graphed(w, bd, x, lam, precond, cfg, errs, was_np, record, t0):
         z = precond._eager(s)
         D.det_reduce([(N.RED_SQ, s, None, None), (N.RED_DOT, z, s, None)], out=S[5:7])
         S[0:1].copy_(S[6:7])
-    p = z.clone()
+    p = ctx["p"]
+    p.copy_(z)
     if errs.active:
         S[9:11].copy_(errs.device_terms(x))
     S_host.copy_(S, non_blocking=True)
@@ -455,11 +476,17 @@ def _cgls_graphed(w, bd, x, lam, precond, cfg, errs, was_np, record, t0):
     record.log(0, 1.0, e2, einf, time.perf_counter() - t0)
     if s0 == 0.0:
         record.status = STATUS_CONVERGED
-        return D.to_caller(x, was_np), record
+        return D.to_caller(x.clone(), was_np), record
 
     n_img, n_sino = Nn, M_
+    # weak references: the cache lives on the preconditioner (or projector), so
+    # the captured body must not keep either alive
+    wref = weakref.ref(w)
+    pref = weakref.ref(precond) if precond is not None else None
 
     def body():
+        w = wref()
+        precond = pref() if pref is not None else None
         w.forward_(p, q)
         D.det_reduce([(N.RED_SQ, q, None, None)], out=S[1:2])
         if lam != 0:
@@ -488,25 +515,28 @@ def _cgls_graphed(w, bd, x, lam, precond, cfg, errs, was_np, record, t0):
             S[9:11].copy_(errs.device_terms(x))
         S_host.copy_(S, non_blocking=True)
 
-    loop = _GraphedLoop(body)
+    loop = ctx["loop"]
+    if loop is None:
+        loop = ctx["loop"] = _GraphedLoop(body)
     for k in range(1, cfg.max_iterations + 1):
         loop.step()
         t.cuda.current_stream(dev).synchronize()
         h = S_host.numpy()
         if h[8] != 0.0:
             record.status = STATUS_BREAKDOWN
-            return D.to_caller(x, was_np), record
+            break
         rel = float(np.sqrt(h[5])) / s0
         e2, einf = errs.finish(h[9:11]) if errs.active else (None, None)
         record.log(k, rel, e2, einf, time.perf_counter() - t0)
         if cfg.residual_tolerance > 0 and rel < cfg.residual_tolerance:
             record.status = STATUS_CONVERGED
-            return D.to_caller(x, was_np), record
+            break
         if h[0] == 0.0:
             record.status = STATUS_CONVERGED
-            return D.to_caller(x, was_np), record
-    record.status = STATUS_MAX_ITERATIONS
-    return D.to_caller(x, was_np), record
+            break
+    else:
+        record.status = STATUS_MAX_ITERATIONS
+    return D.to_caller(x.clone(), was_np), record
 
 
 # --------------------------------------------------------------- CGLS family
