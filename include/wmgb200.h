@@ -32,7 +32,8 @@
  *                                                      wmg_det_reduce
  *   phantom.py:64-75    error_metrics               -> wmg_det_reduce(SQDIFF), wmg_maxabs
  *   multilevel.py:36-79 haar_* / build_intergrid_set-> wmg_haar_restrict / wmg_haar_prolong
- *   multilevel.py:123-130 leaf Gram assembly        -> wmg_leaf_factor (+ DGEMM)
+ *   multilevel.py:123-130 leaf Gram assembly        -> wmg_leaf_gram (sparse) or
+ *                                                      wmg_leaf_factor (+ DGEMM)
  */
 #ifndef WMGB200_H
 #define WMGB200_H
@@ -166,6 +167,15 @@ int wmg_batched_gemv(int batch, int p, const double *A, long long strideA, const
  * for the leaf reached by bands[0..depth) from the root. */
 int wmg_leaf_factor(const wmg_geometry *g, int depth, const int *bands, long long ray0,
                     long long nrays, double *P, void *stream);
+
+/* WMG leaf Gram, sparse: gram (p x p row-major float64, p = (n >> depth)^2,
+ * caller-zeroed) += lower triangle of P_L^T P_L, accumulated per ray bundle
+ * without forming P_L (weights from the fp64 slab formula, <= 1e-12 of the
+ * exact ones).  *overflow (device int, caller-zeroed) is set if a bundle's
+ * footprint exceeded the kernel's window (then the result is incomplete).
+ * Replaces the reference's P^T P of multilevel.py:125-130. */
+int wmg_leaf_gram(const wmg_geometry *g, int depth, const int *bands, double *gram,
+                  int *overflow, void *stream);
 
 #ifdef __cplusplus
 }

@@ -67,6 +67,7 @@ _SIGS = {
     "wmg_haar_restrict": (_i, [_i, _dp, _i, _dp, _vp]),
     "wmg_haar_prolong": (_i, [_i, _dp, _i, _dp, _i, _vp]),
     "wmg_leaf_factor": (_i, [_vp, _i, ctypes.POINTER(_i), _ll, _ll, _dp, _vp]),
+    "wmg_leaf_gram": (_i, [_vp, _i, ctypes.POINTER(_i), _dp, _dp, _vp]),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -55,6 +55,7 @@ cudaError_t batched_gemv(int, int, const double*, long long, const double*, long
 cudaError_t haar_prolong(int, const double*, int, double*, int, cudaStream_t);
 cudaError_t leaf_factor(const GeomDev&, int, const int*, long long, long long, double*,
                         cudaStream_t);
+cudaError_t leaf_gram(const GeomDev&, int, const int*, double*, int*, cudaStream_t);
 bool tma_window_fits(const AngleParams*, int, int, int);
 }  // namespace wmg
 
@@ -427,6 +428,18 @@ int wmg_leaf_factor(const wmg_geometry* g, int depth, const int* bands, long lon
     if (bands[i] < 0 || bands[i] > 3) return fail(WMG_EINVAL, "bad band");
   if (nrays == 0) return WMG_OK;
   return cuda_rc(wmg::leaf_factor(g->dev, depth, bands, ray0, nrays, P, STREAM(stream)));
+}
+
+int wmg_leaf_gram(const wmg_geometry* g, int depth, const int* bands, double* gram,
+                  int* overflow, void* stream) {
+  REQ(g && bands && gram && overflow);
+  if (depth < 1 || depth > 12) return fail(WMG_EINVAL, "bad depth");
+  if ((g->dev.n >> depth) << depth != g->dev.n)
+    return fail(WMG_EINVAL, "n is not divisible by 2^depth");
+  for (int i = 0; i < depth; ++i)
+    if (bands[i] < 0 || bands[i] > 3) return fail(WMG_EINVAL, "bad band");
+  if (g->dev.m == 0 || g->dev.d == 0) return WMG_OK;
+  return cuda_rc(wmg::leaf_gram(g->dev, depth, bands, gram, overflow, STREAM(stream)));
 }
 
 }  // extern "C"

@@ -214,9 +214,13 @@ def _leaf_paths(levels):
     return paths
 
 
-def _assemble_leaf_grams(w, n, lam, levels, ray_chunk=None, paths=None):
-    """Dense Gram P_L^T P_L + lam I for every leaf (or the given band paths of
-    depth levels-1), batched in HBM."""
+def _assemble_leaf_grams(w, n, lam, levels, ray_chunk=None, paths=None, method="sparse"):
+    """Gram P_L^T P_L + lam I for every leaf (or the given band paths of depth
+    levels-1), batched in HBM.
+
+    method "sparse": ``wmg_leaf_gram`` accumulates the lower triangle per ray
+    bundle without forming P_L (fp64 slab weights, <= 1e-12 of the exact
+    ones); "dense": exact P_L slabs from the parity walker + DGEMM."""
     t = D.torch()
     depth = levels - 1
     side_c = n >> depth
@@ -224,6 +228,24 @@ def _assemble_leaf_grams(w, n, lam, levels, ray_chunk=None, paths=None):
     M = w.shape[0]
     paths = _leaf_paths(levels) if paths is None else [tuple(q) for q in paths]
     grams = t.zeros((len(paths), p, p), dtype=t.float64, device=w.device)
+    if method == "sparse":
+        overflow = t.zeros(1, dtype=t.int32, device=w.device)
+        for li, path in enumerate(paths):
+            bands = (N.ctypes.c_int * depth)(*[BAND_CODE[b] for b in path])
+            g = grams[li]
+            N.call("wmg_leaf_gram", w.handle, depth, bands, D.ptr(g), D.ptr(overflow),
+                   D.stream_handle())
+            low = g.tril()
+            g.copy_(low)
+            g.add_(low.tril(-1).T)
+            del low
+            if lam != 0:
+                g.diagonal().add_(lam)
+        if int(overflow.item()):
+            raise RuntimeError("wmg_leaf_gram: ray-bundle window overflow")
+        return paths, grams
+    if method != "dense":
+        raise ValueError(f"unknown Gram method '{method}'")
     if ray_chunk is None:
         # keep the factor slab around 1 GB
         ray_chunk = max(256, min(M, (1 << 30) // (8 * p)))
@@ -244,14 +266,16 @@ def _assemble_leaf_grams(w, n, lam, levels, ray_chunk=None, paths=None):
 
 
 def build_wmg_hierarchy(w, n: int, lam: float, levels: int, nu_pre: int = 0,
-                        nu_post: int = 0, node_mode: str = "fast") -> WmgHierarchy:
+                        nu_post: int = 0, node_mode: str = "fast",
+                        gram: str = "sparse") -> WmgHierarchy:
     """Recursive 4-way splitting of W (multilevel.py:151-166), matrix-free.
 
     ``node_mode``: projector of the internal node systems -- "fast" (float64
     fast kernels, <= 1e-12 relative, default), "fast32" (float32 arithmetic on
     float64 vectors, <= 1e-5 relative: a cheaper, slightly inexact V-cycle for
-    flexible outer solvers) or "parity".  Leaf Grams always come from the exact
-    (parity) weights.
+    flexible outer solvers) or "parity".  ``gram``: leaf Gram assembly --
+    "sparse" (per-ray-bundle accumulation, default) or "dense" (exact parity
+    P_L + DGEMM, O(M p^2) per leaf).
     """
     if levels < 2:
         raise ValueError("levels must be >= 2")
@@ -266,7 +290,7 @@ def build_wmg_hierarchy(w, n: int, lam: float, levels: int, nu_pre: int = 0,
     if not hasattr(w, "handle"):
         raise TypeError("build_wmg_hierarchy needs a LineProjector (build_projector)")
     t = D.require_cuda()
-    paths, grams = _assemble_leaf_grams(w, n, lam, levels)
+    paths, grams = _assemble_leaf_grams(w, n, lam, levels, method=gram)
     n_leaf, p = grams.shape[0], grams.shape[-1]
     # keep the Cholesky factors (API: coarse_solve.lower) only when they are
     # small; the V-cycle itself only needs the inverses

@@ -219,3 +219,34 @@ def test_classical_tg_accelerates_bicgstab(gpu, golden):
     assert tgr.status == "converged" and abs(len(tgr.rel_residual) - len(ref)) <= 0.25 * len(ref)
     with pytest.raises(ValueError):
         classical_tg_preconditioner(w, 16, 0.0, smoother_steps=(-1, 1))
+
+
+@pytest.mark.parametrize("case,levels", [("w16", 2), ("w16", 3), ("w40", 2), ("bench160", 3),
+                                         ("cfg0", 4)])
+def test_sparse_leaf_gram_matches_dense(gpu, golden, case, levels):
+    """wmg_leaf_gram (ray-bundle accumulation, fp64 slab weights) == the exact
+    parity P_L^T P_L (DGEMM) to 1e-12 of the largest entry, for every leaf."""
+    from paper_1310_0956_b200.multilevel import _assemble_leaf_grams
+    w = _w(golden, case)
+    n = w.n
+    paths, gs = _assemble_leaf_grams(w, n, 0.5, levels, method="sparse")
+    _, gd = _assemble_leaf_grams(w, n, 0.5, levels, method="dense")
+    assert gs.shape == gd.shape
+    err = (gs - gd).abs().amax(dim=(1, 2))
+    scale = gd.abs().amax(dim=(1, 2))
+    assert bool((err <= 1e-12 * scale).all()), (err / scale).max().item()
+
+
+def test_sparse_leaf_gram_axis_and_sizes(gpu):
+    """Axis-aligned and 45-degree angles, odd detector counts, rays missing the
+    grid; levels up to the 4x4 coarse limit."""
+    from paper_1310_0956_b200 import Geometry, build_projector
+    from paper_1310_0956_b200.multilevel import _assemble_leaf_grams
+    angles = np.sort(np.array([0.0, np.pi / 4, np.pi / 2, 0.3, 2.0, 3 * np.pi / 4]))
+    for n, d in ((32, 47), (64, 91), (64, 30)):
+        w = build_projector(Geometry(n, d, angles.size, angles=angles))
+        for levels in (2, 3, 4):
+            _, gs = _assemble_leaf_grams(w, n, 0.0, levels, method="sparse")
+            _, gd = _assemble_leaf_grams(w, n, 0.0, levels, method="dense")
+            err = (gs - gd).abs().max().item()
+            assert err <= 1e-12 * max(1.0, gd.abs().max().item()), (n, d, levels, err)
