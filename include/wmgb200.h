@@ -53,6 +53,9 @@ extern "C" {
 /* projector modes */
 #define WMG_MODE_PARITY 0 /* float64, bit-exact reference weights and sum order */
 #define WMG_MODE_FAST 1   /* fixed-point geometry, any summation order */
+/* ray kernels (geometry.py:178-185) */
+#define WMG_KERNEL_LINE 0   /* exact intersection lengths (default) */
+#define WMG_KERNEL_JOSEPH 1 /* two-pixel interpolation per slab; PARITY mode only */
 /* dtypes / precisions */
 #define WMG_F32 0
 #define WMG_F64 1
@@ -84,6 +87,12 @@ int wmg_geometry_shape(const wmg_geometry *g, long long *n_rows, long long *n_co
  * size (testing), 4 forces it with the experimental TMA-staged forward, -1 only
  * queries; *enabled receives the state. */
 int wmg_geometry_symmetry(wmg_geometry *g, int set, int *enabled);
+/* Ray kernel of the geometry's system matrix: set = WMG_KERNEL_LINE or
+ * WMG_KERNEL_JOSEPH (build_projector(g, kernel=...), geometry.py:178-185), -1
+ * only queries.  Joseph geometries support the PARITY projector pair, CSR
+ * export, row/column sums and wmg_leaf_factor; the FAST kernels and
+ * wmg_leaf_gram return WMG_EINVAL for them. */
+int wmg_geometry_kernel(wmg_geometry *g, int set, int *kernel);
 
 /* bytes of caller workspace wmg_forward (mode FAST) needs: zero-padded image
  * copies in both orientations for fp32 arithmetic, a transposed copy otherwise */

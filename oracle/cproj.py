@@ -49,6 +49,8 @@ def lib():
         L.orc_reduceat_segment.argtypes = [_dp, ctypes.c_int64]
         L.orc_set_threads.restype = ctypes.c_int
         L.orc_set_threads.argtypes = [ctypes.c_int]
+        L.orc_set_kernel.restype = ctypes.c_int
+        L.orc_set_kernel.argtypes = [ctypes.c_int]
         L.orc_num_threads.restype = ctypes.c_int
         L.orc_num_threads.argtypes = []
         _lib = L
@@ -85,8 +87,20 @@ def num_threads() -> int:
     return int(lib().orc_num_threads())
 
 
-def build_csr(n, d, angles, return_dups=False):
-    """The reference W (CSR, float64, int64 indices) for an arbitrary angle list."""
+KERNELS = {"line": 0, "joseph": 1}
+
+
+def build_csr(n, d, angles, return_dups=False, kernel="line"):
+    """The reference W (CSR, float64, int64 indices) for an arbitrary angle list
+    (``kernel``: "line" = geometry.py:88-128, "joseph" = geometry.py:131-175)."""
+    lib().orc_set_kernel(KERNELS[kernel])
+    try:
+        return _build_csr(n, d, angles, return_dups)
+    finally:
+        lib().orc_set_kernel(0)
+
+
+def _build_csr(n, d, angles, return_dups):
     c, s = snapped_trig(angles)
     m = c.size
     counts = np.zeros(m * d, dtype=np.int64)

@@ -183,6 +183,57 @@ static int64_t ray_entries(int n, int d, double c, double s, int j,
     return out;
 }
 
+/*
+ * Entries of ray j under the Joseph kernel (geometry.py:131-175): per slab k of
+ * the dominant axis, cont = (o/q - ctr_k * (p/q)) + (n-1)/2, i0 = floor(cont),
+ * w1 = cont - i0; pixels (i0, 1 - w1) and (i0 + 1, w1) inside the grid with a
+ * positive weight, value = weight * (1/|q|).  Sorted by column (no duplicates
+ * can occur within a ray).
+ */
+static int64_t joseph_entries(int n, int d, double c, double s, int j, entry_t *e,
+                              int64_t *cols, double *vals)
+{
+    const double off = ((double)j - (d - 1) / 2.0) * 1.0;
+    const double hc = (n - 1) / 2.0;
+    const int ydom = fabs(c) >= fabs(s);
+    const double q = ydom ? c : s, p = ydom ? s : c;
+    const double t1 = off / q, r = p / q, scale = 1.0 / fabs(q);
+    int64_t ne = 0;
+    for (int k = 0; k < n; ++k) {
+        const double ctr = ((double)k - hc) * 1.0;
+        const double cont = (t1 - ctr * r) + hc;
+        const double f = floor(cont);
+        const int64_t i0 = (int64_t)f;
+        const double w1 = cont - f;
+        for (int t = 0; t < 2; ++t) {
+            const int64_t idx = i0 + t;
+            const double w = t ? w1 : 1.0 - w1;
+            if (idx < 0 || idx >= n || !(w > 0.0)) continue;
+            e[ne].col = ydom ? (int64_t)(n - 1 - k) * n + idx : (int64_t)(n - 1 - idx) * n + k;
+            e[ne].val = w * scale;
+            e[ne].order = ne;
+            ++ne;
+        }
+    }
+    qsort(e, (size_t)ne, sizeof(entry_t), cmp_entry);
+    for (int64_t i = 0; i < ne; ++i) {
+        cols[i] = e[i].col;
+        vals[i] = e[i].val;
+    }
+    return ne;
+}
+
+/* ray kernel of the oracle's entry points: 0 line (default), 1 Joseph */
+static int g_kernel = 0;
+int orc_set_kernel(int k) { g_kernel = k; return 0; }
+
+static int64_t entries(int n, int d, double c, double s, int j, double *t, entry_t *e,
+                       int64_t *cols, double *vals, int64_t *n_dup)
+{
+    if (g_kernel == 1) return joseph_entries(n, d, c, s, j, e, cols, vals);
+    return ray_entries(n, d, c, s, j, t, e, cols, vals, n_dup);
+}
+
 /* scratch for one thread */
 typedef struct {
     double *t;
@@ -270,7 +321,7 @@ static void job_counts(void *ctx, int64_t lo, int64_t hi, void *scr)
     int64_t dd = 0;
     for (int64_t ray = lo; ray < hi; ++ray) {
         const int a = (int)(ray / J->d), j = (int)(ray % J->d);
-        J->counts[ray] = ray_entries(J->n, J->d, J->cs[a], J->sn[a], j, sc->t, sc->e,
+        J->counts[ray] = entries(J->n, J->d, J->cs[a], J->sn[a], j, sc->t, sc->e,
                                      sc->cols, sc->vals, &dd);
     }
     pthread_mutex_lock(&J->mu);
@@ -284,7 +335,7 @@ static void job_fill(void *ctx, int64_t lo, int64_t hi, void *scr)
     scratch_t *sc = (scratch_t *)scr;
     for (int64_t ray = lo; ray < hi; ++ray) {
         const int a = (int)(ray / J->d), j = (int)(ray % J->d);
-        const int64_t k = ray_entries(J->n, J->d, J->cs[a], J->sn[a], j, sc->t, sc->e,
+        const int64_t k = entries(J->n, J->d, J->cs[a], J->sn[a], j, sc->t, sc->e,
                                       sc->cols, sc->vals, NULL);
         memcpy(J->indices + J->indptr[ray], sc->cols, sizeof(int64_t) * (size_t)k);
         memcpy(J->data + J->indptr[ray], sc->vals, sizeof(double) * (size_t)k);
@@ -297,7 +348,7 @@ static void job_forward(void *ctx, int64_t lo, int64_t hi, void *scr)
     scratch_t *sc = (scratch_t *)scr;
     for (int64_t ray = lo; ray < hi; ++ray) {
         const int a = (int)(ray / J->d), j = (int)(ray % J->d);
-        const int64_t k = ray_entries(J->n, J->d, J->cs[a], J->sn[a], j, sc->t, sc->e,
+        const int64_t k = entries(J->n, J->d, J->cs[a], J->sn[a], j, sc->t, sc->e,
                                       sc->cols, sc->vals, NULL);
         double acc = 0.0;
         for (int64_t i = 0; i < k; ++i) acc += sc->vals[i] * J->x[sc->cols[i]];
@@ -352,7 +403,7 @@ int orc_backward(int n, int d, int m, const double *cs, const double *sn,
     for (int64_t p = 0; p < (int64_t)n * n; ++p) x[p] = 0.0;
     for (int64_t ray = 0; ray < (int64_t)m * d; ++ray) {
         const int a = (int)(ray / d), j = (int)(ray % d);
-        const int64_t k = ray_entries(n, d, cs[a], sn[a], j, sc.t, sc.e, sc.cols,
+        const int64_t k = entries(n, d, cs[a], sn[a], j, sc.t, sc.e, sc.cols,
                                       sc.vals, NULL);
         for (int64_t i = 0; i < k; ++i) x[sc.cols[i]] += sc.vals[i] * y[ray];
     }

@@ -20,6 +20,7 @@ CSRC = os.path.join(_PKG, "csrc")
 WMG_OK, WMG_EINVAL, WMG_EDIM, WMG_ENOTSPD, WMG_ECUDA = range(5)
 MODE_PARITY, MODE_FAST = 0, 1
 F32, F64 = 0, 1
+KERNEL_LINE, KERNEL_JOSEPH = 0, 1
 RED_DOT, RED_SQDIFF, RED_SUM, RED_DOTDIFF, RED_SQ = range(5)
 
 _lib = None
@@ -38,6 +39,7 @@ _SIGS = {
     "wmg_geometry_destroy": (_i, [_vp]),
     "wmg_geometry_shape": (_i, [_vp, ctypes.POINTER(_ll), ctypes.POINTER(_ll)]),
     "wmg_geometry_symmetry": (_i, [_vp, _i, ctypes.POINTER(_i)]),
+    "wmg_geometry_kernel": (_i, [_vp, _i, ctypes.POINTER(_i)]),
     "wmg_forward_workspace": (_i, [_vp, _i, _i, ctypes.POINTER(ctypes.c_size_t)]),
     "wmg_forward": (_i, [_vp, _i, _i, _i, _i, _dp, _dp, _dp, _dp, _vp]),
     "wmg_backward": (_i, [_vp, _i, _i, _i, _i, _dp, _dp, _i, _dp, _vp]),

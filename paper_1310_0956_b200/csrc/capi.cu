@@ -190,6 +190,7 @@ int wmg_geometry_create(int n, int n_detectors, int n_angles, const double* cos_
   g->dev.rowmap = nullptr;
   g->dev.sym = sym ? 1 : 0;
   g->dev.tma_ok = (sym && wmg::tma_window_fits(P.data(), n, n_detectors, n_angles)) ? 1 : 0;
+  g->dev.joseph = 0;
   g->sym_capable = sym ? 1 : 0;
   g->axis = g->dev;
   g->axis.m = 2;
@@ -197,6 +198,7 @@ int wmg_geometry_create(int n, int n_detectors, int n_angles, const double* cos_
   g->axis.rowmap = g->d_rowmap;
   g->axis.sym = 0;
   g->axis.tma_ok = 0;
+  g->axis.joseph = 0;
   *out = g;
   return WMG_OK;
 }
@@ -214,6 +216,18 @@ int wmg_geometry_symmetry(wmg_geometry* g, int set, int* enabled) {
   if (!g) return fail(WMG_EINVAL, "geometry is NULL");
   if (set == 0 || set == 1 || set == 2 || set == 4) g->dev.sym = (set && g->sym_capable) ? set : 0;
   if (enabled) *enabled = g->dev.sym;
+  return WMG_OK;
+}
+
+int wmg_geometry_kernel(wmg_geometry* g, int set, int* kernel) {
+  if (!g) return fail(WMG_EINVAL, "geometry is NULL");
+  if (set == WMG_KERNEL_LINE || set == WMG_KERNEL_JOSEPH) {
+    g->dev.joseph = (set == WMG_KERNEL_JOSEPH);
+    g->axis.joseph = g->dev.joseph;
+  } else if (set >= 0) {
+    return fail(WMG_EINVAL, "unknown ray kernel");
+  }
+  if (kernel) *kernel = g->dev.joseph ? WMG_KERNEL_JOSEPH : WMG_KERNEL_LINE;
   return WMG_OK;
 }
 
@@ -253,6 +267,7 @@ int wmg_forward(const wmg_geometry* g, int mode, int precision, int dtype_in, in
   if (mode == WMG_MODE_PARITY)
     return cuda_rc(wmg::parity_forward(g->dev, (const double*)x, (double*)y, anomaly,
                                        STREAM(stream)));
+  if (g->dev.joseph) return fail(WMG_EINVAL, "the Joseph kernel has parity (float64) mode only");
   if (!workspace) return fail(WMG_EINVAL, "fast forward needs a workspace");
   return cuda_rc(wmg::fast_forward(g->dev, precision, dtype_in, dtype_out, x, workspace, y,
                                    STREAM(stream), g->dev.sym ? &g->axis : nullptr));
@@ -267,6 +282,7 @@ int wmg_backward(const wmg_geometry* g, int mode, int precision, int dtype_in, i
     return cuda_rc(wmg::parity_backward(g->dev, (const double*)y, (double*)x, accumulate != 0,
                                         anomaly, STREAM(stream)));
   if (!y) return fail(WMG_EINVAL, "y is NULL");
+  if (g->dev.joseph) return fail(WMG_EINVAL, "the Joseph kernel has parity (float64) mode only");
   return cuda_rc(wmg::fast_backward(g->dev, precision, dtype_in, dtype_out, y, x,
                                     accumulate != 0, STREAM(stream),
                                     g->dev.sym ? &g->axis : nullptr));
@@ -438,6 +454,7 @@ int wmg_leaf_gram(const wmg_geometry* g, int depth, const int* bands, double* gr
     return fail(WMG_EINVAL, "n is not divisible by 2^depth");
   for (int i = 0; i < depth; ++i)
     if (bands[i] < 0 || bands[i] > 3) return fail(WMG_EINVAL, "bad band");
+  if (g->dev.joseph) return fail(WMG_EINVAL, "the sparse leaf Gram implements line weights only");
   if (g->dev.m == 0 || g->dev.d == 0) return WMG_OK;
   return cuda_rc(wmg::leaf_gram(g->dev, depth, bands, gram, overflow, STREAM(stream)));
 }

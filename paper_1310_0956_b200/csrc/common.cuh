@@ -50,6 +50,7 @@ struct GeomDev {
   int sym;            // 1: angle set symmetric under theta -> pi - theta (fast kernels
                       //    may share weights across mirror images), n % 64 == 0
   int tma_ok;         // 1: the TMA-staged forward's window bound holds for every group
+  int joseph;         // 1: Joseph interpolation weights (parity kernels only)
 };
 
 // Fixed-point minor coordinate used by the fast kernels: 64-bit signed with

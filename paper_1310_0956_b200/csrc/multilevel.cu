@@ -11,7 +11,7 @@
 // value the path prolongation R_path^T e_q takes at f (one +-0.4999999999999999
 // factor per level, rounded in prolongation order, as haar_prolong computes).
 // The Gram is then one float64 GEMM P_L^T P_L on the GPU.
-#include "parity_walker.cuh"
+#include "joseph_walker.cuh"
 
 namespace wmg {
 namespace ml {
@@ -31,6 +31,7 @@ struct LeafPath {
 
 // P (rays x p, row-major, zero-initialised by the caller) for ray range
 // [ray0, ray0 + nrays)
+template <typename Walker>
 __global__ void leaf_factor_kernel(GeomDev G, LeafPath path, long long ray0, long long nrays,
                                    double* __restrict__ P) {
   const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -41,7 +42,7 @@ __global__ void leaf_factor_kernel(GeomDev G, LeafPath path, long long ray0, lon
   const int k = path.depth;
   const int side_c = n >> k;
   const long long pdim = (long long)side_c * side_c;
-  parity::RayWalker wk;
+  Walker wk;
   wk.init(n, G.d, G.ang[a].c, G.ang[a].s, j);
   long long flat;
   double w;
@@ -227,8 +228,11 @@ cudaError_t leaf_factor(const GeomDev& G, int depth, const int* bands, long long
   path.depth = depth;
   for (int i = 0; i < 12; ++i) path.bands[i] = i < depth ? bands[i] : 0;
   const int tpb = 128;
-  ml::leaf_factor_kernel<<<(unsigned)((nrays + tpb - 1) / tpb), tpb, 0, st>>>(G, path, ray0,
-                                                                              nrays, P);
+  const unsigned grid = (unsigned)((nrays + tpb - 1) / tpb);
+  if (G.joseph)
+    ml::leaf_factor_kernel<parity::JosephWalker><<<grid, tpb, 0, st>>>(G, path, ray0, nrays, P);
+  else
+    ml::leaf_factor_kernel<parity::RayWalker><<<grid, tpb, 0, st>>>(G, path, ray0, nrays, P);
   return cudaGetLastError();
 }
 

@@ -21,18 +21,19 @@
 // detectors ascending).  A segment whose midpoint falls outside the slab the
 // walk expects (possible only for segments of length ~1e-12 near a grid corner)
 // is counted in a device "anomaly" counter; the parity tests require zero.
-#include "parity_walker.cuh"
+#include "joseph_walker.cuh"
 
 namespace wmg {
 namespace parity {
 
+template <typename Walker>
 __global__ void fwd_kernel(GeomDev G, const double* __restrict__ x, double* __restrict__ y,
                            int* __restrict__ anomaly) {
   const long long ray = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (ray >= (long long)G.m * G.d) return;
   const int a = (int)(ray / G.d), j = (int)(ray % G.d);
   const AngleParams P = G.ang[a];
-  RayWalker wk;
+  Walker wk;
   wk.init(G.n, G.d, P.c, P.s, j);
   double acc = 0.0;
   long long flat;
@@ -43,6 +44,7 @@ __global__ void fwd_kernel(GeomDev G, const double* __restrict__ x, double* __re
 }
 
 // CSR export: counts (pass 0) then fill at indptr (pass 1)
+template <typename Walker>
 __global__ void csr_kernel(GeomDev G, int pass, long long* __restrict__ counts,
                            const long long* __restrict__ indptr, long long* __restrict__ cols,
                            double* __restrict__ vals, int* __restrict__ anomaly) {
@@ -50,7 +52,7 @@ __global__ void csr_kernel(GeomDev G, int pass, long long* __restrict__ counts,
   if (ray >= (long long)G.m * G.d) return;
   const int a = (int)(ray / G.d), j = (int)(ray % G.d);
   const AngleParams P = G.ang[a];
-  RayWalker wk;
+  Walker wk;
   wk.init(G.n, G.d, P.c, P.s, j);
   long long flat, cnt = 0;
   double w;
@@ -69,7 +71,8 @@ __global__ void csr_kernel(GeomDev G, int pass, long long* __restrict__ counts,
 }
 
 // numpy pairwise sum pulled from the walker (loops_utils.h.src, block 128)
-__device__ __forceinline__ double pull(RayWalker& wk) {
+template <typename Walker>
+__device__ __forceinline__ double pull(Walker& wk) {
   long long f;
   double w = 0.0;
   wk.next(f, w);
@@ -77,7 +80,8 @@ __device__ __forceinline__ double pull(RayWalker& wk) {
 }
 
 // one leaf block of numpy's pairwise sum (n <= 128)
-__device__ double pairwise_leaf(RayWalker& wk, long long n) {
+template <typename Walker>
+__device__ double pairwise_leaf(Walker& wk, long long n) {
   if (n < 8) {
     double r = -0.0;
     for (long long i = 0; i < n; ++i) r = dadd(r, pull(wk));
@@ -100,7 +104,8 @@ __device__ double pairwise_leaf(RayWalker& wk, long long n) {
 // numpy pairwise sum of the next n walker entries, evaluated with an explicit
 // post-order task stack (no device recursion): split n -> (h, n - h) with
 // h = n/2 - (n/2) % 8 until n <= 128, then lhs + rhs.
-__device__ double pairwise_pull(RayWalker& wk, long long n) {
+template <typename Walker>
+__device__ double pairwise_pull(Walker& wk, long long n) {
   long long task[48];      // >= 0: evaluate a node of that size; -1: combine
   double val[24];
   int nt = 0, nv = 0;
@@ -124,12 +129,13 @@ __device__ double pairwise_pull(RayWalker& wk, long long n) {
   return val[0];
 }
 
+template <typename Walker>
 __global__ void rowsum_kernel(GeomDev G, double* __restrict__ out) {
   const long long ray = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (ray >= (long long)G.m * G.d) return;
   const int a = (int)(ray / G.d), j = (int)(ray % G.d);
   const AngleParams P = G.ang[a];
-  RayWalker wk;
+  Walker wk;
   wk.init(G.n, G.d, P.c, P.s, j);
   long long flat, cnt = 0;
   double w;
@@ -202,6 +208,35 @@ __global__ void bwd_kernel(GeomDev G, const double* __restrict__ y, double* __re
   if (anomalies && anomaly) atomicAdd(anomaly, anomalies);
 }
 
+// Joseph backprojection, pixel-driven: per angle the (at most ~3) rays whose
+// interpolation pair covers the pixel, ascending ray index (csc order); each
+// weight is re-derived exactly as JosephWalker emits it.
+template <bool kAccumulate>
+__global__ void jbwd_kernel(GeomDev G, const double* __restrict__ y, double* __restrict__ x) {
+  const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const int n = G.n;
+  if (p >= (long long)n * n) return;
+  const int row = (int)(p / n), col = (int)(p % n);
+  double acc = kAccumulate ? x[p] : 0.0;
+  for (int a = 0; a < G.m; ++a) {
+    JosephAngle ja;
+    ja.init(n, G.d, G.ang[a].c, G.ang[a].s);
+    const int kk = ja.ydom ? n - 1 - row : col;
+    const int idx = ja.ydom ? col : n - 1 - row;
+    // cont(j) ~ idx + 1/2 at the centre of the pixel's support
+    const double ctr = (double)kk - ja.hc;
+    const double oest = ((double)idx + 0.5 - ja.hc + ctr * ja.r) * ja.q;
+    const int jc = (int)floor(oest + ja.dc + 0.5);
+    const int j0 = max(jc - 3, 0), j1 = min(jc + 3, G.d - 1);
+    const long long rowbase = (long long)a * G.d;
+    for (int j = j0; j <= j1; ++j) {
+      const double w = ja.weight(j, kk, idx);
+      if (w > 0.0) acc = dadd(acc, y ? dmul(w, __ldg(y + rowbase + j)) : w);
+    }
+  }
+  x[p] = acc;
+}
+
 }  // namespace parity
 
 // ---------------------------------------------------------------------------
@@ -212,7 +247,11 @@ cudaError_t parity_forward(const GeomDev& G, const double* x, double* y, int* an
   const long long rays = (long long)G.m * G.d;
   if (rays == 0) return cudaSuccess;
   const int tpb = 128;
-  parity::fwd_kernel<<<(unsigned)((rays + tpb - 1) / tpb), tpb, 0, st>>>(G, x, y, anomaly);
+  const unsigned grid = (unsigned)((rays + tpb - 1) / tpb);
+  if (G.joseph)
+    parity::fwd_kernel<parity::JosephWalker><<<grid, tpb, 0, st>>>(G, x, y, anomaly);
+  else
+    parity::fwd_kernel<parity::RayWalker><<<grid, tpb, 0, st>>>(G, x, y, anomaly);
   return cudaGetLastError();
 }
 
@@ -222,6 +261,13 @@ cudaError_t parity_backward(const GeomDev& G, const double* y, double* x, bool a
   if (pix == 0) return cudaSuccess;
   const int tpb = 128;
   const unsigned grid = (unsigned)((pix + tpb - 1) / tpb);
+  if (G.joseph) {
+    if (accumulate)
+      parity::jbwd_kernel<true><<<grid, tpb, 0, st>>>(G, y, x);
+    else
+      parity::jbwd_kernel<false><<<grid, tpb, 0, st>>>(G, y, x);
+    return cudaGetLastError();
+  }
   if (accumulate)
     parity::bwd_kernel<true><<<grid, tpb, 0, st>>>(G, y, x, anomaly);
   else
@@ -233,7 +279,11 @@ cudaError_t parity_row_sums(const GeomDev& G, double* out, cudaStream_t st) {
   const long long rays = (long long)G.m * G.d;
   if (rays == 0) return cudaSuccess;
   const int tpb = 64;
-  parity::rowsum_kernel<<<(unsigned)((rays + tpb - 1) / tpb), tpb, 0, st>>>(G, out);
+  const unsigned grid = (unsigned)((rays + tpb - 1) / tpb);
+  if (G.joseph)
+    parity::rowsum_kernel<parity::JosephWalker><<<grid, tpb, 0, st>>>(G, out);
+  else
+    parity::rowsum_kernel<parity::RayWalker><<<grid, tpb, 0, st>>>(G, out);
   return cudaGetLastError();
 }
 
@@ -242,8 +292,13 @@ cudaError_t parity_csr(const GeomDev& G, int pass, long long* counts, const long
   const long long rays = (long long)G.m * G.d;
   if (rays == 0) return cudaSuccess;
   const int tpb = 128;
-  parity::csr_kernel<<<(unsigned)((rays + tpb - 1) / tpb), tpb, 0, st>>>(G, pass, counts, indptr,
-                                                                        cols, vals, anomaly);
+  const unsigned grid = (unsigned)((rays + tpb - 1) / tpb);
+  if (G.joseph)
+    parity::csr_kernel<parity::JosephWalker><<<grid, tpb, 0, st>>>(G, pass, counts, indptr, cols,
+                                                                   vals, anomaly);
+  else
+    parity::csr_kernel<parity::RayWalker><<<grid, tpb, 0, st>>>(G, pass, counts, indptr, cols,
+                                                                vals, anomaly);
   return cudaGetLastError();
 }
 

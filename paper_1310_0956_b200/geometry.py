@@ -125,8 +125,9 @@ class LineProjector:
     format = "matrix-free"
 
     def __init__(self, g: Geometry, precision: str = "float64", mode: str | None = None,
-                 device=None):
+                 device=None, kernel: str = "line"):
         t = D.require_cuda()
+        self.kernel = kernel
         if precision not in _PRECISIONS:
             raise ValueError(f"unknown precision '{precision}'")
         self.geometry = g
@@ -155,6 +156,8 @@ class LineProjector:
                    s.ctypes.data_as(N.ctypes.POINTER(N.ctypes.c_double)),
                    N.ctypes.byref(handle))
         self._h = handle
+        if kernel == "joseph":
+            N.call("wmg_geometry_kernel", handle, N.KERNEL_JOSEPH, None)
         self._ws = {}
         self._anomaly = t.zeros(1, dtype=t.int32, device=self.device)
         self._sums = {}
@@ -380,13 +383,14 @@ class _Transposed:
 
 def build_projector(g: Geometry, kernel: str = "line", precision: str = "float64",
                     mode: str | None = None, device=None) -> LineProjector:
-    """Matrix-free projector with the reference's line-intersection weights."""
-    if kernel == "joseph":
-        raise NotImplementedError(
-            "kernel='joseph' is outside the B200 hot path (SURVEY.md s8(f) row f4)")
-    if kernel != "line":
+    """Matrix-free projector (geometry.py:178-197): ``kernel="line"`` (exact
+    intersection lengths, every mode) or ``"joseph"`` (two-pixel interpolation
+    per slab, geometry.py:131-175; float64 parity mode only)."""
+    if kernel not in ("line", "joseph"):
         raise ValueError(f"unknown kernel '{kernel}'")
-    return LineProjector(g, precision=precision, mode=mode, device=device)
+    if kernel == "joseph" and (precision != "float64" or mode not in (None, "parity")):
+        raise ValueError("kernel='joseph' is implemented in float64 parity mode only")
+    return LineProjector(g, precision=precision, mode=mode, device=device, kernel=kernel)
 
 
 def apply(w, x):

@@ -290,6 +290,10 @@ def build_wmg_hierarchy(w, n: int, lam: float, levels: int, nu_pre: int = 0,
     if not hasattr(w, "handle"):
         raise TypeError("build_wmg_hierarchy needs a LineProjector (build_projector)")
     t = D.require_cuda()
+    if getattr(w, "kernel", "line") == "joseph":
+        # Joseph weights exist in parity mode only: exact leaf factors + DGEMM
+        # and the parity projector for the node systems
+        gram, node_mode = "dense", "parity"
     paths, grams = _assemble_leaf_grams(w, n, lam, levels, method=gram)
     n_leaf, p = grams.shape[0], grams.shape[-1]
     # keep the Cholesky factors (API: coarse_solve.lower) only when they are
@@ -590,7 +594,9 @@ class ClassicalTGPreconditioner(_GraphedOperator):
         self.nu1, self.nu2 = int(nu1), int(nu2)
         sc = sirt_scaling(w)
         self.c, self.r = sc.c_dev, sc.r_dev
-        _, grams = _assemble_leaf_grams(w, n, lam, 2, paths=[("LL",)])
+        _, grams = _assemble_leaf_grams(
+            w, n, lam, 2, paths=[("LL",)],
+            method="dense" if getattr(w, "kernel", "line") == "joseph" else "sparse")
         low, info = t.linalg.cholesky_ex(grams)
         if int(info.max()) > 0:
             raise NotPositiveDefiniteError(

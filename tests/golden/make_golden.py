@@ -12,7 +12,10 @@ What is frozen (all from ``wmgtomo`` itself):
               fixtures, configs 0/1 and exact angle subsets of config 3;
   solvers     sirt_solve trajectories (x and residual history), the normal
               operator, bicgstab_solve (plain and WMG-preconditioned) histories;
-  multilevel  wtg_apply results (hybrid / multiplicative, 2 and 3 levels).
+  multilevel  wtg_apply results (hybrid / multiplicative, 2 and 3 levels);
+  joseph      the same hashes for build_projector(kernel="joseph") (f4);
+  cli         sha256 of the reference CLI's output files (phantom, project
+              with/without noise, SIRT reconstructions) and residual logs (f3).
 """
 from __future__ import annotations
 
@@ -44,11 +47,13 @@ def main():
     meta = {"reference_version": wmgtomo.__version__, "projector": {}, "solvers": {}}
     arrays = {}
 
-    def proj_case(name, n, d, m, subset=None, keep_vectors=True):
+    meta["joseph"] = {}
+
+    def proj_case(name, n, d, m, subset=None, keep_vectors=True, kernel="line"):
         g = build_geometry(n, d, m)
         if subset is not None:
             g = Geometry(n, d, len(subset), angles=g.angles[np.asarray(subset)])
-        w = build_projector(g)
+        w = build_projector(g, kernel=kernel)
         seed = zlib.crc32(name.encode())
         rs = np.random.default_rng(seed)
         x = rs.standard_normal(n * n)
@@ -57,7 +62,7 @@ def main():
         wty = w.T @ y
         rows = np.asarray(w.sum(axis=1)).ravel()
         cols = np.asarray(w.sum(axis=0)).ravel()
-        meta["projector"][name] = {
+        meta["projector" if kernel == "line" else "joseph"][name] = {
             "n": n, "d": d, "m": m, "subset": None if subset is None else list(map(int, subset)),
             "nnz": int(w.nnz), "seed": seed,
             "indptr": sha(w.indptr.astype(np.int64)), "indices": sha(w.indices.astype(np.int64)),
@@ -84,6 +89,58 @@ def main():
         sub = ([0, n // 8, n // 4 + 1, n // 2, 3 * n // 4 - 3, n - 1] if n <= 1024
                else [0, n // 4 + 1, n // 2, 3 * n // 4 - 3])
         proj_case(f"cfg3_{n}_sub", n, d, n, subset=sub, keep_vectors=False)
+
+    # ---- Joseph kernel ------------------------------------
+    for name, (n, d, m) in {"jos_tiny_vertical": (4, 4, 1), "jos_tiny_two": (4, 4, 2),
+                            "jos_diag8": (8, 11, 4), "jos_miss12": (4, 12, 1),
+                            "jos_odd15": (15, 21, 7), "jos_w16": (16, 24, 24),
+                            "jos_cfg0": (64, 91, 90)}.items():
+        proj_case(name, n, d, m, kernel="joseph")
+    proj_case("jos_cfg1", 256, 363, 180, keep_vectors=False, kernel="joseph")
+    proj_case("jos_bench160", 160, 160, 400, keep_vectors=False, kernel="joseph")
+
+    # ---- CLI: output files of the reference CLI ----------
+    import tempfile
+    from wmgtomo import cli as rcli
+    meta["cli"] = {}
+    with tempfile.TemporaryDirectory() as td:
+        def f(nm):
+            return os.path.join(td, nm)
+
+        def run(*argv):
+            rc = rcli.main([str(a) for a in argv])
+            assert rc == 0, argv
+
+        def file_sha(nm):
+            with open(f(nm), "rb") as fh:
+                return hashlib.sha256(fh.read()).hexdigest()
+
+        run("phantom", "--n", 16, "--out", f("ph.bin"))
+        run("project", "--image", f("ph.bin"), "--angles", 24, "--detectors", 24,
+            "--out", f("sino.bin"))
+        run("project", "--image", f("ph.bin"), "--angles", 24, "--detectors", 24,
+            "--noise", 0.01, "--seed", 5, "--out", f("sino_noisy.bin"))
+        run("reconstruct", "--sino", f("sino.bin"), "--n", 16, "--angles", 24,
+            "--detectors", 24, "--solver", "sirt", "--iters", 30, "--xexact", f("ph.bin"),
+            "--out", f("x_sirt.bin"), "--log", f("sirt.csv"))
+        run("reconstruct", "--sino", f("sino_noisy.bin"), "--n", 16, "--angles", 24,
+            "--detectors", 24, "--solver", "sirt", "--iters", 20, "--lambda", 0.25,
+            "--out", f("x_sirt_noisy.bin"), "--log", f("sirt_noisy.csv"))
+        run("reconstruct", "--sino", f("sino.bin"), "--n", 16, "--angles", 24,
+            "--detectors", 24, "--solver", "wmg-bicgstab", "--levels", 2, "--lambda", 1.0,
+            "--iters", 30, "--tol", 1e-10, "--xexact", f("ph.bin"), "--out", f("x_wmg.bin"),
+            "--log", f("wmg.csv"))
+        for nm in ("ph.bin", "sino.bin", "sino_noisy.bin", "x_sirt.bin", "x_sirt_noisy.bin"):
+            meta["cli"][nm] = file_sha(nm)
+        import csv as _csv
+        for nm in ("sirt.csv", "wmg.csv"):
+            with open(f(nm)) as fh:
+                rows = list(_csv.DictReader(fh))
+            arrays[f"cli_{nm[:-4]}_res"] = np.array([float(r["rel_res"]) for r in rows])
+            arrays[f"cli_{nm[:-4]}_err"] = np.array([float(r["rel_err_l2"]) for r in rows])
+        xw = np.frombuffer(open(f("x_wmg.bin"), "rb").read()[16:], dtype="<f8")
+        arrays["cli_wmg_x"] = xw.copy()
+    print("cli done", flush=True)
 
     # ---- solvers -------------------------------------------------------
     ph16 = shepp_logan(16)

@@ -112,3 +112,24 @@ def test_oracle_wtg_matches_reference(golden, oracle_proj, levels):
     for mult, key in ((False, "hyb"), (True, "mul")):
         got = oml.wtg_apply(root, r, mult)
         assert np.abs(got - g[f"wtg_w16_l{levels}_{key}"]).max() <= 1e-12
+
+
+JOSEPH = ["jos_tiny_vertical", "jos_tiny_two", "jos_diag8", "jos_miss12", "jos_odd15",
+          "jos_w16", "jos_cfg0", "jos_cfg1", "jos_bench160"]
+
+
+@pytest.mark.parametrize("name", JOSEPH)
+def test_oracle_joseph_csr_matches_reference(golden, oracle_proj, name):
+    """f4: the oracle's Joseph restatement reproduces the reference's
+    build_projector(kernel="joseph") CSR and both products bit for bit."""
+    meta, _ = golden
+    spec = meta["joseph"][name]
+    n, d, angles = case_geometry(spec)
+    w = oracle_proj.build_csr(n, d, angles, kernel="joseph")
+    assert w.nnz == spec["nnz"]
+    assert sha(w.indptr.astype(np.int64)) == spec["indptr"]
+    assert sha(w.indices.astype(np.int64)) == spec["indices"]
+    assert sha(w.data) == spec["data"]
+    x, y = case_vectors(spec, w.shape[0])
+    assert sha(oracle_proj.csr_matvec(w, x)) == spec["wx"]
+    assert sha(oracle_proj.csr_matvec(w.T.tocsr(), y)) == spec["wty"]   # csc_matvec order
