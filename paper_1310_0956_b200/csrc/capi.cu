@@ -214,7 +214,8 @@ int wmg_geometry_destroy(wmg_geometry* g) {
 
 int wmg_geometry_symmetry(wmg_geometry* g, int set, int* enabled) {
   if (!g) return fail(WMG_EINVAL, "geometry is NULL");
-  if (set == 0 || set == 1 || set == 2 || set == 4) g->dev.sym = (set && g->sym_capable) ? set : 0;
+  if (set == 0 || set == 1 || set == 2 || set == 4 || set == 10)
+    g->dev.sym = (set && g->sym_capable) ? set : 0;
   if (enabled) *enabled = g->dev.sym;
   return WMG_OK;
 }

@@ -536,7 +536,12 @@ __global__ void __launch_bounds__(128) bwd_v2_kernel(GeomDev G, const TIn* __res
 // lines is not mirror symmetric, so they run through bwd_v2 afterwards.
 constexpr int kSymChunk = 8;
 
-template <typename TIn, typename TOut, bool kAccumulate>
+// Warp layout: kWarp2D (default) gives each warp an 8-column x 4-row pixel block
+// per step, so its 32 lanes read a detector span of 7|c| + 3|s| < 8 float4 window
+// entries (mostly one 128-byte shared wavefront) instead of the 32|c| entries
+// (up to four wavefronts) a 32-column row needs; each thread keeps one column
+// and 4 rows spaced 8 apart.  !kWarp2D is the row layout (lane = column).
+template <typename TIn, typename TOut, bool kAccumulate, bool kWarp2D = true>
 __global__ void __launch_bounds__(256, 6) bwd_sym_kernel(GeomDev G, const TIn* __restrict__ sino,
                                                       TOut* __restrict__ img) {
   __shared__ float4 winA[kSymChunk][kBwdWin];   // (y_a[t], y_b[t], y_a[t+1], y_b[t+1])
@@ -553,6 +558,10 @@ __global__ void __launch_bounds__(256, 6) bwd_sym_kernel(GeomDev G, const TIn* _
   const double yc0 = half - (double)row0 - 0.5;
   const double bias = 1.0 / kQ32;
   const int half_m = m / 2;
+  // this thread's tile column and first row; its rows are trow + rstep * i
+  const int tcol = kWarp2D ? (warp & 3) * 8 + (lane & 7) : lane;
+  const int trow = kWarp2D ? (warp >> 2) * 4 + (lane >> 3) : 4 * warp;
+  constexpr int rstep = kWarp2D ? 8 : 1;
   float2 accA[4], accB[4];
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
@@ -599,7 +608,8 @@ __global__ void __launch_bounds__(256, 6) bwd_sym_kernel(GeomDev G, const TIn* _
       const AngleParams& A = G.ang[ang_s[aa]];
       const long long S = A.Sfix;
       const float ca0 = A.a0, icb = A.icb, hwic = A.hwic, w1c = A.w1c, L = A.Lf;
-      long long Q = qx[aa][lane] - (long long)(4 * warp) * S;
+      long long Q = qx[aa][tcol] - (long long)trow * S;
+      const long long SS = (long long)rstep * S;
       const float4* wa = winA[aa];
       const float4* wb = winB[aa];
 #pragma unroll
@@ -616,14 +626,14 @@ __global__ void __launch_bounds__(256, 6) bwd_sym_kernel(GeomDev G, const TIn* _
         accA[i] = __ffma2_rn(W1, make_float2(va.z, va.w), accA[i]);
         accB[i] = __ffma2_rn(W0, make_float2(vb.x, vb.y), accB[i]);
         accB[i] = __ffma2_rn(W1, make_float2(vb.z, vb.w), accB[i]);
-        Q -= S;
+        Q -= SS;
       }
     }
   }
-  const int col = col0 + lane;
+  const int col = col0 + tcol;
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    const int row = row0 + 4 * warp + i;
+    const int row = row0 + trow + rstep * i;
     const long long p1 = (long long)row * n + col;                       // (p, a)
     const long long p2 = (long long)row * n + (n - 1 - col);             // x-mirror, m-a
     const long long p3 = (long long)(n - 1 - row) * n + (n - 1 - col);   // rotation, a rev
@@ -965,7 +975,8 @@ cudaError_t tma_forward(const GeomDev& G, float* P, float* PT, TOut* sino, int* 
 // Path selection.  The symmetric kernels do a quarter of the weight work but
 // expose 4x less parallelism (blocks own four tile/ray images), so they only
 // pay off once the grid still fills the 148 SMs several times over.
-// G.sym: 0 off, 1 on when profitable, 2 forced (tests), 4 forced + TMA-staged
+// G.sym: 0 off, 1 on when profitable, 2 forced (tests), 10 forced with the row
+// warp layout of the symmetric backprojector (A/B tests), 4 forced + TMA-staged
 // forward (experimental: slower than the L2 gather on B200)
 static inline bool use_sym_bwd(const GeomDev& G) {
   return G.sym >= 2 || (G.sym == 1 && G.n >= 1024);
@@ -1037,10 +1048,22 @@ template <typename TIn, typename TOut>
 static cudaError_t bwd_sym_impl(const GeomDev& G, const GeomDev& Gx, const void* y, void* x,
                                 bool accumulate, cudaStream_t st) {
   dim3 grid(G.n / 64, G.n / 64);
-  if (accumulate)
-    fast::bwd_sym_kernel<TIn, TOut, true><<<grid, 256, 0, st>>>(G, (const TIn*)y, (TOut*)x);
-  else
-    fast::bwd_sym_kernel<TIn, TOut, false><<<grid, 256, 0, st>>>(G, (const TIn*)y, (TOut*)x);
+  const bool rowlayout = (G.sym & 8) != 0;   // testing: the lane = column layout
+  if (accumulate) {
+    if (rowlayout)
+      fast::bwd_sym_kernel<TIn, TOut, true, false><<<grid, 256, 0, st>>>(G, (const TIn*)y,
+                                                                        (TOut*)x);
+    else
+      fast::bwd_sym_kernel<TIn, TOut, true, true><<<grid, 256, 0, st>>>(G, (const TIn*)y,
+                                                                       (TOut*)x);
+  } else {
+    if (rowlayout)
+      fast::bwd_sym_kernel<TIn, TOut, false, false><<<grid, 256, 0, st>>>(G, (const TIn*)y,
+                                                                         (TOut*)x);
+    else
+      fast::bwd_sym_kernel<TIn, TOut, false, true><<<grid, 256, 0, st>>>(G, (const TIn*)y,
+                                                                        (TOut*)x);
+  }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   return bwd_v2_impl<TIn, TOut>(Gx, y, x, true, st);   // axis angles, accumulate
