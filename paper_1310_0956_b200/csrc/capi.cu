@@ -6,6 +6,7 @@
 #include <cstring>
 #include <limits>
 #include <new>
+#include <algorithm>
 #include <vector>
 
 #include "../../include/wmgb200.h"
@@ -65,7 +66,7 @@ struct wmg_geometry {
   // symmetric angle sets: the two axis-aligned angles as their own geometry
   wmg::GeomDev axis;
   wmg::AngleParams* d_axis;
-  int* d_rowmap;
+  int* d_mir;      // mirror / primary / half / axis-row tables (symmetric sets)
   int sym_capable;
 };
 
@@ -147,39 +148,75 @@ int wmg_geometry_create(int n, int n_detectors, int n_angles, const double* cos_
     q.hwic = (float)(q.hw * icb);
     q.w1c = (float)((2.0 * q.hw - 3.0) * icb);
   }
-  // mirror symmetry theta_{m-a} = pi - theta_a with exact axis angles at 0, m/2
-  bool sym = (n_angles % 2 == 0) && n_angles >= 4 && (n % 64 == 0);
-  if (sym) {
-    const int h = n_angles / 2;
-    sym = cos_h[0] == 1.0 && sin_h[0] == 0.0 && cos_h[h] == 0.0 && sin_h[h] == 1.0;
-    for (int a = 1; sym && a < n_angles; ++a) {
-      const int b = n_angles - a;
+  // Mirror symmetry: every non-axis angle theta has its mirror pi - theta in
+  // the set (to 1e-12); the axis angles (0, pi/2; any subset of them) run
+  // through the plain kernels as their own sub-geometry.  Any angle subset
+  // closed under the mirror qualifies (e.g. the per-rank shards of
+  // sharding.shard_angles), n % 64 == 0 for the quadrant tiling.
+  std::vector<int> mir((size_t)n_angles, -1), prim, halfv, axis_idx;
+  bool sym = (n % 64 == 0);
+  {
+    std::vector<int> lo, hi;   // 0 < theta < pi/2 ascending; pi/2 < theta < pi ascending
+    for (int a = 0; a < n_angles; ++a) {
+      const double c = cos_h[a], s = sin_h[a];
+      if (c == 0.0 || s == 0.0) axis_idx.push_back(a);
+      else if (c > 0.0) lo.push_back(a);
+      else hi.push_back(a);
+    }
+    auto by_angle = [&](int x, int y) { return cos_h[x] > cos_h[y]; };   // cos decreasing
+    std::sort(lo.begin(), lo.end(), by_angle);
+    std::sort(hi.begin(), hi.end(), by_angle);
+    if (lo.size() != hi.size() || lo.empty()) sym = false;
+    for (size_t i = 0; sym && i < lo.size(); ++i) {
+      const int a = lo[i], b = hi[hi.size() - 1 - i];
       if (std::fabs(cos_h[b] + cos_h[a]) > 1e-12 || std::fabs(sin_h[b] - sin_h[a]) > 1e-12)
         sym = false;
-      if (a != h && (cos_h[a] == 0.0 || sin_h[a] == 0.0)) sym = false;
+      mir[(size_t)a] = b;
+      mir[(size_t)b] = a;
+    }
+    if (sym) {
+      for (int a = 0; a < n_angles; ++a)
+        if (mir[(size_t)a] >= 0) prim.push_back(a);
+      halfv = lo;
     }
   }
+  // the TMA-staged forward (opt-in experiment) assumes the full equiangular layout
+  bool std_layout = sym && n_angles % 2 == 0 && axis_idx.size() == 2 && axis_idx[0] == 0 &&
+                    axis_idx[1] == n_angles / 2;
+  for (int a = 1; std_layout && a < n_angles; ++a)
+    if (a != n_angles / 2 && mir[(size_t)a] != n_angles - a) std_layout = false;
   wmg_geometry* g = new (std::nothrow) wmg_geometry;
   if (!g) return fail(WMG_EINVAL, "out of host memory");
   g->d_ang = nullptr;
   g->d_axis = nullptr;
-  g->d_rowmap = nullptr;
+  g->d_mir = nullptr;
+  const int n_axis = (int)axis_idx.size();
   cudaError_t e = cudaMalloc(&g->d_ang, sizeof(wmg::AngleParams) * (size_t)n_angles);
   if (e == cudaSuccess)
     e = cudaMemcpy(g->d_ang, P.data(), sizeof(wmg::AngleParams) * (size_t)n_angles,
                    cudaMemcpyHostToDevice);
   if (e == cudaSuccess && sym) {
-    wmg::AngleParams ax[2] = {P[0], P[(size_t)(n_angles / 2)]};
-    int rows[2] = {0, n_angles / 2};
-    e = cudaMalloc(&g->d_axis, sizeof(ax));
-    if (e == cudaSuccess) e = cudaMemcpy(g->d_axis, ax, sizeof(ax), cudaMemcpyHostToDevice);
-    if (e == cudaSuccess) e = cudaMalloc(&g->d_rowmap, sizeof(rows));
-    if (e == cudaSuccess) e = cudaMemcpy(g->d_rowmap, rows, sizeof(rows), cudaMemcpyHostToDevice);
+    // one int table: mir (m) | prim (n_prim) | half (n_half) | axis rowmap (n_axis)
+    std::vector<int> tab(mir);
+    tab.insert(tab.end(), prim.begin(), prim.end());
+    tab.insert(tab.end(), halfv.begin(), halfv.end());
+    tab.insert(tab.end(), axis_idx.begin(), axis_idx.end());
+    e = cudaMalloc(&g->d_mir, sizeof(int) * tab.size());
+    if (e == cudaSuccess)
+      e = cudaMemcpy(g->d_mir, tab.data(), sizeof(int) * tab.size(), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess && n_axis > 0) {
+      std::vector<wmg::AngleParams> ax;
+      for (int a : axis_idx) ax.push_back(P[(size_t)a]);
+      e = cudaMalloc(&g->d_axis, sizeof(wmg::AngleParams) * ax.size());
+      if (e == cudaSuccess)
+        e = cudaMemcpy(g->d_axis, ax.data(), sizeof(wmg::AngleParams) * ax.size(),
+                       cudaMemcpyHostToDevice);
+    }
   }
   if (e != cudaSuccess) {
     if (g->d_ang) cudaFree(g->d_ang);
     if (g->d_axis) cudaFree(g->d_axis);
-    if (g->d_rowmap) cudaFree(g->d_rowmap);
+    if (g->d_mir) cudaFree(g->d_mir);
     delete g;
     return cuda_rc(e);
   }
@@ -189,13 +226,19 @@ int wmg_geometry_create(int n, int n_detectors, int n_angles, const double* cos_
   g->dev.ang = g->d_ang;
   g->dev.rowmap = nullptr;
   g->dev.sym = sym ? 1 : 0;
-  g->dev.tma_ok = (sym && wmg::tma_window_fits(P.data(), n, n_detectors, n_angles)) ? 1 : 0;
+  g->dev.tma_ok =
+      (std_layout && wmg::tma_window_fits(P.data(), n, n_detectors, n_angles)) ? 1 : 0;
   g->dev.joseph = 0;
+  g->dev.mir = sym ? g->d_mir : nullptr;
+  g->dev.prim = sym ? g->d_mir + n_angles : nullptr;
+  g->dev.half = sym ? g->d_mir + n_angles + prim.size() : nullptr;
+  g->dev.n_prim = (int)prim.size();
+  g->dev.n_half = (int)halfv.size();
   g->sym_capable = sym ? 1 : 0;
   g->axis = g->dev;
-  g->axis.m = 2;
+  g->axis.m = n_axis;
   g->axis.ang = g->d_axis;
-  g->axis.rowmap = g->d_rowmap;
+  g->axis.rowmap = sym ? g->d_mir + n_angles + prim.size() + halfv.size() : nullptr;
   g->axis.sym = 0;
   g->axis.tma_ok = 0;
   g->axis.joseph = 0;
@@ -207,7 +250,7 @@ int wmg_geometry_destroy(wmg_geometry* g) {
   if (!g) return WMG_OK;
   cudaError_t e = cudaFree(g->d_ang);
   if (g->d_axis) cudaFree(g->d_axis);
-  if (g->d_rowmap) cudaFree(g->d_rowmap);
+  if (g->d_mir) cudaFree(g->d_mir);
   delete g;
   return cuda_rc(e);
 }

@@ -51,6 +51,13 @@ struct GeomDev {
                       //    may share weights across mirror images), n % 64 == 0
   int tma_ok;         // 1: the TMA-staged forward's window bound holds for every group
   int joseph;         // 1: Joseph interpolation weights (parity kernels only)
+  // mirror pairs of a symmetric angle set (sym != 0): mir[a] = local index of
+  // the angle pi - theta_a (-1 for the axis angles 0, pi/2); prim = every
+  // non-axis angle (n_prim); half = the ones with 0 < theta < pi/2 (n_half)
+  const int* mir;
+  const int* prim;
+  const int* half;
+  int n_prim, n_half;
 };
 
 // Fixed-point minor coordinate used by the fast kernels: 64-bit signed with

@@ -542,7 +542,7 @@ constexpr int kSymChunk = 8;
 // (up to four wavefronts) a 32-column row needs; each thread keeps one column
 // and 4 rows spaced 8 apart.  !kWarp2D is the row layout (lane = column).
 template <typename TIn, typename TOut, bool kAccumulate, bool kWarp2D = true>
-__global__ void __launch_bounds__(256, 6) bwd_sym_kernel(GeomDev G, const TIn* __restrict__ sino,
+__global__ void __launch_bounds__(256, 5) bwd_sym_kernel(GeomDev G, const TIn* __restrict__ sino,
                                                       TOut* __restrict__ img) {
   __shared__ float4 winA[kSymChunk][kBwdWin];   // (y_a[t], y_b[t], y_a[t+1], y_b[t+1])
   __shared__ float4 winB[kSymChunk][kBwdWin];   // same with detectors reversed
@@ -550,6 +550,7 @@ __global__ void __launch_bounds__(256, 6) bwd_sym_kernel(GeomDev G, const TIn* _
   __shared__ long long qhead[kSymChunk];
   __shared__ int jlo_s[kSymChunk];
   __shared__ int ang_s[kSymChunk];
+  __shared__ int mir_s[kSymChunk];
   const int n = G.n, m = G.m, d = G.d;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int col0 = blockIdx.x * kBwdTile, row0 = blockIdx.y * kBwdTile;
@@ -557,7 +558,6 @@ __global__ void __launch_bounds__(256, 6) bwd_sym_kernel(GeomDev G, const TIn* _
   const double xc0 = (double)col0 - half + 0.5;
   const double yc0 = half - (double)row0 - 0.5;
   const double bias = 1.0 / kQ32;
-  const int half_m = m / 2;
   // this thread's tile column and first row; its rows are trow + rstep * i
   const int tcol = kWarp2D ? (warp & 3) * 8 + (lane & 7) : lane;
   const int trow = kWarp2D ? (warp >> 2) * 4 + (lane >> 3) : 4 * warp;
@@ -569,14 +569,14 @@ __global__ void __launch_bounds__(256, 6) bwd_sym_kernel(GeomDev G, const TIn* _
     accB[i] = make_float2(0.0f, 0.0f);
   }
   // primary angles: 1 .. m-1 except m/2 (m - 2 of them)
-  const int n_prim = m - 2;
-  for (int c0 = 0; c0 < n_prim; c0 += kSymChunk) {
-    const int na = min(kSymChunk, n_prim - c0);
+  for (int c0 = 0; c0 < G.n_prim; c0 += kSymChunk) {
+    const int na = min(kSymChunk, G.n_prim - c0);
     __syncthreads();
     if (tid < na) {
       const int q = c0 + tid;                       // 0 .. m-3
-      const int a = q + 1 + (q + 1 >= half_m ? 1 : 0);
+      const int a = G.prim[q];
       ang_s[tid] = a;
+      mir_s[tid] = G.mir[a] * d;     // sinogram row offset of the mirror angle
       const AngleParams& A = G.ang[a];
       const double p0 = xc0 * A.c + yc0 * A.s + dc - A.hw - bias;
       const double t = (double)(kBwdTile - 1);
@@ -592,10 +592,9 @@ __global__ void __launch_bounds__(256, 6) bwd_sym_kernel(GeomDev G, const TIn* _
     }
     for (int e = tid; e < na * kBwdWin; e += 256) {
       const int aa = e / kBwdWin, t = e % kBwdWin;
-      const int a = ang_s[aa], b = m - a;
       const int j = jlo_s[aa] + t;
-      const TIn* ya = sino + (long long)a * d;
-      const TIn* yb = sino + (long long)b * d;
+      const TIn* ya = sino + ang_s[aa] * d;     // m * d < 2^31 (n <= 16384)
+      const TIn* yb = sino + mir_s[aa];
       auto ld = [&](const TIn* y, int jj) -> float {
         return (jj >= 0 && jj < d) ? (float)__ldg(y + jj) : 0.0f;
       };
@@ -662,7 +661,8 @@ template <typename TOut>
 __global__ void __launch_bounds__(128) fwd_sym_kernel(GeomDev G, const float* __restrict__ P,
                                                       const float* __restrict__ PT,
                                                       TOut* __restrict__ sino) {
-  const int a = blockIdx.y + 1;
+  const int a = G.half[blockIdx.y];
+  const int b = G.mir[a];
   const int d = G.d, m = G.m, n = G.n;
   const int jh = (d + 1) / 2;
   const int j = blockIdx.x * 128 + threadIdx.x;
@@ -757,10 +757,10 @@ __global__ void __launch_bounds__(128) fwd_sym_kernel(GeomDev G, const float* __
     const float r_m = A.major ? accB.y : accA.y;    // (m-a, j)
     const float r_mr = A.major ? accA.y : accB.y;   // (m-a, d-1-j)
     __stcs(sino + (long long)a * d + j, (TOut)accA.x);   // streaming: keep L2 for the planes
-    __stcs(sino + (long long)(m - a) * d + j, (TOut)r_m);
+    __stcs(sino + (long long)b * d + j, (TOut)r_m);
     if (d - 1 - j != j) {
       __stcs(sino + (long long)a * d + (d - 1 - j), (TOut)accB.x);
-      __stcs(sino + (long long)(m - a) * d + (d - 1 - j), (TOut)r_mr);
+      __stcs(sino + (long long)b * d + (d - 1 - j), (TOut)r_mr);
     }
   }
 }
@@ -796,7 +796,8 @@ template <typename TOut>
 __global__ void __launch_bounds__(128) fwd_sym64_kernel(GeomDev G, const double* __restrict__ P,
                                                         const double* __restrict__ PT,
                                                         TOut* __restrict__ sino) {
-  const int a = blockIdx.y + 1;
+  const int a = G.half[blockIdx.y];
+  const int b = G.mir[a];
   const int d = G.d, m = G.m, n = G.n;
   const int jh = (d + 1) / 2;
   const int j = blockIdx.x * 128 + threadIdx.x;
@@ -852,10 +853,10 @@ __global__ void __launch_bounds__(128) fwd_sym64_kernel(GeomDev G, const double*
     const double r_m = A.major ? a4 : a2;
     const double r_mr = A.major ? a2 : a4;
     sino[(long long)a * d + j] = (TOut)a1;
-    sino[(long long)(m - a) * d + j] = (TOut)r_m;
+    sino[(long long)b * d + j] = (TOut)r_m;
     if (d - 1 - j != j) {
       sino[(long long)a * d + (d - 1 - j)] = (TOut)a3;
-      sino[(long long)(m - a) * d + (d - 1 - j)] = (TOut)r_mr;
+      sino[(long long)b * d + (d - 1 - j)] = (TOut)r_mr;
     }
   }
 }
@@ -873,26 +874,27 @@ __global__ void __launch_bounds__(256) bwd_sym64_kernel(GeomDev G, const TIn* __
   __shared__ long long qhead[kSym64Chunk];
   __shared__ int jlo_s[kSym64Chunk];
   __shared__ int ang_s[kSym64Chunk];
+  __shared__ int mir_s[kSym64Chunk];
   const int n = G.n, m = G.m, d = G.d;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int col0 = blockIdx.x * kBwdTile, row0 = blockIdx.y * kBwdTile;
   const double half = (double)n * 0.5, dc = (double)(d - 1) * 0.5;
   const double xc0 = (double)col0 - half + 0.5;
   const double yc0 = half - (double)row0 - 0.5;
-  const int half_m = m / 2;
   double acc[4][4];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int q = 0; q < 4; ++q) acc[i][q] = 0.0;
-  const int n_prim = m - 2;
+  const int n_prim = G.n_prim;
   for (int c0 = 0; c0 < n_prim; c0 += kSym64Chunk) {
     const int na = min(kSym64Chunk, n_prim - c0);
     __syncthreads();
     if (tid < na) {
       const int q = c0 + tid;
-      const int a = q + 1 + (q + 1 >= half_m ? 1 : 0);
+      const int a = G.prim[q];
       ang_s[tid] = a;
+      mir_s[tid] = G.mir[a];
       const AngleParams& A = G.ang[a];
       const double p0 = xc0 * A.c + yc0 * A.s + dc - A.hw;
       const double t = (double)(kBwdTile - 1);
@@ -908,7 +910,7 @@ __global__ void __launch_bounds__(256) bwd_sym64_kernel(GeomDev G, const TIn* __
     }
     for (int e = tid; e < na * kBwdWin; e += 256) {
       const int aa = e / kBwdWin, t = e % kBwdWin;
-      const int a = ang_s[aa], b = m - a;
+      const int a = ang_s[aa], b = mir_s[aa];
       const int jj = jlo_s[aa] + t;
       const TIn* ya = sino + (long long)a * d;
       const TIn* yb = sino + (long long)b * d;
@@ -982,7 +984,7 @@ static inline bool use_sym_bwd(const GeomDev& G) {
   return G.sym >= 2 || (G.sym == 1 && G.n >= 1024);
 }
 static inline bool use_sym_fwd(const GeomDev& G) {
-  const long long blocks = (long long)(((G.d + 1) / 2 + 127) / 128) * (G.m / 2 - 1);
+  const long long blocks = (long long)(((G.d + 1) / 2 + 127) / 128) * G.n_half;
   return G.sym >= 2 || (G.sym == 1 && blocks >= 4LL * 148);
 }
 static inline bool use_tiled_bwd(const GeomDev& G) { return G.n >= 768; }
@@ -1023,12 +1025,13 @@ static cudaError_t fwd_v2_impl(const GeomDev& G, const void* x, void* ws, void* 
     if (G.sym == 4 && tma_forward_supported(G)) {   // opt-in: TMA-staged forward
       e = tma_forward<TOut>(G, P, PT, (TOut*)y, nullptr, st);
     } else {
-      dim3 sgrid(((G.d + 1) / 2 + 127) / 128, G.m / 2 - 1);
+      dim3 sgrid(((G.d + 1) / 2 + 127) / 128, G.n_half);
       fast::fwd_sym_kernel<TOut><<<sgrid, 128, 0, st>>>(G, P, PT, (TOut*)y);
       e = cudaGetLastError();
     }
     if (e != cudaSuccess) return e;
-    dim3 xgrid((G.d + 127) / 128, Gx->m);   // the two axis-aligned angles
+    if (Gx->m == 0) return cudaSuccess;
+    dim3 xgrid((G.d + 127) / 128, Gx->m);   // the axis-aligned angles of the set
     fast::fwd_v2_kernel<TOut><<<xgrid, 128, 0, st>>>(*Gx, P, PT, (TOut*)y);
     return cudaGetLastError();
   }
@@ -1065,7 +1068,7 @@ static cudaError_t bwd_sym_impl(const GeomDev& G, const GeomDev& Gx, const void*
                                                                         (TOut*)x);
   }
   cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
+  if (e != cudaSuccess || Gx.m == 0) return e;
   return bwd_v2_impl<TIn, TOut>(Gx, y, x, true, st);   // axis angles, accumulate
 }
 
@@ -1110,11 +1113,12 @@ static cudaError_t fwd64_impl(const GeomDev& G, const void* x, void* ws, void* y
   fast::pad_transpose64_kernel<TIn><<<tg, tb, 0, st>>>((const TIn*)x, P, PT, G.n);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  dim3 sgrid(((G.d + 1) / 2 + 127) / 128, G.m / 2 - 1);
+  dim3 sgrid(((G.d + 1) / 2 + 127) / 128, G.n_half);
   fast::fwd_sym64_kernel<TOut><<<sgrid, 128, 0, st>>>(G, P, PT, (TOut*)y);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  // the two axis-aligned angles: generic walk on the padded planes
+  // the axis-aligned angles: generic walk on the padded planes
+  if (Gx->m == 0) return cudaSuccess;
   dim3 xgrid((G.d + 127) / 128, Gx->m);
   fast::fwd_kernel<double, TOut, double><<<xgrid, 128, 0, st>>>(
       *Gx, P + kPadMargin, PT + kPadMargin, (TOut*)y, G.n + 2 * kPadMargin);
@@ -1131,7 +1135,7 @@ static cudaError_t bwd64_impl(const GeomDev& G, const void* y, void* x, bool acc
   else
     fast::bwd_sym64_kernel<TIn, TOut, false><<<grid, 256, 0, st>>>(G, (const TIn*)y, (TOut*)x);
   cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
+  if (e != cudaSuccess || Gx->m == 0) return e;
   dim3 g2((G.n + 31) / 32, (G.n + 7) / 8);
   fast::bwd_kernel<TIn, TOut, double, true><<<g2, 256, 0, st>>>(*Gx, (const TIn*)y, (TOut*)x);
   return cudaGetLastError();

@@ -22,11 +22,23 @@ import numpy as np
 
 
 def shard_angles(n_angles: int, world: int, rank: int, scheme: str = "round_robin"):
-    """Indices of the angles owned by ``rank`` (ascending)."""
+    """Indices of the angles owned by ``rank`` (ascending).
+
+    "round_robin": angle k -> rank k mod world.  "contiguous": equal blocks.
+    "mirror": the units {k, m - k} (mirror pairs theta, pi - theta of an
+    equiangular set) and {0, m/2} (the axis angles) are dealt round-robin, so
+    every shard is closed under the mirror and keeps the symmetric kernels
+    (4 pixel/ray images per weight evaluation); units have equal work."""
     if world < 1 or not 0 <= rank < world:
         raise ValueError("bad world/rank")
     if scheme == "round_robin":
         return np.arange(rank, n_angles, world)
+    if scheme == "mirror":
+        m = n_angles
+        units = [[0] + ([m // 2] if m % 2 == 0 and m > 1 else [])]
+        units += [[k, m - k] for k in range(1, (m + 1) // 2)]
+        mine = [a for u in units[rank::world] for a in u]
+        return np.array(sorted(mine), dtype=np.int64)
     if scheme == "contiguous":
         bounds = np.linspace(0, n_angles, world + 1).round().astype(int)
         return np.arange(bounds[rank], bounds[rank + 1])
@@ -51,13 +63,14 @@ class AngleShardedProjector:
     """W restricted to this rank's angles, with a summed backprojection."""
 
     def __init__(self, g, group=None, precision: str = "float32", mode=None,
-                 scheme: str = "round_robin", local=None, device=None):
+                 scheme: str = "mirror", local=None, device=None):
         import torch.distributed as dist
         self.dist = dist
         self.group = group
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
         self.geometry = g
+        self.scheme = scheme
         self.index = shard_angles(g.n_angles, self.world, self.rank, scheme)
         if local is None:
             from .geometry import build_projector
@@ -85,7 +98,7 @@ class AngleShardedProjector:
         m = self.geometry.n_angles
         if self.world == 1:
             return local
-        counts = [len(shard_angles(m, self.world, r)) for r in range(self.world)]
+        counts = [len(shard_angles(m, self.world, r, self.scheme)) for r in range(self.world)]
         width = max(counts) * d
         buf = torch.zeros(width, dtype=local.dtype, device=local.device)
         buf[: local.numel()] = local
@@ -93,7 +106,8 @@ class AngleShardedProjector:
         self.dist.all_gather(parts, buf, group=self.group)
         out = torch.empty(m * d, dtype=local.dtype, device=local.device).view(m, d)
         for r in range(self.world):
-            idx = torch.as_tensor(shard_angles(m, self.world, r), device=local.device)
+            idx = torch.as_tensor(shard_angles(m, self.world, r, self.scheme),
+                                  device=local.device)
             out.index_copy_(0, idx, parts[r][: counts[r] * d].view(-1, d))
         return out.reshape(-1)
 

@@ -172,7 +172,8 @@ def test_symmetric_fast_paths(gpu, oracle_proj, n, d, m, mode):
 def test_symmetry_not_used_for_asymmetric_sets(gpu):
     from paper_1310_0956_b200.geometry import Geometry, build_geometry, build_projector
     assert not build_projector(build_geometry(100, 145, 64), precision="float32").symmetric
-    assert not build_projector(build_geometry(128, 181, 63), precision="float32").symmetric
+    # odd m: pi/2 is missing, the mirror pairs (k, m - k) and the axis angle 0 remain
+    assert build_projector(build_geometry(128, 181, 63), precision="float32").symmetric
     a = np.sort(np.random.default_rng(0).uniform(0, np.pi, 64))
     assert not build_projector(Geometry(128, 181, 64, angles=a), precision="float32").symmetric
 
@@ -211,3 +212,37 @@ def test_symmetric_fast_n1024_default_dispatch(gpu):
     br = wp.backward(torch.from_numpy(y).cuda())
     assert float((ff - fr).norm()) <= 1e-5 * float(fr.norm())
     assert float((bb - br).norm()) <= 1e-5 * float(br.norm())
+
+
+@pytest.mark.parametrize("n,d,m,world", [(256, 363, 180, 2), (256, 363, 180, 4),
+                                         (256, 363, 180, 8), (128, 181, 63, 3),
+                                         (1024, 1449, 720, 8)])
+def test_symmetric_kernels_on_mirror_shards(gpu, oracle_proj, n, d, m, world):
+    """Per-rank angle shards of sharding.shard_angles(..., "mirror") are closed
+    under theta -> pi - theta; most hold neither axis angle.  They keep the
+    symmetric kernels (table-driven mirror pairs) and stay within 1e-5 of the
+    float64 reference rows of those angles."""
+    torch = gpu
+    from paper_1310_0956_b200.geometry import build_geometry, build_projector
+    from paper_1310_0956_b200.sharding import shard_angles
+    g = build_geometry(n, d, m)
+    rs = np.random.default_rng(n + m + world)
+    x = rs.uniform(0.0, 1.0, n * n)
+    xd = torch.from_numpy(x.astype(np.float32)).cuda()
+    for rank in range(world):
+        idx = shard_angles(m, world, rank, "mirror")
+        sub = g.subset(idx)
+        w = build_projector(sub, precision="float32")
+        assert w.symmetric and w.set_symmetry("force")
+        y = rs.uniform(0.0, 1.0, idx.size * d)
+        ref_f = oracle_proj.forward(n, d, sub.angles, x)
+        ref_b = oracle_proj.backward(n, d, sub.angles, y)
+        got_f = w.forward(xd).double().cpu().numpy()
+        got_b = w.backward(torch.from_numpy(y.astype(np.float32)).cuda()).double().cpu().numpy()
+        assert np.linalg.norm(got_f - ref_f) <= 1e-5 * np.linalg.norm(ref_f), rank
+        assert np.linalg.norm(got_b - ref_b) <= 1e-5 * np.linalg.norm(ref_b), rank
+        if n >= 1024:
+            wd = build_projector(sub, precision="float64", mode="fast")
+            assert wd.set_symmetry("force")
+            f64 = wd.forward(torch.from_numpy(x).cuda()).cpu().numpy()
+            assert np.linalg.norm(f64 - ref_f) <= 1e-12 * np.linalg.norm(ref_f), rank

@@ -34,6 +34,24 @@ def test_partitions_cover_and_balance():
         shard_angles(10, 2, 2)
 
 
+@pytest.mark.parametrize("m", [90, 180, 720, 4096, 7, 1, 2])
+def test_mirror_shards_closed_and_balanced(m):
+    """The "mirror" scheme partitions the angles, every shard is closed under
+    k -> m - k (so it keeps the symmetric kernels) and work is balanced."""
+    a = np.arange(m) * (np.pi / m)
+    w = angle_weights(a)
+    for world in (1, 2, 3, 4, 8):
+        sh = [shard_angles(m, world, r, "mirror") for r in range(world)]
+        assert np.array_equal(np.sort(np.concatenate(sh)), np.arange(m))
+        for ix in sh:
+            assert np.all(np.diff(ix) > 0)
+            s = set(ix.tolist())
+            assert all((m - k) in s for k in s if k != 0 and 2 * k != m)
+        if m >= 90 * world:
+            loads = np.array([w[ix].sum() for ix in sh])
+            assert loads.max() / loads.mean() < 1.02
+
+
 class _CpuLocal:
     """CPU stand-in for a rank-local LineProjector (oracle CSR of its angles)."""
 
@@ -69,7 +87,7 @@ def _worker(rank, world, port, q):
         n, d, m = 32, 47, 30
         angles = np.arange(m) * (np.pi / m)
         g = Geometry(n, d, m, angles=angles)
-        idx = shard_angles(m, world, rank)
+        idx = shard_angles(m, world, rank, "mirror")
         sp = AngleShardedProjector(g, local=_CpuLocal(n, d, angles[idx]))
         rs = np.random.default_rng(0)
         x = torch.from_numpy(rs.standard_normal(n * n))
