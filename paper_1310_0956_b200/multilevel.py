@@ -265,6 +265,11 @@ def _assemble_leaf_grams(w, n, lam, levels, ray_chunk=None, paths=None, method="
     return paths, grams
 
 
+def _is_sharded(w) -> bool:
+    """An AngleShardedProjector (sharding.py) spanning more than one rank."""
+    return hasattr(w, "local") and hasattr(w, "reduce_sino_") and getattr(w, "world", 1) > 1
+
+
 def build_wmg_hierarchy(w, n: int, lam: float, levels: int, nu_pre: int = 0,
                         nu_post: int = 0, node_mode: str = "fast",
                         gram: str = "sparse") -> WmgHierarchy:
@@ -287,14 +292,26 @@ def build_wmg_hierarchy(w, n: int, lam: float, levels: int, nu_pre: int = 0,
         raise ValueError("smoothing counts must be nonnegative")
     if w.shape[1] != n * n:
         raise DimensionMismatchError(f"projector has {w.shape[1]} columns, expected {n * n}")
-    if not hasattr(w, "handle"):
-        raise TypeError("build_wmg_hierarchy needs a LineProjector (build_projector)")
+    sharded = _is_sharded(w)
+    base = w.local if sharded else w
+    if not hasattr(base, "handle"):
+        raise TypeError("build_wmg_hierarchy needs a LineProjector (build_projector) or an "
+                        "AngleShardedProjector")
     t = D.require_cuda()
-    if getattr(w, "kernel", "line") == "joseph":
+    if getattr(base, "kernel", "line") == "joseph":
         # Joseph weights exist in parity mode only: exact leaf factors + DGEMM
         # and the parity projector for the node systems
         gram, node_mode = "dense", "parity"
-    paths, grams = _assemble_leaf_grams(w, n, lam, levels, method=gram)
+    if sharded:
+        # angle-sharded W: every rank accumulates its angles' share of each leaf
+        # Gram (the Gram is a sum over rays), one NCCL allreduce sums them, and
+        # every rank factors all leaves (the V-cycle's coarse solves are local)
+        paths, grams = _assemble_leaf_grams(base, n, 0.0, levels, method=gram)
+        w.dist.all_reduce(grams, group=w.group)
+        if lam != 0:
+            grams.diagonal(dim1=1, dim2=2).add_(lam)
+    else:
+        paths, grams = _assemble_leaf_grams(w, n, lam, levels, method=gram)
     n_leaf, p = grams.shape[0], grams.shape[-1]
     # keep the Cholesky factors (API: coarse_solve.lower) only when they are
     # small; the V-cycle itself only needs the inverses
@@ -323,9 +340,15 @@ def build_wmg_hierarchy(w, n: int, lam: float, levels: int, nu_pre: int = 0,
     if node_mode not in ("fast", "fast32", "parity"):
         raise ValueError(f"unknown node_mode '{node_mode}'")
     from .geometry import LineProjector
-    if node_mode == "parity" or (node_mode == "fast" and getattr(w, "mode", None) == "fast"
-                                 and getattr(w, "precision", None) == N.F64):
+    if node_mode == "parity" or (node_mode == "fast" and getattr(base, "mode", None) == "fast"
+                                 and getattr(base, "precision", None) == N.F64):
         node_w = w
+    elif sharded:
+        # node systems on the same angle shards: pair per rank + allreduce of W^T y
+        from .sharding import AngleShardedProjector
+        node_w = AngleShardedProjector(
+            w.geometry, group=w.group, precision="float64" if node_mode == "fast" else "float32",
+            mode="fast", scheme=w.scheme, device=w.device)
     elif node_mode == "fast":
         node_w = LineProjector(w.geometry, precision="float64", mode="fast", device=w.device)
     else:
@@ -557,7 +580,8 @@ class WmgPreconditioner(_GraphedOperator):
         self.h = h
         self.multiplicative = multiplicative
         self.dim = h.root.dim
-        self._init_graph(graph)
+        # an angle-sharded cycle runs collectives between its kernels: eager
+        self._init_graph(graph and not _is_sharded(h.node_projector))
 
     def _eager(self, v):
         return _node_solve_(self.h.root, v, self.multiplicative)
