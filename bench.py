@@ -214,76 +214,79 @@ def run_reference(args):
 
 
 # ----------------------------------------------------- WMG-CGLS (config 1)
-def run_wmg_cgls(dev, reps=3):
+def run_wmg_cgls(dev, reps=3, world=1):
     """BASELINE config 1: 256^2, 180 angles, 363 detectors, float64, seeded
     20-ellipse phantom (seed 1000), 1 % Gaussian noise (seed 1500); WMG-CGLS
     (flexible PCG on the normal equations, 3 levels, 2 pre + 2 post SIRT-type
     sweeps per level) to normal-equations residual 1e-4 or 100 iterations.
     Setup (hierarchy) and solve are timed separately (device-synchronised wall
-    clock); the plain-CGLS solve is reported beside it."""
+    clock, max over ranks); the plain-CGLS solve and the reference's
+    smoother-free cycle are reported beside it.  Under torchrun every rank owns
+    a mirror shard of the angles (sharded pairs, allreduced leaf Grams)."""
     import torch
+    import torch.distributed as dist
     from paper_1310_0956_b200 import (SolverConfig, add_gaussian_noise, build_geometry,
                                       build_projector, build_wmg_hierarchy, cgls_solve,
                                       random_ellipses, wmg_preconditioner)
     n, d, m = 256, 363, 180
     g = build_geometry(n, d, m)
-    w = build_projector(g, device=dev)                       # parity float64 (exact W)
-    wf = build_projector(g, precision="float64", mode="fast", device=dev)
+    w = _projector(g, world, dev)                                   # parity float64 (exact W)
+    wf = _projector(g, world, dev, precision="float64", mode="fast")
     x_ex = random_ellipses(n, 20, seed=1000)
-    b = add_gaussian_noise(w @ x_ex, 0.01, seed=1500)
-    bd = torch.from_numpy(b).to(dev)
+    b = add_gaussian_noise(build_projector(g, device=dev) @ x_ex, 0.01, seed=1500)
+    bd = _local_rows(wf, b, dev)
     cfg = SolverConfig(max_iterations=100, residual_tolerance=1e-4)
-    setups, solves, iters, status = [], [], None, None
-    for _ in range(reps):
+
+    def timed(fn):
+        if world > 1:
+            dist.barrier()
         torch.cuda.synchronize(dev)
         t0 = time.perf_counter()
-        h = build_wmg_hierarchy(w, n, 0.0, 3, nu_pre=2, nu_post=2)
-        M = wmg_preconditioner(h)
+        r = fn()
         torch.cuda.synchronize(dev)
-        t1 = time.perf_counter()
-        _, rec = cgls_solve(wf, bd, precond=M, cfg=cfg)
-        torch.cuda.synchronize(dev)
-        t2 = time.perf_counter()
-        setups.append(t1 - t0)
-        solves.append(t2 - t1)
+        return time.perf_counter() - t0, r
+
+    setups, solves = [], []
+    for _ in range(reps):
+        tu, M = timed(lambda: wmg_preconditioner(
+            build_wmg_hierarchy(w, n, 0.0, 3, nu_pre=2, nu_post=2)))
+        ts, (_, rec) = timed(lambda: cgls_solve(wf, bd, precond=M, cfg=cfg))
+        setups.append(tu)
+        solves.append(ts)
         iters, status, rel = rec.iterations[-1], rec.status, rec.rel_residual[-1]
-        del h, M
+        del M
     t_cgls = []
     for _ in range(reps):
-        torch.cuda.synchronize(dev)
-        t0 = time.perf_counter()
-        _, rec_c = cgls_solve(wf, bd, cfg=SolverConfig(max_iterations=500,
-                                                       residual_tolerance=1e-4))
-        torch.cuda.synchronize(dev)
-        t_cgls.append(time.perf_counter() - t0)
-    t_cgls = min(t_cgls)
+        tc, (_, rec_c) = timed(lambda: cgls_solve(
+            wf, bd, cfg=SolverConfig(max_iterations=500, residual_tolerance=1e-4)))
+        t_cgls.append(tc)
     # the reference's smoother-free cycle (nu = 0), for the like-for-like CPU comparison
     s0, u0 = [], []
     for _ in range(reps):
-        torch.cuda.synchronize(dev)
-        t0 = time.perf_counter()
-        h0 = build_wmg_hierarchy(w, n, 0.0, 3)
-        M0 = wmg_preconditioner(h0)
-        torch.cuda.synchronize(dev)
-        t1 = time.perf_counter()
-        _, rec0 = cgls_solve(wf, bd, precond=M0, cfg=cfg)
-        torch.cuda.synchronize(dev)
-        t2 = time.perf_counter()
-        u0.append(t1 - t0)
-        s0.append(t2 - t1)
-        del h0, M0
+        tu, M0 = timed(lambda: wmg_preconditioner(build_wmg_hierarchy(w, n, 0.0, 3)))
+        ts, (_, rec0) = timed(lambda: cgls_solve(wf, bd, precond=M0, cfg=cfg))
+        u0.append(tu)
+        s0.append(ts)
+        del M0
+    # per-rep maxima over ranks, then best of the reps
+    k = reps
+    mx = _max_over_ranks(setups + solves + t_cgls + u0 + s0, dev)
+    setups, solves, t_cgls, u0, s0 = (mx[0:k], mx[k:2 * k], mx[2 * k:3 * k], mx[3 * k:4 * k],
+                                      mx[4 * k:5 * k])
     nu0 = {"seconds": min(s0), "setup_seconds": min(u0), "iterations": rec0.iterations[-1]}
     return {"metric": "WMG-CGLS seconds to rel. residual 1e-4", "config": "config1_256_180x363",
-            "seconds": min(solves), "setup_seconds": min(setups),
-            "seconds_incl_setup": min(s + u for s, u in zip(solves, setups)),
+            "n_gpus": world, "seconds": min(solves), "setup_seconds": min(setups),
+            "seconds_incl_setup": min(a + c for a, c in zip(solves, setups)),
             "iterations": iters, "status": status, "final_rel_residual": rel,
             "levels": 3, "nu_pre": 2, "nu_post": 2, "lambda": 0.0,
             "projector": "float64 fast (<=1e-12 of the reference W); sparse leaf Grams "
                          "(<=1e-12 of the exact P_L^T P_L)",
-            "cgls_seconds": t_cgls, "cgls_iterations": rec_c.iterations[-1],
+            "angle_sharding": "mirror pairs" if world > 1 else None,
+            "cgls_seconds": min(t_cgls), "cgls_iterations": rec_c.iterations[-1],
             "nu0": nu0, "b": b, "x_ex": x_ex,
-            "timing": "torch.cuda.synchronize + perf_counter, best of %d; every WMG solve "
-                      "uses a freshly built hierarchy (graph capture included)" % reps}
+            "timing": "torch.cuda.synchronize + perf_counter, max over ranks, best of %d; "
+                      "every WMG solve uses a freshly built hierarchy (graph capture "
+                      "included)" % reps}
 
 
 def cpu_wmg_cgls(b):
@@ -457,12 +460,12 @@ def run_ours(args):
         "gpu_launches": launches,
         "clocks": clk,
     }
-    if rank == 0 and world == 1 and not args.no_wmg:
+    if not args.no_wmg:
         try:
-            wmg = run_wmg_cgls(dev)
+            wmg = run_wmg_cgls(dev, world=world)
             b1 = wmg.pop("b")
             wmg.pop("x_ex")
-            if not args.no_cpu_baseline:
+            if rank == 0 and world == 1 and not args.no_cpu_baseline:
                 wmg["cpu_baseline"] = cpu_wmg_cgls(b1)
             line["wmg_cgls"] = wmg
         except Exception as exc:  # pragma: no cover
@@ -480,44 +483,96 @@ def run_ours(args):
 
 
 # ------------------------------------------------------------ config 2
+def _dist_init():
+    """(world, rank, device); NCCL process group when launched by torchrun."""
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1 and not dist.is_initialized():
+        dist.init_process_group("nccl", device_id=dev)
+    return world, rank, dev
+
+
+def _max_over_ranks(values, dev):
+    """Elementwise max of host floats over all ranks (device-timed spans)."""
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor(values, dtype=torch.float64, device=dev)
+    if dist.is_initialized() and dist.get_world_size() > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return [float(v) for v in t.cpu()]
+
+
+def _projector(g, world, dev, **kw):
+    """Full projector at N = 1, this rank's mirror angle shard at N > 1."""
+    from paper_1310_0956_b200 import build_projector
+    from paper_1310_0956_b200.sharding import AngleShardedProjector
+    if world > 1:
+        return AngleShardedProjector(g, device=dev, **kw)
+    return build_projector(g, device=dev, **kw)
+
+
+def _local_rows(w, b, dev):
+    import torch
+    bd = torch.from_numpy(np.ascontiguousarray(b)).to(dev)
+    return w.scatter_sinogram(bd) if hasattr(w, "scatter_sinogram") else bd
+
+
 def run_config2(args):
     """BASELINE config 2: 1024^2, 720 angles, 1449 detectors; float32 projector
     with float64 Krylov vectors; seeded 50-ellipse phantom (seed 2000, values
     U[0,1]); Poisson data, I0 = 1e5, mu = 2/n, log transform (seed 2500).
     Unpreconditioned CGLS vs WMG-preconditioned GMRES on the normal equations
     (levels = 5, reference smoother-free cycle), each to normal-equations
-    residual 1e-4.  ``--n`` rescales the grid (detectors = ceil(n sqrt 2),
-    angles = 720 n / 1024) for quick checks."""
+    residual 1e-4.  Under torchrun the angles are sharded (mirror pairs per
+    rank, NCCL allreduce of W^T y and of the leaf Grams); times are max over
+    ranks.  ``--n`` rescales the grid (detectors = ceil(n sqrt 2), angles =
+    720 n / 1024) for quick checks."""
     import torch
+    import torch.distributed as dist
     from paper_1310_0956_b200 import (SolverConfig, build_geometry, build_projector,
                                       build_wmg_hierarchy, cgls_solve, gmres_solve,
                                       normal_operator, poisson_log_data, random_ellipses,
                                       wmg_preconditioner)
-    dev = torch.device("cuda", 0)
+    world, rank, dev = _dist_init()
     n = args.n if args.n != 4096 else 1024
     m = int(round(720 * n / 1024))
     m += m % 2
     d = int(math.ceil(n * math.sqrt(2.0)))
     g = build_geometry(n, d, m)
-    w32 = build_projector(g, precision="float32", device=dev)
     x_ex = random_ellipses(n, 50, seed=2000, value_range=(0.0, 1.0))
-    b = poisson_log_data(w32 @ x_ex, 1e5, 2.0 / n, seed=2500)
-    bd = torch.from_numpy(b).to(dev)
+    b = poisson_log_data(build_projector(g, precision="float32", device=dev) @ x_ex, 1e5,
+                         2.0 / n, seed=2500)
+    w32 = _projector(g, world, dev, precision="float32")
+    bd = _local_rows(w32, b, dev)
     out = {"metric": "config2 seconds to rel. residual 1e-4", "n": n, "n_angles": m,
-           "n_detectors": d, "projector": "float32 arithmetic, float64 Krylov vectors",
-           "data": "synthetic: 50-ellipse phantom, Poisson I0=1e5, mu=2/n"}
+           "n_detectors": d, "n_gpus": world, "projector": "float32 arithmetic, float64 "
+           "Krylov vectors", "angle_sharding": "mirror pairs" if world > 1 else None,
+           "data": "synthetic: 50-ellipse phantom, Poisson I0=1e5, mu=2/n",
+           "timing": "torch.cuda.synchronize + perf_counter, max over ranks"}
+    cgls_solve(w32, bd, cfg=SolverConfig(max_iterations=2))          # warm-up
+    if world > 1:
+        dist.barrier()
     torch.cuda.synchronize(dev)
     t0 = time.perf_counter()
     _, rec = cgls_solve(w32, bd, x_ex=x_ex,
                         cfg=SolverConfig(max_iterations=3000, residual_tolerance=1e-4))
     torch.cuda.synchronize(dev)
-    out["cgls"] = {"seconds": time.perf_counter() - t0, "iterations": rec.iterations[-1],
-                   "status": rec.status, "rel_err_l2": rec.rel_err_l2[-1]}
+    t_cgls = time.perf_counter() - t0
+    out["cgls"] = {"iterations": rec.iterations[-1], "status": rec.status,
+                   "rel_err_l2": rec.rel_err_l2[-1]}
     op = normal_operator(w32, 0.0)
     f = w32.T @ bd
+    if world > 1:
+        dist.barrier()
     torch.cuda.synchronize(dev)
     t0 = time.perf_counter()
-    wexact = build_projector(g, device=dev)      # leaf Grams from the exact weights
+    # leaf Grams from the exact line weights (sparse kernel, per-rank angles)
+    wexact = _projector(g, world, dev)
     h = build_wmg_hierarchy(wexact, n, 0.0, args.levels, node_mode="fast32")
     M = wmg_preconditioner(h)
     torch.cuda.synchronize(dev)
@@ -526,12 +581,18 @@ def run_config2(args):
     _, rec = gmres_solve(op, f, precond=M, x_ex=x_ex, restart=100,
                          cfg=SolverConfig(max_iterations=300, residual_tolerance=1e-4))
     torch.cuda.synchronize(dev)
-    out["wmg_gmres"] = {"seconds": time.perf_counter() - t0, "setup_seconds": t_setup,
+    t_gm = time.perf_counter() - t0
+    t_cgls, t_setup, t_gm = _max_over_ranks([t_cgls, t_setup, t_gm], dev)
+    out["cgls"]["seconds"] = t_cgls
+    out["wmg_gmres"] = {"seconds": t_gm, "setup_seconds": t_setup,
                         "iterations": rec.iterations[-1], "status": rec.status,
                         "rel_err_l2": rec.rel_err_l2[-1], "levels": args.levels,
                         "leaves": 4 ** (args.levels - 1),
                         "leaf_dim": (n >> (args.levels - 1)) ** 2}
-    print(json.dumps(out), flush=True)
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
     return 0
 
 
