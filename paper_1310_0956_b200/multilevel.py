@@ -537,6 +537,20 @@ class _GraphedOperator:
     def _eager(self, v):  # pragma: no cover - abstract
         raise NotImplementedError
 
+    def prepare(self):
+        """Warm up and capture the graph now (part of the setup), so the first
+        solve replays instead of capturing."""
+        if self.use_graph and self._graph is None:
+            t = D.torch()
+            z = t.zeros(self.dim, dtype=t.float64, device=self._device())
+            out = t.empty_like(z)
+            while self._graph is None:
+                self.apply_(z, out)
+        return self
+
+    def _device(self):  # pragma: no cover - overridden
+        raise NotImplementedError
+
     def apply_(self, v, out):
         t = D.torch()
         if not self.use_graph:
@@ -586,10 +600,15 @@ class WmgPreconditioner(_GraphedOperator):
     def _eager(self, v):
         return _node_solve_(self.h.root, v, self.multiplicative)
 
+    def _device(self):
+        return self.h.projector.device
+
 
 def wmg_preconditioner(h: WmgHierarchy, multiplicative: bool = False,
                        graph: bool = True) -> Callable:
-    return WmgPreconditioner(h, multiplicative, graph=graph)
+    """One V-cycle as the preconditioner (multilevel.py:201-208); with
+    ``graph`` the cycle is captured as a CUDA graph here, in the setup."""
+    return WmgPreconditioner(h, multiplicative, graph=graph).prepare()
 
 
 # --------------------------------------------- classical two-grid (SURVEY f2)
@@ -655,6 +674,9 @@ class ClassicalTGPreconditioner(_GraphedOperator):
         D.axpy(z, z, 1.0, +1, u)                            # z + C(...)
         return z
 
+    def _device(self):
+        return self.w.device
+
     def _eager(self, v):
         t = D.torch()
         z = t.zeros_like(v)
@@ -678,4 +700,4 @@ class ClassicalTGPreconditioner(_GraphedOperator):
 
 def classical_tg_preconditioner(w, n: int, lam: float, smoother_steps=(1, 1),
                                 graph: bool = True) -> Callable:
-    return ClassicalTGPreconditioner(w, n, lam, smoother_steps, graph=graph)
+    return ClassicalTGPreconditioner(w, n, lam, smoother_steps, graph=graph).prepare()

@@ -444,10 +444,15 @@ def _cgls_graphed(w, bd, x, lam, precond, cfg, errs, was_np, record, t0):
                "x": t.empty(Nn, dtype=t.float64, device=dev),
                "S": t.zeros(16, dtype=t.float64, device=dev),
                "S_host": t.zeros(16, dtype=t.float64).pin_memory(),
-               "loop": None, "wref": weakref.ref(w)}
+               "z": t.empty(Nn, dtype=t.float64, device=dev),
+               "loop": None, "loopB": None, "wref": weakref.ref(w)}
         if cache is not None:
             cache[key] = ctx
     r, q, s, s_old, S, S_host = (ctx[k] for k in ("r", "q", "s", "s_old", "S", "S_host"))
+    # A preconditioner that already holds its own captured graph (captured at
+    # construction, i.e. in the setup) is replayed between two captured halves
+    # of the iteration instead of being re-captured inside it.
+    split = precond is not None and getattr(precond, "_graph", None) is not None
     ctx["x"].copy_(x)
     x = ctx["x"]
     st = D.stream_handle
@@ -461,7 +466,11 @@ def _cgls_graphed(w, bd, x, lam, precond, cfg, errs, was_np, record, t0):
         D.det_reduce([(N.RED_SQ, s, None, None)], out=S[0:1])
         D.det_reduce([(N.RED_SQ, s, None, None)], out=S[5:6])
     else:
-        z = precond._eager(s)
+        if split:
+            z = ctx["z"]
+            precond.apply_(s, z)
+        else:
+            z = precond._eager(s)
         D.det_reduce([(N.RED_SQ, s, None, None), (N.RED_DOT, z, s, None)], out=S[5:7])
         S[0:1].copy_(S[6:7])
     p = ctx["p"]
@@ -504,8 +513,12 @@ def _cgls_graphed(w, bd, x, lam, precond, cfg, errs, was_np, record, t0):
             N.call("wmg_cgls_scalars", D.ptr(S), float(lam), 1, st())
             N.call("wmg_lincomb_dev", n_img, D.ptr(p), 1.0, D.ptr(s), D.ptr(S[4:5]), D.ptr(p),
                    st())
-        else:
-            zz = precond._eager(s)
+            tail()
+        elif not split:
+            tail(precond._eager(s))
+
+    def tail(zz=None):
+        if zz is not None:
             D.det_reduce([(N.RED_SQ, s, None, None), (N.RED_DOT, zz, s, None),
                           (N.RED_DOTDIFF, zz, s, s_old)], out=S[5:8])
             N.call("wmg_cgls_scalars", D.ptr(S), float(lam), 2, st())
@@ -515,11 +528,18 @@ def _cgls_graphed(w, bd, x, lam, precond, cfg, errs, was_np, record, t0):
             S[9:11].copy_(errs.device_terms(x))
         S_host.copy_(S, non_blocking=True)
 
+    zbuf = ctx["z"]
     loop = ctx["loop"]
     if loop is None:
         loop = ctx["loop"] = _GraphedLoop(body)
+    loop_b = ctx["loopB"]
+    if split and loop_b is None:
+        loop_b = ctx["loopB"] = _GraphedLoop(lambda: tail(zbuf))
     for k in range(1, cfg.max_iterations + 1):
         loop.step()
+        if split:
+            precond.apply_(s, zbuf)          # the preconditioner's own graph
+            loop_b.step()
         t.cuda.current_stream(dev).synchronize()
         h = S_host.numpy()
         if h[8] != 0.0:
