@@ -108,6 +108,18 @@ int wmg_forward(const wmg_geometry *g, int mode, int precision, int dtype_in, in
 int wmg_backward(const wmg_geometry *g, int mode, int precision, int dtype_in, int dtype_out,
                  const void *y, void *x, int accumulate, int *anomaly, void *stream);
 
+/* Batched W x / W^T y over `batch` contiguous images (n*n apart) and sinograms
+ * (n_angles*n_detectors apart), each item computed exactly as by wmg_forward /
+ * wmg_backward (the WMG cycle applies sibling node systems together; on small
+ * grids the float64 fast kernels take the batch in one launch).  workspace:
+ * batch * wmg_forward_workspace bytes (FAST mode). */
+int wmg_forward_batch(const wmg_geometry *g, int mode, int precision, int dtype_in,
+                      int dtype_out, const void *x, void *y, int batch, void *workspace,
+                      void *stream);
+int wmg_backward_batch(const wmg_geometry *g, int mode, int precision, int dtype_in,
+                       int dtype_out, const void *y, void *x, int batch, int accumulate,
+                       void *stream);
+
 /* exact reference row sums (np.add.reduceat) and column sums (ones @ W) */
 int wmg_row_sums(const wmg_geometry *g, double *out, void *stream);
 int wmg_col_sums(const wmg_geometry *g, double *out, void *stream);

@@ -22,6 +22,10 @@ cudaError_t fast_forward(const GeomDev&, int, int, int, const void*, void*, void
                          const GeomDev*);
 cudaError_t fast_backward(const GeomDev&, int, int, int, const void*, void*, bool, cudaStream_t,
                           const GeomDev*);
+cudaError_t fast_forward_batch(const GeomDev&, int, int, int, const void*, void*, size_t, void*,
+                               int, cudaStream_t, const GeomDev*);
+cudaError_t fast_backward_batch(const GeomDev&, int, int, int, const void*, void*, bool, int,
+                                cudaStream_t, const GeomDev*);
 size_t fast_forward_workspace_bytes(int, int, int);
 cudaError_t det_reduce(long long, int, const int*, const double* const*, const double* const*,
                        const double* const*, double*, double*, cudaStream_t);
@@ -330,6 +334,52 @@ int wmg_backward(const wmg_geometry* g, int mode, int precision, int dtype_in, i
   return cuda_rc(wmg::fast_backward(g->dev, precision, dtype_in, dtype_out, y, x,
                                     accumulate != 0, STREAM(stream),
                                     g->dev.sym ? &g->axis : nullptr));
+}
+
+int wmg_forward_batch(const wmg_geometry* g, int mode, int precision, int dtype_in,
+                      int dtype_out, const void* x, void* y, int batch, void* workspace,
+                      void* stream) {
+  if (!g || !x || !y) return fail(WMG_EINVAL, "NULL argument");
+  if (batch < 0) return fail(WMG_EINVAL, "negative batch");
+  int rc = check_types(mode, precision, dtype_in, dtype_out);
+  if (rc) return rc;
+  const long long N = (long long)g->dev.n * g->dev.n, M = (long long)g->dev.m * g->dev.d;
+  if (mode == WMG_MODE_PARITY) {
+    for (int b = 0; b < batch; ++b) {
+      cudaError_t e = wmg::parity_forward(g->dev, (const double*)x + b * N, (double*)y + b * M,
+                                          nullptr, STREAM(stream));
+      if (e != cudaSuccess) return cuda_rc(e);
+    }
+    return WMG_OK;
+  }
+  if (g->dev.joseph) return fail(WMG_EINVAL, "the Joseph kernel has parity (float64) mode only");
+  if (!workspace) return fail(WMG_EINVAL, "fast forward needs a workspace");
+  const size_t ws_item = wmg::fast_forward_workspace_bytes(g->dev.n, precision, dtype_in);
+  return cuda_rc(wmg::fast_forward_batch(g->dev, precision, dtype_in, dtype_out, x, workspace,
+                                         ws_item, y, batch, STREAM(stream),
+                                         g->dev.sym ? &g->axis : nullptr));
+}
+
+int wmg_backward_batch(const wmg_geometry* g, int mode, int precision, int dtype_in,
+                       int dtype_out, const void* y, void* x, int batch, int accumulate,
+                       void* stream) {
+  if (!g || !x || !y) return fail(WMG_EINVAL, "NULL argument");
+  if (batch < 0) return fail(WMG_EINVAL, "negative batch");
+  int rc = check_types(mode, precision, dtype_in, dtype_out);
+  if (rc) return rc;
+  const long long N = (long long)g->dev.n * g->dev.n, M = (long long)g->dev.m * g->dev.d;
+  if (mode == WMG_MODE_PARITY) {
+    for (int b = 0; b < batch; ++b) {
+      cudaError_t e = wmg::parity_backward(g->dev, (const double*)y + b * M, (double*)x + b * N,
+                                           accumulate != 0, nullptr, STREAM(stream));
+      if (e != cudaSuccess) return cuda_rc(e);
+    }
+    return WMG_OK;
+  }
+  if (g->dev.joseph) return fail(WMG_EINVAL, "the Joseph kernel has parity (float64) mode only");
+  return cuda_rc(wmg::fast_backward_batch(g->dev, precision, dtype_in, dtype_out, y, x,
+                                          accumulate != 0, batch, STREAM(stream),
+                                          g->dev.sym ? &g->axis : nullptr));
 }
 
 int wmg_row_sums(const wmg_geometry* g, double* out, void* stream) {

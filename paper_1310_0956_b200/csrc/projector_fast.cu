@@ -173,11 +173,19 @@ constexpr int kSplit = 8;
 
 // block (32 rays, kSplit slab segments); grid (ceil(d/32), m)
 template <typename TIn, typename TOut, typename R>
+// blockIdx.z selects one image of a batch (images n*n apart, sinograms bs_sino)
 __global__ void __launch_bounds__(32 * kSplit) fwd_split_kernel(GeomDev G,
                                                                 const TIn* __restrict__ img,
                                                                 const TIn* __restrict__ imgT,
-                                                                TOut* __restrict__ sino) {
+                                                                TOut* __restrict__ sino,
+                                                                long long bs_sino) {
   __shared__ R part[kSplit][33];
+  {
+    const long long zi = (long long)blockIdx.z * G.n * G.n;
+    img += zi;
+    imgT += zi;
+    sino += (long long)blockIdx.z * bs_sino;
+  }
   const int a = blockIdx.y;
   const int lane = threadIdx.x, seg = threadIdx.y;
   const int j = blockIdx.x * 32 + lane;
@@ -242,8 +250,11 @@ __global__ void __launch_bounds__(32 * kSplit) fwd_split_kernel(GeomDev G,
 template <typename TIn, typename TOut, typename R, bool kAccumulate>
 __global__ void __launch_bounds__(32 * kSplit) bwd_split_kernel(GeomDev G,
                                                                 const TIn* __restrict__ sino,
-                                                                TOut* __restrict__ img) {
+                                                                TOut* __restrict__ img,
+                                                                long long bs_sino) {
   __shared__ R part[kSplit][33];
+  sino += (long long)blockIdx.z * bs_sino;
+  img += (long long)blockIdx.z * G.n * G.n;
   const int n = G.n;
   const int lane = threadIdx.x, seg = threadIdx.y;
   const int ix = blockIdx.x * 32 + lane;
@@ -293,6 +304,8 @@ __global__ void __launch_bounds__(32 * kSplit) bwd_split_kernel(GeomDev G,
 template <typename T>
 __global__ void transpose_kernel(const T* __restrict__ in, T* __restrict__ out, int n) {
   __shared__ T tile[32][33];
+  in += (long long)blockIdx.z * n * n;     // batch of images
+  out += (long long)blockIdx.z * n * n;
   const int bx = blockIdx.x * 32, by = blockIdx.y * 32;
   for (int i = threadIdx.y; i < 32; i += 8) {
     const int r = by + i, c = bx + threadIdx.x;
@@ -993,20 +1006,22 @@ static inline bool use_split(const GeomDev& G) { return G.n <= 512; }
 
 template <typename TIn, typename TOut, typename R>
 static cudaError_t bwd_split_launch(const GeomDev& G, const void* y, void* x, bool accumulate,
-                                    cudaStream_t st) {
-  dim3 grid((G.n + 31) / 32, G.n), block(32, fast::kSplit);
+                                    cudaStream_t st, int batch = 1) {
+  dim3 grid((G.n + 31) / 32, G.n, batch), block(32, fast::kSplit);
+  const long long bs = (long long)G.m * G.d;
   if (accumulate)
     fast::bwd_split_kernel<TIn, TOut, R, true><<<grid, block, 0, st>>>(G, (const TIn*)y,
-                                                                       (TOut*)x);
+                                                                       (TOut*)x, bs);
   else
     fast::bwd_split_kernel<TIn, TOut, R, false><<<grid, block, 0, st>>>(G, (const TIn*)y,
-                                                                        (TOut*)x);
+                                                                        (TOut*)x, bs);
   return cudaGetLastError();
 }
 
 template <typename TIn>
-static cudaError_t launch_transpose(const TIn* in, TIn* out, int n, cudaStream_t st) {
-  dim3 grid((n + 31) / 32, (n + 31) / 32), block(32, 8);
+static cudaError_t launch_transpose(const TIn* in, TIn* out, int n, cudaStream_t st,
+                                   int batch = 1) {
+  dim3 grid((n + 31) / 32, (n + 31) / 32, batch), block(32, 8);
   fast::transpose_kernel<TIn><<<grid, block, 0, st>>>(in, out, n);
   return cudaGetLastError();
 }
@@ -1150,7 +1165,7 @@ static cudaError_t fwd_impl(const GeomDev& G, const void* x, void* xT_ws, void* 
   if (e != cudaSuccess) return e;
   if (use_split(G)) {
     dim3 sg((G.d + 31) / 32, G.m), sb(32, fast::kSplit);
-    fast::fwd_split_kernel<TIn, TOut, R><<<sg, sb, 0, st>>>(G, img, imgT, (TOut*)y);
+    fast::fwd_split_kernel<TIn, TOut, R><<<sg, sb, 0, st>>>(G, img, imgT, (TOut*)y, 0);
     return cudaGetLastError();
   }
   dim3 grid((G.d + 127) / 128, G.m);
@@ -1203,6 +1218,62 @@ cudaError_t fast_backward(const GeomDev& G, int precision, int tin, int tout, co
     if (tin == 0 && tout == 0) return bwd_impl<float, float, double>(G, y, x, accumulate, st);
   }
   return cudaErrorInvalidValue;
+}
+
+// ---------------------------------------------------------------------------
+// Batches of images / sinograms (contiguous, n*n and m*d apart): the WMG cycle
+// applies the node systems of sibling subproblems together.  The small-grid
+// float64 split kernels take the batch as gridDim.z (one launch fills the SMs
+// several times over); every other path loops over the batch.  Each item is
+// computed exactly as by the single-image call.
+// ---------------------------------------------------------------------------
+cudaError_t fast_forward_batch(const GeomDev& G, int precision, int tin, int tout, const void* x,
+                               void* ws, size_t ws_item, void* y, int batch, cudaStream_t st,
+                               const GeomDev* Gx) {
+  if (batch < 1) return cudaSuccess;
+  const long long N = (long long)G.n * G.n, M = (long long)G.m * G.d;
+  const size_t si = tin == 1 ? 8 : 4, so = tout == 1 ? 8 : 4;
+  const bool split64 = precision == 1 && tin == 1 && tout == 1 && use_split(G) &&
+                       !(use_sym_fwd(G) && Gx);
+  if (split64 && G.m > 0 && G.d > 0) {
+    const double* img = (const double*)x;
+    double* imgT = (double*)ws;        // batch * n*n transposed copies
+    cudaError_t e = launch_transpose<double>(img, imgT, G.n, st, batch);
+    if (e != cudaSuccess) return e;
+    dim3 sg((G.d + 31) / 32, G.m, batch), sb(32, fast::kSplit);
+    fast::fwd_split_kernel<double, double, double><<<sg, sb, 0, st>>>(G, img, imgT, (double*)y,
+                                                                      M);
+    return cudaGetLastError();
+  }
+  for (int b = 0; b < batch; ++b) {
+    cudaError_t e = fast_forward(G, precision, tin, tout, (const char*)x + b * N * si,
+                                 (char*)ws + b * ws_item, (char*)y + b * M * so, st, Gx);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+cudaError_t fast_backward_batch(const GeomDev& G, int precision, int tin, int tout, const void* y,
+                                void* x, bool accumulate, int batch, cudaStream_t st,
+                                const GeomDev* Gx) {
+  if (batch < 1 || G.n == 0) return cudaSuccess;
+  const long long N = (long long)G.n * G.n, M = (long long)G.m * G.d;
+  const size_t si = tin == 1 ? 8 : 4, so = tout == 1 ? 8 : 4;
+  const bool sym = (precision == 1 ? use_sym_bwd(G) : use_sym_bwd(G)) && Gx;
+  if (use_split(G) && !sym && tin == tout) {
+    if (precision == 1 && tin == 1)
+      return bwd_split_launch<double, double, double>(G, y, x, accumulate, st, batch);
+    if (precision == 0 && tin == 1)
+      return bwd_split_launch<double, double, float>(G, y, x, accumulate, st, batch);
+    if (precision == 0 && tin == 0)
+      return bwd_split_launch<float, float, float>(G, y, x, accumulate, st, batch);
+  }
+  for (int b = 0; b < batch; ++b) {
+    cudaError_t e = fast_backward(G, precision, tin, tout, (const char*)y + b * M * si,
+                                  (char*)x + b * N * so, accumulate, st, Gx);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 }  // namespace wmg

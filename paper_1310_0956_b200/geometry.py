@@ -243,6 +243,37 @@ class LineProjector:
                D.ptr(x), D.ptr(out), D.ptr(ws), D.ptr(anomaly), D.stream_handle())
         return out
 
+    def forward_batch_(self, X, OUT):
+        """OUT[b] = W X[b] for a contiguous batch (B, n*n) -> (B, M) on the device."""
+        t = D.torch()
+        B = X.shape[0]
+        if X.numel() != B * self.shape[1] or OUT.numel() != B * self.shape[0]:
+            raise DimensionMismatchError("forward_batch_: shape mismatch")
+        tin, tout = self._code(X), self._code(OUT)
+        ws = None
+        if self._mode_code == N.MODE_FAST:
+            key = ("batch", tin, B)
+            ws = self._ws.get(key)
+            if ws is None:
+                nbytes = N.ctypes.c_size_t()
+                N.call("wmg_forward_workspace", self._h, self.precision, tin,
+                       N.ctypes.byref(nbytes))
+                ws = t.zeros((B * nbytes.value + 7) // 8, dtype=t.float64, device=self.device)
+                self._ws[key] = ws
+        N.call("wmg_forward_batch", self._h, self._mode_code, self.precision, tin, tout,
+               D.ptr(X), D.ptr(OUT), B, D.ptr(ws), D.stream_handle())
+        return OUT
+
+    def backward_batch_(self, Y, OUT, accumulate=False):
+        """OUT[b] (+)= W^T Y[b] for a contiguous batch (B, M) -> (B, n*n)."""
+        B = Y.shape[0]
+        if Y.numel() != B * self.shape[0] or OUT.numel() != B * self.shape[1]:
+            raise DimensionMismatchError("backward_batch_: shape mismatch")
+        N.call("wmg_backward_batch", self._h, self._mode_code, self.precision, self._code(Y),
+               self._code(OUT), D.ptr(Y), D.ptr(OUT), B, int(bool(accumulate)),
+               D.stream_handle())
+        return OUT
+
     def backward_(self, y, out, accumulate=False, anomaly=None):
         """out (+)= W^T y on device tensors."""
         tin, tout = self._code(y), self._code(out)

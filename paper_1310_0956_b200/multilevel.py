@@ -464,6 +464,141 @@ def _node_solve_(node: WmgNode, r, multiplicative: bool):
     return z
 
 
+# ------------------------------------------------ sibling batches (hybrid cycle)
+# In the hybrid cycle the LH/HL/HH children of a node are solved independently,
+# so nodes of one depth are processed in lockstep: one batched projector pair
+# serves all their node-system applications (on small grids one launch of the
+# batched fp64 kernels instead of one per node).  Every item is computed
+# exactly as by the single-node path (same kernels, same arithmetic), so the
+# batched cycle is bit-identical to the sequential one.
+BATCH_SIBLINGS = True      # tests switch it off to compare with the sequential cycle
+
+
+def _batchable(h) -> bool:
+    w = h.node_projector
+    return BATCH_SIBLINGS and hasattr(w, "forward_batch_") and not _is_sharded(w)
+
+
+def _apply_system_batch_(nodes, V, OUT):
+    """OUT[b] = (P_b^T P_b + lam) V[b] for nodes of one depth (batched pair)."""
+    h = nodes[0].hierarchy
+    w = h.node_projector
+    B = len(nodes)
+    k = len(nodes[0].bands)
+    n2 = h.n * h.n
+    M = w.shape[0]
+    F = h.buf(("bpf", B), B * n2).view(B, n2)
+    for b, nd in enumerate(nodes):
+        cur = V[b]
+        for lv in range(k - 1, -1, -1):
+            side_f = h.n >> lv
+            dst = F[b] if lv == 0 else h.buf(("bpfl", lv, b), side_f * side_f)
+            prolong(side_f, cur, nd.bands[lv], dst, accumulate=False)
+            cur = dst
+    sino = h.buf(("bsino", B), B * M).view(B, M)
+    w.forward_batch_(F, sino)
+    img = h.buf(("bimg", B), B * n2).view(B, n2)
+    w.backward_batch_(sino, img)
+    for b, nd in enumerate(nodes):
+        cur = img[b]
+        for lv in range(k):
+            side_f = h.n >> lv
+            dst = OUT[b] if lv == k - 1 else h.buf(("brs", lv, b), (side_f // 2) ** 2)
+            restrict(side_f, cur, (nd.bands[lv],), out=dst.view(1, -1))
+            cur = dst
+        if nd.lam != 0:
+            D.add_scaled(OUT[b], OUT[b], nd.lam, +1, V[b])
+    return OUT
+
+
+def _leaf_solve_batch_(nodes, R, Z):
+    """Z[b] = G_b^-1 R[b]: one batched GEMV per run of consecutive leaf slots."""
+    h = nodes[0].hierarchy
+    slots = [_leaf_slot(h, nd) for nd in nodes]
+    from .sparse_kernels import batched_gemv
+    i = 0
+    while i < len(slots):
+        j = i + 1
+        while j < len(slots) and slots[j] == slots[j - 1] + 1:
+            j += 1
+        batched_gemv(h.leaf_inverses[slots[i]:slots[i] + (j - i)], R[i:j], out=Z[i:j])
+        i = j
+    return Z
+
+
+def _node_solve_batch_(nodes, R):
+    """Z[b] ~= A_b^-1 R[b] for hybrid-cycle nodes of one depth (R: (B, dim))."""
+    t = D.torch()
+    B = len(nodes)
+    if B == 1:
+        return _node_solve_(nodes[0], R[0].contiguous(), False).view(1, -1)
+    h = nodes[0].hierarchy
+    if nodes[0].is_coarsest:
+        if h is not None and h.leaf_inverses is not None:
+            return _leaf_solve_batch_(nodes, R, t.empty_like(R))
+        return t.stack([_node_solve_(nd, R[b].contiguous(), False)
+                        for b, nd in enumerate(nodes)])
+    if h.nu_pre == 0 and h.nu_post == 0:
+        return _wtg_batch_(nodes, R)
+    Z = t.zeros_like(R)
+    AZ = t.empty_like(R)
+    RES = t.empty_like(R)
+    UPD = t.empty_like(R)
+
+    def sweep(z_is_zero):
+        if z_is_zero:
+            RES.copy_(R)
+        else:
+            _apply_system_batch_(nodes, Z, AZ)
+            D.axpy(RES.view(-1), R.view(-1), 1.0, -1, AZ.view(-1))
+        for b, nd in enumerate(nodes):
+            D.hadamard(UPD[b], nd.smooth_c, RES[b])
+            D.axpy(Z[b], Z[b], nd.smooth_omega, +1, UPD[b])
+
+    zero = True
+    for _ in range(h.nu_pre):
+        sweep(zero)
+        zero = False
+    if zero:
+        Z.copy_(_wtg_batch_(nodes, R))
+    else:
+        _apply_system_batch_(nodes, Z, AZ)
+        D.axpy(RES.view(-1), R.view(-1), 1.0, -1, AZ.view(-1))
+        E = _wtg_batch_(nodes, RES)
+        D.axpy(Z.view(-1), Z.view(-1), 1.0, +1, E.view(-1))
+    for _ in range(h.nu_post):
+        sweep(False)
+    return Z
+
+
+def _wtg_batch_(nodes, R):
+    """Hybrid two-grid correction of several nodes of one depth in lockstep."""
+    t = D.torch()
+    B = len(nodes)
+    side = nodes[0].side
+    nc = (side // 2) ** 2
+    RLL = t.empty((B, nc), dtype=R.dtype, device=R.device)
+    for b in range(B):
+        restrict(side, R[b], ("LL",), out=RLL[b].view(1, -1))
+    ZLL = _node_solve_batch_([nd.children["LL"] for nd in nodes], RLL)
+    E = t.empty_like(R)
+    for b in range(B):
+        prolong(side, ZLL[b], "LL", E[b], accumulate=False)
+    AE = t.empty_like(R)
+    _apply_system_batch_(nodes, E, AE)
+    RW = t.empty_like(R)
+    D.axpy(RW.view(-1), R.view(-1), 1.0, -1, AE.view(-1))
+    RB = t.empty((B, 3, nc), dtype=R.dtype, device=R.device)
+    for b in range(B):
+        restrict(side, RW[b], ("LH", "HL", "HH"), out=RB[b])
+    kids = [nd.children[band] for nd in nodes for band in ("LH", "HL", "HH")]
+    ZK = _node_solve_batch_(kids, RB.view(3 * B, nc))
+    for b in range(B):
+        for i, band in enumerate(("LH", "HL", "HH")):
+            prolong(side, ZK[3 * b + i], band, E[b], accumulate=True)
+    return E
+
+
 def _wtg_(node: WmgNode, r, multiplicative: bool):
     """One wavelet two-grid correction, zero initial guess (multilevel.py:175-198)."""
     t = D.torch()
@@ -487,6 +622,11 @@ def _wtg_(node: WmgNode, r, multiplicative: bool):
             zb3 = batched_gemv(h.leaf_inverses[i0:i0 + 3], rb)
             for i, band in enumerate(("LH", "HL", "HH")):
                 prolong(side, zb3[i], band, e, accumulate=True)
+            return e
+        if h is not None and _batchable(h):
+            zk = _node_solve_batch_(kids, rb)          # the three siblings in lockstep
+            for i, band in enumerate(("LH", "HL", "HH")):
+                prolong(side, zk[i], band, e, accumulate=True)
             return e
         for i, band in enumerate(("LH", "HL", "HH")):
             zb = _node_solve_(kids[i], rb[i].contiguous(), multiplicative)
