@@ -20,6 +20,8 @@
 //
 // Tolerance vs the float64 reference: 1e-5 relative (fp32 data), see
 // tests/test_gpu_projector.py.
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace wmg {
@@ -787,6 +789,12 @@ __global__ void pad_transpose64_kernel(const T* __restrict__ in, double* __restr
                                        double* __restrict__ PT, int n) {
   __shared__ double tile[32][33];
   const int pitch = n + 2 * kPadMargin;
+  {   // batch: images n*n apart, plane pairs 2 * n * pitch apart
+    const long long z = blockIdx.z;
+    in += z * n * n;
+    P += z * 2LL * n * pitch;
+    PT += z * 2LL * n * pitch;
+  }
   const int bx = blockIdx.x * 32, by = blockIdx.y * 32;
   for (int i = threadIdx.y; i < 32; i += 8) {
     const int r = by + i, c = bx + threadIdx.x;
@@ -801,6 +809,83 @@ __global__ void pad_transpose64_kernel(const T* __restrict__ in, double* __restr
   for (int i = threadIdx.y; i < 32; i += 8) {
     const int c = bx + i, r = by + threadIdx.x;
     if (r < n && c < n) PT[(long long)c * pitch + kPadMargin + r] = tile[threadIdx.x][i];
+  }
+}
+
+// Small-grid float64 forward on the padded planes: one ray per lane, kSplit
+// slab segments per ray (threadIdx.y) reduced in shared memory in segment
+// order; u is evaluated directly at every slab end (fma), the two straddling
+// pixels are read without bounds checks (zero margins) and blended as
+// L v0 + wh (v1 - v0).  blockIdx.z = batch item.
+template <typename TOut>
+__global__ void __launch_bounds__(32 * kSplit) fwd_split64_kernel(GeomDev G,
+                                                                  const double* __restrict__ P,
+                                                                  const double* __restrict__ PT,
+                                                                  TOut* __restrict__ sino,
+                                                                  long long bs_sino) {
+  __shared__ double part[kSplit][33];
+  const int a = blockIdx.y;
+  const int lane = threadIdx.x, seg = threadIdx.y;
+  const int j = blockIdx.x * 32 + lane;
+  const int n = G.n;
+  const int pitch = n + 2 * kPadMargin;
+  {
+    const long long zp = (long long)blockIdx.z * 2LL * n * pitch;
+    P += zp;
+    PT += zp;
+    sino += (long long)blockIdx.z * bs_sino;
+  }
+  double acc = 0.0;
+  if (j < G.d) {
+    const AngleParams& A = G.ang[a];
+    const double u0 = A.u0 + ((double)j - (double)(G.d - 1) * 0.5) * A.du;
+    const double slope = A.slope;
+    int r0 = 0, r1 = n - 1;
+    if (slope > 0.0) {
+      const double ra = floor((-1.0 - u0) / slope) - 1.0;
+      const double rb = ceil(((double)n + 1.0 - u0) / slope) + 1.0;
+      r0 = (int)fmax(ra, 0.0);
+      r1 = (int)fmin(rb, (double)(n - 1));
+    } else if (u0 < -1.0 || u0 > (double)n + 1.0) {
+      r1 = -1;
+    }
+    const int len = r1 - r0 + 1;
+    const int rs = r0 + (len > 0 ? (len * seg) / kSplit : 0);
+    const int re = r0 + (len > 0 ? (len * (seg + 1)) / kSplit : 0) - 1;
+    const double* __restrict__ src = (A.major ? PT : P) + kPadMargin;
+    const double L = A.L, Ls = A.Ls;
+    const double* row = src + (long long)rs * pitch;
+    if (!A.mirror) {
+      for (int r = rs; r <= re; ++r) {
+        const double uh = fma((double)(r + 1), slope, u0);
+        const double fk = floor(uh);
+        const double wh = fmin((uh - fk) * Ls, L);     // NaN (0 * inf) -> L
+        const double* p = row + (int)fk;
+        const double v1 = __ldg(p), v0 = __ldg(p - 1);
+        acc = fma(L, v0, acc);
+        acc = fma(wh, v1 - v0, acc);
+        row += pitch;
+      }
+    } else {
+      for (int r = rs; r <= re; ++r) {
+        const double uh = fma((double)(r + 1), slope, u0);
+        const double fk = floor(uh);
+        const double wh = fmin((uh - fk) * Ls, L);
+        const double* p = row + (n - 1 - (int)fk);
+        const double v1 = __ldg(p), v0 = __ldg(p + 1);
+        acc = fma(L, v0, acc);
+        acc = fma(wh, v1 - v0, acc);
+        row += pitch;
+      }
+    }
+  }
+  part[seg][lane] = acc;
+  __syncthreads();
+  if (seg == 0 && j < G.d) {
+    double sum = part[0][lane];
+#pragma unroll
+    for (int q = 1; q < kSplit; ++q) sum += part[q][lane];
+    sino[(long long)(G.rowmap ? G.rowmap[a] : a) * G.d + j] = (TOut)sum;
   }
 }
 
@@ -877,10 +962,15 @@ __global__ void __launch_bounds__(128) fwd_sym64_kernel(GeomDev G, const double*
 // symmetric backprojector in float64: 52-fractional-bit fixed point
 constexpr double kQ52 = 4503599627370496.0;   // 2^52
 constexpr int kSym64Chunk = 8;
+constexpr int kSym64MaxSplit = 32;   // small-grid angle splits (scratch: 32 n^2 doubles)
 
 template <typename TIn, typename TOut, bool kAccumulate>
+// nsplit > 1 (small grids): blockIdx.z takes a slice of the primary angles and
+// the block writes its four partial images to part[z] (full-image layout);
+// sym_reduce_kernel sums the slices in z order (deterministic).
 __global__ void __launch_bounds__(256) bwd_sym64_kernel(GeomDev G, const TIn* __restrict__ sino,
-                                                        TOut* __restrict__ img) {
+                                                        TOut* __restrict__ img, int nsplit,
+                                                        double* __restrict__ part) {
   __shared__ double4 winA[kSym64Chunk][kBwdWin];
   __shared__ double4 winB[kSym64Chunk][kBwdWin];
   __shared__ long long qx[kSym64Chunk][kBwdTile];
@@ -899,9 +989,10 @@ __global__ void __launch_bounds__(256) bwd_sym64_kernel(GeomDev G, const TIn* __
   for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int q = 0; q < 4; ++q) acc[i][q] = 0.0;
-  const int n_prim = G.n_prim;
-  for (int c0 = 0; c0 < n_prim; c0 += kSym64Chunk) {
-    const int na = min(kSym64Chunk, n_prim - c0);
+  const int q_begin = (int)((long long)G.n_prim * blockIdx.z / nsplit);
+  const int q_end = (int)((long long)G.n_prim * (blockIdx.z + 1) / nsplit);
+  for (int c0 = q_begin; c0 < q_end; c0 += kSym64Chunk) {
+    const int na = min(kSym64Chunk, q_end - c0);
     __syncthreads();
     if (tid < na) {
       const int q = c0 + tid;
@@ -969,12 +1060,27 @@ __global__ void __launch_bounds__(256) bwd_sym64_kernel(GeomDev G, const TIn* __
                             (long long)(n - 1 - row) * n + col};
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      if (kAccumulate)
+      if (part)
+        part[(long long)blockIdx.z * n * n + p[q]] = acc[i][q];
+      else if (kAccumulate)
         img[p[q]] = (TOut)((double)img[p[q]] + acc[i][q]);
       else
         img[p[q]] = (TOut)acc[i][q];
     }
   }
+}
+
+template <typename TOut, bool kAccumulate>
+__global__ void sym_reduce_kernel(const double* __restrict__ part, int nsplit, long long N,
+                                  TOut* __restrict__ img) {
+  const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= N) return;
+  double s = part[p];
+  for (int z = 1; z < nsplit; ++z) s += part[(long long)z * N + p];
+  if (kAccumulate)
+    img[p] = (TOut)((double)img[p] + s);
+  else
+    img[p] = (TOut)s;
 }
 
 }  // namespace fast
@@ -1142,14 +1248,31 @@ static cudaError_t fwd64_impl(const GeomDev& G, const void* x, void* ws, void* y
 
 template <typename TIn, typename TOut>
 static cudaError_t bwd64_impl(const GeomDev& G, const void* y, void* x, bool accumulate,
-                              cudaStream_t st, const GeomDev* Gx) {
+                              cudaStream_t st, const GeomDev* Gx, double* scratch = nullptr) {
   if (!(G.sym && Gx)) return cudaErrorNotSupported;
-  dim3 grid(G.n / 64, G.n / 64);
+  const int tiles = (G.n / 64) * (G.n / 64);
+  // small grids: split the angles over blockIdx.z so the grid fills the SMs
+  int nsplit = 1;
+  if (scratch) nsplit = max(1, min(fast::kSym64MaxSplit, min((2 * 148 + tiles - 1) / tiles,
+                                                       G.n_prim / 4)));
+  dim3 grid(G.n / 64, G.n / 64, nsplit);
+  double* part = nsplit > 1 ? scratch : nullptr;
   if (accumulate)
-    fast::bwd_sym64_kernel<TIn, TOut, true><<<grid, 256, 0, st>>>(G, (const TIn*)y, (TOut*)x);
+    fast::bwd_sym64_kernel<TIn, TOut, true><<<grid, 256, 0, st>>>(G, (const TIn*)y, (TOut*)x,
+                                                                  nsplit, part);
   else
-    fast::bwd_sym64_kernel<TIn, TOut, false><<<grid, 256, 0, st>>>(G, (const TIn*)y, (TOut*)x);
+    fast::bwd_sym64_kernel<TIn, TOut, false><<<grid, 256, 0, st>>>(G, (const TIn*)y, (TOut*)x,
+                                                                   nsplit, part);
   cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess && part) {
+    const long long N = (long long)G.n * G.n;
+    const unsigned rb = (unsigned)((N + 255) / 256);
+    if (accumulate)
+      fast::sym_reduce_kernel<TOut, true><<<rb, 256, 0, st>>>(part, nsplit, N, (TOut*)x);
+    else
+      fast::sym_reduce_kernel<TOut, false><<<rb, 256, 0, st>>>(part, nsplit, N, (TOut*)x);
+    e = cudaGetLastError();
+  }
   if (e != cudaSuccess || Gx->m == 0) return e;
   dim3 g2((G.n + 31) / 32, (G.n + 7) / 8);
   fast::bwd_kernel<TIn, TOut, double, true><<<g2, 256, 0, st>>>(*Gx, (const TIn*)y, (TOut*)x);
@@ -1161,6 +1284,18 @@ static cudaError_t fwd_impl(const GeomDev& G, const void* x, void* xT_ws, void* 
                             cudaStream_t st) {
   const TIn* img = (const TIn*)x;
   TIn* imgT = (TIn*)xT_ws;
+  if (sizeof(R) == 8 && use_split(G)) {
+    // padded float64 planes (the workspace holds 2 * n * (n + 2 margin) doubles)
+    double* P = (double*)xT_ws;
+    double* PT = P + (long long)G.n * (G.n + 2 * kPadMargin);
+    dim3 tg((G.n + 31) / 32, (G.n + 31) / 32), tb(32, 8);
+    fast::pad_transpose64_kernel<TIn><<<tg, tb, 0, st>>>(img, P, PT, G.n);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    dim3 sg((G.d + 31) / 32, G.m), sb(32, fast::kSplit);
+    fast::fwd_split64_kernel<TOut><<<sg, sb, 0, st>>>(G, P, PT, (TOut*)y, 0);
+    return cudaGetLastError();
+  }
   cudaError_t e = launch_transpose<TIn>(img, imgT, G.n, st);
   if (e != cudaSuccess) return e;
   if (use_split(G)) {
@@ -1187,7 +1322,8 @@ static cudaError_t bwd_impl(const GeomDev& G, const void* y, void* x, bool accum
 
 // precision: 0 = fp32 arithmetic, 1 = fp64 arithmetic
 cudaError_t fast_forward(const GeomDev& G, int precision, int tin, int tout, const void* x,
-                         void* xT_ws, void* y, cudaStream_t st, const GeomDev* Gx) {
+                         void* xT_ws, void* y, cudaStream_t st, const GeomDev* Gx,
+                         double* scratch) {
   if (G.m == 0 || G.d == 0) return cudaSuccess;
   if (precision == 0) {
     if (tin == 0 && tout == 0) return fwd_v2_impl<float, float>(G, x, xT_ws, y, st, Gx);
@@ -1203,8 +1339,14 @@ cudaError_t fast_forward(const GeomDev& G, int precision, int tin, int tout, con
   return cudaErrorInvalidValue;
 }
 
+size_t fast_backward_scratch_bytes(const GeomDev& G, int precision) {
+  if (precision != 1 || !G.sym || !use_split(G) || G.n % 64) return 0;
+  return sizeof(double) * (size_t)fast::kSym64MaxSplit * (size_t)G.n * (size_t)G.n;
+}
+
 cudaError_t fast_backward(const GeomDev& G, int precision, int tin, int tout, const void* y,
-                          void* x, bool accumulate, cudaStream_t st, const GeomDev* Gx) {
+                          void* x, bool accumulate, cudaStream_t st, const GeomDev* Gx,
+                          double* scratch) {
   if (G.n == 0) return cudaSuccess;
   if (precision == 0) {
     if (tin == 0 && tout == 0) return bwd_v2_impl<float, float>(G, y, x, accumulate, st, Gx);
@@ -1214,6 +1356,9 @@ cudaError_t fast_backward(const GeomDev& G, int precision, int tin, int tout, co
   } else {
     if (use_sym_bwd(G) && Gx && tin == 1 && tout == 1)
       return bwd64_impl<double, double>(G, y, x, accumulate, st, Gx);
+    // small symmetric grids: angle-split symmetric kernel (4 images per weight)
+    if (G.sym == 1 && use_split(G) && Gx && scratch && tin == 1 && tout == 1)
+      return bwd64_impl<double, double>(G, y, x, accumulate, st, Gx, scratch);
     if (tin == 1 && tout == 1) return bwd_impl<double, double, double>(G, y, x, accumulate, st);
     if (tin == 0 && tout == 0) return bwd_impl<float, float, double>(G, y, x, accumulate, st);
   }
@@ -1229,25 +1374,28 @@ cudaError_t fast_backward(const GeomDev& G, int precision, int tin, int tout, co
 // ---------------------------------------------------------------------------
 cudaError_t fast_forward_batch(const GeomDev& G, int precision, int tin, int tout, const void* x,
                                void* ws, size_t ws_item, void* y, int batch, cudaStream_t st,
-                               const GeomDev* Gx) {
+                               const GeomDev* Gx, double* scratch) {
   if (batch < 1) return cudaSuccess;
   const long long N = (long long)G.n * G.n, M = (long long)G.m * G.d;
   const size_t si = tin == 1 ? 8 : 4, so = tout == 1 ? 8 : 4;
   const bool split64 = precision == 1 && tin == 1 && tout == 1 && use_split(G) &&
                        !(use_sym_fwd(G) && Gx);
   if (split64 && G.m > 0 && G.d > 0) {
-    const double* img = (const double*)x;
-    double* imgT = (double*)ws;        // batch * n*n transposed copies
-    cudaError_t e = launch_transpose<double>(img, imgT, G.n, st, batch);
+    // batch * (P, PT) padded planes; ws_item = 2 * n * (n + 2 margin) doubles
+    double* P = (double*)ws;
+    double* PT = P + (long long)G.n * (G.n + 2 * kPadMargin);
+    dim3 tg((G.n + 31) / 32, (G.n + 31) / 32, batch), tb(32, 8);
+    fast::pad_transpose64_kernel<double><<<tg, tb, 0, st>>>((const double*)x, P, PT, G.n);
+    cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     dim3 sg((G.d + 31) / 32, G.m, batch), sb(32, fast::kSplit);
-    fast::fwd_split_kernel<double, double, double><<<sg, sb, 0, st>>>(G, img, imgT, (double*)y,
-                                                                      M);
+    fast::fwd_split64_kernel<double><<<sg, sb, 0, st>>>(G, P, PT, (double*)y, M);
     return cudaGetLastError();
   }
   for (int b = 0; b < batch; ++b) {
     cudaError_t e = fast_forward(G, precision, tin, tout, (const char*)x + b * N * si,
-                                 (char*)ws + b * ws_item, (char*)y + b * M * so, st, Gx);
+                                 (char*)ws + b * ws_item, (char*)y + b * M * so, st, Gx,
+                                 scratch);
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;
@@ -1255,11 +1403,12 @@ cudaError_t fast_forward_batch(const GeomDev& G, int precision, int tin, int tou
 
 cudaError_t fast_backward_batch(const GeomDev& G, int precision, int tin, int tout, const void* y,
                                 void* x, bool accumulate, int batch, cudaStream_t st,
-                                const GeomDev* Gx) {
+                                const GeomDev* Gx, double* scratch) {
   if (batch < 1 || G.n == 0) return cudaSuccess;
   const long long N = (long long)G.n * G.n, M = (long long)G.m * G.d;
   const size_t si = tin == 1 ? 8 : 4, so = tout == 1 ? 8 : 4;
-  const bool sym = (precision == 1 ? use_sym_bwd(G) : use_sym_bwd(G)) && Gx;
+  const bool sym = (use_sym_bwd(G) || (precision == 1 && G.sym == 1 && scratch && tin == 1 &&
+                                       tout == 1)) && Gx;
   if (use_split(G) && !sym && tin == tout) {
     if (precision == 1 && tin == 1)
       return bwd_split_launch<double, double, double>(G, y, x, accumulate, st, batch);
@@ -1270,7 +1419,7 @@ cudaError_t fast_backward_batch(const GeomDev& G, int precision, int tin, int to
   }
   for (int b = 0; b < batch; ++b) {
     cudaError_t e = fast_backward(G, precision, tin, tout, (const char*)y + b * M * si,
-                                  (char*)x + b * N * so, accumulate, st, Gx);
+                                  (char*)x + b * N * so, accumulate, st, Gx, scratch);
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;
