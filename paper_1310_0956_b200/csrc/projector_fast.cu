@@ -172,6 +172,7 @@ __global__ void __launch_bounds__(256) bwd_kernel(GeomDev G, const TIn* __restri
 // kSplit threads -- consecutive slab (angle) segments -- and reduce the
 // partial sums in shared memory in segment order (deterministic).
 constexpr int kSplit = 8;
+constexpr int kSplitF = 8;   // slab segments per ray of the padded-plane fp64 forward
 
 // block (32 rays, kSplit slab segments); grid (ceil(d/32), m)
 template <typename TIn, typename TOut, typename R>
@@ -818,12 +819,12 @@ __global__ void pad_transpose64_kernel(const T* __restrict__ in, double* __restr
 // pixels are read without bounds checks (zero margins) and blended as
 // L v0 + wh (v1 - v0).  blockIdx.z = batch item.
 template <typename TOut>
-__global__ void __launch_bounds__(32 * kSplit) fwd_split64_kernel(GeomDev G,
+__global__ void __launch_bounds__(32 * kSplitF) fwd_split64_kernel(GeomDev G,
                                                                   const double* __restrict__ P,
                                                                   const double* __restrict__ PT,
                                                                   TOut* __restrict__ sino,
                                                                   long long bs_sino) {
-  __shared__ double part[kSplit][33];
+  __shared__ double part[kSplitF][33];
   const int a = blockIdx.y;
   const int lane = threadIdx.x, seg = threadIdx.y;
   const int j = blockIdx.x * 32 + lane;
@@ -850,8 +851,8 @@ __global__ void __launch_bounds__(32 * kSplit) fwd_split64_kernel(GeomDev G,
       r1 = -1;
     }
     const int len = r1 - r0 + 1;
-    const int rs = r0 + (len > 0 ? (len * seg) / kSplit : 0);
-    const int re = r0 + (len > 0 ? (len * (seg + 1)) / kSplit : 0) - 1;
+    const int rs = r0 + (len > 0 ? (len * seg) / kSplitF : 0);
+    const int re = r0 + (len > 0 ? (len * (seg + 1)) / kSplitF : 0) - 1;
     const double* __restrict__ src = (A.major ? PT : P) + kPadMargin;
     const double L = A.L, Ls = A.Ls;
     const double* row = src + (long long)rs * pitch;
@@ -884,7 +885,7 @@ __global__ void __launch_bounds__(32 * kSplit) fwd_split64_kernel(GeomDev G,
   if (seg == 0 && j < G.d) {
     double sum = part[0][lane];
 #pragma unroll
-    for (int q = 1; q < kSplit; ++q) sum += part[q][lane];
+    for (int q = 1; q < kSplitF; ++q) sum += part[q][lane];
     sino[(long long)(G.rowmap ? G.rowmap[a] : a) * G.d + j] = (TOut)sum;
   }
 }
@@ -1292,7 +1293,7 @@ static cudaError_t fwd_impl(const GeomDev& G, const void* x, void* xT_ws, void* 
     fast::pad_transpose64_kernel<TIn><<<tg, tb, 0, st>>>(img, P, PT, G.n);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    dim3 sg((G.d + 31) / 32, G.m), sb(32, fast::kSplit);
+    dim3 sg((G.d + 31) / 32, G.m), sb(32, fast::kSplitF);
     fast::fwd_split64_kernel<TOut><<<sg, sb, 0, st>>>(G, P, PT, (TOut*)y, 0);
     return cudaGetLastError();
   }
@@ -1388,7 +1389,7 @@ cudaError_t fast_forward_batch(const GeomDev& G, int precision, int tin, int tou
     fast::pad_transpose64_kernel<double><<<tg, tb, 0, st>>>((const double*)x, P, PT, G.n);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    dim3 sg((G.d + 31) / 32, G.m, batch), sb(32, fast::kSplit);
+    dim3 sg((G.d + 31) / 32, G.m, batch), sb(32, fast::kSplitF);
     fast::fwd_split64_kernel<double><<<sg, sb, 0, st>>>(G, P, PT, (double*)y, M);
     return cudaGetLastError();
   }
