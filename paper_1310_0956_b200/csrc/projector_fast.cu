@@ -173,6 +173,7 @@ __global__ void __launch_bounds__(256) bwd_kernel(GeomDev G, const TIn* __restri
 // partial sums in shared memory in segment order (deterministic).
 constexpr int kSplit = 8;
 constexpr int kSplitF = 8;   // slab segments per ray of the padded-plane fp64 forward
+constexpr int kFwdAG = 4;    // adjacent angles per symmetric-forward block
 
 // block (32 rays, kSplit slab segments); grid (ceil(d/32), m)
 template <typename TIn, typename TOut, typename R>
@@ -673,15 +674,28 @@ __global__ void __launch_bounds__(256, 5) bwd_sym_kernel(GeomDev G, const TIn* _
 // (n-1-s, q) of one walk (x-mirror / 180-degree rotation of the grid), so one
 // thread walks a representative ray a in [1, m/2), j < ceil(d/2) and
 // accumulates all four.  Representative angles are never mirrored (slope > 0).
-template <typename TOut>
-__global__ void __launch_bounds__(128) fwd_sym_kernel(GeomDev G, const float* __restrict__ P,
+// Block layout: kAG == 1 -> 128 consecutive rays of one angle; kAG == 4 -> the
+// same 32 rays of 4 adjacent angles (one warp each).  Adjacent angles walk
+// nearly the same pixels slab after slab (the rays drift apart by ~n * dtheta
+// pixels over the whole image), so the co-resident warps of a block share
+// their L1 lines.
+template <typename TOut, int kAG>
+__global__ void __launch_bounds__(kAG == 1 ? 128 : 32 * kAG) fwd_sym_kernel(GeomDev G, const float* __restrict__ P,
                                                       const float* __restrict__ PT,
                                                       TOut* __restrict__ sino) {
-  const int a = G.half[blockIdx.y];
+  int hidx, j;
+  if (kAG == 1) {
+    hidx = blockIdx.y;
+    j = blockIdx.x * 128 + threadIdx.x;
+  } else {
+    hidx = blockIdx.y * kAG + (threadIdx.x >> 5);
+    j = blockIdx.x * 32 + (threadIdx.x & 31);
+    if (hidx >= G.n_half) return;          // whole warp
+  }
+  const int a = G.half[hidx];
   const int b = G.mir[a];
   const int d = G.d, m = G.m, n = G.n;
   const int jh = (d + 1) / 2;
-  const int j = blockIdx.x * 128 + threadIdx.x;
   const AngleParams& A = G.ang[a];
   const int pitch = n + 2 * kPadMargin;
   const double off = (double)j - (double)(d - 1) * 0.5;
@@ -1104,7 +1118,7 @@ static inline bool use_sym_bwd(const GeomDev& G) {
   return G.sym >= 2 || (G.sym == 1 && G.n >= 1024);
 }
 static inline bool use_sym_fwd(const GeomDev& G) {
-  const long long blocks = (long long)(((G.d + 1) / 2 + 127) / 128) * G.n_half;
+  const long long blocks = (long long)(((G.d + 1) / 2 + 127) / 128) * G.n_half;   // 128-ray units
   return G.sym >= 2 || (G.sym == 1 && blocks >= 4LL * 148);
 }
 static inline bool use_tiled_bwd(const GeomDev& G) { return G.n >= 768; }
@@ -1147,8 +1161,14 @@ static cudaError_t fwd_v2_impl(const GeomDev& G, const void* x, void* ws, void* 
     if (G.sym == 4 && tma_forward_supported(G)) {   // opt-in: TMA-staged forward
       e = tma_forward<TOut>(G, P, PT, (TOut*)y, nullptr, st);
     } else {
-      dim3 sgrid(((G.d + 1) / 2 + 127) / 128, G.n_half);
-      fast::fwd_sym_kernel<TOut><<<sgrid, 128, 0, st>>>(G, P, PT, (TOut*)y);
+      if (G.sym & 16) {   // testing: one angle per block
+        dim3 sgrid(((G.d + 1) / 2 + 127) / 128, G.n_half);
+        fast::fwd_sym_kernel<TOut, 1><<<sgrid, 128, 0, st>>>(G, P, PT, (TOut*)y);
+      } else {
+        constexpr int ag = fast::kFwdAG;
+        dim3 sgrid(((G.d + 1) / 2 + 31) / 32, (G.n_half + ag - 1) / ag);
+        fast::fwd_sym_kernel<TOut, ag><<<sgrid, 32 * ag, 0, st>>>(G, P, PT, (TOut*)y);
+      }
       e = cudaGetLastError();
     }
     if (e != cudaSuccess) return e;

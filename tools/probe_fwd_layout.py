@@ -1,0 +1,37 @@
+"""A/B: symmetric forward block layouts (4 adjacent angles x 32 rays vs 128 rays)."""
+import json
+import sys
+
+import torch
+
+sys.path.insert(0, ".")
+from paper_1310_0956_b200 import build_geometry, build_projector  # noqa: E402
+
+
+def ev_time(fn, reps=10):
+    fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps
+
+
+out = {}
+for n in (1024, 2048, 4096):
+    d = int(-(-n * 2 ** 0.5 // 1))
+    w = build_projector(build_geometry(n, d, n), precision="float32")
+    x = torch.rand(n * n, device="cuda")
+    s1 = torch.empty(n * d, device="cuda")
+    s2 = torch.empty(n * d, device="cuda")
+    w.set_symmetry("force")
+    t4 = ev_time(lambda: w.forward_(x, s1))
+    w.set_symmetry("fwd1")
+    t1 = ev_time(lambda: w.forward_(x, s2))
+    torch.cuda.synchronize()
+    out[n] = {"fwd_4angles_ms": t4, "fwd_1angle_ms": t1,
+              "max_abs_diff": float((s1 - s2).abs().max())}
+print(json.dumps(out, indent=1))
