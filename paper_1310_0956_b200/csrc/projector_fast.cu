@@ -679,7 +679,7 @@ __global__ void __launch_bounds__(256, 5) bwd_sym_kernel(GeomDev G, const TIn* _
 // nearly the same pixels slab after slab (the rays drift apart by ~n * dtheta
 // pixels over the whole image), so the co-resident warps of a block share
 // their L1 lines.
-template <typename TOut, int kAG>
+template <typename TOut, int kAG, bool kLock = false>
 __global__ void __launch_bounds__(kAG == 1 ? 128 : 32 * kAG) fwd_sym_kernel(GeomDev G, const float* __restrict__ P,
                                                       const float* __restrict__ PT,
                                                       TOut* __restrict__ sino) {
@@ -690,8 +690,10 @@ __global__ void __launch_bounds__(kAG == 1 ? 128 : 32 * kAG) fwd_sym_kernel(Geom
   } else {
     hidx = blockIdx.y * kAG + (threadIdx.x >> 5);
     j = blockIdx.x * 32 + (threadIdx.x & 31);
-    if (hidx >= G.n_half) return;          // whole warp
+    if (!kLock && hidx >= G.n_half) return;          // whole warp
   }
+  const bool hvalid = hidx < G.n_half;
+  if (kLock && !hvalid) hidx = G.n_half - 1;         // keeps the block's barriers whole
   const int a = G.half[hidx];
   const int b = G.mir[a];
   const int d = G.d, m = G.m, n = G.n;
@@ -712,8 +714,20 @@ __global__ void __launch_bounds__(kAG == 1 ? 128 : 32 * kAG) fwd_sym_kernel(Geom
   } else if (u0 < -1.0 || u0 > (double)n + 1.0) {
     r0 = n; r1 = -1;
   }
-  const int rw0 = __reduce_min_sync(0xffffffffu, r0);
-  const int rw1 = __reduce_max_sync(0xffffffffu, r1);
+  int rw0 = __reduce_min_sync(0xffffffffu, r0);
+  int rw1 = __reduce_max_sync(0xffffffffu, r1);
+  if (kLock) {
+    // lockstep: the block's warps (adjacent angles) walk the union slab range
+    // together, so each image line is fetched into L1 once for all of them;
+    // slabs outside a ray's own range read the zero margins (k clamped)
+    __shared__ int s_lo, s_hi;
+    if (threadIdx.x == 0) { s_lo = 0x7fffffff; s_hi = -1; }
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) { atomicMin(&s_lo, rw0); atomicMax(&s_hi, rw1); }
+    __syncthreads();
+    rw0 = s_lo;
+    rw1 = s_hi;
+  }
   float2 accA = make_float2(0.0f, 0.0f);   // (s, q), (s, n-1-q)
   float2 accB = make_float2(0.0f, 0.0f);   // (n-1-s, n-1-q), (n-1-s, q)
   if (rw0 <= rw1) {
@@ -730,12 +744,14 @@ __global__ void __launch_bounds__(kAG == 1 ? 128 : 32 * kAG) fwd_sym_kernel(Geom
     int r = rw0;
     // batches of 4 slabs: all 32 loads are issued before any is consumed
     for (; r + 3 <= rw1; r += 4) {
+      if (kLock) __syncthreads();
       float2 v1A[4], v0A[4], v1B[4], v0B[4];
       float wh[4];
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         U += S;
-        const int k = hi32(U);
+        int k = hi32(U);
+        if (kLock) k = min(max(k, 2 - kPadMargin), n + kPadMargin - 3);
         const float f = frac1((unsigned)U);
         wh[q] = fminf(fmaf(f, Ls, -Ls), L);
         const int km = n - 1 - k;
@@ -761,7 +777,8 @@ __global__ void __launch_bounds__(kAG == 1 ? 128 : 32 * kAG) fwd_sym_kernel(Geom
     }
     for (; r <= rw1; ++r) {
       U += S;
-      const int k = hi32(U);
+      int k = hi32(U);
+      if (kLock) k = min(max(k, 2 - kPadMargin), n + kPadMargin - 3);
       const float f = frac1((unsigned)U);
       const float wh = fminf(fmaf(f, Ls, -Ls), L);
       const float2 W = make_float2(wh, wh);
@@ -782,7 +799,7 @@ __global__ void __launch_bounds__(kAG == 1 ? 128 : 32 * kAG) fwd_sym_kernel(Geom
       rowB -= up;
     }
   }
-  if (j < jh) {
+  if (j < jh && hvalid) {
     // slab-coordinate images -> rays; x-major swaps which image is the x-mirror
     const float r_m = A.major ? accB.y : accA.y;    // (m-a, j)
     const float r_mr = A.major ? accA.y : accB.y;   // (m-a, d-1-j)
@@ -1167,7 +1184,10 @@ static cudaError_t fwd_v2_impl(const GeomDev& G, const void* x, void* ws, void* 
       } else {
         constexpr int ag = fast::kFwdAG;
         dim3 sgrid(((G.d + 1) / 2 + 31) / 32, (G.n_half + ag - 1) / ag);
-        fast::fwd_sym_kernel<TOut, ag><<<sgrid, 32 * ag, 0, st>>>(G, P, PT, (TOut*)y);
+        if (G.sym & 32)   // testing: lockstep angle groups
+          fast::fwd_sym_kernel<TOut, ag, true><<<sgrid, 32 * ag, 0, st>>>(G, P, PT, (TOut*)y);
+        else
+          fast::fwd_sym_kernel<TOut, ag><<<sgrid, 32 * ag, 0, st>>>(G, P, PT, (TOut*)y);
       }
       e = cudaGetLastError();
     }

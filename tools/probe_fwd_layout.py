@@ -31,7 +31,12 @@ for n in (1024, 2048, 4096):
     t4 = ev_time(lambda: w.forward_(x, s1))
     w.set_symmetry("fwd1")
     t1 = ev_time(lambda: w.forward_(x, s2))
+    s3 = torch.empty(n * d, device="cuda")
+    w.set_symmetry("lockstep")
+    tl = ev_time(lambda: w.forward_(x, s3))
     torch.cuda.synchronize()
-    out[n] = {"fwd_4angles_ms": t4, "fwd_1angle_ms": t1,
-              "max_abs_diff": float((s1 - s2).abs().max())}
+    torch.cuda.synchronize()
+    out[n] = {"fwd_4angles_ms": t4, "fwd_1angle_ms": t1, "fwd_lockstep_ms": tl,
+              "max_abs_diff": float((s1 - s2).abs().max()),
+              "lockstep_max_rel_diff": float((s1 - s3).abs().max() / s1.abs().max())}
 print(json.dumps(out, indent=1))
