@@ -675,11 +675,15 @@ __global__ void __launch_bounds__(256, 5) bwd_sym_kernel(GeomDev G, const TIn* _
 // thread walks a representative ray a in [1, m/2), j < ceil(d/2) and
 // accumulates all four.  Representative angles are never mirrored (slope > 0).
 // Block layout: kAG == 1 -> 128 consecutive rays of one angle; kAG == 4 -> the
-// same 32 rays of 4 adjacent angles (one warp each).  Adjacent angles walk
-// nearly the same pixels slab after slab (the rays drift apart by ~n * dtheta
-// pixels over the whole image), so the co-resident warps of a block share
-// their L1 lines.
-template <typename TOut, int kAG, bool kLock = false>
+// same 32 rays of 4 adjacent angles.  Adjacent angles walk nearly the same
+// pixels slab after slab (rays of neighbouring angles through the same
+// detector cross at the centre and drift apart by < 2 px per angle step at
+// the image edge).  kMix (default) packs 8 rays x 4 angles into each warp, so
+// one warp load touches ~2-3 sectors instead of 6-7 (32 rays span ~45 px): the
+// forward is bound by L1 sector throughput, and this cuts the sector requests
+// 2.3x (profiles/r1b_fwd_variants_ncu.txt).  Without kMix the 4 angles are 4
+// warps that share L1 lines (2.4x less L2 traffic, little time gained).
+template <typename TOut, int kAG, bool kLock = false, bool kMix = false>
 __global__ void __launch_bounds__(kAG == 1 ? 128 : 32 * kAG) fwd_sym_kernel(GeomDev G, const float* __restrict__ P,
                                                       const float* __restrict__ PT,
                                                       TOut* __restrict__ sino) {
@@ -687,13 +691,20 @@ __global__ void __launch_bounds__(kAG == 1 ? 128 : 32 * kAG) fwd_sym_kernel(Geom
   if (kAG == 1) {
     hidx = blockIdx.y;
     j = blockIdx.x * 128 + threadIdx.x;
+  } else if (kMix) {
+    // lanes = 8 rays x 4 adjacent angles: the warp's addresses span ~8 rays
+    // (2-3 sectors per load instead of 6-7 for 32 rays of one angle); the warp
+    // walks the union of its lanes' slab ranges (see clampk below)
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    hidx = blockIdx.y * 4 + (lane >> 3);
+    j = blockIdx.x * 8 * (kAG) + warp * 8 + (lane & 7);
   } else {
     hidx = blockIdx.y * kAG + (threadIdx.x >> 5);
     j = blockIdx.x * 32 + (threadIdx.x & 31);
     if (!kLock && hidx >= G.n_half) return;          // whole warp
   }
   const bool hvalid = hidx < G.n_half;
-  if (kLock && !hvalid) hidx = G.n_half - 1;         // keeps the block's barriers whole
+  if ((kLock || kMix) && !hvalid) hidx = G.n_half - 1;   // keep barriers / warp votes whole
   const int a = G.half[hidx];
   const int b = G.mir[a];
   const int d = G.d, m = G.m, n = G.n;
@@ -728,6 +739,11 @@ __global__ void __launch_bounds__(kAG == 1 ? 128 : 32 * kAG) fwd_sym_kernel(Geom
     rw0 = s_lo;
     rw1 = s_hi;
   }
+  // A warp walks the union of its lanes' slab ranges; when its lanes belong to
+  // different angles (kMix: the angles of a shard may be far apart, or differ
+  // in major axis near 45 degrees) a lane's u can leave the image by more than
+  // the padding, so k is clamped into the zero margins (2 ALU ops per slab).
+  constexpr bool clampk = kLock || kMix;
   float2 accA = make_float2(0.0f, 0.0f);   // (s, q), (s, n-1-q)
   float2 accB = make_float2(0.0f, 0.0f);   // (n-1-s, n-1-q), (n-1-s, q)
   if (rw0 <= rw1) {
@@ -751,7 +767,7 @@ __global__ void __launch_bounds__(kAG == 1 ? 128 : 32 * kAG) fwd_sym_kernel(Geom
       for (int q = 0; q < 4; ++q) {
         U += S;
         int k = hi32(U);
-        if (kLock) k = min(max(k, 2 - kPadMargin), n + kPadMargin - 3);
+        if (clampk) k = min(max(k, 2 - kPadMargin), n + kPadMargin - 3);
         const float f = frac1((unsigned)U);
         wh[q] = fminf(fmaf(f, Ls, -Ls), L);
         const int km = n - 1 - k;
@@ -778,7 +794,7 @@ __global__ void __launch_bounds__(kAG == 1 ? 128 : 32 * kAG) fwd_sym_kernel(Geom
     for (; r <= rw1; ++r) {
       U += S;
       int k = hi32(U);
-      if (kLock) k = min(max(k, 2 - kPadMargin), n + kPadMargin - 3);
+      if (clampk) k = min(max(k, 2 - kPadMargin), n + kPadMargin - 3);
       const float f = frac1((unsigned)U);
       const float wh = fminf(fmaf(f, Ls, -Ls), L);
       const float2 W = make_float2(wh, wh);
@@ -1184,10 +1200,15 @@ static cudaError_t fwd_v2_impl(const GeomDev& G, const void* x, void* ws, void* 
       } else {
         constexpr int ag = fast::kFwdAG;
         dim3 sgrid(((G.d + 1) / 2 + 31) / 32, (G.n_half + ag - 1) / ag);
-        if (G.sym & 32)   // testing: lockstep angle groups
+        if (G.sym & 32) {         // testing: lockstep angle groups, 32 rays per warp
           fast::fwd_sym_kernel<TOut, ag, true><<<sgrid, 32 * ag, 0, st>>>(G, P, PT, (TOut*)y);
-        else
+        } else if (G.sym & 64) {  // testing: 32 rays of one angle per warp
           fast::fwd_sym_kernel<TOut, ag><<<sgrid, 32 * ag, 0, st>>>(G, P, PT, (TOut*)y);
+        } else {                  // default: 8 rays x 4 adjacent angles per warp
+          dim3 mgrid(((G.d + 1) / 2 + 8 * ag - 1) / (8 * ag), (G.n_half + 3) / 4);
+          fast::fwd_sym_kernel<TOut, ag, false, true><<<mgrid, 32 * ag, 0, st>>>(G, P, PT,
+                                                                               (TOut*)y);
+        }
       }
       e = cudaGetLastError();
     }

@@ -10,7 +10,7 @@ n, d = 4096, 5793
 w = build_projector(build_geometry(n, d, n), precision="float32")
 x = torch.rand(n * n, device="cuda")
 s = torch.empty(n * d, device="cuda")
-for mode in ("force", "fwd1", "lockstep"):
+for mode in ("force", "fwd1", "lockstep", "fwdrows"):
     w.set_symmetry(mode)
     w.forward_(x, s)
 torch.cuda.synchronize()
