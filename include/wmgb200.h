@@ -190,9 +190,10 @@ int wmg_leaf_factor(const wmg_geometry *g, int depth, const int *bands, long lon
                     long long nrays, double *P, void *stream);
 
 /* WMG leaf Gram, sparse: gram (p x p row-major float64, p = (n >> depth)^2,
- * caller-zeroed) += lower triangle of P_L^T P_L, accumulated per ray bundle
- * without forming P_L (weights from the fp64 slab formula, <= 1e-12 of the
- * exact ones).  *overflow (device int, caller-zeroed) is set if a bundle's
+ * zeroed by the caller) receives the lower triangle of P_L^T P_L, accumulated
+ * per ray bundle without forming P_L (weights from the fp64 slab formula,
+ * <= 1e-12 of the exact ones) in 64-bit fixed point, so the result is
+ * bit-reproducible; *overflow (device int, caller-zeroed) is set if a bundle's
  * footprint exceeded the kernel's window (then the result is incomplete).
  * Replaces the reference's P^T P of multilevel.py:125-130. */
 int wmg_leaf_gram(const wmg_geometry *g, int depth, const int *bands, double *gram,

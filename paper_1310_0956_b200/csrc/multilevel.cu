@@ -83,7 +83,8 @@ __global__ void leaf_factor_kernel(GeomDev G, LeafPath path, long long ray0, lon
 constexpr int kWc = 4;
 
 __global__ void __launch_bounds__(256) leaf_gram_kernel(GeomDev G, LeafPath path, int NB,
-                                                        double* __restrict__ gram,
+                                                        unsigned long long* __restrict__ gram,
+                                                        double scale,
                                                         int* __restrict__ overflow) {
   extern __shared__ double smem[];
   const int a = blockIdx.y;
@@ -192,8 +193,16 @@ __global__ void __launch_bounds__(256) leaf_gram_kernel(GeomDev G, LeafPath path
     long long gi = A.major ? (long long)ci * sc + Ri : (long long)Ri * sc + ci;
     long long gj = A.major ? (long long)cj * sc + Rj : (long long)Rj * sc + cj;
     if (gi < gj) { const long long tmp = gi; gi = gj; gj = tmp; }
-    atomicAdd(&gram[gi * p + gj], sum);   // slots map 1:1 to coarse blocks
+    // fixed-point accumulation: integer adds are associative, so the Gram is
+    // bit-reproducible whatever order the bundles' atomics land in
+    atomicAdd(&gram[gi * p + gj], (unsigned long long)llrint(sum * scale));
   }
+}
+
+// fixed point (int64 bits stored in the Gram buffer) -> float64, in place
+__global__ void fixed_to_double_kernel(double* __restrict__ g, long long count, double inv) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < count) g[i] = (double)__double_as_longlong(g[i]) * inv;
 }
 
 }  // namespace ml
@@ -217,7 +226,23 @@ cudaError_t leaf_gram(const GeomDev& G, int depth, const int* bands, double* gra
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   dim3 grid((G.d + nb - 1) / nb, G.m);
-  ml::leaf_gram_kernel<<<grid, 256, smem, st>>>(G, path, nb, gram, overflow);
+  // Fixed-point scale: every |entry| <= m (sqrt2 B + 2) * 2 (a block's P entry
+  // is at most sqrt2 in magnitude, at most sqrt2 B + 2 rays of an angle cross
+  // a block), so 2^e with e = 61 - ceil(log2(bound)) leaves headroom for the
+  // sum and a resolution ~1e-13 of the bound (cf. the 1e-16 relative rounding
+  // of a float64 sum over ~1e3 terms).
+  const double B = (double)(1 << depth);
+  const double bound = 2.0 * (double)G.m * (1.4142135623730951 * B + 2.0);
+  const int ex = 61 - (int)ceil(log2(bound));
+  const double scale = ldexp(1.0, ex);
+  ml::leaf_gram_kernel<<<grid, 256, smem, st>>>(G, path, nb, (unsigned long long*)gram, scale,
+                                                overflow);
+  cudaError_t err = cudaGetLastError();
+  if (err != cudaSuccess) return err;
+  const long long count = (long long)(G.n >> depth) * (G.n >> depth);
+  const long long total = count * count;
+  ml::fixed_to_double_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(gram, total,
+                                                                            1.0 / scale);
   return cudaGetLastError();
 }
 

@@ -273,3 +273,14 @@ def test_batched_sibling_cycle_bit_identical(gpu, golden, nu, levels, lam):
         finally:
             ml.BATCH_SIBLINGS = True
     assert np.array_equal(outs[0], outs[1])
+
+
+def test_sparse_leaf_gram_bit_reproducible(gpu, golden):
+    """Fixed-point accumulation: repeated assemblies are bit-identical (the
+    bundles' atomics land in a different order every run)."""
+    from paper_1310_0956_b200.multilevel import _assemble_leaf_grams
+    w = _w(golden, "bench160")
+    _, g1 = _assemble_leaf_grams(w, 160, 0.0, 3, method="sparse")
+    for _ in range(2):
+        _, g2 = _assemble_leaf_grams(w, 160, 0.0, 3, method="sparse")
+        assert bool((g1 == g2).all())
