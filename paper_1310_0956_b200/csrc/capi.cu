@@ -220,12 +220,45 @@ int wmg_geometry_create(int n, int n_detectors, int n_angles, const double* cos_
   if (e == cudaSuccess)
     e = cudaMemcpy(g->d_ang, P.data(), sizeof(wmg::AngleParams) * (size_t)n_angles,
                    cudaMemcpyHostToDevice);
+  // Per 4-angle group of the symmetric forward (warps of 8 rays x 4 angles walk
+  // the union of their lanes' slab ranges): 1 when every lane's minor
+  // coordinate stays within kPadMargin - 4 pixels of the image over that
+  // union, so the zero margins absorb it and k needs no clamp.  u is linear in
+  // the detector offset and the slab, so the spread between two lanes is
+  // largest at a corner (j in {0, d/2}, slab in {0, n}); same major axis only.
+  std::vector<int> gsafe;
+  if (sym) {
+    const int ng = ((int)halfv.size() + 3) / 4;
+    const double jh = (double)((n_detectors + 1) / 2), dcen = (n_detectors - 1) * 0.5;
+    for (int gi = 0; gi < ng; ++gi) {
+      bool safe = true;
+      double dmax = 0.0;
+      const int g0 = gi * 4, g1 = std::min((int)halfv.size(), g0 + 4);
+      for (int x = g0; x < g1 && safe; ++x) {
+        const wmg::AngleParams& A = P[(size_t)halfv[(size_t)x]];
+        dmax = std::max(dmax, 8.0 * std::fabs(A.du));        // rays of one lane group
+        for (int y = g0; y < g1; ++y) {
+          const wmg::AngleParams& Bq = P[(size_t)halfv[(size_t)y]];
+          if (A.major != Bq.major) { safe = false; break; }
+          for (double jj : {0.0, jh})
+            for (double rr : {0.0, (double)n}) {
+              const double ua = A.u0 + (jj - dcen) * A.du + rr * A.slope;
+              const double ub = Bq.u0 + (jj - dcen) * Bq.du + rr * Bq.slope;
+              dmax = std::max(dmax, std::fabs(ua - ub) + 8.0 * std::fabs(A.du));
+            }
+        }
+      }
+      gsafe.push_back(safe && dmax + 4.0 < (double)wmg::kPadMargin ? 1 : 0);
+    }
+  }
   if (e == cudaSuccess && sym) {
     // one int table: mir (m) | prim (n_prim) | half (n_half) | axis rowmap (n_axis)
+    //                | group-safe flags (ceil(n_half / 4))
     std::vector<int> tab(mir);
     tab.insert(tab.end(), prim.begin(), prim.end());
     tab.insert(tab.end(), halfv.begin(), halfv.end());
     tab.insert(tab.end(), axis_idx.begin(), axis_idx.end());
+    tab.insert(tab.end(), gsafe.begin(), gsafe.end());
     e = cudaMalloc(&g->d_mir, sizeof(int) * tab.size());
     if (e == cudaSuccess)
       e = cudaMemcpy(g->d_mir, tab.data(), sizeof(int) * tab.size(), cudaMemcpyHostToDevice);
@@ -259,6 +292,8 @@ int wmg_geometry_create(int n, int n_detectors, int n_angles, const double* cos_
   g->dev.half = sym ? g->d_mir + n_angles + prim.size() : nullptr;
   g->dev.n_prim = (int)prim.size();
   g->dev.n_half = (int)halfv.size();
+  g->dev.gsafe = sym ? g->d_mir + n_angles + prim.size() + halfv.size() + axis_idx.size()
+                     : nullptr;
   g->sym_capable = sym ? 1 : 0;
   g->axis = g->dev;
   g->axis.m = n_axis;

@@ -57,6 +57,7 @@ struct GeomDev {
   const int* mir;
   const int* prim;
   const int* half;
+  const int* gsafe;   // per 4-angle group of half: 1 = forward needs no k clamp
   int n_prim, n_half;
 };
 

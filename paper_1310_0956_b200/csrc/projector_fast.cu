@@ -21,6 +21,7 @@
 // Tolerance vs the float64 reference: 1e-5 relative (fp32 data), see
 // tests/test_gpu_projector.py.
 #include <algorithm>
+#include <type_traits>
 
 #include "common.cuh"
 
@@ -740,10 +741,11 @@ __global__ void __launch_bounds__(kAG == 1 ? 128 : 32 * kAG) fwd_sym_kernel(Geom
     rw1 = s_hi;
   }
   // A warp walks the union of its lanes' slab ranges; when its lanes belong to
-  // different angles (kMix: the angles of a shard may be far apart, or differ
-  // in major axis near 45 degrees) a lane's u can leave the image by more than
-  // the padding, so k is clamped into the zero margins (2 ALU ops per slab).
-  constexpr bool clampk = kLock || kMix;
+  // different angles (kMix) a lane's u can leave the image by more than the
+  // padding (angles far apart in a shard, or of different major axis near 45
+  // degrees): then k is clamped into the zero margins.  The host marks the
+  // 4-angle groups where the margins suffice (GeomDev::gsafe).
+  const bool clampk = kLock || (kMix && !G.gsafe[blockIdx.y]);   // block-uniform
   float2 accA = make_float2(0.0f, 0.0f);   // (s, q), (s, n-1-q)
   float2 accB = make_float2(0.0f, 0.0f);   // (n-1-s, n-1-q), (n-1-s, q)
   if (rw0 <= rw1) {
@@ -757,63 +759,70 @@ __global__ void __launch_bounds__(kAG == 1 ? 128 : 32 * kAG) fwd_sym_kernel(Geom
     unsigned rowB = (unsigned)((n - 1 - rw0) * pitch + kPadMargin);
     const float* __restrict__ base = src - kPadMargin;
     const unsigned up = (unsigned)pitch;
-    int r = rw0;
-    // batches of 4 slabs: all 32 loads are issued before any is consumed
-    for (; r + 3 <= rw1; r += 4) {
-      if (kLock) __syncthreads();
-      float2 v1A[4], v0A[4], v1B[4], v0B[4];
-      float wh[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
+    // the walk, versioned on the clamp (the flag is block-uniform)
+    auto walk = [&](auto clampTag) {
+      int r = rw0;
+      // batches of 4 slabs: all 32 loads are issued before any is consumed
+      for (; r + 3 <= rw1; r += 4) {
+        if (kLock) __syncthreads();
+        float2 v1A[4], v0A[4], v1B[4], v0B[4];
+        float wh[4];
+  #pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          U += S;
+          int k = hi32(U);
+          if constexpr (decltype(clampTag)::value) k = min(max(k, 2 - kPadMargin), n + kPadMargin - 3);
+          const float f = frac1((unsigned)U);
+          wh[q] = fminf(fmaf(f, Ls, -Ls), L);
+          const int km = n - 1 - k;
+          const float* pa1 = base + (rowA + (unsigned)k);
+          const float* pa2 = base + (rowA + (unsigned)km);
+          const float* pb1 = base + (rowB + (unsigned)km);
+          const float* pb2 = base + (rowB + (unsigned)k);
+          v1A[q] = make_float2(__ldg(pa1), __ldg(pa2));
+          v0A[q] = make_float2(__ldg(pa1 - 1), __ldg(pa2 + 1));
+          v1B[q] = make_float2(__ldg(pb1), __ldg(pb2));
+          v0B[q] = make_float2(__ldg(pb1 + 1), __ldg(pb2 - 1));
+          rowA += up;
+          rowB -= up;
+        }
+  #pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float2 W = make_float2(wh[q], wh[q]);
+          accA = __ffma2_rn(LL, v0A[q], accA);
+          accA = __ffma2_rn(W, __fadd2_rn(v1A[q], make_float2(-v0A[q].x, -v0A[q].y)), accA);
+          accB = __ffma2_rn(LL, v0B[q], accB);
+          accB = __ffma2_rn(W, __fadd2_rn(v1B[q], make_float2(-v0B[q].x, -v0B[q].y)), accB);
+        }
+      }
+      for (; r <= rw1; ++r) {
         U += S;
         int k = hi32(U);
-        if (clampk) k = min(max(k, 2 - kPadMargin), n + kPadMargin - 3);
+        if constexpr (decltype(clampTag)::value) k = min(max(k, 2 - kPadMargin), n + kPadMargin - 3);
         const float f = frac1((unsigned)U);
-        wh[q] = fminf(fmaf(f, Ls, -Ls), L);
+        const float wh = fminf(fmaf(f, Ls, -Ls), L);
+        const float2 W = make_float2(wh, wh);
         const int km = n - 1 - k;
         const float* pa1 = base + (rowA + (unsigned)k);
         const float* pa2 = base + (rowA + (unsigned)km);
         const float* pb1 = base + (rowB + (unsigned)km);
         const float* pb2 = base + (rowB + (unsigned)k);
-        v1A[q] = make_float2(__ldg(pa1), __ldg(pa2));
-        v0A[q] = make_float2(__ldg(pa1 - 1), __ldg(pa2 + 1));
-        v1B[q] = make_float2(__ldg(pb1), __ldg(pb2));
-        v0B[q] = make_float2(__ldg(pb1 + 1), __ldg(pb2 - 1));
+        const float2 v1A = make_float2(__ldg(pa1), __ldg(pa2));
+        const float2 v0A = make_float2(__ldg(pa1 - 1), __ldg(pa2 + 1));
+        const float2 v1B = make_float2(__ldg(pb1), __ldg(pb2));
+        const float2 v0B = make_float2(__ldg(pb1 + 1), __ldg(pb2 - 1));
+        accA = __ffma2_rn(LL, v0A, accA);
+        accA = __ffma2_rn(W, __fadd2_rn(v1A, make_float2(-v0A.x, -v0A.y)), accA);
+        accB = __ffma2_rn(LL, v0B, accB);
+        accB = __ffma2_rn(W, __fadd2_rn(v1B, make_float2(-v0B.x, -v0B.y)), accB);
         rowA += up;
         rowB -= up;
       }
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const float2 W = make_float2(wh[q], wh[q]);
-        accA = __ffma2_rn(LL, v0A[q], accA);
-        accA = __ffma2_rn(W, __fadd2_rn(v1A[q], make_float2(-v0A[q].x, -v0A[q].y)), accA);
-        accB = __ffma2_rn(LL, v0B[q], accB);
-        accB = __ffma2_rn(W, __fadd2_rn(v1B[q], make_float2(-v0B[q].x, -v0B[q].y)), accB);
-      }
-    }
-    for (; r <= rw1; ++r) {
-      U += S;
-      int k = hi32(U);
-      if (clampk) k = min(max(k, 2 - kPadMargin), n + kPadMargin - 3);
-      const float f = frac1((unsigned)U);
-      const float wh = fminf(fmaf(f, Ls, -Ls), L);
-      const float2 W = make_float2(wh, wh);
-      const int km = n - 1 - k;
-      const float* pa1 = base + (rowA + (unsigned)k);
-      const float* pa2 = base + (rowA + (unsigned)km);
-      const float* pb1 = base + (rowB + (unsigned)km);
-      const float* pb2 = base + (rowB + (unsigned)k);
-      const float2 v1A = make_float2(__ldg(pa1), __ldg(pa2));
-      const float2 v0A = make_float2(__ldg(pa1 - 1), __ldg(pa2 + 1));
-      const float2 v1B = make_float2(__ldg(pb1), __ldg(pb2));
-      const float2 v0B = make_float2(__ldg(pb1 + 1), __ldg(pb2 - 1));
-      accA = __ffma2_rn(LL, v0A, accA);
-      accA = __ffma2_rn(W, __fadd2_rn(v1A, make_float2(-v0A.x, -v0A.y)), accA);
-      accB = __ffma2_rn(LL, v0B, accB);
-      accB = __ffma2_rn(W, __fadd2_rn(v1B, make_float2(-v0B.x, -v0B.y)), accB);
-      rowA += up;
-      rowB -= up;
-    }
+    };
+    if (clampk)
+      walk(std::true_type{});
+    else
+      walk(std::false_type{});
   }
   if (j < jh && hvalid) {
     // slab-coordinate images -> rays; x-major swaps which image is the x-mirror
