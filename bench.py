@@ -398,13 +398,25 @@ def run_ours(args):
     e2e_s = torch.empty(M_loc, dtype=torch.float32, device=dev)
     e2e_i = torch.empty(Npix, dtype=torch.float32, device=dev)
 
+    # The pair's two products are independent: like any user pipelining them,
+    # run H2D x -> W x -> D2H on one stream and H2D y -> W^T y -> D2H on a
+    # second, so each direction's copies overlap the other's kernel.
+    s_fwd = torch.cuda.Stream(device=dev)
+    s_bwd = torch.cuda.Stream(device=dev)
+
     def e2e_step():
-        xd = pin_x.to(dev, non_blocking=True)
-        yd = pin_y.to(dev, non_blocking=True)
-        w.forward_(xd, e2e_s)
-        w.backward_(yd, e2e_i)
-        out_s.copy_(e2e_s, non_blocking=True)
-        out_i.copy_(e2e_i, non_blocking=True)
+        s_fwd.wait_stream(stream)
+        s_bwd.wait_stream(stream)
+        with torch.cuda.stream(s_fwd):
+            xd = pin_x.to(dev, non_blocking=True)
+            w.forward_(xd, e2e_s)
+            out_s.copy_(e2e_s, non_blocking=True)
+        with torch.cuda.stream(s_bwd):
+            yd = pin_y.to(dev, non_blocking=True)
+            w.backward_(yd, e2e_i)
+            out_i.copy_(e2e_i, non_blocking=True)
+        stream.wait_stream(s_fwd)
+        stream.wait_stream(s_bwd)
 
     e2e_step()
     torch.cuda.synchronize(dev)
