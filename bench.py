@@ -130,6 +130,29 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def onchip_roofline(n, t_fwd, t_bwd, n_sm, f_sm, world):
+    """The on-chip resources that bind the pair (DESIGN.md kernel table): L1
+    sector requests of the forward gathers (peak 4 sectors/clk/SM) and shared
+    wavefronts of the backprojector (peak 1/clk/SM); per-launch counts from the
+    committed ncu capture, times live from this run."""
+    t = ncu_traffic()
+    out = {}
+    sec = t.get(f"l1_sectors_forward_n{n}")
+    if sec and t_fwd > 0 and world == 1:
+        peak = 4.0 * n_sm * f_sm
+        out["forward_l1_sectors"] = {"achieved": sec / t_fwd / 1e9, "peak": peak / 1e9,
+                                     "unit": "Gsectors/s", "frac": sec / t_fwd / peak,
+                                     "per_launch": sec}
+    wf = t.get(f"smem_wavefronts_backward_n{n}")
+    if wf and t_bwd > 0 and world == 1:
+        peak = 1.0 * n_sm * f_sm
+        out["backward_smem_wavefronts"] = {"achieved": wf / t_bwd / 1e9, "peak": peak / 1e9,
+                                           "unit": "Gwavefronts/s", "frac": wf / t_bwd / peak,
+                                           "per_launch": wf}
+    out["source"] = "profiles/traffic.json (ncu --set full), live kernel times"
+    return out
+
+
 def measured_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -468,6 +491,7 @@ def run_ours(args):
                             "peak": gather_peak / 1e9, "unit": "Gupdates/s",
                             "frac": upd_rate / gather_peak,
                             "definition": "SURVEY s8(d): 148 SMs x 32 lanes x f_SM"},
+        "roofline_onchip": onchip_roofline(n, fwd_avg, bwd_avg, n_sm, f_sm, world),
         "kernels_ms": {"forward": fwd_avg * 1e3, "backward": bwd_avg * 1e3},
         "gpu_launches": launches,
         "clocks": clk,
