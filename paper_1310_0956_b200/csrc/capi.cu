@@ -402,6 +402,7 @@ int wmg_backward(const wmg_geometry* g, int mode, int precision, int dtype_in, i
 int wmg_forward_batch(const wmg_geometry* g, int mode, int precision, int dtype_in,
                       int dtype_out, const void* x, void* y, int batch, void* workspace,
                       void* stream) {
+  if (batch == 0 && g) return WMG_OK;
   if (!g || !x || !y) return fail(WMG_EINVAL, "NULL argument");
   if (batch < 0) return fail(WMG_EINVAL, "negative batch");
   int rc = check_types(mode, precision, dtype_in, dtype_out);
@@ -428,6 +429,7 @@ int wmg_forward_batch(const wmg_geometry* g, int mode, int precision, int dtype_
 int wmg_backward_batch(const wmg_geometry* g, int mode, int precision, int dtype_in,
                        int dtype_out, const void* y, void* x, int batch, int accumulate,
                        void* stream) {
+  if (batch == 0 && g) return WMG_OK;
   if (!g || !x || !y) return fail(WMG_EINVAL, "NULL argument");
   if (batch < 0) return fail(WMG_EINVAL, "negative batch");
   int rc = check_types(mode, precision, dtype_in, dtype_out);

@@ -246,3 +246,57 @@ def test_symmetric_kernels_on_mirror_shards(gpu, oracle_proj, n, d, m, world):
             assert wd.set_symmetry("force")
             f64 = wd.forward(torch.from_numpy(x).cuda()).cpu().numpy()
             assert np.linalg.norm(f64 - ref_f) <= 1e-12 * np.linalg.norm(ref_f), rank
+
+
+@pytest.mark.parametrize("n,d,m", [(1, 1, 1), (2, 3, 2), (3, 5, 3), (17, 9, 7), (64, 91, 8),
+                                   (64, 30, 2), (100, 147, 12), (128, 181, 4), (128, 50, 16)])
+@pytest.mark.parametrize("precision", ["float32", "float64"])
+def test_fast_paths_edge_geometries(gpu, oracle_proj, n, d, m, precision):
+    """Tiny / odd grids, few detectors (rays missing the grid), few angles,
+    equiangular and random angle sets: the fast kernels stay within their
+    tolerance of the exact reference weights (and never read out of bounds)."""
+    torch = gpu
+    from paper_1310_0956_b200.geometry import Geometry, build_geometry, build_projector
+    rs = np.random.default_rng(n * 131 + d * 7 + m)
+    geoms = [build_geometry(n, d, m)]
+    if m > 1:
+        geoms.append(Geometry(n, d, m, angles=np.sort(rs.uniform(0.0, np.pi, m))))
+    tol = 1e-5 if precision == "float32" else 1e-12
+    dt = torch.float32 if precision == "float32" else torch.float64
+    for g in geoms:
+        w = build_projector(g, precision=precision, mode="fast")
+        x = rs.uniform(0.0, 1.0, n * n)
+        y = rs.uniform(0.0, 1.0, m * d)
+        ref_f = oracle_proj.forward(n, d, g.angles, x)
+        ref_b = oracle_proj.backward(n, d, g.angles, y)
+        for sym in (True, "force", False):
+            w.set_symmetry(sym)
+            f = w.forward(torch.from_numpy(x).to(dt).cuda()).double().cpu().numpy()
+            b = w.backward(torch.from_numpy(y).to(dt).cuda()).double().cpu().numpy()
+            assert np.linalg.norm(f - ref_f) <= tol * max(np.linalg.norm(ref_f), 1e-30) + 1e-30
+            assert np.linalg.norm(b - ref_b) <= tol * max(np.linalg.norm(ref_b), 1e-30) + 1e-30
+
+
+@pytest.mark.parametrize("n,d,m,precision", [(256, 363, 180, "float64"), (256, 363, 180, "float32"),
+                                             (1024, 1449, 64, "float32"), (100, 147, 12, "float64")])
+def test_batched_pair_matches_single_calls(gpu, n, d, m, precision):
+    """wmg_forward_batch / wmg_backward_batch give each item bit-identically
+    what the single-image calls give (batch 0 is a no-op)."""
+    torch = gpu
+    from paper_1310_0956_b200.geometry import build_geometry, build_projector
+    w = build_projector(build_geometry(n, d, m), precision=precision, mode="fast")
+    dt = torch.float32 if precision == "float32" else torch.float64
+    X = torch.rand(3, n * n, dtype=dt, device="cuda")
+    Y = torch.rand(3, m * d, dtype=dt, device="cuda")
+    SF = torch.empty(3, m * d, dtype=dt, device="cuda")
+    SB = torch.empty(3, n * n, dtype=dt, device="cuda")
+    w.forward_batch_(X, SF)
+    w.backward_batch_(Y, SB)
+    for b in range(3):
+        f = torch.empty(m * d, dtype=dt, device="cuda")
+        o = torch.empty(n * n, dtype=dt, device="cuda")
+        w.forward_(X[b], f)
+        w.backward_(Y[b], o)
+        assert torch.equal(f, SF[b]) and torch.equal(o, SB[b])
+    w.forward_batch_(X[:0], SF[:0])
+    w.backward_batch_(Y[:0], SB[:0])
