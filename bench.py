@@ -341,13 +341,8 @@ def run_ours(args):
     import torch
     import torch.distributed as dist
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+    world, rank, dev = _dist_init()
+    local = dev.index
 
     from paper_1310_0956_b200.geometry import build_geometry, build_projector
     from paper_1310_0956_b200.sharding import AngleShardedProjector
@@ -475,7 +470,7 @@ def run_ours(args):
     traffic = ncu_traffic().get(f"{dom}_n{n}")
     # per step: pad/transpose + forward (+ the axis-angle forward) + backward
     # (+ the axis-angle backward) on symmetric grids (profiles/r1b_launches_*)
-    sym = bool(getattr(w, "symmetric", False)) and n >= 1024
+    sym = bool(getattr(getattr(w, "local", w), "symmetric", False)) and n >= 1024
     launches = args.steps * (5 if sym else 3)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -520,16 +515,22 @@ def run_ours(args):
 
 # ------------------------------------------------------------ config 2
 def _dist_init():
-    """(world, rank, device); NCCL process group when launched by torchrun."""
+    """(world, rank, device); NCCL process group when launched by torchrun.
+    Test-only overrides: WMG_BENCH_BACKEND=gloo and WMG_BENCH_DEVICE=<index>
+    run the multi-rank logic with host-side collectives on one GPU."""
     import torch
     import torch.distributed as dist
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = int(os.environ.get("WMG_BENCH_DEVICE", os.environ.get("LOCAL_RANK", "0")))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1 and not dist.is_initialized():
-        dist.init_process_group("nccl", device_id=dev)
+        backend = os.environ.get("WMG_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     return world, rank, dev
 
 
@@ -646,13 +647,7 @@ def run_config4(args):
     import torch.distributed as dist
     from paper_1310_0956_b200 import (SolverConfig, add_gaussian_noise, build_geometry,
                                       build_projector, cgls_solve, random_ellipses)
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+    world, rank, dev = _dist_init()
     n = args.n if args.n != 4096 else 2048
     m = int(round(1024 * n / 2048))
     m += m % 2
