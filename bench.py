@@ -46,7 +46,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--n", type=int, default=4096)
+    ap.add_argument("--n", "--grid", dest="n", type=int, default=4096)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-angles", type=int, default=4)
     ap.add_argument("--no-wmg", action="store_true",
@@ -69,7 +69,7 @@ def workload(n):
 
 def config_dict(n, d, m, world, extra=None):
     c = {"workload": f"config3_pair_n{n}", "n": n, "n_angles": m, "n_detectors": d,
-         "dtype_data": "float32", "geometry": "fixed-point64", "angle_sharding": "round-robin",
+         "dtype_data": "float32", "geometry": "fixed-point64", "angle_sharding": "mirror pairs",
          "parallelism": f"angles{world}", "l2": ("inputs larger than L2" if n >= 4096
                                                   else "L2 flushed between steps")}
     if extra:

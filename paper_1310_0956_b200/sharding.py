@@ -136,8 +136,38 @@ class AngleShardedProjector:
     def device(self):
         return self.local.device
 
+    # matrix protocol the reference solvers use (w @ x, w.T @ y), on this
+    # rank's rows: x is replicated, y holds this rank's sinogram rows
+    def __matmul__(self, x):
+        from . import _device as D
+        t = D.torch()
+        xd, was_np = D.to_device(x, device=self.device)
+        out = t.empty(self.shape[0], dtype=xd.dtype, device=self.device)
+        self.forward_(xd.reshape(-1), out)
+        return D.to_caller(out, was_np)
+
+    @property
+    def T(self):
+        return _ShardedTranspose(self)
+
     def reduce_sino_(self, t):
         """Sum rank-local sinogram-space partial reductions (in place)."""
         if self.world > 1:
             self.dist.all_reduce(t, group=self.group)
         return t
+
+
+class _ShardedTranspose:
+    """W^T of an AngleShardedProjector: local backprojection + allreduce."""
+
+    def __init__(self, w):
+        self._w = w
+        self.shape = (w.shape[1], w.shape[0])
+
+    def __matmul__(self, y):
+        from . import _device as D
+        t = D.torch()
+        yd, was_np = D.to_device(y, device=self._w.device)
+        out = t.empty(self.shape[0], dtype=yd.dtype, device=self._w.device)
+        self._w.backward_(yd.reshape(-1), out)
+        return D.to_caller(out, was_np)
