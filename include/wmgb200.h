@@ -2,13 +2,16 @@
  * wmgb200.h -- C ABI of the B200-native WMG tomography hot path.
  *
  * Library: paper_1310_0956_b200/lib/libwmgb200.so (sm_100a).  Every entry point
- * takes plain pointers and sizes; device buffers are CALLER-OWNED (no
- * allocation inside kernels; the only internal allocation is the small
- * per-angle table made by wmg_geometry_create and freed by
- * wmg_geometry_destroy).  All work is asynchronous on the caller's CUDA stream
- * (cudaStream_t passed as void*, NULL = legacy default stream).  Functions are
- * reentrant; a geometry handle is immutable after creation and may be shared
- * read-only across threads and streams.
+ * takes plain pointers and sizes; device buffers are CALLER-OWNED.  The only
+ * internal allocations belong to a geometry handle: its per-angle and
+ * mirror-pair tables (wmg_geometry_create) and, on small symmetric grids
+ * (n <= 512), a scratch for the split float64 backprojector allocated on first
+ * use outside stream capture (all freed by wmg_geometry_destroy).  All work is
+ * asynchronous on the caller's CUDA stream (cudaStream_t passed as void*, NULL =
+ * legacy default stream).  Functions are reentrant; a geometry may be shared
+ * across threads and streams, except that fast float64 projections of one
+ * small-grid geometry must not run concurrently (shared scratch) and the
+ * setters (wmg_geometry_symmetry / wmg_geometry_kernel) must not race launches.
  *
  * Return codes (mapped by the Python host layer the way the reference raises):
  *   WMG_OK        0
@@ -34,6 +37,11 @@
  *   multilevel.py:36-79 haar_* / build_intergrid_set-> wmg_haar_restrict / wmg_haar_prolong
  *   multilevel.py:123-130 leaf Gram assembly        -> wmg_leaf_gram (sparse) or
  *                                                      wmg_leaf_factor (+ DGEMM)
+ *   sparse_kernels.py:68-75 cho_solve in the V-cycle -> wmg_batched_gemv (stored inverse)
+ *   multilevel.py:109-113 node systems, siblings     -> wmg_forward_batch / wmg_backward_batch
+ *   geometry.py:131-175 _joseph_entries             -> wmg_geometry_kernel (JOSEPH)
+ *   (CGLS / PCG-NE, not in the reference)           -> wmg_cgls_scalars, wmg_axpy_dev,
+ *                                                      wmg_lincomb_dev (device scalars)
  */
 #ifndef WMGB200_H
 #define WMGB200_H
