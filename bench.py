@@ -8,11 +8,16 @@ float32 data, x ~ U[0,1] seed 3000, y ~ U[0,1] seed 3001).  Default n = 4096
 than the 126 MB L2 together, so no explicit flush is needed; for n < 4096 an
 L2 flush is done between steps outside the timed events).
 
-Multi-GPU (torchrun, one process per GPU): angles are dealt round-robin to the
-ranks (angle k -> rank k mod N), each rank projects its angles and
-backprojects its sinogram rows, and the partial A^T y images are summed with an
-NCCL allreduce -- total work fixed ("strong" scaling).  Time = max over ranks of
-the CUDA-event time.
+Multi-GPU (torchrun, one process per GPU): the mirror pairs of angles {k, m-k}
+are dealt round-robin to the ranks (each shard keeps the symmetric kernels),
+each rank projects its angles and backprojects its sinogram rows, and the
+partial A^T y images are summed with an NCCL allreduce -- total work fixed
+("strong" scaling).  Time = max over ranks of the CUDA-event time.
+
+The same JSON line carries ``wmg_cgls`` (BASELINE config 1 WMG-CGLS seconds to
+rel. residual 1e-4, setup separate, plain CGLS beside it), the end-to-end
+number with host buffers (``e2e``), the CPU baselines and the rooflines;
+``--workload config2|config4`` runs the other BASELINE configurations.
 
 Prints ONE JSON line (rank 0).  ``--impl reference`` times the reference
 algorithm on the host CPU instead (the pinned C oracle: the reference's CSR
