@@ -380,10 +380,62 @@ __global__ void pad_transpose_kernel(const T* __restrict__ in, float* __restrict
   }
 }
 
+// Mirror-packed padded planes for the symmetric forward: PM[r][M + k] =
+// (img[r][k], img[r][n-1-k]) and PMT[c][M + r] = (img[r][c], img[n-1-r][c]),
+// float2, margins zero.  A ray's pixel pair in an image and in its x-mirror
+// image (k-1, k) / (n-1-k, n-k) then comes from two 64-bit loads of one plane
+// (PM[k-1], PM[k]) instead of four 32-bit loads.
+template <typename T>
+__global__ void pad_mirror_kernel(const T* __restrict__ in, float2* __restrict__ PM,
+                                  float2* __restrict__ PMT, int n) {
+  __shared__ float tile[32][33];
+  __shared__ float tilem[32][33];    // the column-mirrored input tile
+  const int pitch = n + 2 * kPadMargin;
+  const int bx = blockIdx.x * 32, by = blockIdx.y * 32;
+  for (int i = threadIdx.y; i < 32; i += 8) {
+    const int r = by + i, c = bx + threadIdx.x;
+    float v = 0.0f, vm = 0.0f, vr = 0.0f;
+    if (r < n && c < n) {
+      v = (float)in[(long long)r * n + c];
+      vm = (float)in[(long long)r * n + (n - 1 - c)];
+      vr = (float)in[(long long)(n - 1 - r) * n + c];
+      PM[(long long)r * pitch + kPadMargin + c] = make_float2(v, vm);
+    }
+    tile[i][threadIdx.x] = v;
+    tilem[i][threadIdx.x] = vr;
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += 8) {
+    const int c = bx + i, r = by + threadIdx.x;
+    if (r < n && c < n)
+      PMT[(long long)c * pitch + kPadMargin + r] =
+          make_float2(tile[threadIdx.x][i], tilem[threadIdx.x][i]);
+  }
+  if (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1) {
+    for (int i = threadIdx.y; i < 32; i += 8) {
+      const int r = by + i;
+      if (r >= n) continue;
+      for (int k = threadIdx.x; k < kPadMargin; k += 32) {
+        const float2 z = make_float2(0.0f, 0.0f);
+        if (blockIdx.x == 0) {
+          PM[(long long)r * pitch + k] = z;
+          PMT[(long long)r * pitch + k] = z;
+        }
+        if (blockIdx.x == gridDim.x - 1) {
+          PM[(long long)r * pitch + kPadMargin + n + k] = z;
+          PMT[(long long)r * pitch + kPadMargin + n + k] = z;
+        }
+      }
+    }
+  }
+}
+
 // Forward: one thread per ray, 128 consecutive detectors of one angle per
 // block.  Each warp walks the union of its lanes' slab ranges; the zero margin
 // makes out-of-grid reads harmless, so the inner loop has no branches.
-template <typename TOut>
+// ES = element stride of the planes (1: P / PT; 2: the x-component of the
+// mirror-packed float2 planes PM / PMT of the symmetric forward)
+template <typename TOut, int ES = 1>
 __global__ void __launch_bounds__(128) fwd_v2_kernel(GeomDev G, const float* __restrict__ P,
                                                      const float* __restrict__ PT,
                                                      TOut* __restrict__ sino) {
@@ -410,7 +462,7 @@ __global__ void __launch_bounds__(128) fwd_v2_kernel(GeomDev G, const float* __r
   const int rw1 = __reduce_max_sync(0xffffffffu, r1);
   float acc = 0.0f;
   if (rw0 <= rw1) {
-    const float* __restrict__ src = (A.major ? PT : P) + kPadMargin;
+    const float* __restrict__ src = (A.major ? PT : P) + ES * kPadMargin;
     const long long S = llrint(slope * kQ32);
     long long U = llrint(u0 * kQ32) + (long long)rw0 * S;
     const float L = A.Lf, Ls = A.Lsf;
@@ -426,8 +478,8 @@ __global__ void __launch_bounds__(128) fwd_v2_kernel(GeomDev G, const float* __r
         const int k = hi32(U);
         const float f = frac1((unsigned)U);
         const float wh = fminf(fmaf(f, Ls, -Ls), L);    // NaN (axis: inf-inf) -> L
-        const float* p = src + rowoff + k;
-        const float v1 = __ldg(p), v0 = __ldg(p - 1);
+        const float* p = src + ES * (rowoff + k);
+        const float v1 = __ldg(p), v0 = __ldg(p - ES);
         acc = fmaf(L, v0, acc);
         acc = fmaf(wh, v1 - v0, acc);
         rowoff += rowstep;
@@ -439,8 +491,8 @@ __global__ void __launch_bounds__(128) fwd_v2_kernel(GeomDev G, const float* __r
         const int k = hi32(U);
         const float f = frac1((unsigned)U);
         const float wh = fminf(fmaf(f, Ls, -Ls), L);
-        const float* p = src + rowoff + (n - 1 - k);
-        const float v1 = __ldg(p), v0 = __ldg(p + 1);
+        const float* p = src + ES * (rowoff + (n - 1 - k));
+        const float v1 = __ldg(p), v0 = __ldg(p + ES);
         acc = fmaf(L, v0, acc);
         acc = fmaf(wh, v1 - v0, acc);
         rowoff += rowstep;
@@ -684,7 +736,7 @@ __global__ void __launch_bounds__(256, 5) bwd_sym_kernel(GeomDev G, const TIn* _
 // forward is bound by L1 sector throughput, and this cuts the sector requests
 // 2.3x (profiles/r1b_fwd_variants_ncu.txt).  Without kMix the 4 angles are 4
 // warps that share L1 lines (2.4x less L2 traffic, little time gained).
-template <typename TOut, int kAG, bool kLock = false, bool kMix = false>
+template <typename TOut, int kAG, bool kLock = false, bool kMix = false, bool kPM = false>
 __global__ void __launch_bounds__(kAG == 1 ? 128 : 32 * kAG) fwd_sym_kernel(GeomDev G, const float* __restrict__ P,
                                                       const float* __restrict__ PT,
                                                       TOut* __restrict__ sino) {
@@ -775,14 +827,27 @@ __global__ void __launch_bounds__(kAG == 1 ? 128 : 32 * kAG) fwd_sym_kernel(Geom
           const float f = frac1((unsigned)U);
           wh[q] = fminf(fmaf(f, Ls, -Ls), L);
           const int km = n - 1 - k;
-          const float* pa1 = base + (rowA + (unsigned)k);
-          const float* pa2 = base + (rowA + (unsigned)km);
-          const float* pb1 = base + (rowB + (unsigned)km);
-          const float* pb2 = base + (rowB + (unsigned)k);
-          v1A[q] = make_float2(__ldg(pa1), __ldg(pa2));
-          v0A[q] = make_float2(__ldg(pa1 - 1), __ldg(pa2 + 1));
-          v1B[q] = make_float2(__ldg(pb1), __ldg(pb2));
-          v0B[q] = make_float2(__ldg(pb1 + 1), __ldg(pb2 - 1));
+          if constexpr (kPM) {
+            // mirror-packed planes: (pixel, x-mirror pixel) per 64-bit load
+            const float2* b2 = reinterpret_cast<const float2*>(base);
+            const float2 a1 = __ldg(b2 + (rowA + (unsigned)k));
+            const float2 a0 = __ldg(b2 + (rowA + (unsigned)k - 1u));
+            const float2 c1 = __ldg(b2 + (rowB + (unsigned)k));
+            const float2 c0 = __ldg(b2 + (rowB + (unsigned)k - 1u));
+            v1A[q] = a1;
+            v0A[q] = a0;
+            v1B[q] = make_float2(c1.y, c1.x);
+            v0B[q] = make_float2(c0.y, c0.x);
+          } else {
+            const float* pa1 = base + (rowA + (unsigned)k);
+            const float* pa2 = base + (rowA + (unsigned)km);
+            const float* pb1 = base + (rowB + (unsigned)km);
+            const float* pb2 = base + (rowB + (unsigned)k);
+            v1A[q] = make_float2(__ldg(pa1), __ldg(pa2));
+            v0A[q] = make_float2(__ldg(pa1 - 1), __ldg(pa2 + 1));
+            v1B[q] = make_float2(__ldg(pb1), __ldg(pb2));
+            v0B[q] = make_float2(__ldg(pb1 + 1), __ldg(pb2 - 1));
+          }
           rowA += up;
           rowB -= up;
         }
@@ -803,14 +868,25 @@ __global__ void __launch_bounds__(kAG == 1 ? 128 : 32 * kAG) fwd_sym_kernel(Geom
         const float wh = fminf(fmaf(f, Ls, -Ls), L);
         const float2 W = make_float2(wh, wh);
         const int km = n - 1 - k;
-        const float* pa1 = base + (rowA + (unsigned)k);
-        const float* pa2 = base + (rowA + (unsigned)km);
-        const float* pb1 = base + (rowB + (unsigned)km);
-        const float* pb2 = base + (rowB + (unsigned)k);
-        const float2 v1A = make_float2(__ldg(pa1), __ldg(pa2));
-        const float2 v0A = make_float2(__ldg(pa1 - 1), __ldg(pa2 + 1));
-        const float2 v1B = make_float2(__ldg(pb1), __ldg(pb2));
-        const float2 v0B = make_float2(__ldg(pb1 + 1), __ldg(pb2 - 1));
+        float2 v1A, v0A, v1B, v0B;
+        if constexpr (kPM) {
+          const float2* b2 = reinterpret_cast<const float2*>(base);
+          v1A = __ldg(b2 + (rowA + (unsigned)k));
+          v0A = __ldg(b2 + (rowA + (unsigned)k - 1u));
+          const float2 c1 = __ldg(b2 + (rowB + (unsigned)k));
+          const float2 c0 = __ldg(b2 + (rowB + (unsigned)k - 1u));
+          v1B = make_float2(c1.y, c1.x);
+          v0B = make_float2(c0.y, c0.x);
+        } else {
+          const float* pa1 = base + (rowA + (unsigned)k);
+          const float* pa2 = base + (rowA + (unsigned)km);
+          const float* pb1 = base + (rowB + (unsigned)km);
+          const float* pb2 = base + (rowB + (unsigned)k);
+          v1A = make_float2(__ldg(pa1), __ldg(pa2));
+          v0A = make_float2(__ldg(pa1 - 1), __ldg(pa2 + 1));
+          v1B = make_float2(__ldg(pb1), __ldg(pb2));
+          v0B = make_float2(__ldg(pb1 + 1), __ldg(pb2 - 1));
+        }
         accA = __ffma2_rn(LL, v0A, accA);
         accA = __ffma2_rn(W, __fadd2_rn(v1A, make_float2(-v0A.x, -v0A.y)), accA);
         accB = __ffma2_rn(LL, v0B, accB);
@@ -1196,6 +1272,25 @@ static cudaError_t fwd_v2_impl(const GeomDev& G, const void* x, void* ws, void* 
   float* P = (float*)ws;
   float* PT = P + plane;
   dim3 tg((G.n + 31) / 32, (G.n + 31) / 32), tb(32, 8);
+  // default symmetric forward: mirror-packed float2 planes (PM, PMT)
+  const bool packed = use_sym_fwd(G) && Gx && !(G.sym & (4 | 16 | 32 | 64 | 128));
+  if (packed) {
+    float2* PM = (float2*)ws;
+    float2* PMT = PM + plane;
+    fast::pad_mirror_kernel<TIn><<<tg, tb, 0, st>>>((const TIn*)x, PM, PMT, G.n);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    constexpr int ag = fast::kFwdAG;
+    dim3 mgrid(((G.d + 1) / 2 + 8 * ag - 1) / (8 * ag), (G.n_half + 3) / 4);
+    fast::fwd_sym_kernel<TOut, ag, false, true, true><<<mgrid, 32 * ag, 0, st>>>(
+        G, (const float*)PM, (const float*)PMT, (TOut*)y);
+    e = cudaGetLastError();
+    if (e != cudaSuccess || Gx->m == 0) return e;
+    dim3 xgrid((G.d + 127) / 128, Gx->m);   // the axis-aligned angles of the set
+    fast::fwd_v2_kernel<TOut, 2><<<xgrid, 128, 0, st>>>(*Gx, (const float*)PM,
+                                                         (const float*)PMT, (TOut*)y);
+    return cudaGetLastError();
+  }
   fast::pad_transpose_kernel<TIn><<<tg, tb, 0, st>>>((const TIn*)x, P, PT, G.n);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
@@ -1213,7 +1308,7 @@ static cudaError_t fwd_v2_impl(const GeomDev& G, const void* x, void* ws, void* 
           fast::fwd_sym_kernel<TOut, ag, true><<<sgrid, 32 * ag, 0, st>>>(G, P, PT, (TOut*)y);
         } else if (G.sym & 64) {  // testing: 32 rays of one angle per warp
           fast::fwd_sym_kernel<TOut, ag><<<sgrid, 32 * ag, 0, st>>>(G, P, PT, (TOut*)y);
-        } else {                  // default: 8 rays x 4 adjacent angles per warp
+        } else {                  // (sym & 128) testing: mixed warps on the plain planes
           dim3 mgrid(((G.d + 1) / 2 + 8 * ag - 1) / (8 * ag), (G.n_half + 3) / 4);
           fast::fwd_sym_kernel<TOut, ag, false, true><<<mgrid, 32 * ag, 0, st>>>(G, P, PT,
                                                                                (TOut*)y);
@@ -1288,7 +1383,8 @@ static cudaError_t bwd_v2_impl(const GeomDev& G, const void* y, void* x, bool ac
 }
 
 size_t fast_forward_workspace_bytes(int n, int precision, int tin) {
-  if (precision == 0) return sizeof(float) * 2 * (size_t)n * (size_t)(n + 2 * kPadMargin);
+  // fp32: P and PT, or the mirror-packed float2 planes PM and PMT (twice the size)
+  if (precision == 0) return sizeof(float) * 4 * (size_t)n * (size_t)(n + 2 * kPadMargin);
   // float64: padded double planes (symmetric path) -- also holds the transposed
   // copy of the generic path
   return sizeof(double) * 2 * (size_t)n * (size_t)(n + 2 * kPadMargin);

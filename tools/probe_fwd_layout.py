@@ -37,9 +37,13 @@ for n in (1024, 2048, 4096):
     s4 = torch.empty(n * d, device="cuda")
     w.set_symmetry("fwdrows")
     tm = ev_time(lambda: w.forward_(x, s4))
+    s5 = torch.empty(n * d, device="cuda")
+    w.set_symmetry("plainplanes")
+    tp = ev_time(lambda: w.forward_(x, s5))
     torch.cuda.synchronize()
     torch.cuda.synchronize()
-    out[n] = {"fwd_default_ms": t4, "fwd_1angle_ms": t1, "fwd_lockstep_ms": tl, "fwd_rows_ms": tm,
+    out[n] = {"fwd_default_ms": t4, "fwd_1angle_ms": t1, "fwd_lockstep_ms": tl, "fwd_rows_ms": tm, "fwd_plainplanes_ms": tp,
+              "plain_max_rel_diff": float((s1 - s5).abs().max() / s1.abs().max()),
               "rows_max_rel_diff": float((s1 - s4).abs().max() / s1.abs().max()),
               "max_abs_diff": float((s1 - s2).abs().max()),
               "lockstep_max_rel_diff": float((s1 - s3).abs().max() / s1.abs().max())}
