@@ -853,11 +853,14 @@ __global__ void __launch_bounds__(kAG == 1 ? 128 : 32 * kAG) fwd_sym_kernel(Geom
         }
   #pragma unroll
         for (int q = 0; q < 4; ++q) {
+          // (L - wh) v0 + wh v1: two packed FMAs per image pair, no subtraction
           const float2 W = make_float2(wh[q], wh[q]);
-          accA = __ffma2_rn(LL, v0A[q], accA);
-          accA = __ffma2_rn(W, __fadd2_rn(v1A[q], make_float2(-v0A[q].x, -v0A[q].y)), accA);
-          accB = __ffma2_rn(LL, v0B[q], accB);
-          accB = __ffma2_rn(W, __fadd2_rn(v1B[q], make_float2(-v0B[q].x, -v0B[q].y)), accB);
+          const float wl = L - wh[q];
+          const float2 WL = make_float2(wl, wl);
+          accA = __ffma2_rn(WL, v0A[q], accA);
+          accA = __ffma2_rn(W, v1A[q], accA);
+          accB = __ffma2_rn(WL, v0B[q], accB);
+          accB = __ffma2_rn(W, v1B[q], accB);
         }
       }
       for (; r <= rw1; ++r) {
@@ -887,10 +890,11 @@ __global__ void __launch_bounds__(kAG == 1 ? 128 : 32 * kAG) fwd_sym_kernel(Geom
           v1B = make_float2(__ldg(pb1), __ldg(pb2));
           v0B = make_float2(__ldg(pb1 + 1), __ldg(pb2 - 1));
         }
-        accA = __ffma2_rn(LL, v0A, accA);
-        accA = __ffma2_rn(W, __fadd2_rn(v1A, make_float2(-v0A.x, -v0A.y)), accA);
-        accB = __ffma2_rn(LL, v0B, accB);
-        accB = __ffma2_rn(W, __fadd2_rn(v1B, make_float2(-v0B.x, -v0B.y)), accB);
+        const float2 WL = make_float2(L - wh, L - wh);
+        accA = __ffma2_rn(WL, v0A, accA);
+        accA = __ffma2_rn(W, v1A, accA);
+        accB = __ffma2_rn(WL, v0B, accB);
+        accB = __ffma2_rn(W, v1B, accB);
         rowA += up;
         rowB -= up;
       }
