@@ -830,10 +830,10 @@ __global__ void __launch_bounds__(kAG == 1 ? 128 : 32 * kAG) fwd_sym_kernel(Geom
           if constexpr (kPM) {
             // mirror-packed planes: (pixel, x-mirror pixel) per 64-bit load
             const float2* b2 = reinterpret_cast<const float2*>(base);
-            const float2 a1 = __ldg(b2 + (rowA + (unsigned)k));
-            const float2 a0 = __ldg(b2 + (rowA + (unsigned)k - 1u));
-            const float2 c1 = __ldg(b2 + (rowB + (unsigned)k));
-            const float2 c0 = __ldg(b2 + (rowB + (unsigned)k - 1u));
+            const float2* pA = b2 + (rowA + (unsigned)k);   // k - 1 is pA[-1]: one
+            const float2* pB = b2 + (rowB + (unsigned)k);   // address per row
+            const float2 a1 = __ldg(pA), a0 = __ldg(pA - 1);
+            const float2 c1 = __ldg(pB), c0 = __ldg(pB - 1);
             v1A[q] = a1;
             v0A[q] = a0;
             v1B[q] = make_float2(c1.y, c1.x);
@@ -874,10 +874,11 @@ __global__ void __launch_bounds__(kAG == 1 ? 128 : 32 * kAG) fwd_sym_kernel(Geom
         float2 v1A, v0A, v1B, v0B;
         if constexpr (kPM) {
           const float2* b2 = reinterpret_cast<const float2*>(base);
-          v1A = __ldg(b2 + (rowA + (unsigned)k));
-          v0A = __ldg(b2 + (rowA + (unsigned)k - 1u));
-          const float2 c1 = __ldg(b2 + (rowB + (unsigned)k));
-          const float2 c0 = __ldg(b2 + (rowB + (unsigned)k - 1u));
+          const float2* pA = b2 + (rowA + (unsigned)k);
+          const float2* pB = b2 + (rowB + (unsigned)k);
+          v1A = __ldg(pA);
+          v0A = __ldg(pA - 1);
+          const float2 c1 = __ldg(pB), c0 = __ldg(pB - 1);
           v1B = make_float2(c1.y, c1.x);
           v0B = make_float2(c0.y, c0.x);
         } else {
