@@ -198,3 +198,33 @@ def test_device_tensors_stay_on_device(gpu, golden):
     b = torch.from_numpy(np.ones(w.shape[0])).cuda()
     x, rec = cgls_solve(w, b, cfg=SolverConfig(max_iterations=3))
     assert isinstance(x, torch.Tensor) and x.is_cuda
+
+
+def test_zero_and_degenerate_inputs(gpu, golden):
+    """Zero data: every solver returns x = 0 with a converged record at
+    iteration 0 (SIRT: zero residual); zero iteration budget is rejected by
+    SolverConfig; rays missing the grid (empty rows) do not disturb SIRT."""
+    from paper_1310_0956_b200 import (SolverConfig, bicgstab_solve, build_geometry,
+                                      build_projector, cgls_solve, gmres_solve,
+                                      normal_operator, sirt_solve)
+    g = build_geometry(16, 40, 12)          # 40 detectors: many rays miss the 16^2 grid
+    w = build_projector(g)
+    zb = np.zeros(g.n_data)
+    cfg = SolverConfig(max_iterations=5, residual_tolerance=1e-8)
+    x, rec = cgls_solve(w, zb, cfg=cfg)
+    assert np.all(x == 0) and rec.status == "converged" and rec.iterations == [0]
+    x, rec = gmres_solve(normal_operator(w, 0.0), np.zeros(g.n_image), cfg=cfg)
+    assert np.all(x == 0) and rec.status == "converged"
+    x, rec = bicgstab_solve(normal_operator(w, 0.0), np.zeros(g.n_image), cfg=cfg)
+    assert np.all(x == 0) and rec.status == "converged"
+    x, rec = sirt_solve(w, zb, None, cfg)
+    assert np.all(x == 0)
+    with pytest.raises(ValueError):
+        SolverConfig(max_iterations=0)
+    rs = np.random.default_rng(5)
+    xt = rs.uniform(0, 1, g.n_image)
+    b = w @ xt
+    rows = np.asarray(w.sum(axis=1)).ravel()
+    assert (rows == 0).any()                  # empty rows exist
+    x, rec = sirt_solve(w, b, None, SolverConfig(max_iterations=50))
+    assert np.all(np.isfinite(x)) and rec.rel_residual[-1] < rec.rel_residual[0]
