@@ -1028,15 +1028,27 @@ __global__ void __launch_bounds__(32 * kSplitF) fwd_split64_kernel(GeomDev G,
 }
 
 // symmetric forward in float64: u evaluated directly at every slab end
-template <typename TOut>
+// kMix: warps of 8 rays x 4 adjacent angles, like the fp32 kernel (k clamped
+// into the margins in the groups the host did not mark safe)
+template <typename TOut, bool kMix = false>
 __global__ void __launch_bounds__(128) fwd_sym64_kernel(GeomDev G, const double* __restrict__ P,
                                                         const double* __restrict__ PT,
                                                         TOut* __restrict__ sino) {
-  const int a = G.half[blockIdx.y];
+  int hidx, j;
+  if (kMix) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    hidx = blockIdx.y * 4 + (lane >> 3);
+    j = blockIdx.x * 32 + warp * 8 + (lane & 7);
+  } else {
+    hidx = blockIdx.y;
+    j = blockIdx.x * 128 + threadIdx.x;
+  }
+  const bool hvalid = hidx < G.n_half;
+  if (!hvalid) hidx = G.n_half - 1;
+  const int a = G.half[hidx];
   const int b = G.mir[a];
   const int d = G.d, m = G.m, n = G.n;
   const int jh = (d + 1) / 2;
-  const int j = blockIdx.x * 128 + threadIdx.x;
   const AngleParams& A = G.ang[a];
   const int pitch = n + 2 * kPadMargin;
   const double off = (double)j - (double)(d - 1) * 0.5;
@@ -1055,6 +1067,7 @@ __global__ void __launch_bounds__(128) fwd_sym64_kernel(GeomDev G, const double*
   }
   const int rw0 = __reduce_min_sync(0xffffffffu, r0);
   const int rw1 = __reduce_max_sync(0xffffffffu, r1);
+  const bool clampk = kMix && !G.gsafe[blockIdx.y];
   double a1 = 0.0, a2 = 0.0, a3 = 0.0, a4 = 0.0;
   if (rw0 <= rw1) {
     const double* __restrict__ base = (A.major ? PT : P);
@@ -1062,30 +1075,38 @@ __global__ void __launch_bounds__(128) fwd_sym64_kernel(GeomDev G, const double*
     unsigned rowA = (unsigned)(rw0 * pitch + kPadMargin);
     unsigned rowB = (unsigned)((n - 1 - rw0) * pitch + kPadMargin);
     const unsigned up = (unsigned)pitch;
+    auto walk = [&](auto clampTag) {
 #pragma unroll 2
-    for (int r = rw0; r <= rw1; ++r) {
-      const double uh = fma((double)(r + 1), slope, u0);
-      const double fk = floor(uh);
-      const int k = (int)fk;
-      const double wh = fmin((uh - fk) * Ls, L);
-      const int km = n - 1 - k;
-      const double* pa1 = base + (rowA + (unsigned)k);
-      const double* pa2 = base + (rowA + (unsigned)km);
-      const double* pb1 = base + (rowB + (unsigned)km);
-      const double* pb2 = base + (rowB + (unsigned)k);
-      const double u1 = __ldg(pa1), v1 = __ldg(pa1 - 1);
-      const double u2 = __ldg(pa2), v2 = __ldg(pa2 + 1);
-      const double u3 = __ldg(pb1), v3 = __ldg(pb1 + 1);
-      const double u4 = __ldg(pb2), v4 = __ldg(pb2 - 1);
-      a1 = fma(wh, u1 - v1, fma(L, v1, a1));
-      a2 = fma(wh, u2 - v2, fma(L, v2, a2));
-      a3 = fma(wh, u3 - v3, fma(L, v3, a3));
-      a4 = fma(wh, u4 - v4, fma(L, v4, a4));
-      rowA += up;
-      rowB -= up;
-    }
+      for (int r = rw0; r <= rw1; ++r) {
+        const double uh = fma((double)(r + 1), slope, u0);
+        const double fk = floor(uh);
+        int k = (int)fk;
+        if constexpr (decltype(clampTag)::value) k = min(max(k, 2 - kPadMargin), n + kPadMargin - 3);
+        const double wh = fmin((uh - fk) * Ls, L);
+        const double wl = L - wh;
+        const int km = n - 1 - k;
+        const double* pa1 = base + (rowA + (unsigned)k);
+        const double* pa2 = base + (rowA + (unsigned)km);
+        const double* pb1 = base + (rowB + (unsigned)km);
+        const double* pb2 = base + (rowB + (unsigned)k);
+        const double u1 = __ldg(pa1), v1 = __ldg(pa1 - 1);
+        const double u2 = __ldg(pa2), v2 = __ldg(pa2 + 1);
+        const double u3 = __ldg(pb1), v3 = __ldg(pb1 + 1);
+        const double u4 = __ldg(pb2), v4 = __ldg(pb2 - 1);
+        a1 = fma(wh, u1, fma(wl, v1, a1));
+        a2 = fma(wh, u2, fma(wl, v2, a2));
+        a3 = fma(wh, u3, fma(wl, v3, a3));
+        a4 = fma(wh, u4, fma(wl, v4, a4));
+        rowA += up;
+        rowB -= up;
+      }
+    };
+    if (clampk)
+      walk(std::true_type{});
+    else
+      walk(std::false_type{});
   }
-  if (j < jh) {
+  if (j < jh && hvalid) {
     const double r_m = A.major ? a4 : a2;
     const double r_mr = A.major ? a2 : a4;
     sino[(long long)a * d + j] = (TOut)a1;
@@ -1406,8 +1427,13 @@ static cudaError_t fwd64_impl(const GeomDev& G, const void* x, void* ws, void* y
   fast::pad_transpose64_kernel<TIn><<<tg, tb, 0, st>>>((const TIn*)x, P, PT, G.n);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  dim3 sgrid(((G.d + 1) / 2 + 127) / 128, G.n_half);
-  fast::fwd_sym64_kernel<TOut><<<sgrid, 128, 0, st>>>(G, P, PT, (TOut*)y);
+  if (G.sym & 64) {   // testing: 128 rays of one angle per block
+    dim3 sgrid(((G.d + 1) / 2 + 127) / 128, G.n_half);
+    fast::fwd_sym64_kernel<TOut><<<sgrid, 128, 0, st>>>(G, P, PT, (TOut*)y);
+  } else {            // default: warps of 8 rays x 4 adjacent angles
+    dim3 mgrid(((G.d + 1) / 2 + 31) / 32, (G.n_half + 3) / 4);
+    fast::fwd_sym64_kernel<TOut, true><<<mgrid, 128, 0, st>>>(G, P, PT, (TOut*)y);
+  }
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   // the axis-aligned angles: generic walk on the padded planes
