@@ -289,13 +289,14 @@ __global__ void haar_prolong_kernel(int side, const double* __restrict__ coarse,
 // read once, coalesced; x_b is staged in shared memory; each warp reduces its
 // rows with a fixed shuffle tree (deterministic).
 // ---------------------------------------------------------------------------
-constexpr int kGemvRows = 32;   // rows per block (4 per warp)
 
+// rpw rows per warp (8 warps per block): chosen by the launcher so that even a
+// single 4096^2 matrix spreads over enough blocks to stream at HBM rate
 __global__ void __launch_bounds__(256) batched_gemv_kernel(int p, const double* __restrict__ A,
                                                            long long sA,
                                                            const double* __restrict__ x,
                                                            long long sx, double* __restrict__ y,
-                                                           long long sy) {
+                                                           long long sy, int rpw) {
   extern __shared__ double xs[];
   const int b = blockIdx.y;
   const double* Ab = A + (long long)b * sA;
@@ -303,14 +304,30 @@ __global__ void __launch_bounds__(256) batched_gemv_kernel(int p, const double* 
   for (int i = threadIdx.x; i < p; i += blockDim.x) xs[i] = xb[i];
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int row0 = blockIdx.x * kGemvRows + warp * (kGemvRows / 8);
-#pragma unroll
-  for (int rr = 0; rr < kGemvRows / 8; ++rr) {
+  const int row0 = blockIdx.x * 8 * rpw + warp * rpw;
+  for (int rr = 0; rr < rpw; ++rr) {
     const int row = row0 + rr;
     if (row >= p) break;
     const double* Ar = Ab + (long long)row * p;
     double acc = 0.0;
-    for (int c = lane; c < p; c += 32) acc = fma(__ldg(Ar + c), xs[c], acc);
+    if ((p & 1) == 0) {
+      // 16-byte loads, two accumulators, 4 loads in flight per lane: the
+      // stored inverses are streamed at HBM rate
+      const double2* Ar2 = reinterpret_cast<const double2*>(Ar);
+      const double2* xs2 = reinterpret_cast<const double2*>(xs);
+      double acc1 = 0.0;
+      const int p2 = p >> 1;
+#pragma unroll 4
+      for (int c = lane; c < p2; c += 32) {
+        const double2 a = __ldg(Ar2 + c);
+        const double2 xv = xs2[c];
+        acc = fma(a.x, xv.x, acc);
+        acc1 = fma(a.y, xv.y, acc1);
+      }
+      acc += acc1;
+    } else {
+      for (int c = lane; c < p; c += 32) acc = fma(__ldg(Ar + c), xs[c], acc);
+    }
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, off);
     if (lane == 0) y[(long long)b * sy + row] = acc;
@@ -469,8 +486,11 @@ cudaError_t batched_gemv(int batch, int p, const double* A, long long sA, const 
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
-  dim3 grid((p + vec::kGemvRows - 1) / vec::kGemvRows, batch);
-  vec::batched_gemv_kernel<<<grid, 256, smem, st>>>(p, A, sA, x, sx, y, sy);
+  // rows per warp: 4 when the batch alone fills the GPU, down to 1 otherwise
+  int rpw = 4;
+  while (rpw > 1 && (long long)((p + 8 * rpw - 1) / (8 * rpw)) * batch < 4LL * 148) rpw >>= 1;
+  dim3 grid((p + 8 * rpw - 1) / (8 * rpw), batch);
+  vec::batched_gemv_kernel<<<grid, 256, smem, st>>>(p, A, sA, x, sx, y, sy, rpw);
   return cudaGetLastError();
 }
 
