@@ -1229,13 +1229,29 @@ __global__ void __launch_bounds__(256) bwd_sym64_kernel(GeomDev G, const TIn* __
   }
 }
 
-template <typename TOut, bool kAccumulate>
+// Sums the angle slices and adds the axis-aligned angles of the set (Gx: the
+// reference's tie rule for rays on grid lines; at most two angles) in the
+// same pass -- one launch instead of reduce + axis backprojection.
+template <typename TIn, typename TOut, bool kAccumulate>
 __global__ void sym_reduce_kernel(const double* __restrict__ part, int nsplit, long long N,
-                                  TOut* __restrict__ img) {
+                                  TOut* __restrict__ img, GeomDev Gx,
+                                  const TIn* __restrict__ sino) {
   const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= N) return;
   double s = part[p];
   for (int z = 1; z < nsplit; ++z) s += part[(long long)z * N + p];
+  const int n = Gx.n;
+  const int row = (int)(p / n), ix = (int)(p % n);
+  const double xc = (double)ix - (double)n * 0.5 + 0.5;
+  const double yc = (double)n * 0.5 - (double)row - 0.5;
+  const double dc = (double)(Gx.d - 1) * 0.5;
+  for (int a = 0; a < Gx.m; ++a) {
+    const AngleParams& P = Gx.ang[a];
+    const double pj = xc * P.c + yc * P.s + dc;
+    const int j = (int)ceil(pj - 0.5);
+    if (j >= 0 && j < Gx.d)
+      s += (double)__ldg(sino + (long long)(Gx.rowmap ? Gx.rowmap[a] : a) * Gx.d + j);
+  }
   if (kAccumulate)
     img[p] = (TOut)((double)img[p] + s);
   else
@@ -1463,13 +1479,16 @@ static cudaError_t bwd64_impl(const GeomDev& G, const void* y, void* x, bool acc
                                                                    nsplit, part);
   cudaError_t e = cudaGetLastError();
   if (e == cudaSuccess && part) {
+    // slice sum + the axis angles in one pass
     const long long N = (long long)G.n * G.n;
     const unsigned rb = (unsigned)((N + 255) / 256);
     if (accumulate)
-      fast::sym_reduce_kernel<TOut, true><<<rb, 256, 0, st>>>(part, nsplit, N, (TOut*)x);
+      fast::sym_reduce_kernel<TIn, TOut, true><<<rb, 256, 0, st>>>(part, nsplit, N, (TOut*)x,
+                                                                   *Gx, (const TIn*)y);
     else
-      fast::sym_reduce_kernel<TOut, false><<<rb, 256, 0, st>>>(part, nsplit, N, (TOut*)x);
-    e = cudaGetLastError();
+      fast::sym_reduce_kernel<TIn, TOut, false><<<rb, 256, 0, st>>>(part, nsplit, N, (TOut*)x,
+                                                                    *Gx, (const TIn*)y);
+    return cudaGetLastError();
   }
   if (e != cudaSuccess || Gx->m == 0) return e;
   dim3 g2((G.n + 31) / 32, (G.n + 7) / 8);
