@@ -159,6 +159,10 @@ int wmg_bicg_x(long long n, double *x, double alpha, const double *ph, double om
 int wmg_scale(long long n, double *out, double a, const double *x, const double *y,
               void *stream);
 int wmg_recip(long long n, double *out, const double *s, void *stream);
+/* WMG node smoother sweep: z += omega * (c .* (r - az)),
+ * az may be NULL (z = 0 before the first sweep). */
+int wmg_smooth_update(long long n, double *z, double omega, const double *c, const double *r,
+                      const double *az, void *stream);
 int wmg_sirt_update(long long n, double *x, const double *c, const double *g, double lam,
                     void *stream);
 int wmg_add_scaled(long long n, double *out, const double *g, double lam, int sgn,

@@ -141,6 +141,13 @@ def add_scaled(out, g, lam, sgn, v):
     return out
 
 
+def smooth_update(z, omega, c, r, az=None):
+    """z += omega * (c .* (r - az)) in one kernel (az None: az = 0)."""
+    N.call("wmg_smooth_update", z.numel(), ptr(z), float(omega), ptr(c), ptr(r), ptr(az),
+           stream_handle())
+    return z
+
+
 def hadamard(out, x, y):
     N.call("wmg_scale", out.numel(), ptr(out), 1.0, ptr(x), ptr(y), stream_handle())
     return out

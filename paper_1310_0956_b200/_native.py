@@ -59,6 +59,7 @@ _SIGS = {
     "wmg_bicg_x": (_i, [_ll, _dp, _d, _dp, _d, _dp, _vp]),
     "wmg_scale": (_i, [_ll, _dp, _d, _dp, _dp, _vp]),
     "wmg_recip": (_i, [_ll, _dp, _dp, _vp]),
+    "wmg_smooth_update": (_i, [_ll, _dp, _d, _dp, _dp, _dp, _vp]),
     "wmg_sirt_update": (_i, [_ll, _dp, _dp, _dp, _d, _vp]),
     "wmg_add_scaled": (_i, [_ll, _dp, _dp, _d, _i, _dp, _vp]),
     "wmg_cgs_update": (_i, [_ll, _i, _dp, _dp, _ll, _dp, _vp]),

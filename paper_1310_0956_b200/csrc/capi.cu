@@ -41,6 +41,8 @@ cudaError_t ew_bicg_x(long long, double*, double, const double*, double, const d
                       cudaStream_t);
 cudaError_t ew_scale(long long, double*, double, const double*, const double*, cudaStream_t);
 cudaError_t ew_recip(long long, double*, const double*, cudaStream_t);
+cudaError_t ew_smooth_update(long long, double*, double, const double*, const double*,
+                            const double*, cudaStream_t);
 cudaError_t ew_sirt_update(long long, double*, const double*, const double*, double,
                            cudaStream_t);
 cudaError_t ew_add_scaled(long long, double*, const double*, double, int, const double*,
@@ -529,6 +531,11 @@ int wmg_scale(long long n, double* out, double a, const double* x, const double*
 int wmg_recip(long long n, double* out, const double* s, void* stream) {
   REQ(out && s);
   return cuda_rc(wmg::ew_recip(n, out, s, STREAM(stream)));
+}
+int wmg_smooth_update(long long n, double* z, double omega, const double* c, const double* r,
+                      const double* az, void* stream) {
+  REQ(z && c && r);
+  return cuda_rc(wmg::ew_smooth_update(n, z, omega, c, r, az, STREAM(stream)));
 }
 int wmg_sirt_update(long long n, double* x, const double* c, const double* g, double lam,
                     void* stream) {

@@ -168,6 +168,16 @@ __global__ void scale_kernel(long long n, double* out, double a, const double* x
   GRID_LOOP(i, n) { out[i] = y ? dmul(x[i], y[i]) : dmul(a, x[i]); }
 }
 
+// WMG node smoother sweep, fused: z += omega * (c .* (r - az))  (az == nullptr: az = 0);
+// the same rounded operations as the unfused axpy / hadamard / axpy sequence
+__global__ void smooth_update_kernel(long long n, double* z, double omega, const double* c,
+                                     const double* r, const double* az) {
+  GRID_LOOP(i, n) {
+    const double res = az ? dsub(r[i], az[i]) : r[i];
+    z[i] = dadd(z[i], dmul(omega, dmul(c[i], res)));
+  }
+}
+
 // inverse with the SIRT zero convention: out = s > 0 ? 1/s : 0 (solvers.py:84-85)
 __global__ void recip_kernel(long long n, double* out, const double* s) {
   GRID_LOOP(i, n) { out[i] = s[i] > 0.0 ? __drcp_rn(s[i]) : 0.0; }
@@ -452,6 +462,10 @@ cudaError_t ew_scale(long long n, double* out, double a, const double* x, const 
 }
 cudaError_t ew_recip(long long n, double* out, const double* s, cudaStream_t st) {
   LAUNCH_EW(vec::recip_kernel, n, out, s);
+}
+cudaError_t ew_smooth_update(long long n, double* z, double omega, const double* c,
+                            const double* r, const double* az, cudaStream_t st) {
+  LAUNCH_EW(vec::smooth_update_kernel, n, z, omega, c, r, az);
 }
 cudaError_t ew_sirt_update(long long n, double* x, const double* c, const double* g, double lam,
                            cudaStream_t st) {

@@ -436,16 +436,14 @@ def _node_solve_(node: WmgNode, r, multiplicative: bool):
     z = t.zeros_like(r)
     az = t.empty_like(r)
     res = t.empty_like(r)
-    upd = t.empty_like(r)
 
     def sweep(z_is_zero):
+        # z += omega C (r - A z), one fused kernel (same rounding as the unfused form)
         if z_is_zero:
-            res.copy_(r)
+            D.smooth_update(z, node.smooth_omega, node.smooth_c, r)
         else:
             node.apply_system_(z, az)
-            D.axpy(res, r, 1.0, -1, az)
-        D.hadamard(upd, node.smooth_c, res)
-        D.axpy(z, z, node.smooth_omega, +1, upd)
+            D.smooth_update(z, node.smooth_omega, node.smooth_c, r, az)
 
     zero = True
     for _ in range(h.nu_pre):
@@ -543,17 +541,13 @@ def _node_solve_batch_(nodes, R):
     Z = t.zeros_like(R)
     AZ = t.empty_like(R)
     RES = t.empty_like(R)
-    UPD = t.empty_like(R)
 
     def sweep(z_is_zero):
-        if z_is_zero:
-            RES.copy_(R)
-        else:
+        if not z_is_zero:
             _apply_system_batch_(nodes, Z, AZ)
-            D.axpy(RES.view(-1), R.view(-1), 1.0, -1, AZ.view(-1))
         for b, nd in enumerate(nodes):
-            D.hadamard(UPD[b], nd.smooth_c, RES[b])
-            D.axpy(Z[b], Z[b], nd.smooth_omega, +1, UPD[b])
+            D.smooth_update(Z[b], nd.smooth_omega, nd.smooth_c, R[b],
+                            None if z_is_zero else AZ[b])
 
     zero = True
     for _ in range(h.nu_pre):
