@@ -955,16 +955,18 @@ __global__ void pad_transpose64_kernel(const T* __restrict__ in, double* __restr
 // order; u is evaluated directly at every slab end (fma), the two straddling
 // pixels are read without bounds checks (zero margins) and blended as
 // L v0 + wh (v1 - v0).  blockIdx.z = batch item.
-template <typename TOut>
+// kMix: lanes = 8 rays x 4 adjacent angles (fewer sectors per warp load)
+template <typename TOut, bool kMix = false>
 __global__ void __launch_bounds__(32 * kSplitF) fwd_split64_kernel(GeomDev G,
                                                                   const double* __restrict__ P,
                                                                   const double* __restrict__ PT,
                                                                   TOut* __restrict__ sino,
                                                                   long long bs_sino) {
   __shared__ double part[kSplitF][33];
-  const int a = blockIdx.y;
   const int lane = threadIdx.x, seg = threadIdx.y;
-  const int j = blockIdx.x * 32 + lane;
+  const int a = kMix ? blockIdx.y * 4 + (lane >> 3) : blockIdx.y;
+  const int j = kMix ? blockIdx.x * 8 + (lane & 7) : blockIdx.x * 32 + lane;
+  const bool live = j < G.d && a < G.m;
   const int n = G.n;
   const int pitch = n + 2 * kPadMargin;
   {
@@ -974,7 +976,7 @@ __global__ void __launch_bounds__(32 * kSplitF) fwd_split64_kernel(GeomDev G,
     sino += (long long)blockIdx.z * bs_sino;
   }
   double acc = 0.0;
-  if (j < G.d) {
+  if (live) {
     const AngleParams& A = G.ang[a];
     const double u0 = A.u0 + ((double)j - (double)(G.d - 1) * 0.5) * A.du;
     const double slope = A.slope;
@@ -1019,7 +1021,7 @@ __global__ void __launch_bounds__(32 * kSplitF) fwd_split64_kernel(GeomDev G,
   }
   part[seg][lane] = acc;
   __syncthreads();
-  if (seg == 0 && j < G.d) {
+  if (seg == 0 && live) {
     double sum = part[0][lane];
 #pragma unroll
     for (int q = 1; q < kSplitF; ++q) sum += part[q][lane];
@@ -1509,8 +1511,8 @@ static cudaError_t fwd_impl(const GeomDev& G, const void* x, void* xT_ws, void* 
     fast::pad_transpose64_kernel<TIn><<<tg, tb, 0, st>>>(img, P, PT, G.n);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    dim3 sg((G.d + 31) / 32, G.m), sb(32, fast::kSplitF);
-    fast::fwd_split64_kernel<TOut><<<sg, sb, 0, st>>>(G, P, PT, (TOut*)y, 0);
+    dim3 sg((G.d + 7) / 8, (G.m + 3) / 4), sb(32, fast::kSplitF);
+    fast::fwd_split64_kernel<TOut, true><<<sg, sb, 0, st>>>(G, P, PT, (TOut*)y, 0);
     return cudaGetLastError();
   }
   cudaError_t e = launch_transpose<TIn>(img, imgT, G.n, st);
@@ -1605,8 +1607,8 @@ cudaError_t fast_forward_batch(const GeomDev& G, int precision, int tin, int tou
     fast::pad_transpose64_kernel<double><<<tg, tb, 0, st>>>((const double*)x, P, PT, G.n);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    dim3 sg((G.d + 31) / 32, G.m, batch), sb(32, fast::kSplitF);
-    fast::fwd_split64_kernel<double><<<sg, sb, 0, st>>>(G, P, PT, (double*)y, M);
+    dim3 sg((G.d + 7) / 8, (G.m + 3) / 4, batch), sb(32, fast::kSplitF);
+    fast::fwd_split64_kernel<double, true><<<sg, sb, 0, st>>>(G, P, PT, (double*)y, M);
     return cudaGetLastError();
   }
   for (int b = 0; b < batch; ++b) {
