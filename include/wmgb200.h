@@ -4,14 +4,11 @@
  * Library: paper_1310_0956_b200/lib/libwmgb200.so (sm_100a).  Every entry point
  * takes plain pointers and sizes; device buffers are CALLER-OWNED.  The only
  * internal allocations belong to a geometry handle: its per-angle and
- * mirror-pair tables (wmg_geometry_create) and, on small symmetric grids
- * (n <= 512), a scratch for the split float64 backprojector allocated on first
- * use outside stream capture (all freed by wmg_geometry_destroy).  All work is
- * asynchronous on the caller's CUDA stream (cudaStream_t passed as void*, NULL =
- * legacy default stream).  Functions are reentrant; a geometry may be shared
- * across threads and streams, except that fast float64 projections of one
- * small-grid geometry must not run concurrently (shared scratch) and the
- * setters (wmg_geometry_symmetry / wmg_geometry_kernel) must not race launches.
+ * mirror-pair tables (wmg_geometry_create, freed by wmg_geometry_destroy).  All
+ * work is asynchronous on the caller's CUDA stream (cudaStream_t passed as
+ * void*, NULL = legacy default stream).  Functions are reentrant; a geometry may
+ * be shared across threads and streams, except that the setters
+ * (wmg_geometry_symmetry / wmg_geometry_kernel) must not race launches.
  *
  * Return codes (mapped by the Python host layer the way the reference raises):
  *   WMG_OK        0

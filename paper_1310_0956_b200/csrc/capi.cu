@@ -19,14 +19,13 @@ cudaError_t parity_row_sums(const GeomDev&, double*, cudaStream_t);
 cudaError_t parity_csr(const GeomDev&, int, long long*, const long long*, long long*, double*,
                        int*, cudaStream_t);
 cudaError_t fast_forward(const GeomDev&, int, int, int, const void*, void*, void*, cudaStream_t,
-                         const GeomDev*, double*);
+                         const GeomDev*);
 cudaError_t fast_backward(const GeomDev&, int, int, int, const void*, void*, bool, cudaStream_t,
-                          const GeomDev*, double*);
-size_t fast_backward_scratch_bytes(const GeomDev&, int);
+                          const GeomDev*);
 cudaError_t fast_forward_batch(const GeomDev&, int, int, int, const void*, void*, size_t, void*,
-                               int, cudaStream_t, const GeomDev*, double*);
+                               int, cudaStream_t, const GeomDev*);
 cudaError_t fast_backward_batch(const GeomDev&, int, int, int, const void*, void*, bool, int,
-                                cudaStream_t, const GeomDev*, double*);
+                                cudaStream_t, const GeomDev*);
 size_t fast_forward_workspace_bytes(int, int, int);
 cudaError_t det_reduce(long long, int, const int*, const double* const*, const double* const*,
                        const double* const*, double*, double*, cudaStream_t);
@@ -75,26 +74,7 @@ struct wmg_geometry {
   wmg::AngleParams* d_axis;
   int* d_mir;      // mirror / primary / half / axis-row tables (symmetric sets)
   int sym_capable;
-  double* scratch; // small-grid fp64 backprojector partial images (lazy)
 };
-
-// Scratch of the split small-grid symmetric kernels (partial images / rays),
-// allocated on first use
-// outside stream capture (a capturing caller falls back to the unsplit kernel).
-// One geometry must not run two fast float64 projections concurrently.
-static double* bwd_scratch(wmg_geometry* g, int precision, cudaStream_t st) {
-  if (g->scratch) return g->scratch;
-  const size_t bytes = wmg::fast_backward_scratch_bytes(g->dev, precision);
-  if (!bytes) return nullptr;
-  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-  if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone)
-    return nullptr;
-  if (cudaMalloc(&g->scratch, bytes) != cudaSuccess) {
-    cudaGetLastError();
-    g->scratch = nullptr;
-  }
-  return g->scratch;
-}
 
 static thread_local char g_err[512] = "";
 
@@ -216,7 +196,6 @@ int wmg_geometry_create(int n, int n_detectors, int n_angles, const double* cos_
   g->d_ang = nullptr;
   g->d_axis = nullptr;
   g->d_mir = nullptr;
-  g->scratch = nullptr;
   const int n_axis = (int)axis_idx.size();
   cudaError_t e = cudaMalloc(&g->d_ang, sizeof(wmg::AngleParams) * (size_t)n_angles);
   if (e == cudaSuccess)
@@ -313,7 +292,6 @@ int wmg_geometry_destroy(wmg_geometry* g) {
   cudaError_t e = cudaFree(g->d_ang);
   if (g->d_axis) cudaFree(g->d_axis);
   if (g->d_mir) cudaFree(g->d_mir);
-  if (g->scratch) cudaFree(g->scratch);
   delete g;
   return cuda_rc(e);
 }
@@ -379,9 +357,7 @@ int wmg_forward(const wmg_geometry* g, int mode, int precision, int dtype_in, in
   if (g->dev.joseph) return fail(WMG_EINVAL, "the Joseph kernel has parity (float64) mode only");
   if (!workspace) return fail(WMG_EINVAL, "fast forward needs a workspace");
   return cuda_rc(wmg::fast_forward(g->dev, precision, dtype_in, dtype_out, x, workspace, y,
-                                   STREAM(stream), g->dev.sym ? &g->axis : nullptr,
-                                   bwd_scratch(const_cast<wmg_geometry*>(g), precision,
-                                               STREAM(stream))));
+                                   STREAM(stream), g->dev.sym ? &g->axis : nullptr));
 }
 
 int wmg_backward(const wmg_geometry* g, int mode, int precision, int dtype_in, int dtype_out,
@@ -396,9 +372,7 @@ int wmg_backward(const wmg_geometry* g, int mode, int precision, int dtype_in, i
   if (g->dev.joseph) return fail(WMG_EINVAL, "the Joseph kernel has parity (float64) mode only");
   return cuda_rc(wmg::fast_backward(g->dev, precision, dtype_in, dtype_out, y, x,
                                     accumulate != 0, STREAM(stream),
-                                    g->dev.sym ? &g->axis : nullptr,
-                                    bwd_scratch(const_cast<wmg_geometry*>(g), precision,
-                                                STREAM(stream))));
+                                    g->dev.sym ? &g->axis : nullptr));
 }
 
 int wmg_forward_batch(const wmg_geometry* g, int mode, int precision, int dtype_in,
@@ -423,9 +397,7 @@ int wmg_forward_batch(const wmg_geometry* g, int mode, int precision, int dtype_
   const size_t ws_item = wmg::fast_forward_workspace_bytes(g->dev.n, precision, dtype_in);
   return cuda_rc(wmg::fast_forward_batch(g->dev, precision, dtype_in, dtype_out, x, workspace,
                                          ws_item, y, batch, STREAM(stream),
-                                         g->dev.sym ? &g->axis : nullptr,
-                                         bwd_scratch(const_cast<wmg_geometry*>(g), precision,
-                                                     STREAM(stream))));
+                                         g->dev.sym ? &g->axis : nullptr));
 }
 
 int wmg_backward_batch(const wmg_geometry* g, int mode, int precision, int dtype_in,
@@ -448,9 +420,7 @@ int wmg_backward_batch(const wmg_geometry* g, int mode, int precision, int dtype
   if (g->dev.joseph) return fail(WMG_EINVAL, "the Joseph kernel has parity (float64) mode only");
   return cuda_rc(wmg::fast_backward_batch(g->dev, precision, dtype_in, dtype_out, y, x,
                                           accumulate != 0, batch, STREAM(stream),
-                                          g->dev.sym ? &g->axis : nullptr,
-                                          bwd_scratch(const_cast<wmg_geometry*>(g), precision,
-                                                      STREAM(stream))));
+                                          g->dev.sym ? &g->axis : nullptr));
 }
 
 int wmg_row_sums(const wmg_geometry* g, double* out, void* stream) {

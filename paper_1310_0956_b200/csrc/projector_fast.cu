@@ -23,6 +23,8 @@
 #include <algorithm>
 #include <type_traits>
 
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 
 namespace wmg {
@@ -30,6 +32,12 @@ namespace fast {
 
 template <typename T>
 __device__ __forceinline__ float to_f(T v) { return (float)v; }
+
+// float64 min / max as one DSETP + two selects (fmin / fmax on doubles are a
+// NaN-aware ~7-instruction sequence on sm_100a).  A NaN x yields the bound,
+// exactly as fmin(x, hi) / fmax(x, 0) do.
+__device__ __forceinline__ double dmin_to(double x, double hi) { return x < hi ? x : hi; }
+__device__ __forceinline__ double dmax_0(double x) { return x > 0.0 ? x : 0.0; }
 
 template <typename R>
 __device__ __forceinline__ R frac_of(long long U);
@@ -999,7 +1007,7 @@ __global__ void __launch_bounds__(32 * kSplitF) fwd_split64_kernel(GeomDev G,
       for (int r = rs; r <= re; ++r) {
         const double uh = fma((double)(r + 1), slope, u0);
         const double fk = floor(uh);
-        const double wh = fmin((uh - fk) * Ls, L);     // NaN (0 * inf) -> L
+        const double wh = dmin_to((uh - fk) * Ls, L);     // NaN (0 * inf) -> L
         const double* p = row + (int)fk;
         const double v1 = __ldg(p), v0 = __ldg(p - 1);
         acc = fma(L, v0, acc);
@@ -1010,7 +1018,7 @@ __global__ void __launch_bounds__(32 * kSplitF) fwd_split64_kernel(GeomDev G,
       for (int r = rs; r <= re; ++r) {
         const double uh = fma((double)(r + 1), slope, u0);
         const double fk = floor(uh);
-        const double wh = fmin((uh - fk) * Ls, L);
+        const double wh = dmin_to((uh - fk) * Ls, L);
         const double* p = row + (n - 1 - (int)fk);
         const double v1 = __ldg(p), v0 = __ldg(p + 1);
         acc = fma(L, v0, acc);
@@ -1084,7 +1092,7 @@ __global__ void __launch_bounds__(128) fwd_sym64_kernel(GeomDev G, const double*
         const double fk = floor(uh);
         int k = (int)fk;
         if constexpr (decltype(clampTag)::value) k = min(max(k, 2 - kPadMargin), n + kPadMargin - 3);
-        const double wh = fmin((uh - fk) * Ls, L);
+        const double wh = dmin_to((uh - fk) * Ls, L);
         const double wl = L - wh;
         const int km = n - 1 - k;
         const double* pa1 = base + (rowA + (unsigned)k);
@@ -1123,35 +1131,49 @@ __global__ void __launch_bounds__(128) fwd_sym64_kernel(GeomDev G, const double*
 // symmetric backprojector in float64: 52-fractional-bit fixed point
 constexpr double kQ52 = 4503599627370496.0;   // 2^52
 constexpr int kSym64Chunk = 8;
-constexpr int kSym64MaxSplit = 32;   // small-grid angle splits (scratch: 32 n^2 doubles)
+constexpr int kSym64MaxCluster = 16;   // small-grid angle splits = cluster size (non-portable)
 
-template <typename TIn, typename TOut, bool kAccumulate>
-// nsplit > 1 (small grids): blockIdx.z takes a slice of the primary angles and
-// the block writes its four partial images to part[z] (full-image layout);
-// sym_reduce_kernel sums the slices in z order (deterministic).
-__global__ void __launch_bounds__(256) bwd_sym64_kernel(GeomDev G, const TIn* __restrict__ sino,
+// kCluster (small grids): the nsplit CTAs of one tile form a thread-block
+// cluster along z, each taking a slice of the primary angles.  After the angle
+// loop every CTA parks its four partial tiles in shared memory; CTA r then sums
+// its 1/nsplit share of the tile over the peers in rank order through DSMEM,
+// adds the axis-aligned angles of Gx and stores -- deterministic, no global
+// scratch, no second launch.  blockIdx.z = batch item * nsplit + rank.
+template <typename TIn, typename TOut, bool kAccumulate, bool kCluster = false>
+__global__ void __launch_bounds__(256, kCluster ? 3 : 4) bwd_sym64_kernel(GeomDev G, const TIn* __restrict__ sino,
                                                         TOut* __restrict__ img, int nsplit,
-                                                        double* __restrict__ part) {
-  __shared__ double4 winA[kSym64Chunk][kBwdWin];
-  __shared__ double4 winB[kSym64Chunk][kBwdWin];
+                                                        GeomDev Gx) {
+  // winA = win[0] (y_a[t], y_b[t], y_a[t+1], y_b[t+1]), winB = win[1] reversed
+  // detectors; in cluster mode the same 32 KB hold the partial tile at the end
+  __shared__ double4 win[2][kSym64Chunk][kBwdWin];
+  double4 (*winA)[kBwdWin] = win[0];
+  double4 (*winB)[kBwdWin] = win[1];
   __shared__ long long qx[kSym64Chunk][kBwdTile];
   __shared__ long long qhead[kSym64Chunk];
+  // per-angle constants, computed once per chunk: (S as bits, ic), (L, ca0), (hwic, w1c)
+  __shared__ double2 angc[kSym64Chunk][3];
   __shared__ int jlo_s[kSym64Chunk];
   __shared__ int ang_s[kSym64Chunk];
   __shared__ int mir_s[kSym64Chunk];
-  const int n = G.n, m = G.m, d = G.d;
+  const int n = G.n, d = G.d;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int col0 = blockIdx.x * kBwdTile, row0 = blockIdx.y * kBwdTile;
   const double half = (double)n * 0.5, dc = (double)(d - 1) * 0.5;
   const double xc0 = (double)col0 - half + 0.5;
   const double yc0 = half - (double)row0 - 0.5;
+  const int rank = kCluster ? (int)(blockIdx.z % nsplit) : 0;
+  if (kCluster) {
+    const long long item = blockIdx.z / nsplit;
+    sino += item * G.m * d;
+    img += item * n * n;
+  }
   double acc[4][4];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int q = 0; q < 4; ++q) acc[i][q] = 0.0;
-  const int q_begin = (int)((long long)G.n_prim * blockIdx.z / nsplit);
-  const int q_end = (int)((long long)G.n_prim * (blockIdx.z + 1) / nsplit);
+  const int q_begin = (int)((long long)G.n_prim * rank / nsplit);
+  const int q_end = (int)((long long)G.n_prim * (rank + 1) / nsplit);
   for (int c0 = q_begin; c0 < q_end; c0 += kSym64Chunk) {
     const int na = min(kSym64Chunk, q_end - c0);
     __syncthreads();
@@ -1167,6 +1189,10 @@ __global__ void __launch_bounds__(256) bwd_sym64_kernel(GeomDev G, const TIn* __
       const int jlo = (int)floor(pmin) - 1;
       jlo_s[tid] = jlo;
       qhead[tid] = llrint((p0 - (double)jlo) * kQ52);
+      const double hw = A.hw, ic = A.inv_cs;
+      angc[tid][0] = make_double2(__longlong_as_double(llrint(A.s * kQ52)), ic);
+      angc[tid][1] = make_double2(A.L, 2.0 - hw);
+      angc[tid][2] = make_double2(hw * ic, (2.0 * hw - 3.0) * ic);
     }
     __syncthreads();
     for (int e = tid; e < na * kBwdTile; e += 256) {
@@ -1188,10 +1214,9 @@ __global__ void __launch_bounds__(256) bwd_sym64_kernel(GeomDev G, const TIn* __
     }
     __syncthreads();
     for (int aa = 0; aa < na; ++aa) {
-      const AngleParams& A = G.ang[ang_s[aa]];
-      const long long S = llrint(A.s * kQ52);
-      const double hw = A.hw, ic = A.inv_cs, L = A.L;
-      const double ca0 = 2.0 - hw, hwic = hw * ic, w1c = (2.0 * hw - 3.0) * ic;
+      const double2 c0 = angc[aa][0], c1 = angc[aa][1], c2 = angc[aa][2];
+      const long long S = __double_as_longlong(c0.x);
+      const double ic = c0.y, L = c1.x, ca0 = c1.y, hwic = c2.x, w1c = c2.y;
       long long Q = qx[aa][lane] - (long long)(4 * warp) * S;
       const double4* wa = winA[aa];
       const double4* wb = winB[aa];
@@ -1200,8 +1225,8 @@ __global__ void __launch_bounds__(256) bwd_sym64_kernel(GeomDev G, const TIn* __
         const int hi = (int)(Q >> 52);
         const double f = __longlong_as_double(0x3FF0000000000000LL | (Q & 0xFFFFFFFFFFFFFLL));
         const double d0 = ca0 - f;
-        const double w0 = fmin(fma(-fabs(d0), ic, hwic), L);
-        const double w1 = fmax(fma(f, ic, w1c), 0.0);
+        const double w0 = dmin_to(fma(-fabs(d0), ic, hwic), L);
+        const double w1 = dmax_0(fma(f, ic, w1c));
         const double4 va = wa[hi + 1];
         const double4 vb = wb[hi + 1];
         acc[i][0] = fma(w0, va.x, fma(w1, va.z, acc[i][0]));
@@ -1212,52 +1237,63 @@ __global__ void __launch_bounds__(256) bwd_sym64_kernel(GeomDev G, const TIn* __
       }
     }
   }
-  const int col = col0 + lane;
+  auto pixel = [&](int i, int q, int w, int l) -> long long {
+    const int row = row0 + 4 * w + i, col = col0 + l;
+    const int r = (q < 2) ? row : n - 1 - row;
+    const int c = (q == 0 || q == 3) ? col : n - 1 - col;
+    return (long long)r * n + c;
+  };
+  if constexpr (!kCluster) {
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int row = row0 + 4 * warp + i;
-    const long long p[4] = {(long long)row * n + col, (long long)row * n + (n - 1 - col),
-                            (long long)(n - 1 - row) * n + (n - 1 - col),
-                            (long long)(n - 1 - row) * n + col};
+    for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      if (part)
-        part[(long long)blockIdx.z * n * n + p[q]] = acc[i][q];
-      else if (kAccumulate)
-        img[p[q]] = (TOut)((double)img[p[q]] + acc[i][q]);
+      for (int q = 0; q < 4; ++q) {
+        const long long p = pixel(i, q, warp, lane);
+        if (kAccumulate)
+          img[p] = (TOut)((double)img[p] + acc[i][q]);
+        else
+          img[p] = (TOut)acc[i][q];
+      }
+  } else {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cl = cg::this_cluster();
+    double* part = reinterpret_cast<double*>(&win[0][0][0]);   // [16][256]
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) part[(i * 4 + q) * 256 + tid] = acc[i][q];
+    cl.sync();
+    const int k0 = 16 * rank / nsplit, k1 = 16 * (rank + 1) / nsplit;
+    const double dcx = (double)(Gx.d - 1) * 0.5;
+    for (int k = k0; k < k1; ++k) {
+      double s = 0.0;   // rank order; loads issued four at a time
+      for (int z0 = 0; z0 < nsplit; z0 += 4) {
+        double v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          v[u] = (z0 + u < nsplit) ? cl.map_shared_rank(part, z0 + u)[k * 256 + tid] : 0.0;
+        s = (z0 == 0) ? v[0] : s + v[0];
+#pragma unroll
+        for (int u = 1; u < 4; ++u)
+          if (z0 + u < nsplit) s += v[u];
+      }
+      const long long p = pixel(k >> 2, k & 3, warp, lane);
+      const int prow = (int)(p / n), pix = (int)(p % n);
+      const double xc = (double)pix - half + 0.5, yc = half - (double)prow - 0.5;
+      for (int a = 0; a < Gx.m; ++a) {   // axis-aligned angles (Gx: the tie rule)
+        const AngleParams& P = Gx.ang[a];
+        const int j = (int)ceil(xc * P.c + yc * P.s + dcx - 0.5);
+        if (j >= 0 && j < Gx.d)
+          s += (double)__ldg(sino + (long long)(Gx.rowmap ? Gx.rowmap[a] : a) * Gx.d + j);
+      }
+      if (kAccumulate)
+        img[p] = (TOut)((double)img[p] + s);
       else
-        img[p[q]] = (TOut)acc[i][q];
+        img[p] = (TOut)s;
     }
+    cl.sync();   // peers' shared memory must outlive the remote reads
   }
-}
-
-// Sums the angle slices and adds the axis-aligned angles of the set (Gx: the
-// reference's tie rule for rays on grid lines; at most two angles) in the
-// same pass -- one launch instead of reduce + axis backprojection.
-template <typename TIn, typename TOut, bool kAccumulate>
-__global__ void sym_reduce_kernel(const double* __restrict__ part, int nsplit, long long N,
-                                  TOut* __restrict__ img, GeomDev Gx,
-                                  const TIn* __restrict__ sino) {
-  const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= N) return;
-  double s = part[p];
-  for (int z = 1; z < nsplit; ++z) s += part[(long long)z * N + p];
-  const int n = Gx.n;
-  const int row = (int)(p / n), ix = (int)(p % n);
-  const double xc = (double)ix - (double)n * 0.5 + 0.5;
-  const double yc = (double)n * 0.5 - (double)row - 0.5;
-  const double dc = (double)(Gx.d - 1) * 0.5;
-  for (int a = 0; a < Gx.m; ++a) {
-    const AngleParams& P = Gx.ang[a];
-    const double pj = xc * P.c + yc * P.s + dc;
-    const int j = (int)ceil(pj - 0.5);
-    if (j >= 0 && j < Gx.d)
-      s += (double)__ldg(sino + (long long)(Gx.rowmap ? Gx.rowmap[a] : a) * Gx.d + j);
-  }
-  if (kAccumulate)
-    img[p] = (TOut)((double)img[p] + s);
-  else
-    img[p] = (TOut)s;
 }
 
 }  // namespace fast
@@ -1462,36 +1498,59 @@ static cudaError_t fwd64_impl(const GeomDev& G, const void* x, void* ws, void* y
   return cudaGetLastError();
 }
 
+// cluster launch of the small-grid symmetric backprojector (nsplit CTAs per
+// tile along z; > 8 needs the non-portable cluster-size attribute)
+template <typename TIn, typename TOut, bool kAcc>
+static cudaError_t bwd_sym64_cluster(const GeomDev& G, const GeomDev& Gx, const void* y, void* x,
+                                     int nsplit, int batch, cudaStream_t st) {
+  auto kern = fast::bwd_sym64_kernel<TIn, TOut, kAcc, true>;
+  static bool attr = false;   // per instantiation
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(G.n / 64, G.n / 64, nsplit * batch);
+  cfg.blockDim = dim3(256);
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 1;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = nsplit;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, G, (const TIn*)y, (TOut*)x, nsplit, Gx);
+}
+
+// angle splits for the small-grid path: ~192 CTAs (1.3 per SM; the sweep at
+// 256^2 / 180 angles: 4 -> 44 us, 8 -> 37, 12 -> 29, 16 -> 31), at most one
+// cluster of kSym64MaxCluster, at least 4 primary angles per CTA.  Independent
+// of the batch: every item is summed exactly like a single call.
+static inline int sym64_nsplit(const GeomDev& G) {
+  const int tiles = (G.n / 64) * (G.n / 64);
+  return max(1, min(fast::kSym64MaxCluster, min((192 + tiles - 1) / tiles, G.n_prim / 4)));
+}
+
 template <typename TIn, typename TOut>
 static cudaError_t bwd64_impl(const GeomDev& G, const void* y, void* x, bool accumulate,
-                              cudaStream_t st, const GeomDev* Gx, double* scratch = nullptr) {
+                              cudaStream_t st, const GeomDev* Gx, bool small = false,
+                              int batch = 1) {
   if (!(G.sym && Gx)) return cudaErrorNotSupported;
-  const int tiles = (G.n / 64) * (G.n / 64);
-  // small grids: split the angles over blockIdx.z so the grid fills the SMs
-  int nsplit = 1;
-  if (scratch) nsplit = max(1, min(fast::kSym64MaxSplit, min((2 * 148 + tiles - 1) / tiles,
-                                                       G.n_prim / 4)));
-  dim3 grid(G.n / 64, G.n / 64, nsplit);
-  double* part = nsplit > 1 ? scratch : nullptr;
-  if (accumulate)
-    fast::bwd_sym64_kernel<TIn, TOut, true><<<grid, 256, 0, st>>>(G, (const TIn*)y, (TOut*)x,
-                                                                  nsplit, part);
-  else
-    fast::bwd_sym64_kernel<TIn, TOut, false><<<grid, 256, 0, st>>>(G, (const TIn*)y, (TOut*)x,
-                                                                   nsplit, part);
-  cudaError_t e = cudaGetLastError();
-  if (e == cudaSuccess && part) {
-    // slice sum + the axis angles in one pass
-    const long long N = (long long)G.n * G.n;
-    const unsigned rb = (unsigned)((N + 255) / 256);
-    if (accumulate)
-      fast::sym_reduce_kernel<TIn, TOut, true><<<rb, 256, 0, st>>>(part, nsplit, N, (TOut*)x,
-                                                                   *Gx, (const TIn*)y);
-    else
-      fast::sym_reduce_kernel<TIn, TOut, false><<<rb, 256, 0, st>>>(part, nsplit, N, (TOut*)x,
-                                                                    *Gx, (const TIn*)y);
-    return cudaGetLastError();
+  if (small) {   // small grids: angle splits over a cluster, reduced through DSMEM
+    const int nsplit = sym64_nsplit(G);
+    return accumulate ? bwd_sym64_cluster<TIn, TOut, true>(G, *Gx, y, x, nsplit, batch, st)
+                      : bwd_sym64_cluster<TIn, TOut, false>(G, *Gx, y, x, nsplit, batch, st);
   }
+  dim3 grid(G.n / 64, G.n / 64, 1);
+  if (accumulate)
+    fast::bwd_sym64_kernel<TIn, TOut, true><<<grid, 256, 0, st>>>(G, (const TIn*)y, (TOut*)x, 1,
+                                                                  *Gx);
+  else
+    fast::bwd_sym64_kernel<TIn, TOut, false><<<grid, 256, 0, st>>>(G, (const TIn*)y, (TOut*)x, 1,
+                                                                   *Gx);
+  cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess || Gx->m == 0) return e;
   dim3 g2((G.n + 31) / 32, (G.n + 7) / 8);
   fast::bwd_kernel<TIn, TOut, double, true><<<g2, 256, 0, st>>>(*Gx, (const TIn*)y, (TOut*)x);
@@ -1541,8 +1600,7 @@ static cudaError_t bwd_impl(const GeomDev& G, const void* y, void* x, bool accum
 
 // precision: 0 = fp32 arithmetic, 1 = fp64 arithmetic
 cudaError_t fast_forward(const GeomDev& G, int precision, int tin, int tout, const void* x,
-                         void* xT_ws, void* y, cudaStream_t st, const GeomDev* Gx,
-                         double* scratch) {
+                         void* xT_ws, void* y, cudaStream_t st, const GeomDev* Gx) {
   if (G.m == 0 || G.d == 0) return cudaSuccess;
   if (precision == 0) {
     if (tin == 0 && tout == 0) return fwd_v2_impl<float, float>(G, x, xT_ws, y, st, Gx);
@@ -1558,14 +1616,13 @@ cudaError_t fast_forward(const GeomDev& G, int precision, int tin, int tout, con
   return cudaErrorInvalidValue;
 }
 
-size_t fast_backward_scratch_bytes(const GeomDev& G, int precision) {
-  if (precision != 1 || !G.sym || !use_split(G) || G.n % 64) return 0;
-  return sizeof(double) * (size_t)fast::kSym64MaxSplit * (size_t)G.n * (size_t)G.n;
+// small symmetric float64 grids: the cluster-reduced angle-split backprojector
+static inline bool use_small_sym64(const GeomDev& G) {
+  return G.sym == 1 && use_split(G) && G.n % 64 == 0 && G.n >= 64;
 }
 
 cudaError_t fast_backward(const GeomDev& G, int precision, int tin, int tout, const void* y,
-                          void* x, bool accumulate, cudaStream_t st, const GeomDev* Gx,
-                          double* scratch) {
+                          void* x, bool accumulate, cudaStream_t st, const GeomDev* Gx) {
   if (G.n == 0) return cudaSuccess;
   if (precision == 0) {
     if (tin == 0 && tout == 0) return bwd_v2_impl<float, float>(G, y, x, accumulate, st, Gx);
@@ -1576,8 +1633,8 @@ cudaError_t fast_backward(const GeomDev& G, int precision, int tin, int tout, co
     if (use_sym_bwd(G) && Gx && tin == 1 && tout == 1)
       return bwd64_impl<double, double>(G, y, x, accumulate, st, Gx);
     // small symmetric grids: angle-split symmetric kernel (4 images per weight)
-    if (G.sym == 1 && use_split(G) && Gx && scratch && tin == 1 && tout == 1)
-      return bwd64_impl<double, double>(G, y, x, accumulate, st, Gx, scratch);
+    if (use_small_sym64(G) && Gx && tin == 1 && tout == 1)
+      return bwd64_impl<double, double>(G, y, x, accumulate, st, Gx, true);
     if (tin == 1 && tout == 1) return bwd_impl<double, double, double>(G, y, x, accumulate, st);
     if (tin == 0 && tout == 0) return bwd_impl<float, float, double>(G, y, x, accumulate, st);
   }
@@ -1593,7 +1650,7 @@ cudaError_t fast_backward(const GeomDev& G, int precision, int tin, int tout, co
 // ---------------------------------------------------------------------------
 cudaError_t fast_forward_batch(const GeomDev& G, int precision, int tin, int tout, const void* x,
                                void* ws, size_t ws_item, void* y, int batch, cudaStream_t st,
-                               const GeomDev* Gx, double* scratch) {
+                               const GeomDev* Gx) {
   if (batch < 1) return cudaSuccess;
   const long long N = (long long)G.n * G.n, M = (long long)G.m * G.d;
   const size_t si = tin == 1 ? 8 : 4, so = tout == 1 ? 8 : 4;
@@ -1613,8 +1670,7 @@ cudaError_t fast_forward_batch(const GeomDev& G, int precision, int tin, int tou
   }
   for (int b = 0; b < batch; ++b) {
     cudaError_t e = fast_forward(G, precision, tin, tout, (const char*)x + b * N * si,
-                                 (char*)ws + b * ws_item, (char*)y + b * M * so, st, Gx,
-                                 scratch);
+                                 (char*)ws + b * ws_item, (char*)y + b * M * so, st, Gx);
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;
@@ -1622,12 +1678,15 @@ cudaError_t fast_forward_batch(const GeomDev& G, int precision, int tin, int tou
 
 cudaError_t fast_backward_batch(const GeomDev& G, int precision, int tin, int tout, const void* y,
                                 void* x, bool accumulate, int batch, cudaStream_t st,
-                                const GeomDev* Gx, double* scratch) {
+                                const GeomDev* Gx) {
   if (batch < 1 || G.n == 0) return cudaSuccess;
   const long long N = (long long)G.n * G.n, M = (long long)G.m * G.d;
   const size_t si = tin == 1 ? 8 : 4, so = tout == 1 ? 8 : 4;
-  const bool sym = (use_sym_bwd(G) || (precision == 1 && G.sym == 1 && scratch && tin == 1 &&
-                                       tout == 1)) && Gx;
+  const bool small64 = precision == 1 && tin == 1 && tout == 1 && use_small_sym64(G) && Gx &&
+                       !use_sym_bwd(G);
+  if (small64)   // one cluster launch for the whole batch
+    return bwd64_impl<double, double>(G, y, x, accumulate, st, Gx, true, batch);
+  const bool sym = use_sym_bwd(G) && Gx;
   if (use_split(G) && !sym && tin == tout) {
     if (precision == 1 && tin == 1)
       return bwd_split_launch<double, double, double>(G, y, x, accumulate, st, batch);
@@ -1638,7 +1697,7 @@ cudaError_t fast_backward_batch(const GeomDev& G, int precision, int tin, int to
   }
   for (int b = 0; b < batch; ++b) {
     cudaError_t e = fast_backward(G, precision, tin, tout, (const char*)y + b * M * si,
-                                  (char*)x + b * N * so, accumulate, st, Gx, scratch);
+                                  (char*)x + b * N * so, accumulate, st, Gx);
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;
