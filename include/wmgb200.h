@@ -34,6 +34,7 @@
  *   multilevel.py:36-79 haar_* / build_intergrid_set-> wmg_haar_restrict / wmg_haar_prolong
  *   multilevel.py:123-130 leaf Gram assembly        -> wmg_leaf_gram (sparse) or
  *                                                      wmg_leaf_factor (+ DGEMM)
+ *   sparse_kernels.py:53-65 potrf of the leaf Grams  -> wmg_spd_inverse (batched fp64 DMMA sweep)
  *   sparse_kernels.py:68-75 cho_solve in the V-cycle -> wmg_batched_gemv (stored inverse)
  *   multilevel.py:109-113 node systems, siblings     -> wmg_forward_batch / wmg_backward_batch
  *   geometry.py:131-175 _joseph_entries             -> wmg_geometry_kernel (JOSEPH)
@@ -207,6 +208,20 @@ int wmg_leaf_factor(const wmg_geometry *g, int depth, const int *bands, long lon
  * Replaces the reference's P^T P of multilevel.py:125-130. */
 int wmg_leaf_gram(const wmg_geometry *g, int depth, const int *bands, double *gram,
                   int *overflow, void *stream);
+
+/* bytes of caller workspace wmg_spd_inverse needs for `batch` matrices of order p */
+int wmg_spd_inverse_workspace(int batch, int p, size_t *bytes);
+
+/* In-place inverse of `batch` SPD matrices G_b (p x p row-major float64 at
+ * G + b * strideG; only the lower triangle is read; p % 128 == 0 -- pad with an
+ * identity block otherwise): on return G_b holds the full symmetric G_b^-1.
+ * Blocked symmetric sweep on the fp64 tensor cores (DMMA), p^3 flops per
+ * matrix.  info (device int[batch], written) = 0, or the order of the first
+ * leading minor that is not positive definite (potrf's convention; G_b is then
+ * garbage).  Replaces the reference's per-leaf potrf (sparse_kernels.py:53-65,
+ * called at multilevel.py:125-137) plus the inverse the V-cycle's GEMV needs. */
+int wmg_spd_inverse(int batch, int p, double *G, long long strideG, int *info, void *work,
+                    void *stream);
 
 #ifdef __cplusplus
 }

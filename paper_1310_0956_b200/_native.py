@@ -73,6 +73,8 @@ _SIGS = {
     "wmg_haar_prolong": (_i, [_i, _dp, _i, _dp, _i, _vp]),
     "wmg_leaf_factor": (_i, [_vp, _i, ctypes.POINTER(_i), _ll, _ll, _dp, _vp]),
     "wmg_leaf_gram": (_i, [_vp, _i, ctypes.POINTER(_i), _dp, _dp, _vp]),
+    "wmg_spd_inverse_workspace": (_i, [_i, _i, ctypes.POINTER(ctypes.c_size_t)]),
+    "wmg_spd_inverse": (_i, [_i, _i, _dp, _ll, _dp, _dp, _vp]),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -63,6 +63,8 @@ cudaError_t haar_prolong(int, const double*, int, double*, int, cudaStream_t);
 cudaError_t leaf_factor(const GeomDev&, int, const int*, long long, long long, double*,
                         cudaStream_t);
 cudaError_t leaf_gram(const GeomDev&, int, const int*, double*, int*, cudaStream_t);
+size_t spd_inverse_workspace(int, int);
+cudaError_t spd_inverse(int, int, double*, long long, int*, double*, cudaStream_t);
 bool tma_window_fits(const AngleParams*, int, int, int);
 }  // namespace wmg
 
@@ -597,6 +599,24 @@ int wmg_leaf_gram(const wmg_geometry* g, int depth, const int* bands, double* gr
   if (g->dev.joseph) return fail(WMG_EINVAL, "the sparse leaf Gram implements line weights only");
   if (g->dev.m == 0 || g->dev.d == 0) return WMG_OK;
   return cuda_rc(wmg::leaf_gram(g->dev, depth, bands, gram, overflow, STREAM(stream)));
+}
+
+int wmg_spd_inverse_workspace(int batch, int p, size_t* bytes) {
+  REQ(bytes);
+  if (batch < 0 || p < 0) return fail(WMG_EINVAL, "negative size");
+  *bytes = wmg::spd_inverse_workspace(batch, p);
+  return WMG_OK;
+}
+
+int wmg_spd_inverse(int batch, int p, double* G, long long strideG, int* info, void* work,
+                    void* stream) {
+  REQ(G && info && work);
+  if (batch < 0 || p < 0) return fail(WMG_EINVAL, "negative size");
+  if (p % 128) return fail(WMG_EINVAL, "p must be a multiple of 128 (pad with identity)");
+  if (batch > 1 && strideG < (long long)p * p) return fail(WMG_EDIM, "batch stride < p*p");
+  if (batch > 65535) return fail(WMG_EINVAL, "batch > 65535");
+  return cuda_rc(wmg::spd_inverse(batch, p, G, strideG, info, static_cast<double*>(work),
+                                  STREAM(stream)));
 }
 
 }  // extern "C"

@@ -35,7 +35,7 @@ import scipy.sparse as sp
 from . import _device as D
 from . import _native as N
 from .sparse_kernels import (DenseFactorization, DimensionMismatchError,
-                             NotPositiveDefiniteError)
+                             NotPositiveDefiniteError, spd_inverse_)
 
 BAND_IDS = ("LL", "LH", "HL", "HH")
 BAND_CODE = {"LL": 0, "LH": 1, "HL": 2, "HH": 3}
@@ -214,13 +214,16 @@ def _leaf_paths(levels):
     return paths
 
 
-def _assemble_leaf_grams(w, n, lam, levels, ray_chunk=None, paths=None, method="sparse"):
+def _assemble_leaf_grams(w, n, lam, levels, ray_chunk=None, paths=None, method="sparse",
+                         full=True):
     """Gram P_L^T P_L + lam I for every leaf (or the given band paths of depth
     levels-1), batched in HBM.
 
     method "sparse": ``wmg_leaf_gram`` accumulates the lower triangle per ray
     bundle without forming P_L (fp64 slab weights, <= 1e-12 of the exact
-    ones); "dense": exact P_L slabs from the parity walker + DGEMM."""
+    ones); "dense": exact P_L slabs from the parity walker + DGEMM.
+    ``full=False`` leaves the sparse Grams lower-triangular (upper zero): all
+    the factorisations read only the lower triangle."""
     t = D.torch()
     depth = levels - 1
     side_c = n >> depth
@@ -235,10 +238,11 @@ def _assemble_leaf_grams(w, n, lam, levels, ray_chunk=None, paths=None, method="
             g = grams[li]
             N.call("wmg_leaf_gram", w.handle, depth, bands, D.ptr(g), D.ptr(overflow),
                    D.stream_handle())
-            low = g.tril()
-            g.copy_(low)
-            g.add_(low.tril(-1).T)
-            del low
+            if full:
+                low = g.tril()
+                g.copy_(low)
+                g.add_(low.tril(-1).T)
+                del low
             if lam != 0:
                 g.diagonal().add_(lam)
         if int(overflow.item()):
@@ -306,35 +310,28 @@ def build_wmg_hierarchy(w, n: int, lam: float, levels: int, nu_pre: int = 0,
         # angle-sharded W: every rank accumulates its angles' share of each leaf
         # Gram (the Gram is a sum over rays), one NCCL allreduce sums them, and
         # every rank factors all leaves (the V-cycle's coarse solves are local)
-        paths, grams = _assemble_leaf_grams(base, n, 0.0, levels, method=gram)
+        paths, grams = _assemble_leaf_grams(base, n, 0.0, levels, method=gram, full=False)
         w.dist.all_reduce(grams, group=w.group)
         if lam != 0:
             grams.diagonal(dim1=1, dim2=2).add_(lam)
     else:
-        paths, grams = _assemble_leaf_grams(w, n, lam, levels, method=gram)
+        paths, grams = _assemble_leaf_grams(w, n, lam, levels, method=gram, full=False)
     n_leaf, p = grams.shape[0], grams.shape[-1]
-    # keep the Cholesky factors (API: coarse_solve.lower) only when they are
-    # small; the V-cycle itself only needs the inverses
-    keep_lower = grams.numel() * 8 <= (8 << 30)
-    lower_all = t.empty_like(grams) if keep_lower else None
+    # keep a copy of the Grams (API: coarse_solve.lower, a Cholesky factor
+    # computed on first access) only when they are small; the V-cycle itself
+    # only needs the inverses
+    keep_gram = grams.numel() * 8 <= (8 << 30)
+    gram_copy = grams.clone() if keep_gram else None
+    names = ["/".join(q) or "root" for q in paths]
     batch = max(1, min(n_leaf, (4 << 30) // max(1, p * p * 8)))
     for b0 in range(0, n_leaf, batch):
-        g = grams[b0:b0 + batch]
-        low, info = t.linalg.cholesky_ex(g)
-        bad = info.cpu().numpy()
-        for li, code in enumerate(bad):
-            if code > 0:
-                name = "/".join(paths[b0 + li]) or "root"
-                raise NotPositiveDefiniteError(
-                    f"coarsest subproblem '{name}' is singular (lambda={lam}): "
-                    f"leading minor of order {int(code)} is not positive definite")
-        if keep_lower:
-            lower_all[b0:b0 + batch].copy_(low)
-        inv = t.cholesky_inverse(low)
-        # symmetrise into the (now consumed) Gram storage, row-major for the GEMV
-        g.copy_(inv)
-        g.add_(inv.transpose(1, 2)).mul_(0.5)
-        del low, inv
+        try:
+            # hand-written batched SPD inverse on the fp64 tensor cores (in place)
+            spd_inverse_(grams[b0:b0 + batch], names=names[b0:b0 + batch])
+        except NotPositiveDefiniteError as exc:
+            name, _, why = str(exc).partition(": ")
+            raise NotPositiveDefiniteError(
+                f"coarsest subproblem '{name}' is singular (lambda={lam}): {why}") from None
     inverses = grams
     leaf_index = {path: i for i, path in enumerate(paths)}
     if node_mode not in ("fast", "fast32", "parity"):
@@ -361,8 +358,8 @@ def build_wmg_hierarchy(w, n: int, lam: float, levels: int, nu_pre: int = 0,
             li = leaf_index[bands]
             return WmgNode(side=side, level=level, path=path, factor=None, lam=lam,
                            coarse_solve=DenseFactorization(
-                               dimension=p, lower=None if lower_all is None else lower_all[li],
-                               inverse=inverses[li]),
+                               dimension=p, inverse=inverses[li],
+                               gram=None if gram_copy is None else gram_copy[li]),
                            bands=bands)
         node = WmgNode(side=side, level=level, path=path, factor=w, lam=lam,
                        intergrid=None, bands=bands)
@@ -372,7 +369,7 @@ def build_wmg_hierarchy(w, n: int, lam: float, levels: int, nu_pre: int = 0,
 
     root = make((), 1)
     h = WmgHierarchy(levels=levels, lam=lam, root=root, projector=w, n=n, nu_pre=nu_pre,
-                     nu_post=nu_post, leaf_factors=lower_all, leaf_inverses=inverses,
+                     nu_post=nu_post, leaf_factors=None, leaf_inverses=inverses,
                      node_projector=node_w)
     for nd in h.nodes():
         nd.hierarchy = h
@@ -772,16 +769,15 @@ class ClassicalTGPreconditioner(_GraphedOperator):
         sc = sirt_scaling(w)
         self.c, self.r = sc.c_dev, sc.r_dev
         _, grams = _assemble_leaf_grams(
-            w, n, lam, 2, paths=[("LL",)],
+            w, n, lam, 2, paths=[("LL",)], full=False,
             method="dense" if getattr(w, "kernel", "line") == "joseph" else "sparse")
-        low, info = t.linalg.cholesky_ex(grams)
-        if int(info.max()) > 0:
+        gram = grams[0].clone() if grams[0].numel() * 8 <= (2 << 30) else None
+        try:
+            spd_inverse_(grams)
+        except NotPositiveDefiniteError:
             raise NotPositiveDefiniteError(
-                f"coarse LL Galerkin operator is singular (lambda={lam})")
-        inv = t.cholesky_inverse(low)
-        self.coarse = DenseFactorization(dimension=grams.shape[-1], lower=low[0],
-                                         inverse=(0.5 * (inv + inv.transpose(1, 2)))[0]
-                                         .contiguous())
+                f"coarse LL Galerkin operator is singular (lambda={lam})") from None
+        self.coarse = DenseFactorization(dimension=grams.shape[-1], inverse=grams[0], gram=gram)
         M, N_ = w.shape
         dev = w.device
         self._sino = t.empty(M, dtype=t.float64, device=dev)

@@ -4,13 +4,13 @@ Mirrors /root/reference/pkg/src/wmgtomo/sparse_kernels.py:
   * ``DimensionMismatchError`` / ``NotPositiveDefiniteError`` (:22-27),
   * ``DenseFactorization`` / ``cholesky_factor`` / ``cholesky_solve`` (:42-75),
     here holding a float64 lower factor in HBM (cuSOLVER potrf through torch)
-    and solving with two triangular solves on the device.
+    and solving with two triangular solves on the device,
+  * ``spd_inverse_``: the WMG leaves' batched SPD inverse on the fp64 tensor
+    cores (hand-written DMMA sweep, ``wmg_spd_inverse``).
 ``spgemm`` / ``seeded_uniform`` are not on the B200 path (the hierarchy is
 matrix-free, inputs are generated host-side) -- SURVEY.md s2 row 4.
 """
 from __future__ import annotations
-
-from dataclasses import dataclass
 
 SPGEMM_DROP_TOL = 1e-15
 
@@ -23,19 +23,39 @@ class NotPositiveDefiniteError(ValueError):
     """A matrix expected to be symmetric positive definite is not."""
 
 
-@dataclass(frozen=True)
 class DenseFactorization:
     """Lower Cholesky factor(s) of SPD matrices resident on the GPU.
 
-    ``lower`` is a torch float64 tensor of shape (dim, dim) or (batch, dim, dim).
-    ``inverse`` (optional) holds G^-1 = L^-T L^-1 for the WMG coarse solves: one
-    bandwidth-bound GEMV per solve instead of two latency-bound triangular
-    solves (same kappa * eps forward-error class).
+    ``lower`` is a torch float64 tensor of shape (dim, dim) or (batch, dim, dim)
+    (reference field, sparse_kernels.py:40-45).  ``inverse`` (optional) holds
+    G^-1 for the WMG coarse solves: one bandwidth-bound GEMV per solve instead
+    of two latency-bound triangular solves (same kappa * eps forward-error
+    class).  When the inverse came from ``spd_inverse_`` (no Cholesky at setup)
+    the factor is computed on first access from the kept ``gram`` copy.
+    Immutable like the reference's frozen dataclass.
     """
 
-    dimension: int
-    lower: object
-    inverse: object = None
+    __slots__ = ("dimension", "_lower", "inverse", "_gram")
+
+    def __init__(self, dimension: int, lower=None, inverse=None, gram=None):
+        object.__setattr__(self, "dimension", dimension)
+        object.__setattr__(self, "_lower", lower)
+        object.__setattr__(self, "inverse", inverse)
+        object.__setattr__(self, "_gram", gram)
+
+    def __setattr__(self, name, value):
+        raise AttributeError("DenseFactorization is immutable")
+
+    def __repr__(self):
+        return f"DenseFactorization(dimension={self.dimension})"
+
+    @property
+    def lower(self):
+        if self._lower is None and self._gram is not None:
+            import torch
+            low, _ = torch.linalg.cholesky_ex(self._gram)
+            object.__setattr__(self, "_lower", low)
+        return self._lower
 
     def solve(self, rhs):
         return cholesky_solve(self, rhs)
@@ -46,6 +66,50 @@ class DenseFactorization:
         if self.inverse is None:
             return cholesky_solve(self, rhs)
         return batched_gemv(self.inverse, rhs, out)
+
+
+def spd_inverse_(g, names=None):
+    """In-place inverse of SPD matrices g ((p,p) or (b,p,p) float64 CUDA,
+    row-major; only the lower triangle is read) with the hand-written DMMA sweep
+    (``wmg_spd_inverse``): on return g holds the full symmetric inverse.
+
+    Replaces potrf + cho_solve of the reference (sparse_kernels.py:53-75) for the
+    WMG leaves.  Orders that are not a multiple of 128 go through an identity-
+    padded copy.  Raises NotPositiveDefiniteError naming the first failing
+    matrix (``names[i]``) and its leading minor, like potrf's info."""
+    import ctypes
+    import torch
+    from . import _native as N
+    g3 = g if g.dim() == 3 else g.unsqueeze(0)
+    if g3.shape[-1] != g3.shape[-2]:
+        raise DimensionMismatchError(f"spd_inverse_: matrix is not square {tuple(g.shape)}")
+    if not (g3.is_cuda and g3.dtype == torch.float64 and g3.is_contiguous()):
+        raise ValueError("spd_inverse_: expects contiguous float64 CUDA matrices")
+    b, p = g3.shape[0], g3.shape[-1]
+    if b == 0 or p == 0:
+        return g
+    q = -(-p // 128) * 128
+    work_mat = g3
+    if q != p:
+        work_mat = torch.zeros((b, q, q), dtype=torch.float64, device=g.device)
+        work_mat[:, :p, :p].copy_(g3)
+        work_mat.diagonal(dim1=1, dim2=2)[:, p:].fill_(1.0)
+    nbytes = ctypes.c_size_t()
+    N.call("wmg_spd_inverse_workspace", b, q, ctypes.byref(nbytes))
+    work = torch.empty(nbytes.value // 8, dtype=torch.float64, device=g.device)
+    info = torch.empty(b, dtype=torch.int32, device=g.device)
+    st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    N.call("wmg_spd_inverse", b, q, ctypes.c_void_p(work_mat.data_ptr()), q * q,
+           ctypes.c_void_p(info.data_ptr()), ctypes.c_void_p(work.data_ptr()), st)
+    bad = info.cpu().numpy()
+    for i, code in enumerate(bad):
+        if 0 < code <= p:
+            name = names[i] if names is not None else f"matrix {i}"
+            raise NotPositiveDefiniteError(
+                f"{name}: leading minor of order {int(code)} is not positive definite")
+    if q != p:
+        g3.copy_(work_mat[:, :p, :p])
+    return g
 
 
 def batched_gemv(A, x, out=None):
