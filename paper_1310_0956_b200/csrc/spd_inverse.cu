@@ -32,6 +32,10 @@ constexpr int LDSM = KC + 4;      // padded smem row (doubles): conflict-free fr
 constexpr int OPND = T * LDSM;    // doubles per staged operand chunk
 constexpr int STAGE = 2 * OPND;   // A + B chunk
 constexpr int GEMM_SMEM = 2 * STAGE * (int)sizeof(double);   // double-buffered: 147456 B
+// update kernel: 128 x 64 tiles, two CTAs per SM (one loads/stores C while the
+// other multiplies): 2 x (A 128 + B 64 rows) x LDSM doubles = 110592 B
+constexpr int UPD_NC = 64;
+constexpr int UPD_SMEM = 2 * (T + UPD_NC) * LDSM * (int)sizeof(double);
 constexpr int SQ = T + 1;         // padded row of a full 128x128 tile in smem
 constexpr int TILE_SMEM = T * SQ * (int)sizeof(double);      // 132096 B
 
@@ -51,50 +55,56 @@ __device__ __forceinline__ void cp_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N));
 }
 
-// chunk [k0, k0+KC) of 128 rows of A and of B (row-major, leading dims lda/ldb)
+// chunk [k0, k0+KC) of 128 rows of A and NC rows of B (row-major, leading dims lda/ldb)
+template <int NC>
 __device__ __forceinline__ void load_stage(double* sA, double* sB, const double* A, long long lda,
                                            const double* B, long long ldb, int k0) {
 #pragma unroll
   for (int i = threadIdx.x; i < T * (KC / 2); i += 256) {
     const int r = i >> 4, v = (i & 15) * 2;
     cp16(sA + r * LDSM + v, A + r * lda + k0 + v);
-    cp16(sB + r * LDSM + v, B + r * ldb + k0 + v);
+    if (NC == T || r < NC) cp16(sB + r * LDSM + v, B + r * ldb + k0 + v);
   }
 }
 
-// acc (this warp's 64x32 part of a 128x128 tile) += A(128 x T) * B(128 x T)^T.
-// 8 warps as 2 (rows) x 4 (cols); fragment (i, j): rows wr*64 + 8i + g,
-// cols wc*32 + 8j + 2t + {0, 1} (g = lane / 4, t = lane % 4).
-__device__ __forceinline__ void tile_gemm(double (&acc)[8][4][2], const double* A, long long lda,
-                                          const double* B, long long ldb, double* smem) {
+// acc (this warp's part of a 128 x NC tile) += A(128 x T) * B(NC x T)^T.
+// 8 warps as (8 / CW) rows x CW cols of warp tiles (MI*8) x 32, CW = NC / 32,
+// MI = NC / 16; fragment (i, j): rows wr*MI*8 + 8i + g, cols wc*32 + 8j + 2t + {0,1}
+// (g = lane / 4, t = lane % 4).  Staged operands: A chunk then B chunk per stage.
+template <int NC>
+__device__ __forceinline__ void tile_gemm(double (&acc)[NC / 16][4][2], const double* A,
+                                          long long lda, const double* B, long long ldb,
+                                          double* smem) {
+  constexpr int CW = NC / 32, MI = NC / 16;
+  constexpr int OPB = NC * LDSM, STG = OPND + OPB;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
-  const int wr = warp >> 2, wc = warp & 3;
-  load_stage(smem, smem + OPND, A, lda, B, ldb, 0);
+  const int wr = warp / CW, wc = warp % CW;
+  load_stage<NC>(smem, smem + OPND, A, lda, B, ldb, 0);
   cp_commit();
 #pragma unroll 1
   for (int kc = 0; kc < T / KC; ++kc) {
-    double* cur = smem + (kc & 1) * STAGE;
+    double* cur = smem + (kc & 1) * STG;
     if (kc + 1 < T / KC) {
-      double* nxt = smem + ((kc + 1) & 1) * STAGE;
-      load_stage(nxt, nxt + OPND, A, lda, B, ldb, (kc + 1) * KC);
+      double* nxt = smem + ((kc + 1) & 1) * STG;
+      load_stage<NC>(nxt, nxt + OPND, A, lda, B, ldb, (kc + 1) * KC);
       cp_commit();
       cp_wait<1>();
     } else {
       cp_wait<0>();
     }
     __syncthreads();
-    const double* sA = cur + (wr * 64 + g) * LDSM + t;
+    const double* sA = cur + (wr * MI * 8 + g) * LDSM + t;
     const double* sB = cur + OPND + (wc * 32 + g) * LDSM + t;
 #pragma unroll
     for (int kk = 0; kk < KC; kk += 4) {
-      double a[8], b[4];
+      double a[MI], b[4];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) a[i] = sA[i * 8 * LDSM + kk];
+      for (int i = 0; i < MI; ++i) a[i] = sA[i * 8 * LDSM + kk];
 #pragma unroll
       for (int j = 0; j < 4; ++j) b[j] = sB[j * 8 * LDSM + kk];
 #pragma unroll
-      for (int i = 0; i < 8; ++i)
+      for (int i = 0; i < MI; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
     }
@@ -105,49 +115,69 @@ __device__ __forceinline__ void tile_gemm(double (&acc)[8][4][2], const double* 
 // ---------------------------------------------------------------- kernels
 // workspace per leaf: Dneg (T x T) | Uneg (p x T) | P (p x T)
 
-// Sweep the pivot block in shared memory: S = -A_kk^-1 -> Dneg and tile (k,k).
-__global__ void __launch_bounds__(512) sweep_diag_kernel(int p, double* __restrict__ G,
-                                                         long long sG, double* __restrict__ work,
-                                                         long long sW, int k,
-                                                         int* __restrict__ info) {
-  extern __shared__ double S[];   // T x SQ
-  __shared__ double row[T];
+// Sweep the pivot block: S = -A_kk^-1 -> Dneg and tile (k,k).  512 threads;
+// thread (q = tid / 128, c = tid % 128) keeps S[q + 4i][c], i < 32, in
+// registers.  By symmetry the pivot row is the pivot column, which the four
+// threads owning column j publish to shared memory (double-buffered: one
+// barrier per step).
+__global__ void __launch_bounds__(512, 1) sweep_diag_kernel(int p, double* __restrict__ G,
+                                                            long long sG,
+                                                            double* __restrict__ work,
+                                                            long long sW, int k,
+                                                            int* __restrict__ info) {
+  __shared__ double col[2][T];
   const int leaf = blockIdx.x;
+  const int c = threadIdx.x & (T - 1), q = threadIdx.x >> 7;
   double* Gb = G + leaf * sG + (long long)k * T * p + (long long)k * T;
-  for (int idx = threadIdx.x; idx < T * T; idx += blockDim.x) {
-    const int r = idx >> 7, c = idx & (T - 1);
-    S[r * SQ + c] = c <= r ? Gb[(long long)r * p + c] : Gb[(long long)c * p + r];
+  double v[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    const int r = q + 4 * i;
+    v[i] = c <= r ? Gb[(long long)r * p + c] : Gb[(long long)c * p + r];
   }
-  __syncthreads();
+  int bad = 0;
+#pragma unroll 1
   for (int j = 0; j < T; ++j) {
-    double d = S[j * SQ + j];
+    double* cj = col[j & 1];
+    if (c == j) {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) cj[q + 4 * i] = v[i];
+    }
+    __syncthreads();
+    double d = cj[j];
     if (!(d > 0.0)) {
-      if (threadIdx.x == 0 && info[leaf] == 0) info[leaf] = k * T + j + 1;
+      if (!bad) bad = k * T + j + 1;
       d = 1.0;   // keep going (the host raises); no NaN/inf spread
     }
-    if (threadIdx.x < T) row[threadIdx.x] = S[j * SQ + threadIdx.x];
-    __syncthreads();
     const double inv = 1.0 / d;
-    for (int idx = threadIdx.x; idx < T * T; idx += blockDim.x) {
-      const int r = idx >> 7, c = idx & (T - 1);
-      double v;
-      if (r != j && c != j) {
-        v = S[r * SQ + c] - (row[r] * row[c]) * inv;   // symmetric rounding
-      } else if (r == j && c == j) {
-        v = -inv;
-      } else {
-        v = (r == j ? row[c] : row[r]) * inv;
+    const double rc = cj[c];
+    const int jq = j & 3, ji = j >> 2;
+    if (c == j) {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] = cj[q + 4 * i] * inv;
+      if (q == jq) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          if (i == ji) v[i] = -inv;
       }
-      S[r * SQ + c] = v;
+    } else {
+      const double rci = rc * inv;
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] = fma(-cj[q + 4 * i], rci, v[i]);
+      if (q == jq) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          if (i == ji) v[i] = rci;
+      }
     }
-    __syncthreads();
   }
+  if (bad && c == 0 && q == 0 && info[leaf] == 0) info[leaf] = bad;
   double* Dn = work + leaf * sW;
-  for (int idx = threadIdx.x; idx < T * T; idx += blockDim.x) {
-    const int r = idx >> 7, c = idx & (T - 1);
-    const double v = S[r * SQ + c];
-    Dn[idx] = v;
-    Gb[(long long)r * p + c] = v;
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    const int r = q + 4 * i;
+    Dn[r * T + c] = v[i];
+    Gb[(long long)r * p + c] = v[i];
   }
 }
 
@@ -191,7 +221,7 @@ __global__ void __launch_bounds__(256, 1) sweep_panel_kernel(int p, double* __re
   for (int i = 0; i < 8; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-  tile_gemm(acc, PI, T, Dn, T, smem);   // Dneg is symmetric: rows of Dneg = columns
+  tile_gemm<T>(acc, PI, T, Dn, T, smem);   // Dneg is symmetric: rows of Dneg = columns
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
   const int wr = warp >> 2, wc = warp & 3;
@@ -220,39 +250,42 @@ __device__ __forceinline__ void lower_tile(int lin, int& I, int& J) {
   J = lin - i * (i + 1) / 2;
 }
 
-// Trailing update of every lower tile (I, J) off the pivot strip:
-// A_IJ += Uneg_I P_J^T.
-__global__ void __launch_bounds__(256, 1) sweep_update_kernel(int p, double* __restrict__ G,
+// Trailing update of every lower tile (I, J) off the pivot strip, in two
+// 128 x 64 halves (blockIdx.x = 2 * tile + half): A_IJ += Uneg_I P_J^T.
+__global__ void __launch_bounds__(256, 2) sweep_update_kernel(int p, double* __restrict__ G,
                                                               long long sG,
                                                               const double* __restrict__ work,
                                                               long long sW, int k) {
   extern __shared__ double smem[];
+  constexpr int MI = UPD_NC / 16, CW = UPD_NC / 32;
   int I, J;
-  lower_tile(blockIdx.x, I, J);
+  lower_tile(blockIdx.x >> 1, I, J);
   if (I == k || J == k) return;
+  const int half = blockIdx.x & 1;
   const int leaf = blockIdx.y;
-  double* Cb = G + leaf * sG + (long long)I * T * p + (long long)J * T;
+  double* Cb = G + leaf * sG + (long long)I * T * p + (long long)J * T + half * UPD_NC;
   const double* Un = work + leaf * sW + (long long)T * T;
   const double* P = Un + (long long)p * T;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
-  const int wr = warp >> 2, wc = warp & 3;
-  double acc[8][4][2];
+  const int wr = warp / CW, wc = warp % CW;
+  double acc[MI][4][2];
 #pragma unroll
-  for (int i = 0; i < 8; ++i)
+  for (int i = 0; i < MI; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      const int r = wr * 64 + i * 8 + g, c = wc * 32 + j * 8 + 2 * t;
+      const int r = wr * MI * 8 + i * 8 + g, c = wc * 32 + j * 8 + 2 * t;
       const double2 v = __ldcs(reinterpret_cast<const double2*>(Cb + (long long)r * p + c));
       acc[i][j][0] = v.x;
       acc[i][j][1] = v.y;
     }
-  tile_gemm(acc, Un + (long long)I * T * T, T, P + (long long)J * T * T, T, smem);
+  tile_gemm<UPD_NC>(acc, Un + (long long)I * T * T, T,
+                    P + (long long)J * T * T + (long long)half * UPD_NC * T, T, smem);
 #pragma unroll
-  for (int i = 0; i < 8; ++i)
+  for (int i = 0; i < MI; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      const int r = wr * 64 + i * 8 + g, c = wc * 32 + j * 8 + 2 * t;
+      const int r = wr * MI * 8 + i * 8 + g, c = wc * 32 + j * 8 + 2 * t;
       *reinterpret_cast<double2*>(Cb + (long long)r * p + c) =
           make_double2(acc[i][j][0], acc[i][j][1]);
     }
@@ -306,7 +339,7 @@ cudaError_t spd_inverse(int batch, int p, double* G, long long sG, int* info, do
                                   GEMM_SMEM)) != cudaSuccess)
       return e;
     if ((e = cudaFuncSetAttribute(sweep_update_kernel,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM)) !=
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, UPD_SMEM)) !=
         cudaSuccess)
       return e;
     if ((e = cudaFuncSetAttribute(sweep_finish_kernel,
@@ -323,7 +356,7 @@ cudaError_t spd_inverse(int batch, int p, double* G, long long sG, int* info, do
     sweep_diag_kernel<<<batch, 512, TILE_SMEM, st>>>(p, G, sG, work, sW, k, info);
     if (nt > 1) {
       sweep_panel_kernel<<<dim3(nt, batch), 256, GEMM_SMEM, st>>>(p, G, sG, work, sW, k);
-      sweep_update_kernel<<<dim3(ntri, batch), 256, GEMM_SMEM, st>>>(p, G, sG, work, sW, k);
+      sweep_update_kernel<<<dim3(2 * ntri, batch), 256, UPD_SMEM, st>>>(p, G, sG, work, sW, k);
     }
   }
   sweep_finish_kernel<<<dim3(ntri, batch), 256, TILE_SMEM, st>>>(p, G, sG);
