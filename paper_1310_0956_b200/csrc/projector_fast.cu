@@ -730,6 +730,139 @@ __global__ void __launch_bounds__(256, 5) bwd_sym_kernel(GeomDev G, const TIn* _
 }
 
 
+// Symmetric backprojector, run layout (default).  Same four-image weight
+// sharing as bwd_sym_kernel, but lane = tile column and every thread owns R
+// CONSECUTIVE rows.  Going one row down moves the detector coordinate by
+// -sin(theta) in (-1, 0), so the detector pair (j, j+1) of the next row is
+// either the same pair or (j-1, j): the thread carries the pair in registers
+// and loads only the new lower detector per row -- one float2 (y_a, y_b) and
+// one reversed float2 per (pixel, angle) for four images, half the shared
+// wavefronts of the float4 windows.  A half-warp is 16 consecutive columns of
+// one row: its detector indices span <= 16 consecutive entries, so the LDS.64
+// are conflict-free (2 wavefronts each).  Tile: 32 columns x 8R rows.
+template <typename TIn, typename TOut, bool kAccumulate, int R>
+__global__ void __launch_bounds__(256, R == 4 ? 5 : 3) bwd_symrun_kernel(GeomDev G,
+                                                            const TIn* __restrict__ sino,
+                                                            TOut* __restrict__ img) {
+  constexpr int TR = 8 * R;                  // tile rows
+  constexpr int WIN = R == 4 ? 64 : 96;      // window entries (>= span + 3)
+  constexpr int OFF = kSymChunk * WIN;       // winB - winA (float2 entries)
+  // win[0][aa][t] = (y_a[jlo+t], y_b[jlo+t]); win[1]: same at detector d-1-(jlo+t)
+  __shared__ float2 win[2][kSymChunk][WIN];
+  __shared__ long long qx[kSymChunk][kBwdTile];
+  __shared__ float4 wc_s[kSymChunk];         // (a0, icb, hwic, w1c)
+  __shared__ float2 ls_s[kSymChunk];         // (L, low word of S as bits)
+  __shared__ long long qhead[kSymChunk];
+  __shared__ int jlo_s[kSymChunk];
+  __shared__ int ang_s[kSymChunk];
+  __shared__ int mir_s[kSymChunk];
+  const int n = G.n, d = G.d;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int col0 = blockIdx.x * kBwdTile, row0 = blockIdx.y * TR;
+  const double half = (double)n * 0.5, dc = (double)(d - 1) * 0.5;
+  const double xc0 = (double)col0 - half + 0.5;
+  const double yc0 = half - (double)row0 - 0.5;
+  const double bias = 1.0 / kQ32;
+  const int trow = warp * R;
+  float2 accA[R], accB[R];
+#pragma unroll
+  for (int i = 0; i < R; ++i) {
+    accA[i] = make_float2(0.0f, 0.0f);
+    accB[i] = make_float2(0.0f, 0.0f);
+  }
+  for (int c0 = 0; c0 < G.n_prim; c0 += kSymChunk) {
+    const int na = min(kSymChunk, G.n_prim - c0);
+    __syncthreads();
+    if (tid < na) {
+      const int q = c0 + tid;
+      const int a = G.prim[q];
+      ang_s[tid] = a;
+      mir_s[tid] = G.mir[a] * d;
+      const AngleParams& A = G.ang[a];
+      const double p0 = xc0 * A.c + yc0 * A.s + dc - A.hw - bias;
+      const double pmin = p0 + fmin(0.0, (double)(kBwdTile - 1) * A.c) +
+                          fmin(0.0, -(double)(TR - 1) * A.s);
+      const int jlo = (int)floor(pmin) - 1;
+      jlo_s[tid] = jlo;
+      qhead[tid] = llrint((p0 - (double)jlo) * kQ32);
+      wc_s[tid] = make_float4(A.a0, A.icb, A.hwic, A.w1c);
+      // 0 < sin < 1 for every non-axis angle: S < 2^32, one word
+      ls_s[tid] = make_float2(A.Lf, __uint_as_float((unsigned)A.Sfix));
+    }
+    __syncthreads();
+    for (int e = tid; e < na * kBwdTile; e += 256) {
+      const int aa = e / kBwdTile, l = e % kBwdTile;
+      qx[aa][l] = qhead[aa] + (long long)l * G.ang[ang_s[aa]].Cfix;
+    }
+    for (int e = tid; e < na * WIN; e += 256) {
+      const int aa = e / WIN, t = e % WIN;
+      const int j = jlo_s[aa] + t;
+      const TIn* ya = sino + ang_s[aa] * d;
+      const TIn* yb = sino + mir_s[aa];
+      auto ld = [&](const TIn* y, int jj) -> float {
+        return (jj >= 0 && jj < d) ? (float)__ldg(y + jj) : 0.0f;
+      };
+      win[0][aa][t] = make_float2(ld(ya, j), ld(yb, j));
+      const int r0 = d - 1 - j;
+      win[1][aa][t] = make_float2(ld(ya, r0), ld(yb, r0));
+    }
+    __syncthreads();
+    for (int aa = 0; aa < na; ++aa) {
+      const float4 wc = wc_s[aa];
+      const float2 ls = ls_s[aa];
+      const float ca0 = wc.x, icb = wc.y, hwic = wc.z, w1c = wc.w, L = ls.x;
+      const unsigned Slo = __float_as_uint(ls.y);
+      const long long Q = qx[aa][lane] - (long long)trow * (long long)Slo;
+      unsigned lo = (unsigned)Q;
+      const float2* pw = &win[0][aa][hi32(Q) + 1];   // first detector of the pair
+      float2 fa = pw[0], sa = pw[1];
+      float2 fb = pw[OFF], sb = pw[OFF + 1];
+#pragma unroll
+      for (int i = 0; i < R; ++i) {
+        if (i > 0) {
+          const unsigned lo2 = lo - Slo;
+          const bool moved = lo2 > lo;   // borrow: the pair slid down one detector
+          lo = lo2;
+          pw -= moved ? 1 : 0;
+          sa = moved ? fa : sa;
+          sb = moved ? fb : sb;
+          fa = pw[0];
+          fb = pw[OFF];
+        }
+        const float f = frac1(lo);
+        const float d0 = ca0 - f;
+        const float w0 = fminf(fmaf(-fabsf(d0), icb, hwic), L);
+        const float w1 = fmaxf(fmaf(f, icb, w1c), 0.0f);
+        const float2 W0 = make_float2(w0, w0), W1 = make_float2(w1, w1);
+        accA[i] = __ffma2_rn(W0, fa, accA[i]);
+        accA[i] = __ffma2_rn(W1, sa, accA[i]);
+        accB[i] = __ffma2_rn(W0, fb, accB[i]);
+        accB[i] = __ffma2_rn(W1, sb, accB[i]);
+      }
+    }
+  }
+  const int col = col0 + lane;
+#pragma unroll
+  for (int i = 0; i < R; ++i) {
+    const int row = row0 + trow + i;
+    const long long p1 = (long long)row * n + col;                       // (p, a)
+    const long long p2 = (long long)row * n + (n - 1 - col);             // x-mirror, m-a
+    const long long p3 = (long long)(n - 1 - row) * n + (n - 1 - col);   // rotation, a rev
+    const long long p4 = (long long)(n - 1 - row) * n + col;             // y-mirror, m-a rev
+    if (kAccumulate) {
+      img[p1] = (TOut)((float)img[p1] + accA[i].x);
+      img[p2] = (TOut)((float)img[p2] + accA[i].y);
+      img[p3] = (TOut)((float)img[p3] + accB[i].x);
+      img[p4] = (TOut)((float)img[p4] + accB[i].y);
+    } else {
+      img[p1] = (TOut)accA[i].x;
+      img[p2] = (TOut)accA[i].y;
+      img[p3] = (TOut)accB[i].x;
+      img[p4] = (TOut)accB[i].y;
+    }
+  }
+}
+
 // Symmetric forward.  Rays (a, j), (m-a, j), (a, d-1-j), (m-a, d-1-j) see the
 // same weights on the slab-coordinate images (s, q), (s, n-1-q), (n-1-s, n-1-q),
 // (n-1-s, q) of one walk (x-mirror / 180-degree rotation of the grid), so one
@@ -1414,12 +1547,33 @@ template <typename TIn, typename TOut>
 static cudaError_t bwd_v2_impl(const GeomDev& G, const void* y, void* x, bool accumulate,
                                cudaStream_t st, const GeomDev* G_axis = nullptr);
 
+template <typename TIn, typename TOut, int R>
+static void bwd_symrun_launch(const GeomDev& G, const void* y, void* x, bool accumulate,
+                              cudaStream_t st) {
+  dim3 grid(G.n / 64, G.n / (16 * R));   // the top-left quadrant in 32 x 8R tiles
+  if (accumulate)
+    fast::bwd_symrun_kernel<TIn, TOut, true, R><<<grid, 256, 0, st>>>(G, (const TIn*)y,
+                                                                     (TOut*)x);
+  else
+    fast::bwd_symrun_kernel<TIn, TOut, false, R><<<grid, 256, 0, st>>>(G, (const TIn*)y,
+                                                                      (TOut*)x);
+}
+
 template <typename TIn, typename TOut>
 static cudaError_t bwd_sym_impl(const GeomDev& G, const GeomDev& Gx, const void* y, void* x,
                                 bool accumulate, cudaStream_t st) {
   dim3 grid(G.n / 64, G.n / 64);
-  const bool rowlayout = (G.sym & 8) != 0;   // testing: the lane = column layout
-  if (accumulate) {
+  const bool rowlayout = (G.sym & 8) != 0;    // testing: the lane = column layout
+  const bool blocks8x4 = (G.sym & 256) != 0;  // testing: 8x4 warp blocks, float4 windows
+  if (!rowlayout && !blocks8x4) {
+    // run layout: 64-row tiles (fewer window loads per pixel) when the quadrant
+    // allows and the grid still fills the SMs (n >= ~3400), else 32-row tiles
+    if ((G.n / 2) % 64 == 0 && (long long)(G.n / 64) * (G.n / 128) >= 12LL * 148 &&
+        !(G.sym & 512))
+      bwd_symrun_launch<TIn, TOut, 8>(G, y, x, accumulate, st);
+    else
+      bwd_symrun_launch<TIn, TOut, 4>(G, y, x, accumulate, st);
+  } else if (accumulate) {
     if (rowlayout)
       fast::bwd_sym_kernel<TIn, TOut, true, false><<<grid, 256, 0, st>>>(G, (const TIn*)y,
                                                                         (TOut*)x);
