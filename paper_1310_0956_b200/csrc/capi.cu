@@ -302,9 +302,10 @@ int wmg_geometry_symmetry(wmg_geometry* g, int set, int* enabled) {
   if (!g) return fail(WMG_EINVAL, "geometry is NULL");
   // 0 off, 1 auto, 2 forced, 4 forced + TMA forward; testing variants of the
   // forced mode: +8 row-layout backprojector, +16 one-angle forward blocks,
-  // +256 the 8x4-block float4-window backprojector, +512 run layout with R = 4
+  // +256 the 8x4-block float4-window backprojector, +512 / +1024 run layout with
+  // R = 4 / R = 8 rows per thread at any size
   if (set == 0 || set == 1 || set == 2 || set == 4 || set == 10 || set == 18 || set == 26 || set == 34 || set == 66 || set == 130 ||
-      set == 258 || set == 514)
+      set == 258 || set == 514 || set == 1026)
     g->dev.sym = (set && g->sym_capable) ? set : 0;
   if (enabled) *enabled = g->dev.sym;
   return WMG_OK;

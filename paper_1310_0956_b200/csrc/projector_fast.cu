@@ -1568,7 +1568,9 @@ static cudaError_t bwd_sym_impl(const GeomDev& G, const GeomDev& Gx, const void*
   if (!rowlayout && !blocks8x4) {
     // run layout: 64-row tiles (fewer window loads per pixel) when the quadrant
     // allows and the grid still fills the SMs (n >= ~3400), else 32-row tiles
-    if ((G.n / 2) % 64 == 0 && (long long)(G.n / 64) * (G.n / 128) >= 12LL * 148 &&
+    // (sym & 1024: testing, 64-row tiles at any size; sym & 512: 32-row tiles)
+    if ((G.n / 2) % 64 == 0 &&
+        ((long long)(G.n / 64) * (G.n / 128) >= 12LL * 148 || (G.sym & 1024)) &&
         !(G.sym & 512))
       bwd_symrun_launch<TIn, TOut, 8>(G, y, x, accumulate, st);
     else
