@@ -741,7 +741,8 @@ __global__ void __launch_bounds__(256, 5) bwd_sym_kernel(GeomDev G, const TIn* _
 // one row: its detector indices span <= 16 consecutive entries, so the LDS.64
 // are conflict-free (2 wavefronts each).  Tile: 32 columns x 8R rows.
 template <typename TIn, typename TOut, bool kAccumulate, int R>
-__global__ void __launch_bounds__(256, R == 4 ? 5 : 3) bwd_symrun_kernel(GeomDev G,
+__global__ void __launch_bounds__(256, R == 4 ? 5 : (sizeof(TOut) == 4 ? 4 : 3))
+bwd_symrun_kernel(GeomDev G,
                                                             const TIn* __restrict__ sino,
                                                             TOut* __restrict__ img) {
   constexpr int TR = 8 * R;                  // tile rows
