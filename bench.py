@@ -136,12 +136,21 @@ class ClockSampler:
 
 
 def onchip_roofline(n, t_fwd, t_bwd, n_sm, f_sm, world):
-    """The on-chip resources that bind the pair (DESIGN.md kernel table): L1
-    sector requests of the forward gathers (peak 4 sectors/clk/SM) and shared
-    wavefronts of the backprojector (peak 1/clk/SM); per-launch counts from the
-    committed ncu capture, times live from this run."""
+    """The on-chip resources that bind the pair (DESIGN.md kernel table).  The
+    binding one is the L1 data pipe that returns load data to the registers
+    (l1tex__data_pipe_lsu_wavefronts, peak 1 wavefront/clk/SM): the forward's
+    pixel gathers run it at ~94 %.  Also: L1 sector requests of the forward
+    gathers (peak 4 sectors/clk/SM) and the backprojector's shared wavefronts.
+    Per-launch counts from the committed ncu capture, times live from this run."""
     t = ncu_traffic()
     out = {}
+    for kern, tk in (("forward", t_fwd), ("backward", t_bwd)):
+        wf = t.get(f"l1_datapipe_wavefronts_{kern}_n{n}")
+        if wf and tk > 0 and world == 1:
+            peak = 1.0 * n_sm * f_sm
+            out[f"{kern}_l1_data_pipe"] = {"achieved": wf / tk / 1e9, "peak": peak / 1e9,
+                                           "unit": "Gwavefronts/s", "frac": wf / tk / peak,
+                                           "per_launch": wf}
     sec = t.get(f"l1_sectors_forward_n{n}")
     if sec and t_fwd > 0 and world == 1:
         peak = 4.0 * n_sm * f_sm

@@ -35,7 +35,8 @@
  *   multilevel.py:123-130 leaf Gram assembly        -> wmg_leaf_gram (sparse) or
  *                                                      wmg_leaf_factor (+ DGEMM)
  *   sparse_kernels.py:53-65 potrf of the leaf Grams  -> wmg_spd_inverse (batched fp64 DMMA sweep)
- *   sparse_kernels.py:68-75 cho_solve in the V-cycle -> wmg_batched_gemv (stored inverse)
+ *   sparse_kernels.py:68-75 cho_solve in the V-cycle -> wmg_packed_symv (packed symmetric
+ *                                                      inverse) / wmg_batched_gemv (dense)
  *   multilevel.py:109-113 node systems, siblings     -> wmg_forward_batch / wmg_backward_batch
  *   geometry.py:131-175 _joseph_entries             -> wmg_geometry_kernel (JOSEPH)
  *   (CGLS / PCG-NE, not in the reference)           -> wmg_cgls_scalars, wmg_axpy_dev,
@@ -221,6 +222,25 @@ int wmg_spd_inverse_workspace(int batch, int p, size_t *bytes);
  * garbage).  Replaces the reference's per-leaf potrf (sparse_kernels.py:53-65,
  * called at multilevel.py:125-137) plus the inverse the V-cycle's GEMV needs. */
 int wmg_spd_inverse(int batch, int p, double *G, long long strideG, int *info, void *work,
+                    void *stream);
+
+/* Packed symmetric storage (p % 128 == 0): the lower 128 x 128 tiles of a
+ * symmetric matrix, tile (I, J), I >= J, at index I (I + 1) / 2 + J, each
+ * row-major, diagonal tiles full.  *elems_per_matrix = doubles per packed
+ * matrix; *scratch_bytes = device scratch wmg_packed_symv needs for `batch`
+ * matrices (either pointer may be NULL). */
+int wmg_packed_sym_sizes(int batch, int p, long long *elems_per_matrix, size_t *scratch_bytes);
+
+/* packed_b <- lower tiles of the full symmetric A_b (row-major p x p) */
+int wmg_sym_pack(int batch, int p, const double *A, long long strideA, double *packed,
+                 long long strideP, void *stream);
+
+/* y_b = A_b x_b for packed symmetric A_b: every tile is read once (its
+ * transpose product serves the mirrored block), partial products summed in a
+ * fixed order (deterministic).  The WMG coarse solves (reference cho_solve,
+ * sparse_kernels.py:68-75) with half the bytes of wmg_batched_gemv. */
+int wmg_packed_symv(int batch, int p, const double *packed, long long strideP, const double *x,
+                    long long stridex, double *y, long long stridey, double *scratch,
                     void *stream);
 
 #ifdef __cplusplus

@@ -65,6 +65,11 @@ cudaError_t leaf_factor(const GeomDev&, int, const int*, long long, long long, d
 cudaError_t leaf_gram(const GeomDev&, int, const int*, double*, int*, cudaStream_t);
 size_t spd_inverse_workspace(int, int);
 cudaError_t spd_inverse(int, int, double*, long long, int*, double*, cudaStream_t);
+size_t packed_sym_elems(int);
+size_t packed_symv_scratch(int, int);
+cudaError_t sym_pack(int, int, const double*, long long, double*, long long, cudaStream_t);
+cudaError_t packed_symv(int, int, const double*, long long, const double*, long long, double*,
+                        long long, double*, cudaStream_t);
 bool tma_window_fits(const AngleParams*, int, int, int);
 }  // namespace wmg
 
@@ -619,6 +624,36 @@ int wmg_spd_inverse(int batch, int p, double* G, long long strideG, int* info, v
   if (batch > 1 && strideG < (long long)p * p) return fail(WMG_EDIM, "batch stride < p*p");
   if (batch > 65535) return fail(WMG_EINVAL, "batch > 65535");
   return cuda_rc(wmg::spd_inverse(batch, p, G, strideG, info, static_cast<double*>(work),
+                                  STREAM(stream)));
+}
+
+int wmg_packed_sym_sizes(int batch, int p, long long* elems_per_matrix, size_t* scratch_bytes) {
+  if (batch < 0 || p < 0) return fail(WMG_EINVAL, "negative size");
+  if (p % 128) return fail(WMG_EINVAL, "p must be a multiple of 128");
+  if (elems_per_matrix) *elems_per_matrix = (long long)wmg::packed_sym_elems(p);
+  if (scratch_bytes) *scratch_bytes = wmg::packed_symv_scratch(batch, p);
+  return WMG_OK;
+}
+
+int wmg_sym_pack(int batch, int p, const double* A, long long strideA, double* packed,
+                 long long strideP, void* stream) {
+  REQ(A && packed);
+  if (batch < 0 || p < 0) return fail(WMG_EINVAL, "negative size");
+  if (p % 128) return fail(WMG_EINVAL, "p must be a multiple of 128");
+  if (batch > 1 && (strideA < (long long)p * p || strideP < (long long)wmg::packed_sym_elems(p)))
+    return fail(WMG_EDIM, "batch stride too small");
+  if (batch > 65535) return fail(WMG_EINVAL, "batch > 65535");
+  return cuda_rc(wmg::sym_pack(batch, p, A, strideA, packed, strideP, STREAM(stream)));
+}
+
+int wmg_packed_symv(int batch, int p, const double* packed, long long strideP, const double* x,
+                    long long stridex, double* y, long long stridey, double* scratch,
+                    void* stream) {
+  REQ(packed && x && y && scratch);
+  if (batch < 0 || p < 0) return fail(WMG_EINVAL, "negative size");
+  if (p % 128) return fail(WMG_EINVAL, "p must be a multiple of 128");
+  if (batch > 65535) return fail(WMG_EINVAL, "batch > 65535");
+  return cuda_rc(wmg::packed_symv(batch, p, packed, strideP, x, stridex, y, stridey, scratch,
                                   STREAM(stream)));
 }
 

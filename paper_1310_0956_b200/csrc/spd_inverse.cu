@@ -319,6 +319,105 @@ __global__ void __launch_bounds__(256) sweep_finish_kernel(int p, double* __rest
   }
 }
 
+
+// ------------------------------------------------- packed symmetric storage
+// A symmetric p x p matrix (p % 128 == 0) kept as its lower 128 x 128 tiles,
+// tile (I, J), I >= J, at index I (I + 1) / 2 + J, each row-major; diagonal
+// tiles hold the full (mirrored) tile.  Half the bytes of the dense inverse:
+// the V-cycle's coarse solves (one symmetric GEMV per leaf per cycle) stream
+// 67 MB instead of 134 MB per 4096^2 leaf.
+
+// pack the lower tiles of a full symmetric matrix (mirrors the diagonal tiles
+// from their lower triangles)
+__global__ void __launch_bounds__(256) sym_pack_kernel(int p, const double* __restrict__ A,
+                                                       long long sA, double* __restrict__ Pk,
+                                                       long long sP) {
+  int I, J;
+  lower_tile(blockIdx.x, I, J);
+  const double* src = A + blockIdx.y * sA + (long long)I * T * p + (long long)J * T;
+  double* dst = Pk + blockIdx.y * sP + (long long)blockIdx.x * T * T;
+  for (int idx = threadIdx.x; idx < T * T / 2; idx += 256) {
+    const int r = idx >> 6, c = (idx & 63) * 2;
+    double2 v = *reinterpret_cast<const double2*>(src + (long long)r * p + c);
+    if (I == J) {
+      if (c > r) v.x = src[(long long)c * p + r];
+      if (c + 1 > r) v.y = src[(long long)(c + 1) * p + r];
+    }
+    *reinterpret_cast<double2*>(dst + r * T + c) = v;
+  }
+}
+
+// One packed tile per CTA, read once: u = A_IJ x_J -> S[K=I][L=J], and for
+// I != J also v = A_IJ^T x_I -> S[K=J][L=I].  8 warps x 16 rows; lane = 4
+// columns (two 16-byte loads per row, 8 rows in flight); rows reduced with a
+// fixed shuffle tree, columns over the warps in warp order (deterministic).
+__global__ void __launch_bounds__(256) sym_tile_gemv_kernel(int p, const double* __restrict__ Pk,
+                                                            long long sP,
+                                                            const double* __restrict__ x,
+                                                            long long sx,
+                                                            double* __restrict__ S) {
+  __shared__ double colp[8][T];
+  int I, J;
+  lower_tile(blockIdx.x, I, J);
+  const int nt = p / T;
+  const int b = blockIdx.y;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const double* tile = Pk + b * sP + (long long)blockIdx.x * T * T + (warp * 16) * T + lane * 4;
+  const double* xb = x + b * sx;
+  const double4 xj = *reinterpret_cast<const double4*>(xb + J * T + lane * 4);
+  double* Sb = S + (long long)b * nt * nt * T;
+  double cacc[4] = {0.0, 0.0, 0.0, 0.0};
+  double rsum = 0.0;   // lane i < 16 ends with row 16 warp + i
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    double2 v[8][2];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      v[i][0] = __ldcs(reinterpret_cast<const double2*>(tile + (h * 8 + i) * T));
+      v[i][1] = __ldcs(reinterpret_cast<const double2*>(tile + (h * 8 + i) * T + 2));
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int row = warp * 16 + h * 8 + i;
+      double r = v[i][0].x * xj.x;
+      r = fma(v[i][0].y, xj.y, r);
+      r = fma(v[i][1].x, xj.z, r);
+      r = fma(v[i][1].y, xj.w, r);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
+      if (lane == h * 8 + i) rsum = r;
+      if (I != J) {
+        const double xi = xb[I * T + row];
+        cacc[0] = fma(v[i][0].x, xi, cacc[0]);
+        cacc[1] = fma(v[i][0].y, xi, cacc[1]);
+        cacc[2] = fma(v[i][1].x, xi, cacc[2]);
+        cacc[3] = fma(v[i][1].y, xi, cacc[3]);
+      }
+    }
+  }
+  if (lane < 16) Sb[((long long)I * nt + J) * T + warp * 16 + lane] = rsum;
+  if (I == J) return;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) colp[warp][lane * 4 + q] = cacc[q];
+  __syncthreads();
+  if (threadIdx.x < T) {
+    double s = colp[0][threadIdx.x];
+#pragma unroll
+    for (int w = 1; w < 8; ++w) s += colp[w][threadIdx.x];
+    Sb[((long long)J * nt + I) * T + threadIdx.x] = s;
+  }
+}
+
+// y_K = sum over L of S[K][L], L ascending
+__global__ void __launch_bounds__(T) sym_reduce_kernel(int p, const double* __restrict__ S,
+                                                       double* __restrict__ y, long long sy) {
+  const int K = blockIdx.x, b = blockIdx.y, nt = p / T;
+  const double* src = S + ((long long)b * nt + K) * nt * T + threadIdx.x;
+  double s = 0.0;
+  for (int L = 0; L < nt; ++L) s += src[(long long)L * T];
+  y[b * sy + K * T + threadIdx.x] = s;
+}
+
 }  // namespace spd
 
 size_t spd_inverse_workspace(int batch, int p) {
@@ -360,6 +459,37 @@ cudaError_t spd_inverse(int batch, int p, double* G, long long sG, int* info, do
     }
   }
   sweep_finish_kernel<<<dim3(ntri, batch), 256, TILE_SMEM, st>>>(p, G, sG);
+  return cudaGetLastError();
+}
+
+size_t packed_sym_elems(int p) {
+  const long long nt = p / spd::T;
+  return (size_t)(nt * (nt + 1) / 2) * spd::T * spd::T;
+}
+
+size_t packed_symv_scratch(int batch, int p) {
+  const long long nt = p / spd::T;
+  return (size_t)batch * (size_t)(nt * nt) * spd::T * sizeof(double);
+}
+
+cudaError_t sym_pack(int batch, int p, const double* A, long long sA, double* Pk, long long sP,
+                     cudaStream_t st) {
+  if (batch <= 0 || p <= 0) return cudaSuccess;
+  const int nt = p / spd::T;
+  spd::sym_pack_kernel<<<dim3(nt * (nt + 1) / 2, batch), 256, 0, st>>>(p, A, sA, Pk, sP);
+  return cudaGetLastError();
+}
+
+cudaError_t packed_symv(int batch, int p, const double* Pk, long long sP, const double* x,
+                        long long sx, double* y, long long sy, double* scratch,
+                        cudaStream_t st) {
+  if (batch <= 0 || p <= 0) return cudaSuccess;
+  const int nt = p / spd::T;
+  spd::sym_tile_gemv_kernel<<<dim3(nt * (nt + 1) / 2, batch), 256, 0, st>>>(p, Pk, sP, x, sx,
+                                                                           scratch);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  spd::sym_reduce_kernel<<<dim3(nt, batch), spd::T, 0, st>>>(p, scratch, y, sy);
   return cudaGetLastError();
 }
 

@@ -276,7 +276,7 @@ def _is_sharded(w) -> bool:
 
 def build_wmg_hierarchy(w, n: int, lam: float, levels: int, nu_pre: int = 0,
                         nu_post: int = 0, node_mode: str = "fast",
-                        gram: str = "sparse") -> WmgHierarchy:
+                        gram: str = "sparse", packed: bool = True) -> WmgHierarchy:
     """Recursive 4-way splitting of W (multilevel.py:151-166), matrix-free.
 
     ``node_mode``: projector of the internal node systems -- "fast" (float64
@@ -284,7 +284,9 @@ def build_wmg_hierarchy(w, n: int, lam: float, levels: int, nu_pre: int = 0,
     float64 vectors, <= 1e-5 relative: a cheaper, slightly inexact V-cycle for
     flexible outer solvers) or "parity".  ``gram``: leaf Gram assembly --
     "sparse" (per-ray-bundle accumulation, default) or "dense" (exact parity
-    P_L + DGEMM, O(M p^2) per leaf).
+    P_L + DGEMM, O(M p^2) per leaf).  ``packed``: keep the leaf inverses as
+    packed symmetric tiles (half the bytes per coarse solve) when the leaf
+    order is a multiple of 128; else dense row-major.
     """
     if levels < 2:
         raise ValueError("levels must be >= 2")
@@ -332,6 +334,12 @@ def build_wmg_hierarchy(w, n: int, lam: float, levels: int, nu_pre: int = 0,
             name, _, why = str(exc).partition(": ")
             raise NotPositiveDefiniteError(
                 f"coarsest subproblem '{name}' is singular (lambda={lam}): {why}") from None
+    if packed and p % 128 == 0:
+        # packed symmetric storage: the V-cycle's coarse solves stream half the bytes
+        from .sparse_kernels import PackedSymmetric
+        packed = PackedSymmetric.pack(grams)
+        del grams
+        grams = packed
     inverses = grams
     leaf_index = {path: i for i, path in enumerate(paths)}
     if node_mode not in ("fast", "fast32", "parity"):
@@ -777,7 +785,12 @@ class ClassicalTGPreconditioner(_GraphedOperator):
         except NotPositiveDefiniteError:
             raise NotPositiveDefiniteError(
                 f"coarse LL Galerkin operator is singular (lambda={lam})") from None
-        self.coarse = DenseFactorization(dimension=grams.shape[-1], inverse=grams[0], gram=gram)
+        inv = grams[0]
+        if inv.shape[-1] % 128 == 0:
+            from .sparse_kernels import PackedSymmetric
+            inv = PackedSymmetric.pack(grams)
+            del grams
+        self.coarse = DenseFactorization(dimension=inv.shape[-1], inverse=inv, gram=gram)
         M, N_ = w.shape
         dev = w.device
         self._sino = t.empty(M, dtype=t.float64, device=dev)

@@ -35,13 +35,21 @@ class DenseFactorization:
     Immutable like the reference's frozen dataclass.
     """
 
-    __slots__ = ("dimension", "_lower", "inverse", "_gram")
+    __slots__ = ("dimension", "_lower", "_inv", "_gram")
 
     def __init__(self, dimension: int, lower=None, inverse=None, gram=None):
         object.__setattr__(self, "dimension", dimension)
         object.__setattr__(self, "_lower", lower)
-        object.__setattr__(self, "inverse", inverse)
+        object.__setattr__(self, "_inv", inverse)   # dense tensor or PackedSymmetric
         object.__setattr__(self, "_gram", gram)
+
+    @property
+    def inverse(self):
+        """G^-1 as a dense (dim, dim) tensor (unpacked on access when stored
+        packed; the coarse solves use the packed form directly)."""
+        if isinstance(self._inv, PackedSymmetric):
+            return self._inv.dense()[0]
+        return self._inv
 
     def __setattr__(self, name, value):
         raise AttributeError("DenseFactorization is immutable")
@@ -63,9 +71,9 @@ class DenseFactorization:
     def apply_inverse(self, rhs, out=None):
         """G^-1 rhs via the stored inverse: our batched GEMV kernel (falls back to
         the triangular solves when no inverse is stored)."""
-        if self.inverse is None:
+        if self._inv is None:
             return cholesky_solve(self, rhs)
-        return batched_gemv(self.inverse, rhs, out)
+        return batched_gemv(self._inv, rhs, out)
 
 
 def spd_inverse_(g, names=None):
@@ -112,11 +120,91 @@ def spd_inverse_(g, names=None):
     return g
 
 
+class PackedSymmetric:
+    """Symmetric float64 matrices (p % 128 == 0) stored as their lower 128 x 128
+    tiles (``wmg_sym_pack`` layout): half the bytes of the dense storage.  The
+    WMG leaf inverses live in this form; ``batched_gemv`` on it runs
+    ``wmg_packed_symv`` (every tile read once, fixed-order partial sums).
+    Indexing with a slice selects matrices (a view); ``dense()`` unpacks."""
+
+    def __init__(self, data, p: int):
+        self.data = data            # (batch, elems) float64, contiguous rows
+        self.p = int(p)
+
+    @classmethod
+    def pack(cls, full):
+        """Pack full symmetric (b, p, p) (or (p, p)) CUDA float64 matrices."""
+        import ctypes
+        import torch
+        from . import _native as N
+        f3 = full if full.dim() == 3 else full.unsqueeze(0)
+        b, p = f3.shape[0], f3.shape[-1]
+        elems = ctypes.c_longlong()
+        N.call("wmg_packed_sym_sizes", b, p, ctypes.byref(elems), None)
+        data = torch.empty((b, elems.value), dtype=torch.float64, device=full.device)
+        st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+        N.call("wmg_sym_pack", b, p, ctypes.c_void_p(f3.data_ptr()), p * p,
+               ctypes.c_void_p(data.data_ptr()), elems.value, st)
+        return cls(data, p)
+
+    @property
+    def shape(self):
+        return (self.data.shape[0], self.p, self.p)
+
+    def __len__(self):
+        return self.data.shape[0]
+
+    def __getitem__(self, idx):
+        if isinstance(idx, slice):
+            return PackedSymmetric(self.data[idx], self.p)
+        return PackedSymmetric(self.data[idx:idx + 1], self.p)
+
+    def dense(self):
+        """(b, p, p) full matrices (API / tests; not on the hot path)."""
+        import torch
+        T = 128
+        nt = self.p // T
+        b = self.data.shape[0]
+        tiles = self.data.view(b, -1, T, T)
+        out = torch.empty((b, self.p, self.p), dtype=torch.float64, device=self.data.device)
+        t = 0
+        for i in range(nt):
+            for j in range(i + 1):
+                blk = tiles[:, t]
+                out[:, i * T:(i + 1) * T, j * T:(j + 1) * T] = blk
+                if i != j:
+                    out[:, j * T:(j + 1) * T, i * T:(i + 1) * T] = blk.transpose(1, 2)
+                t += 1
+        return out
+
+    def gemv(self, x, out=None):
+        import ctypes
+        import torch
+        from . import _native as N
+        x2 = x if x.dim() == 2 else x.unsqueeze(0)
+        b, p = self.data.shape[0], self.p
+        if tuple(x2.shape) != (b, p):
+            raise DimensionMismatchError(f"packed symv: rhs {tuple(x.shape)} vs {self.shape}")
+        x2 = x2.contiguous()
+        y = torch.empty((b, p), dtype=torch.float64, device=x.device) if out is None else out
+        nbytes = ctypes.c_size_t()
+        N.call("wmg_packed_sym_sizes", b, p, None, ctypes.byref(nbytes))
+        scratch = torch.empty(nbytes.value // 8, dtype=torch.float64, device=x.device)
+        st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+        N.call("wmg_packed_symv", b, p, ctypes.c_void_p(self.data.data_ptr()),
+               self.data.stride(0), ctypes.c_void_p(x2.data_ptr()), p,
+               ctypes.c_void_p(y.data_ptr()), p, ctypes.c_void_p(scratch.data_ptr()), st)
+        return y if x.dim() == 2 else y.view(p)
+
+
 def batched_gemv(A, x, out=None):
-    """y_b = A_b x_b (A: (p,p) or (b,p,p) float64 CUDA, x: (p,) or (b,p))."""
+    """y_b = A_b x_b (A: (p,p) or (b,p,p) float64 CUDA, or PackedSymmetric;
+    x: (p,) or (b,p))."""
     import ctypes
     import torch
     from . import _native as N
+    if isinstance(A, PackedSymmetric):
+        return A.gemv(x, out)
     A3 = A if A.dim() == 3 else A.unsqueeze(0)
     x2 = x if x.dim() == 2 else x.unsqueeze(0)
     b, p = A3.shape[0], A3.shape[-1]
