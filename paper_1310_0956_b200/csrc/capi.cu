@@ -193,6 +193,40 @@ int wmg_geometry_create(int n, int n_detectors, int n_angles, const double* cos_
       halfv = lo;
     }
   }
+  // Transposition symmetry (theta -> pi/2 - theta, to 1e-12): every primary with
+  // |cos| > sin has its partners pi/2 -+ theta in the set, and each primary with
+  // |cos| < sin is the partner of exactly one mirror pair; pi/4 and 3pi/4 (their
+  // own transposes) stay four-image primaries.  Then the backprojector shares one
+  // weight evaluation among eight (pixel, angle) pairs.
+  std::vector<int> q8, l4;
+  bool tsym = sym;
+  if (tsym) {
+    std::vector<int> byc(prim);
+    std::sort(byc.begin(), byc.end(), [&](int x, int y) { return cos_h[x] < cos_h[y]; });
+    std::vector<int> cover((size_t)n_angles, 0);
+    for (int a : prim) {
+      const double c = cos_h[a], s = sin_h[a];
+      if (std::fabs(std::fabs(c) - s) <= 1e-12) { l4.push_back(a); continue; }
+      if (std::fabs(c) < s) continue;   // a partner of some |cos| > sin primary
+      auto it = std::lower_bound(byc.begin(), byc.end(), s - 1e-12,
+                                 [&](int x, double v) { return cos_h[x] < v; });
+      int ta = -1;
+      for (; it != byc.end() && cos_h[*it] <= s + 1e-12; ++it)
+        if (std::fabs(sin_h[*it] - std::fabs(c)) <= 1e-12) { ta = *it; break; }
+      if (ta < 0 || mir[(size_t)ta] < 0) { tsym = false; break; }
+      const int tb = mir[(size_t)ta];
+      ++cover[(size_t)ta];
+      ++cover[(size_t)tb];
+      if (c > 0.0) q8.insert(q8.end(), {a, ta, tb, 0});
+      else q8.insert(q8.end(), {a, tb, ta, 1});
+    }
+    for (size_t i = 0; tsym && i < prim.size(); ++i) {
+      const int a = prim[i];
+      const double c = std::fabs(cos_h[a]), s = sin_h[a];
+      if (c < s && std::fabs(c - s) > 1e-12 && cover[(size_t)a] != 2) tsym = false;
+    }
+    if (!tsym) { q8.clear(); l4.clear(); }
+  }
   // the TMA-staged forward (opt-in experiment) assumes the full equiangular layout
   bool std_layout = sym && n_angles % 2 == 0 && axis_idx.size() == 2 && axis_idx[0] == 0 &&
                     axis_idx[1] == n_angles / 2;
@@ -247,6 +281,8 @@ int wmg_geometry_create(int n, int n_detectors, int n_angles, const double* cos_
     tab.insert(tab.end(), halfv.begin(), halfv.end());
     tab.insert(tab.end(), axis_idx.begin(), axis_idx.end());
     tab.insert(tab.end(), gsafe.begin(), gsafe.end());
+    tab.insert(tab.end(), q8.begin(), q8.end());   // | q8 (4 n_q8) | l4 (n_l4)
+    tab.insert(tab.end(), l4.begin(), l4.end());
     e = cudaMalloc(&g->d_mir, sizeof(int) * tab.size());
     if (e == cudaSuccess)
       e = cudaMemcpy(g->d_mir, tab.data(), sizeof(int) * tab.size(), cudaMemcpyHostToDevice);
@@ -282,12 +318,22 @@ int wmg_geometry_create(int n, int n_detectors, int n_angles, const double* cos_
   g->dev.n_half = (int)halfv.size();
   g->dev.gsafe = sym ? g->d_mir + n_angles + prim.size() + halfv.size() + axis_idx.size()
                      : nullptr;
+  {
+    const size_t off_q8 = (size_t)n_angles + prim.size() + halfv.size() + axis_idx.size() +
+                          gsafe.size();
+    g->dev.tsym = (sym && tsym) ? 1 : 0;
+    g->dev.q8 = g->dev.tsym ? g->d_mir + off_q8 : nullptr;
+    g->dev.l4 = g->dev.tsym ? g->d_mir + off_q8 + q8.size() : nullptr;
+    g->dev.n_q8 = g->dev.tsym ? (int)(q8.size() / 4) : 0;
+    g->dev.n_l4 = g->dev.tsym ? (int)l4.size() : 0;
+  }
   g->sym_capable = sym ? 1 : 0;
   g->axis = g->dev;
   g->axis.m = n_axis;
   g->axis.ang = g->d_axis;
   g->axis.rowmap = sym ? g->d_mir + n_angles + prim.size() + halfv.size() : nullptr;
   g->axis.sym = 0;
+  g->axis.tsym = 0;
   g->axis.tma_ok = 0;
   g->axis.joseph = 0;
   *out = g;
@@ -308,9 +354,11 @@ int wmg_geometry_symmetry(wmg_geometry* g, int set, int* enabled) {
   // 0 off, 1 auto, 2 forced, 4 forced + TMA forward; testing variants of the
   // forced mode: +8 row-layout backprojector, +16 one-angle forward blocks,
   // +256 the 8x4-block float4-window backprojector, +512 / +1024 run layout with
-  // R = 4 / R = 8 rows per thread at any size
+  // R = 4 / R = 8 rows per thread at any size, +8192 / +16384 the eight-image
+  // backprojector forced at any size / disabled
   if (set == 0 || set == 1 || set == 2 || set == 4 || set == 10 || set == 18 || set == 26 || set == 34 || set == 66 || set == 130 ||
-      set == 258 || set == 514 || set == 1026)
+      set == 258 || set == 514 || set == 1026 || set == 8194 ||
+      set == 16386)
     g->dev.sym = (set && g->sym_capable) ? set : 0;
   if (enabled) *enabled = g->dev.sym;
   return WMG_OK;

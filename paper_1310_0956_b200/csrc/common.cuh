@@ -59,6 +59,15 @@ struct GeomDev {
   const int* half;
   const int* gsafe;   // per 4-angle group of half: 1 = forward needs no k clamp
   int n_prim, n_half;
+  // transposition symmetry (theta -> pi/2 - theta, sym != 0 and tsym != 0): the
+  // 8-image backprojector walks q8 (n_q8 entries of 4 ints: primary angle
+  // alpha with |cos| > sin, rows u1, u2 of the transposed images and a flag:
+  // 1 = their direct / reversed windows swap) and l4 (n_l4 self-transposed
+  // primaries, pi/4 and 3pi/4, taken with four images)
+  const int* q8;
+  const int* l4;
+  int n_q8, n_l4;
+  int tsym;
 };
 
 // Fixed-point minor coordinate used by the fast kernels: 64-bit signed with
@@ -68,5 +77,14 @@ constexpr double kFixScale = 1099511627776.0;  // 2^40
 // zero margin (pixels) around the padded image copies read by the fast
 // forward kernel: >= 31 * sqrt(2) + 2 so a warp can walk its union slab range
 constexpr int kPadMargin = 64;
+
+// linear index -> (I, J), I >= J, of the lower triangle in row order
+__device__ __forceinline__ void tri_unrank(int lin, int& I, int& J) {
+  int i = (int)((sqrtf(8.0f * (float)lin + 1.0f) - 1.0f) * 0.5f);
+  while ((i + 1) * (i + 2) / 2 <= lin) ++i;
+  while (i * (i + 1) / 2 > lin) --i;
+  I = i;
+  J = lin - i * (i + 1) / 2;
+}
 
 }  // namespace wmg

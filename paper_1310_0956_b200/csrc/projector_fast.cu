@@ -864,6 +864,249 @@ bwd_symrun_kernel(GeomDev G,
   }
 }
 
+// Eight-image backprojector (transposition-closed symmetric sets: with every
+// theta in (0, pi/4) also pi/2 - theta).  Pixel (x, y) at theta and the
+// transposed pixel (y, x) at pi/2 - theta share the detector coordinate and the
+// trapezoid (|cos|, |sin| swap), so one weight evaluation serves the four
+// mirror/rotation images of bwd_symrun and their four transposes.  The
+// primaries are the angles with |cos| > sin (q8; their transposed rows u1, u2
+// read through windows C, D); pi/4 and 3 pi/4 run with four images (l4).
+// A block owns the tile pair (tau, tau^T) of the top-left quadrant (32 x 32
+// tiles, lane = column, 4 consecutive rows per thread, the run-layout window
+// slide): phase 1 walks base tile tau, phase 2 base tau^T.  Each base adds its
+// mirror images to its own orbit and its transposed images to the other
+// tile's orbit; the two orbits are combined in shared memory (every element
+// has one writer per step) and each output pixel is written once -- no
+// atomics, deterministic.  Diagonal tiles (tau = tau^T) take phase 1 only.
+constexpr int kS8Win = 64;
+template <typename TIn, typename TOut, bool kAccumulate>
+__global__ void __launch_bounds__(256, 4) bwd_sym8_kernel(GeomDev G,
+                                                          const TIn* __restrict__ sino,
+                                                          TOut* __restrict__ img) {
+  constexpr int R = 4;
+  constexpr int OFF = kSymChunk * kS8Win;      // window stride (float2 entries)
+  __shared__ float2 win[4][kSymChunk][kS8Win]; // A (a, mir a), B reversed, C, D (u1, u2)
+  __shared__ long long qx[kSymChunk][kBwdTile];
+  __shared__ float4 wc_s[kSymChunk];
+  __shared__ float2 ls_s[kSymChunk];
+  __shared__ long long qhead[kSymChunk];
+  __shared__ int jlo_s[kSymChunk];
+  __shared__ int rows_s[kSymChunk][4];         // a, mir a, u1, u2 (sinogram rows)
+  __shared__ int rev_s[kSymChunk];
+  // orbit(tau), orbit(tau^T): [2][4][32][33] floats of dynamic shared memory
+  extern __shared__ float orb_dyn[];
+  float(*orb)[4][kBwdTile][kBwdTile + 1] =
+      reinterpret_cast<float(*)[4][kBwdTile][kBwdTile + 1]>(orb_dyn);
+  const int n = G.n, d = G.d;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  int ti, tj;
+  tri_unrank(blockIdx.x, ti, tj);
+  const bool diag = ti == tj;
+  const int trow = warp * R;
+  const double half = (double)n * 0.5, dc = (double)(d - 1) * 0.5;
+  const double bias = 1.0 / kQ32;
+  float2 accA[R], accB[R], accC[R], accD[R];
+
+  for (int phase = 0; phase < (diag ? 1 : 2); ++phase) {
+    __syncthreads();   // phase 0's orbit writes before phase 1 accumulates onto them
+    // base tile: rows R0.., cols C0..
+    const int R0 = (phase == 0 ? ti : tj) * kBwdTile, C0 = (phase == 0 ? tj : ti) * kBwdTile;
+    const double xc0 = (double)C0 - half + 0.5;
+    const double yc0 = half - (double)R0 - 0.5;
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      accA[i] = accB[i] = accC[i] = accD[i] = make_float2(0.0f, 0.0f);
+    }
+    // list 0: q8 (eight images), list 1: l4 (four images)
+    for (int list = 0; list < 2; ++list) {
+      const int cnt = list == 0 ? G.n_q8 : G.n_l4;
+      for (int c0 = 0; c0 < cnt; c0 += kSymChunk) {
+        const int na = min(kSymChunk, cnt - c0);
+        __syncthreads();
+        if (tid < na) {
+          int a, u1 = 0, u2 = 0, rv = 0;
+          if (list == 0) {
+            const int* e = G.q8 + 4 * (c0 + tid);
+            a = e[0]; u1 = e[1]; u2 = e[2]; rv = e[3];
+          } else {
+            a = G.l4[c0 + tid];
+          }
+          rows_s[tid][0] = a;
+          rows_s[tid][1] = G.mir[a];
+          rows_s[tid][2] = u1;
+          rows_s[tid][3] = u2;
+          rev_s[tid] = rv;
+          const AngleParams& A = G.ang[a];
+          const double p0 = xc0 * A.c + yc0 * A.s + dc - A.hw - bias;
+          const double pmin = p0 + fmin(0.0, (double)(kBwdTile - 1) * A.c) +
+                              fmin(0.0, -(double)(kBwdTile - 1) * A.s);
+          const int jlo = (int)floor(pmin) - 1;
+          jlo_s[tid] = jlo;
+          qhead[tid] = llrint((p0 - (double)jlo) * kQ32);
+          wc_s[tid] = make_float4(A.a0, A.icb, A.hwic, A.w1c);
+          ls_s[tid] = make_float2(A.Lf, __uint_as_float((unsigned)A.Sfix));
+        }
+        __syncthreads();
+        for (int e = tid; e < na * kBwdTile; e += 256) {
+          const int aa = e / kBwdTile, l = e % kBwdTile;
+          qx[aa][l] = qhead[aa] + (long long)l * G.ang[rows_s[aa][0]].Cfix;
+        }
+        const int nwin = list == 0 ? 4 : 2;
+        for (int e = tid; e < na * kS8Win; e += 256) {
+          const int aa = e / kS8Win, t = e % kS8Win;
+          const int j = jlo_s[aa] + t, jr = d - 1 - j;
+          auto ld = [&](int row, int jj) -> float {
+            return (jj >= 0 && jj < d) ? (float)__ldg(sino + (long long)row * d + jj) : 0.0f;
+          };
+          const int ra = rows_s[aa][0], rb = rows_s[aa][1];
+          win[0][aa][t] = make_float2(ld(ra, j), ld(rb, j));
+          win[1][aa][t] = make_float2(ld(ra, jr), ld(rb, jr));
+          if (nwin == 4) {
+            const int r1 = rows_s[aa][2], r2 = rows_s[aa][3];
+            const bool rv = rev_s[aa] != 0;
+            const float2 dir = make_float2(ld(r1, j), ld(r2, j));
+            const float2 rvs = make_float2(ld(r1, jr), ld(r2, jr));
+            win[2][aa][t] = rv ? rvs : dir;
+            win[3][aa][t] = rv ? dir : rvs;
+          }
+        }
+        __syncthreads();
+        for (int aa = 0; aa < na; ++aa) {
+          const float4 wc = wc_s[aa];
+          const float2 ls = ls_s[aa];
+          const float ca0 = wc.x, icb = wc.y, hwic = wc.z, w1c = wc.w, L = ls.x;
+          const unsigned Slo = __float_as_uint(ls.y);
+          const long long Q = qx[aa][lane] - (long long)trow * (long long)Slo;
+          unsigned lo = (unsigned)Q;
+          const float2* pw = &win[0][aa][hi32(Q) + 1];
+          float2 fa = pw[0], sa = pw[1], fb = pw[OFF], sb = pw[OFF + 1];
+          if (list == 0) {
+            float2 fc = pw[2 * OFF], sc = pw[2 * OFF + 1], fd = pw[3 * OFF], sd = pw[3 * OFF + 1];
+#pragma unroll
+            for (int i = 0; i < R; ++i) {
+              if (i > 0) {
+                const unsigned lo2 = lo - Slo;
+                const bool moved = lo2 > lo;
+                lo = lo2;
+                pw -= moved ? 1 : 0;
+                sa = moved ? fa : sa;
+                sb = moved ? fb : sb;
+                sc = moved ? fc : sc;
+                sd = moved ? fd : sd;
+                fa = pw[0];
+                fb = pw[OFF];
+                fc = pw[2 * OFF];
+                fd = pw[3 * OFF];
+              }
+              const float f = frac1(lo);
+              const float d0 = ca0 - f;
+              const float w0 = fminf(fmaf(-fabsf(d0), icb, hwic), L);
+              const float w1 = fmaxf(fmaf(f, icb, w1c), 0.0f);
+              const float2 W0 = make_float2(w0, w0), W1 = make_float2(w1, w1);
+              accA[i] = __ffma2_rn(W1, sa, __ffma2_rn(W0, fa, accA[i]));
+              accB[i] = __ffma2_rn(W1, sb, __ffma2_rn(W0, fb, accB[i]));
+              accC[i] = __ffma2_rn(W1, sc, __ffma2_rn(W0, fc, accC[i]));
+              accD[i] = __ffma2_rn(W1, sd, __ffma2_rn(W0, fd, accD[i]));
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < R; ++i) {
+              if (i > 0) {
+                const unsigned lo2 = lo - Slo;
+                const bool moved = lo2 > lo;
+                lo = lo2;
+                pw -= moved ? 1 : 0;
+                sa = moved ? fa : sa;
+                sb = moved ? fb : sb;
+                fa = pw[0];
+                fb = pw[OFF];
+              }
+              const float f = frac1(lo);
+              const float d0 = ca0 - f;
+              const float w0 = fminf(fmaf(-fabsf(d0), icb, hwic), L);
+              const float w1 = fmaxf(fmaf(f, icb, w1c), 0.0f);
+              const float2 W0 = make_float2(w0, w0), W1 = make_float2(w1, w1);
+              accA[i] = __ffma2_rn(W1, sa, __ffma2_rn(W0, fa, accA[i]));
+              accB[i] = __ffma2_rn(W1, sb, __ffma2_rn(W0, fb, accB[i]));
+            }
+          }
+        }
+      }
+    }
+    // orbit images, local (row, col) in the base tile: 0 (r, c), 1 (r, n-1-c),
+    // 2 (n-1-r, n-1-c), 3 (n-1-r, c).  The transposed images of base pixel
+    // (lr, lc) are the images {0: D.x, 1: D.y, 2: C.x, 3: C.y} of pixel (lc, lr)
+    // of the other tile.
+    float(*own)[kBwdTile][kBwdTile + 1] = orb[phase];
+    float(*oth)[kBwdTile][kBwdTile + 1] = orb[diag ? 0 : 1 - phase];
+    if (phase == 0) {
+#pragma unroll
+      for (int i = 0; i < R; ++i) {
+        own[0][trow + i][lane] = accA[i].x;
+        own[1][trow + i][lane] = accA[i].y;
+        own[2][trow + i][lane] = accB[i].x;
+        own[3][trow + i][lane] = accB[i].y;
+      }
+      if (!diag) {
+#pragma unroll
+        for (int i = 0; i < R; ++i) {
+          oth[0][lane][trow + i] = accD[i].x;
+          oth[1][lane][trow + i] = accD[i].y;
+          oth[2][lane][trow + i] = accC[i].x;
+          oth[3][lane][trow + i] = accC[i].y;
+        }
+      } else {
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < R; ++i) {
+          oth[0][lane][trow + i] += accD[i].x;
+          oth[1][lane][trow + i] += accD[i].y;
+          oth[2][lane][trow + i] += accC[i].x;
+          oth[3][lane][trow + i] += accC[i].y;
+        }
+      }
+    } else {
+      // own = orbit(tau^T) already holds phase 1's transposed images
+#pragma unroll
+      for (int i = 0; i < R; ++i) {
+        own[0][trow + i][lane] += accA[i].x;
+        own[1][trow + i][lane] += accA[i].y;
+        own[2][trow + i][lane] += accB[i].x;
+        own[3][trow + i][lane] += accB[i].y;
+        oth[0][lane][trow + i] += accD[i].x;
+        oth[1][lane][trow + i] += accD[i].y;
+        oth[2][lane][trow + i] += accC[i].x;
+        oth[3][lane][trow + i] += accC[i].y;
+      }
+    }
+  }
+  __syncthreads();
+  for (int t = 0; t < (diag ? 1 : 2); ++t) {
+    const int R0 = (t == 0 ? ti : tj) * kBwdTile, C0 = (t == 0 ? tj : ti) * kBwdTile;
+    const float(*o)[kBwdTile][kBwdTile + 1] = orb[t];
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const int lr = trow + i;
+      const int row = R0 + lr, col = C0 + lane;
+      const long long p1 = (long long)row * n + col;
+      const long long p2 = (long long)row * n + (n - 1 - col);
+      const long long p3 = (long long)(n - 1 - row) * n + (n - 1 - col);
+      const long long p4 = (long long)(n - 1 - row) * n + col;
+      if (kAccumulate) {
+        img[p1] = (TOut)((float)img[p1] + o[0][lr][lane]);
+        img[p2] = (TOut)((float)img[p2] + o[1][lr][lane]);
+        img[p3] = (TOut)((float)img[p3] + o[2][lr][lane]);
+        img[p4] = (TOut)((float)img[p4] + o[3][lr][lane]);
+      } else {
+        img[p1] = (TOut)o[0][lr][lane];
+        img[p2] = (TOut)o[1][lr][lane];
+        img[p3] = (TOut)o[2][lr][lane];
+        img[p4] = (TOut)o[3][lr][lane];
+      }
+    }
+  }
+}
+
 // Symmetric forward.  Rays (a, j), (m-a, j), (a, d-1-j), (m-a, d-1-j) see the
 // same weights on the slab-coordinate images (s, q), (s, n-1-q), (n-1-s, n-1-q),
 // (n-1-s, q) of one walk (x-mirror / 180-degree rotation of the grid), so one
@@ -1566,7 +1809,23 @@ static cudaError_t bwd_sym_impl(const GeomDev& G, const GeomDev& Gx, const void*
   dim3 grid(G.n / 64, G.n / 64);
   const bool rowlayout = (G.sym & 8) != 0;    // testing: the lane = column layout
   const bool blocks8x4 = (G.sym & 256) != 0;  // testing: 8x4 warp blocks, float4 windows
-  if (!rowlayout && !blocks8x4) {
+  const int qt = G.n / 64;                      // quadrant tiles per side
+  // eight images per weight where the tile pairs fill the SMs (sym & 8192:
+  // testing, at any size; sym & 16384: testing, the four-image run layout)
+  if (G.tsym && !rowlayout && !blocks8x4 && !(G.sym & (512 | 1024 | 16384)) &&
+      ((long long)qt * (qt + 1) / 2 >= 3LL * 148 || (G.sym & 8192))) {
+    const unsigned grid8 = (unsigned)(qt * (qt + 1) / 2);
+    constexpr int smem8 = 2 * 4 * fast::kBwdTile * (fast::kBwdTile + 1) * (int)sizeof(float);
+    static bool attr[2] = {false, false};   // per instantiation
+    auto k8 = accumulate ? fast::bwd_sym8_kernel<TIn, TOut, true>
+                         : fast::bwd_sym8_kernel<TIn, TOut, false>;
+    if (!attr[accumulate]) {
+      cudaError_t ea = cudaFuncSetAttribute(k8, cudaFuncAttributeMaxDynamicSharedMemorySize, smem8);
+      if (ea != cudaSuccess) return ea;
+      attr[accumulate] = true;
+    }
+    k8<<<grid8, 256, smem8, st>>>(G, (const TIn*)y, (TOut*)x);
+  } else if (!rowlayout && !blocks8x4) {
     // run layout: 64-row tiles (fewer window loads per pixel) when the quadrant
     // allows and the grid still fills the SMs (n >= ~3400), else 32-row tiles
     // (sym & 1024: testing, 64-row tiles at any size; sym & 512: 32-row tiles)

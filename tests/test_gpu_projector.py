@@ -141,14 +141,17 @@ def test_dimension_checks(gpu):
         apply_transpose(w, np.ones(7))
 
 
-@pytest.mark.parametrize("mode", ["force", "tma", "bwd8x4", "bwdrun32", "bwdrun64"])
+@pytest.mark.parametrize("mode", ["force", "tma", "bwd8x4", "bwdrun32", "bwdrun64", "bwdsym8",
+                                  "bwdrun"])
 @pytest.mark.parametrize("n,d,m", [(256, 363, 180), (512, 725, 512), (320, 453, 64)])
 def test_symmetric_fast_paths(gpu, oracle_proj, n, d, m, mode):
     """Full equiangular grids take the mirror-symmetric kernels: same result as
     the plain fast kernels (1e-6) and within 1e-5 of the float64 reference.
     Modes: the default kernels; the TMA forward; the backprojector's 8x4-block
     float4-window layout and its run layout with 4 / 8 rows per thread (the
-    64-row tiles are the n = 4096 default; n = 320 falls back to 32 rows)."""
+    64-row tiles are the n = 4096 default; n = 320 falls back to 32 rows); the
+    eight-image (transposition) backprojector forced at these sizes, and
+    disabled (m = 180, 512 and 64 are multiples of 4: transposition-closed)."""
     torch = gpu
     from paper_1310_0956_b200.geometry import build_geometry, build_projector
     g = build_geometry(n, d, m)

@@ -29,7 +29,7 @@ for n in [int(a) for a in sys.argv[1:]] or (1024, 2048, 4096):
     y = torch.rand(n * d, device="cuda")
     res = {}
     outs = {}
-    for mode in (True, "bwdrun32", "bwd8x4"):
+    for mode in (True, "bwdrun", "bwdsym8", "bwd8x4"):
         w.set_symmetry(mode)
         o = torch.empty(n * n, device="cuda")
         res[str(mode)] = ev_time(lambda: w.backward_(y, o))
