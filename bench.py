@@ -8,7 +8,8 @@ float32 data, x ~ U[0,1] seed 3000, y ~ U[0,1] seed 3001).  Default n = 4096
 than the 126 MB L2 together, so no explicit flush is needed; for n < 4096 an
 L2 flush is done between steps outside the timed events).
 
-Multi-GPU (torchrun, one process per GPU): the mirror pairs of angles {k, m-k}
+Multi-GPU (torchrun, one process per GPU): the quad units of angles
+{k, m-k, m/2-k, m/2+k} (mirror pairs when m % 4 != 0)
 are dealt round-robin to the ranks (each shard keeps the symmetric kernels),
 each rank projects its angles and backprojects its sinogram rows, and the
 partial A^T y images are summed with an NCCL allreduce -- total work fixed
@@ -74,7 +75,7 @@ def workload(n):
 
 def config_dict(n, d, m, world, extra=None):
     c = {"workload": f"config3_pair_n{n}", "n": n, "n_angles": m, "n_detectors": d,
-         "dtype_data": "float32", "geometry": "fixed-point64", "angle_sharding": "mirror pairs",
+         "dtype_data": "float32", "geometry": "fixed-point64", "angle_sharding": "quad units",
          "parallelism": f"angles{world}", "l2": ("inputs larger than L2" if n >= 4096
                                                   else "L2 flushed between steps")}
     if extra:
@@ -259,7 +260,7 @@ def run_wmg_cgls(dev, reps=3, world=1):
     Setup (hierarchy) and solve are timed separately (device-synchronised wall
     clock, max over ranks); the plain-CGLS solve and the reference's
     smoother-free cycle are reported beside it.  Under torchrun every rank owns
-    a mirror shard of the angles (sharded pairs, allreduced leaf Grams)."""
+    a quad shard of the angles (sharded pairs, allreduced leaf Grams)."""
     import torch
     import torch.distributed as dist
     from paper_1310_0956_b200 import (SolverConfig, add_gaussian_noise, build_geometry,
@@ -318,7 +319,7 @@ def run_wmg_cgls(dev, reps=3, world=1):
             "levels": 3, "nu_pre": 2, "nu_post": 2, "lambda": 0.0,
             "projector": "float64 fast (<=1e-12 of the reference W); sparse leaf Grams "
                          "(<=1e-12 of the exact P_L^T P_L)",
-            "angle_sharding": "mirror pairs" if world > 1 else None,
+            "angle_sharding": "quad units" if world > 1 else None,
             "cgls_seconds": min(t_cgls), "cgls_iterations": rec_c.iterations[-1],
             "nu0": nu0, "b": b, "x_ex": x_ex,
             "timing": "torch.cuda.synchronize + perf_counter, max over ranks, best of %d; "
@@ -559,7 +560,7 @@ def _max_over_ranks(values, dev):
 
 
 def _projector(g, world, dev, **kw):
-    """Full projector at N = 1, this rank's mirror angle shard at N > 1."""
+    """Full projector at N = 1, this rank's quad angle shard at N > 1."""
     from paper_1310_0956_b200 import build_projector
     from paper_1310_0956_b200.sharding import AngleShardedProjector
     if world > 1:
@@ -579,7 +580,7 @@ def run_config2(args):
     U[0,1]); Poisson data, I0 = 1e5, mu = 2/n, log transform (seed 2500).
     Unpreconditioned CGLS vs WMG-preconditioned GMRES on the normal equations
     (levels = 5, reference smoother-free cycle), each to normal-equations
-    residual 1e-4.  Under torchrun the angles are sharded (mirror pairs per
+    residual 1e-4.  Under torchrun the angles are sharded (quad units per
     rank, NCCL allreduce of W^T y and of the leaf Grams); times are max over
     ranks.  ``--n`` rescales the grid (detectors = ceil(n sqrt 2), angles =
     720 n / 1024) for quick checks."""
@@ -602,7 +603,7 @@ def run_config2(args):
     bd = _local_rows(w32, b, dev)
     out = {"metric": "config2 seconds to rel. residual 1e-4", "n": n, "n_angles": m,
            "n_detectors": d, "n_gpus": world, "projector": "float32 arithmetic, float64 "
-           "Krylov vectors", "angle_sharding": "mirror pairs" if world > 1 else None,
+           "Krylov vectors", "angle_sharding": "quad units" if world > 1 else None,
            "data": "synthetic: 50-ellipse phantom, Poisson I0=1e5, mu=2/n",
            "timing": "torch.cuda.synchronize + perf_counter, max over ranks"}
     cgls_solve(w32, bd, cfg=SolverConfig(max_iterations=2))          # warm-up

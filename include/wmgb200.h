@@ -94,6 +94,10 @@ int wmg_geometry_shape(const wmg_geometry *g, long long *n_rows, long long *n_co
  * size (testing), 4 forces it with the experimental TMA-staged forward, -1 only
  * queries; *enabled receives the state. */
 int wmg_geometry_symmetry(wmg_geometry *g, int set, int *enabled);
+
+/* *closed = 1 when the angle set is also closed under theta -> pi/2 - theta
+ * (the eight-image backprojector applies), else 0 */
+int wmg_geometry_transposition(const wmg_geometry *g, int *closed);
 /* Ray kernel of the geometry's system matrix: set = WMG_KERNEL_LINE or
  * WMG_KERNEL_JOSEPH (build_projector(g, kernel=...), geometry.py:178-185), -1
  * only queries.  Joseph geometries support the PARITY projector pair, CSR

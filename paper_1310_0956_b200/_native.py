@@ -39,6 +39,7 @@ _SIGS = {
     "wmg_geometry_destroy": (_i, [_vp]),
     "wmg_geometry_shape": (_i, [_vp, ctypes.POINTER(_ll), ctypes.POINTER(_ll)]),
     "wmg_geometry_symmetry": (_i, [_vp, _i, ctypes.POINTER(_i)]),
+    "wmg_geometry_transposition": (_i, [_vp, ctypes.POINTER(_i)]),
     "wmg_geometry_kernel": (_i, [_vp, _i, ctypes.POINTER(_i)]),
     "wmg_forward_workspace": (_i, [_vp, _i, _i, ctypes.POINTER(ctypes.c_size_t)]),
     "wmg_forward": (_i, [_vp, _i, _i, _i, _i, _dp, _dp, _dp, _dp, _vp]),

@@ -364,6 +364,12 @@ int wmg_geometry_symmetry(wmg_geometry* g, int set, int* enabled) {
   return WMG_OK;
 }
 
+int wmg_geometry_transposition(const wmg_geometry* g, int* closed) {
+  if (!g || !closed) return fail(WMG_EINVAL, "NULL argument");
+  *closed = g->dev.tsym;
+  return WMG_OK;
+}
+
 int wmg_geometry_kernel(wmg_geometry* g, int set, int* kernel) {
   if (!g) return fail(WMG_EINVAL, "geometry is NULL");
   if (set == WMG_KERNEL_LINE || set == WMG_KERNEL_JOSEPH) {

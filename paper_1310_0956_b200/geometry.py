@@ -187,6 +187,14 @@ class LineProjector:
         N.call("wmg_geometry_symmetry", self._h, -1, N.ctypes.byref(st))
         return bool(st.value)
 
+    @property
+    def transposition_closed(self) -> bool:
+        """Whether the angle set is also closed under theta -> pi/2 - theta (the
+        backprojector then shares each weight among eight pixel/angle pairs)."""
+        st = N.ctypes.c_int()
+        N.call("wmg_geometry_transposition", self._h, N.ctypes.byref(st))
+        return bool(st.value)
+
     def set_symmetry(self, enable) -> bool:
         """Enable (True: where profitable), force ("force": at every size; "tma":
         forced with the experimental TMA-staged forward) or disable (False) the

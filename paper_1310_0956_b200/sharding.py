@@ -28,11 +28,26 @@ def shard_angles(n_angles: int, world: int, rank: int, scheme: str = "round_robi
     "mirror": the units {k, m - k} (mirror pairs theta, pi - theta of an
     equiangular set) and {0, m/2} (the axis angles) are dealt round-robin, so
     every shard is closed under the mirror and keeps the symmetric kernels
-    (4 pixel/ray images per weight evaluation); units have equal work."""
+    (4 pixel/ray images per weight evaluation); units have equal work.
+    "quad" (default of AngleShardedProjector): mirror-and-transposition
+    closed units of four angles, see below."""
     if world < 1 or not 0 <= rank < world:
         raise ValueError("bad world/rank")
     if scheme == "round_robin":
         return np.arange(rank, n_angles, world)
+    if scheme == "quad":
+        # units {k, m-k, m/2-k, m/2+k} (theta, pi - theta, pi/2 -+ theta), the
+        # diagonal pair {m/4, 3m/4} and the axis pair {0, m/2}, dealt
+        # round-robin: every shard is closed under the mirror AND the
+        # transposition, so ranks keep the eight-image backprojector; equal work
+        # per quad.  Needs m % 4 == 0 (else the mirror scheme).
+        m = n_angles
+        if m % 4 or m < 4:
+            return shard_angles(n_angles, world, rank, "mirror")
+        units = [[0, m // 2], [m // 4, 3 * m // 4]]
+        units += [[k, m - k, m // 2 - k, m // 2 + k] for k in range(1, m // 4)]
+        mine = [a for u in units[rank::world] for a in u]
+        return np.array(sorted(mine), dtype=np.int64)
     if scheme == "mirror":
         m = n_angles
         units = [[0] + ([m // 2] if m % 2 == 0 and m > 1 else [])]
@@ -63,7 +78,7 @@ class AngleShardedProjector:
     """W restricted to this rank's angles, with a summed backprojection."""
 
     def __init__(self, g, group=None, precision: str = "float32", mode=None,
-                 scheme: str = "mirror", local=None, device=None):
+                 scheme: str = "quad", local=None, device=None):
         import torch.distributed as dist
         self.dist = dist
         self.group = group

@@ -37,7 +37,7 @@ def test_bench_pair_and_wmg_two_ranks(gpu):
     d = _torchrun(["--gpus", "2", "--steps", "2", "--warmup", "3", "--grid", "512",
                    "--no-cpu-baseline"])
     assert d["n_gpus"] == 2 and d["value"] > 0 and d["e2e"]["value"] > 0
-    assert d["config"]["angle_sharding"] == "mirror pairs"
+    assert d["config"]["angle_sharding"] == "quad units"
     w = d["wmg_cgls"]
     assert w["n_gpus"] == 2 and w["status"] == "converged" and w["iterations"] == 15
 

@@ -254,6 +254,36 @@ def test_symmetric_kernels_on_mirror_shards(gpu, oracle_proj, n, d, m, world):
             assert np.linalg.norm(f64 - ref_f) <= 1e-12 * np.linalg.norm(ref_f), rank
 
 
+@pytest.mark.parametrize("n,d,m,world", [(256, 363, 180, 2), (256, 363, 180, 8),
+                                         (512, 725, 512, 4), (1024, 1449, 720, 8)])
+def test_eight_image_backprojector_on_quad_shards(gpu, oracle_proj, n, d, m, world):
+    """Shards of the "quad" scheme are mirror- and transposition-closed: the
+    eight-image backprojector (forced) stays within 1e-5 of the float64
+    reference rows of the shard's angles, like the four-image run layout."""
+    torch = gpu
+    from paper_1310_0956_b200.geometry import build_geometry, build_projector
+    from paper_1310_0956_b200.sharding import shard_angles
+    g = build_geometry(n, d, m)
+    rs = np.random.default_rng(7 * n + world)
+    for rank in range(world):
+        idx = shard_angles(m, world, rank, "quad")
+        sub = g.subset(idx)
+        w = build_projector(sub, precision="float32")
+        assert w.symmetric and w.transposition_closed
+        y = rs.uniform(0.0, 1.0, idx.size * d)
+        yd = torch.from_numpy(y.astype(np.float32)).cuda()
+        ref_b = oracle_proj.backward(n, d, sub.angles, y)
+        for mode in ("bwdsym8", "bwdrun"):
+            assert w.set_symmetry(mode)
+            got = w.backward(yd).double().cpu().numpy()
+            assert np.linalg.norm(got - ref_b) <= 1e-5 * np.linalg.norm(ref_b), (rank, mode)
+    # a mirror shard need not be transposition-closed (m = 180, 4 ranks: rank 0
+    # holds theta_4 but not theta_86 = pi/2 - theta_4); then the run layout runs
+    if m == 180:
+        wm = build_projector(g.subset(shard_angles(m, 4, 0, "mirror")), precision="float32")
+        assert wm.symmetric and not wm.transposition_closed
+
+
 @pytest.mark.parametrize("n,d,m", [(1, 1, 1), (2, 3, 2), (3, 5, 3), (17, 9, 7), (64, 91, 8),
                                    (64, 30, 2), (100, 147, 12), (128, 181, 4), (128, 50, 16)])
 @pytest.mark.parametrize("precision", ["float32", "float64"])

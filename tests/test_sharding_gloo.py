@@ -52,6 +52,34 @@ def test_mirror_shards_closed_and_balanced(m):
             assert loads.max() / loads.mean() < 1.02
 
 
+@pytest.mark.parametrize("m", [180, 720, 4096, 8, 4, 90, 7])
+def test_quad_shards_closed_and_balanced(m):
+    """The "quad" scheme (AngleShardedProjector's default) partitions the
+    angles into shards closed under the mirror k -> m - k AND the transposition
+    theta -> pi/2 -+ theta (k -> m/2 - k, or 3m/2 - k past pi/2), so ranks keep
+    the eight-image backprojector; m % 4 != 0 falls back to the mirror scheme."""
+    a = np.arange(m) * (np.pi / m)
+    w = angle_weights(a)
+    for world in (1, 2, 3, 4, 8):
+        sh = [shard_angles(m, world, r, "quad") for r in range(world)]
+        assert np.array_equal(np.sort(np.concatenate(sh)), np.arange(m))
+        if m % 4:
+            assert all(np.array_equal(x, shard_angles(m, world, r, "mirror"))
+                       for r, x in enumerate(sh))
+            continue
+        for ix in sh:
+            s = set(ix.tolist())
+            assert all((m - k) in s for k in s if k != 0 and 2 * k != m)
+            for k in s:
+                if k in (0, m // 2):
+                    continue
+                t = m // 2 - k if k < m // 2 else 3 * m // 2 - k
+                assert t in s, (m, world, k)
+        if m >= 180 * world:
+            loads = np.array([w[ix].sum() for ix in sh])
+            assert loads.max() / loads.mean() < 1.03
+
+
 class _CpuLocal:
     """CPU stand-in for a rank-local LineProjector (oracle CSR of its angles)."""
 
