@@ -66,6 +66,26 @@ def to_caller(tensor, was_numpy):
     return tensor
 
 
+def capture_graph(fn, device):
+    """Capture fn() into a new CUDA graph on a side stream (private memory pool)
+    and return (graph, fn's result).  Unlike ``torch.cuda.graph`` this does not
+    empty the caching allocator first: a capture right after a hierarchy build
+    would otherwise pay ~10 ms of cudaFree for the released setup buffers."""
+    t = torch()
+    cur = t.cuda.current_stream(device)
+    side = t.cuda.Stream(device=device)
+    side.wait_stream(cur)
+    g = t.cuda.CUDAGraph()
+    with t.cuda.stream(side):
+        g.capture_begin()
+        try:
+            out = fn()
+        finally:
+            g.capture_end()
+    cur.wait_stream(side)
+    return g, out
+
+
 def scratch(n: int, K: int, device):
     """Cached device scratch for wmg_det_reduce (+ K result slots)."""
     t = torch()

@@ -702,13 +702,7 @@ class _GraphedOperator:
                 return out
             self._gin = t.empty_like(v)
             self._gin.copy_(v)
-            side = t.cuda.Stream(device=v.device)
-            side.wait_stream(t.cuda.current_stream(v.device))
-            with t.cuda.stream(side):
-                g = t.cuda.CUDAGraph()
-                with t.cuda.graph(g, stream=side):
-                    self._gout = self._eager(self._gin)
-            t.cuda.current_stream(v.device).wait_stream(side)
+            g, self._gout = D.capture_graph(lambda: self._eager(self._gin), v.device)
             self._graph = g
         self._gin.copy_(v)
         self._graph.replay()

@@ -398,15 +398,7 @@ class _GraphedLoop:
             self.body()
             return
         if self.graph is None:
-            dev = t.cuda.current_device()
-            side = t.cuda.Stream(device=dev)
-            side.wait_stream(t.cuda.current_stream(dev))
-            with t.cuda.stream(side):
-                g = t.cuda.CUDAGraph()
-                with t.cuda.graph(g, stream=side):
-                    self.body()
-            t.cuda.current_stream(dev).wait_stream(side)
-            self.graph = g
+            self.graph, _ = D.capture_graph(self.body, t.cuda.current_device())
         self.graph.replay()
 
 
