@@ -252,15 +252,26 @@ __device__ __forceinline__ void lower_tile(int lin, int& I, int& J) {
 
 // Trailing update of every lower tile (I, J) off the pivot strip, in two
 // 128 x 64 halves (blockIdx.x = 2 * tile + half): A_IJ += Uneg_I P_J^T.
+// mode 0: every lower tile off the pivot strip k; mode 1 (look-ahead): only the
+// strip c = k + 1 (the next pivot's row and column, blockIdx.x over its nt
+// tiles); mode 2: every tile off the strips k and c.
 __global__ void __launch_bounds__(256, 2) sweep_update_kernel(int p, double* __restrict__ G,
                                                               long long sG,
                                                               const double* __restrict__ work,
-                                                              long long sW, int k) {
+                                                              long long sW, int k, int c,
+                                                              int mode) {
   extern __shared__ double smem[];
   constexpr int MI = UPD_NC / 16, CW = UPD_NC / 32;
   int I, J;
-  lower_tile(blockIdx.x >> 1, I, J);
+  if (mode == 1) {
+    const int t = blockIdx.x >> 1;
+    I = t <= c ? c : t;
+    J = t <= c ? t : c;
+  } else {
+    lower_tile(blockIdx.x >> 1, I, J);
+  }
   if (I == k || J == k) return;
+  if (mode == 2 && (I == c || J == c)) return;
   const int half = blockIdx.x & 1;
   const int leaf = blockIdx.y;
   double* Cb = G + leaf * sG + (long long)I * T * p + (long long)J * T + half * UPD_NC;
@@ -420,9 +431,40 @@ __global__ void __launch_bounds__(T) sym_reduce_kernel(int p, const double* __re
 
 }  // namespace spd
 
+// two buffer sets (pivot steps alternate): the look-ahead forms step k+1's
+// panel while step k's trailing update still reads step k's
 size_t spd_inverse_workspace(int batch, int p) {
-  return (size_t)batch * ((size_t)spd::T * spd::T + 2ull * (size_t)p * spd::T) * sizeof(double);
+  return 2ull * (size_t)batch * ((size_t)spd::T * spd::T + 2ull * (size_t)p * spd::T) *
+         sizeof(double);
 }
+
+namespace {
+// per-device auxiliary stream + fork/join events of the look-ahead (created once)
+struct AuxStreams {
+  cudaStream_t s = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+cudaError_t aux_for_device(AuxStreams*& out) {
+  static AuxStreams aux[64];
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+  AuxStreams& a = aux[dev];
+  if (!a.s) {
+    int lo = 0, hi = 0;
+    if ((e = cudaDeviceGetStreamPriorityRange(&lo, &hi)) != cudaSuccess) return e;
+    // high priority: the pivot sweep and panel (on the critical path) get SMs
+    // as soon as trailing-update CTAs retire
+    if ((e = cudaStreamCreateWithPriority(&a.s, cudaStreamNonBlocking, hi)) != cudaSuccess)
+      return e;
+    if ((e = cudaEventCreateWithFlags(&a.fork, cudaEventDisableTiming)) != cudaSuccess) return e;
+    if ((e = cudaEventCreateWithFlags(&a.join, cudaEventDisableTiming)) != cudaSuccess) return e;
+  }
+  out = &a;
+  return cudaSuccess;
+}
+}  // namespace
 
 cudaError_t spd_inverse(int batch, int p, double* G, long long sG, int* info, double* work,
                         cudaStream_t st) {
@@ -450,12 +492,37 @@ cudaError_t spd_inverse(int batch, int p, double* G, long long sG, int* info, do
   if ((e = cudaMemsetAsync(info, 0, sizeof(int) * (size_t)batch, st)) != cudaSuccess) return e;
   const int nt = p / T;
   const int ntri = nt * (nt + 1) / 2;
-  const long long sW = (long long)T * T + 2LL * p * T;
-  for (int k = 0; k < nt; ++k) {
-    sweep_diag_kernel<<<batch, 512, TILE_SMEM, st>>>(p, G, sG, work, sW, k, info);
-    if (nt > 1) {
-      sweep_panel_kernel<<<dim3(nt, batch), 256, GEMM_SMEM, st>>>(p, G, sG, work, sW, k);
-      sweep_update_kernel<<<dim3(2 * ntri, batch), 256, UPD_SMEM, st>>>(p, G, sG, work, sW, k);
+  const long long sW1 = (long long)T * T + 2LL * p * T;   // one buffer set per leaf
+  const long long sW = 2 * sW1;                          // leaf stride (two sets)
+  auto buf = [&](int k) { return work + (k & 1) * sW1; };
+  AuxStreams* aux = nullptr;
+  if (nt > 2 && (e = aux_for_device(aux)) != cudaSuccess) return e;
+  // step 0's pivot sweep and panel
+  sweep_diag_kernel<<<batch, 512, TILE_SMEM, st>>>(p, G, sG, buf(0), sW, 0, info);
+  if (nt > 1)
+    sweep_panel_kernel<<<dim3(nt, batch), 256, GEMM_SMEM, st>>>(p, G, sG, buf(0), sW, 0);
+  for (int k = 0; k < nt && nt > 1; ++k) {
+    const int c = k + 1;
+    if (c < nt && aux) {
+      // look-ahead: update strip c first, then form pivot c's sweep and panel on
+      // the auxiliary stream while the rest of step k's update runs
+      sweep_update_kernel<<<dim3(2 * nt, batch), 256, UPD_SMEM, st>>>(p, G, sG, buf(k), sW, k,
+                                                                       c, 1);
+      if ((e = cudaEventRecord(aux->fork, st)) != cudaSuccess) return e;
+      if ((e = cudaStreamWaitEvent(aux->s, aux->fork, 0)) != cudaSuccess) return e;
+      sweep_diag_kernel<<<batch, 512, TILE_SMEM, aux->s>>>(p, G, sG, buf(c), sW, c, info);
+      sweep_panel_kernel<<<dim3(nt, batch), 256, GEMM_SMEM, aux->s>>>(p, G, sG, buf(c), sW, c);
+      if ((e = cudaEventRecord(aux->join, aux->s)) != cudaSuccess) return e;
+      sweep_update_kernel<<<dim3(2 * ntri, batch), 256, UPD_SMEM, st>>>(p, G, sG, buf(k), sW, k,
+                                                                        c, 2);
+      if ((e = cudaStreamWaitEvent(st, aux->join, 0)) != cudaSuccess) return e;
+    } else {
+      sweep_update_kernel<<<dim3(2 * ntri, batch), 256, UPD_SMEM, st>>>(p, G, sG, buf(k), sW, k,
+                                                                        -1, 0);
+      if (c < nt) {
+        sweep_diag_kernel<<<batch, 512, TILE_SMEM, st>>>(p, G, sG, buf(c), sW, c, info);
+        sweep_panel_kernel<<<dim3(nt, batch), 256, GEMM_SMEM, st>>>(p, G, sG, buf(c), sW, c);
+      }
     }
   }
   sweep_finish_kernel<<<dim3(ntri, batch), 256, TILE_SMEM, st>>>(p, G, sG);
