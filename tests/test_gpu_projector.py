@@ -284,6 +284,29 @@ def test_eight_image_backprojector_on_quad_shards(gpu, oracle_proj, n, d, m, wor
         assert wm.symmetric and not wm.transposition_closed
 
 
+@pytest.mark.parametrize("mode", ["bwdsym8", "bwdrun", "bwdrun64"])
+def test_fp32_backprojector_float64_vectors_and_accumulate(gpu, oracle_proj, mode):
+    """fp32 arithmetic on float64 vectors (configs 2 and 4: float64 Krylov
+    vectors) and x += W^T y, through each symmetric backprojector layout."""
+    torch = gpu
+    from paper_1310_0956_b200.geometry import build_geometry, build_projector
+    n, d, m = 256, 363, 180
+    g = build_geometry(n, d, m)
+    w = build_projector(g, precision="float32")
+    assert w.set_symmetry(mode)
+    rs = np.random.default_rng(17)
+    y = rs.uniform(-1.0, 1.0, m * d)
+    x0 = rs.uniform(-1.0, 1.0, n * n)
+    ref = oracle_proj.backward(n, d, g.angles, y)
+    yd = torch.from_numpy(y).cuda()
+    out = torch.empty(n * n, dtype=torch.float64, device="cuda")
+    w.backward_(yd, out)
+    assert np.linalg.norm(out.cpu().numpy() - ref) <= 1e-5 * np.linalg.norm(ref)
+    acc = torch.from_numpy(x0).cuda()
+    w.backward_(yd, acc, accumulate=True)
+    assert np.linalg.norm(acc.cpu().numpy() - (x0 + ref)) <= 1e-5 * np.linalg.norm(x0 + ref)
+
+
 @pytest.mark.parametrize("n,d,m", [(1, 1, 1), (2, 3, 2), (3, 5, 3), (17, 9, 7), (64, 91, 8),
                                    (64, 30, 2), (100, 147, 12), (128, 181, 4), (128, 50, 16)])
 @pytest.mark.parametrize("precision", ["float32", "float64"])
