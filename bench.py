@@ -20,6 +20,14 @@ rel. residual 1e-4, setup separate, plain CGLS beside it), the end-to-end
 number with host buffers (``e2e``), the CPU baselines and the rooflines;
 ``--workload config2|config4`` runs the other BASELINE configurations.
 
+``value`` times the two products back to back on one stream (kernel times
+reported separately).  ``e2e`` is what a user streaming pairs through the
+public API sees: every step copies x and y from pinned host memory and both
+results back, with copies on their own streams (double-buffered, overlapping
+the kernels) and the two independent products on two streams, so the
+forward (bound by the L1 data pipe) and the backprojection (more ALU / issue
+bound) share the SMs -- which is why ``e2e`` can exceed ``value``.
+
 Prints ONE JSON line (rank 0).  ``--impl reference`` times the reference
 algorithm on the host CPU instead (the pinned C oracle: the reference's CSR
 built exactly, then CSR SpMV pairs with all host threads, on a bounded angle
@@ -434,38 +442,85 @@ def run_ours(args):
     out_s = torch.empty(M_loc, dtype=torch.float32).pin_memory()
     out_i = torch.empty(Npix, dtype=torch.float32).pin_memory()
 
-    e2e_s = torch.empty(M_loc, dtype=torch.float32, device=dev)
-    e2e_i = torch.empty(Npix, dtype=torch.float32, device=dev)
-
-    # The pair's two products are independent: like any user pipelining them,
-    # run H2D x -> W x -> D2H on one stream and H2D y -> W^T y -> D2H on a
-    # second, so each direction's copies overlap the other's kernel.
+    # Pipelined like a user streaming many pairs: H2D copies of step i+1 and
+    # D2H copies of step i overlap the kernels (copy engines on their own
+    # streams, device buffers double-buffered); the forwards stay on one
+    # stream and the backprojections on another (each direction reuses its
+    # projector workspace), and the two directions overlap each other.
+    e2e_s = [torch.empty(M_loc, dtype=torch.float32, device=dev) for _ in range(2)]
+    e2e_i = [torch.empty(Npix, dtype=torch.float32, device=dev) for _ in range(2)]
+    xd_b = [torch.empty(Npix, dtype=torch.float32, device=dev) for _ in range(2)]
+    yd_b = [torch.empty(M_loc, dtype=torch.float32, device=dev) for _ in range(2)]
+    out_s2 = [out_s, torch.empty(M_loc, dtype=torch.float32).pin_memory()]
+    out_i2 = [out_i, torch.empty(Npix, dtype=torch.float32).pin_memory()]
     s_fwd = torch.cuda.Stream(device=dev)
     s_bwd = torch.cuda.Stream(device=dev)
+    c_in = torch.cuda.Stream(device=dev)
+    c_out = torch.cuda.Stream(device=dev)
+    ev = {}
+
+    def mark(name, i, st):
+        e = torch.cuda.Event()
+        e.record(st)
+        ev[(name, i)] = e
+
+    def wait(st, name, i):
+        e = ev.get((name, i))
+        if e is not None:
+            st.wait_event(e)
+
+    step_no = [0]
 
     def e2e_step():
-        s_fwd.wait_stream(stream)
-        s_bwd.wait_stream(stream)
+        i = step_no[0]
+        step_no[0] += 1
+        b = i & 1
+        # inputs: the buffers of step i-2 must have been consumed
+        wait(c_in, "fwd", i - 2)
+        wait(c_in, "bwd", i - 2)
+        with torch.cuda.stream(c_in):
+            xd_b[b].copy_(pin_x, non_blocking=True)
+            mark("x", i, c_in)
+            yd_b[b].copy_(pin_y, non_blocking=True)
+            mark("y", i, c_in)
+        # kernels: outputs of step i-2 must have been copied out
+        wait(s_fwd, "x", i)
+        wait(s_fwd, "out_s", i - 2)
         with torch.cuda.stream(s_fwd):
-            xd = pin_x.to(dev, non_blocking=True)
-            w.forward_(xd, e2e_s)
-            out_s.copy_(e2e_s, non_blocking=True)
+            w.forward_(xd_b[b], e2e_s[b])
+        mark("fwd", i, s_fwd)
+        wait(s_bwd, "y", i)
+        wait(s_bwd, "out_i", i - 2)
         with torch.cuda.stream(s_bwd):
-            yd = pin_y.to(dev, non_blocking=True)
-            w.backward_(yd, e2e_i)
-            out_i.copy_(e2e_i, non_blocking=True)
-        stream.wait_stream(s_fwd)
-        stream.wait_stream(s_bwd)
+            w.backward_(yd_b[b], e2e_i[b])
+        mark("bwd", i, s_bwd)
+        wait(c_out, "fwd", i)
+        with torch.cuda.stream(c_out):
+            out_s2[b].copy_(e2e_s[b], non_blocking=True)
+        mark("out_s", i, c_out)
+        wait(c_out, "bwd", i)
+        with torch.cuda.stream(c_out):
+            out_i2[b].copy_(e2e_i[b], non_blocking=True)
+        mark("out_i", i, c_out)
+
+    def e2e_drain():
+        stream.wait_stream(c_out)
 
     e2e_step()
+    e2e_drain()
     torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
     s0 = torch.cuda.Event(enable_timing=True)
     s1 = torch.cuda.Event(enable_timing=True)
     s0.record(stream)
+    for st_ in (c_in, c_out, s_fwd, s_bwd):
+        st_.wait_stream(stream)
     for _ in range(args.steps):
         e2e_step()
+    e2e_drain()
+    stream.wait_stream(s_fwd)
+    stream.wait_stream(s_bwd)
     s1.record(stream)
     torch.cuda.synchronize(dev)
     te = torch.tensor([s0.elapsed_time(s1) / 1e3], dtype=torch.float64, device=dev)
