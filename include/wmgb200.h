@@ -199,6 +199,18 @@ int wmg_haar_prolong(int side, const double *coarse, int band, double *fine, int
 int wmg_batched_gemv(int batch, int p, const double *A, long long strideA, const double *x,
                      long long stridex, double *y, long long stridey, void *stream);
 
+/* Band-path Haar operators of a batch of WMG nodes (bands: host int[batch *
+ * depth], item i's bands of levels 0..depth-1, level 0 = the finest, codes
+ * LL 0, LH 1, HL 2, HH 3): fine_i (n x n) = R_path_i^T coarse_i and coarse_i =
+ * R_path_i fine_i ((n >> depth)^2 each; items contiguous).  The per-level
+ * wmg_haar_prolong / wmg_haar_restrict fused into one launch, bit-identical to
+ * applying them level by level (the reference's Kronecker products,
+ * multilevel.py:36-79, along the node's path). */
+int wmg_haar_prolong_path(int n, int depth, int batch, const int *bands, const double *coarse,
+                          double *fine, void *stream);
+int wmg_haar_restrict_path(int n, int depth, int batch, const int *bands, const double *fine,
+                           double *coarse, void *stream);
+
 /* WMG leaf factor rows P_L[ray0 : ray0 + nrays, :] (row-major, caller zeroes P)
  * for the leaf reached by bands[0..depth) from the root. */
 int wmg_leaf_factor(const wmg_geometry *g, int depth, const int *bands, long long ray0,

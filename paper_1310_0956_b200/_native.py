@@ -72,6 +72,8 @@ _SIGS = {
     "wmg_batched_gemv": (_i, [_i, _i, _dp, _ll, _dp, _ll, _dp, _ll, _vp]),
     "wmg_haar_restrict": (_i, [_i, _dp, _i, _dp, _vp]),
     "wmg_haar_prolong": (_i, [_i, _dp, _i, _dp, _i, _vp]),
+    "wmg_haar_prolong_path": (_i, [_i, _i, _i, ctypes.POINTER(_i), _dp, _dp, _vp]),
+    "wmg_haar_restrict_path": (_i, [_i, _i, _i, ctypes.POINTER(_i), _dp, _dp, _vp]),
     "wmg_leaf_factor": (_i, [_vp, _i, ctypes.POINTER(_i), _ll, _ll, _dp, _vp]),
     "wmg_leaf_gram": (_i, [_vp, _i, ctypes.POINTER(_i), _dp, _dp, _vp]),
     "wmg_spd_inverse_workspace": (_i, [_i, _i, ctypes.POINTER(ctypes.c_size_t)]),

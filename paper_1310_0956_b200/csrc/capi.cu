@@ -52,6 +52,8 @@ cudaError_t ew_combo(long long, int, double*, const double*, long long, const do
                      cudaStream_t);
 cudaError_t ew_cast(long long, int, void*, const void*, cudaStream_t);
 cudaError_t haar_restrict(int, const double*, int, double*, cudaStream_t);
+cudaError_t haar_prolong_path(int, int, int, const int*, const double*, double*, cudaStream_t);
+cudaError_t haar_restrict_path(int, int, int, const int*, const double*, double*, cudaStream_t);
 cudaError_t ew_axpy_dev(long long, double*, const double*, const double*, int, const double*,
                         cudaStream_t);
 cudaError_t ew_lincomb_dev(long long, double*, double, const double*, const double*,
@@ -634,6 +636,34 @@ int wmg_haar_prolong(int side, const double* coarse, int band, double* fine, int
   if (side < 2 || side % 2) return fail(WMG_EINVAL, "grid side must be even and >= 2");
   if (band < 0 || band > 3) return fail(WMG_EINVAL, "bad band");
   return cuda_rc(wmg::haar_prolong(side, coarse, band, fine, accumulate, STREAM(stream)));
+}
+
+static int check_path(int n, int depth, int batch, const int* bands) {
+  if (!bands && batch > 0 && depth > 0) return fail(WMG_EINVAL, "bands is NULL");
+  if (depth < 0 || depth > 7) return fail(WMG_EINVAL, "depth must be in [0, 7]");
+  if (batch < 0) return fail(WMG_EINVAL, "negative batch");
+  if (n < 1 || (n >> depth) << depth != n) return fail(WMG_EINVAL, "n is not divisible by 2^depth");
+  for (long long i = 0; i < (long long)batch * depth; ++i)
+    if (bands[i] < 0 || bands[i] > 3) return fail(WMG_EINVAL, "bad band");
+  return WMG_OK;
+}
+
+int wmg_haar_prolong_path(int n, int depth, int batch, const int* bands, const double* coarse,
+                          double* fine, void* stream) {
+  REQ(coarse && fine);
+  int rc = check_path(n, depth, batch, bands);
+  if (rc) return rc;
+  if (batch == 0) return WMG_OK;
+  return cuda_rc(wmg::haar_prolong_path(n, depth, batch, bands, coarse, fine, STREAM(stream)));
+}
+
+int wmg_haar_restrict_path(int n, int depth, int batch, const int* bands, const double* fine,
+                           double* coarse, void* stream) {
+  REQ(coarse && fine);
+  int rc = check_path(n, depth, batch, bands);
+  if (rc) return rc;
+  if (batch == 0) return WMG_OK;
+  return cuda_rc(wmg::haar_restrict_path(n, depth, batch, bands, fine, coarse, STREAM(stream)));
 }
 
 int wmg_leaf_factor(const wmg_geometry* g, int depth, const int* bands, long long ray0,

@@ -277,6 +277,80 @@ __global__ void haar_restrict_kernel(int side, const double* __restrict__ fine, 
   }
 }
 
+// Band paths of a batch of WMG nodes (item i: bands of levels 0..depth-1 in
+// 2-bit fields, level 0 = the finest restriction) -- kernel parameters, so the
+// launches stay graph-capturable.
+constexpr int kPathBatch = 128;
+struct BandPaths {
+  int depth;
+  unsigned short code[kPathBatch];
+};
+
+// fine_i (n x n) = R_{b0}^T ... R_{b(k-1)}^T coarse_i, coarsest level first:
+// the level-by-level prolongations (haar_prolong_kernel) fused into one pass,
+// the same sequence of sign * h products per fine pixel (bit-identical).
+// blockIdx.y = batch item; coarse items nc apart, fine items n^2 apart.
+__global__ void haar_prolong_path_kernel(int n, BandPaths bp, const double* __restrict__ coarse,
+                                         double* __restrict__ fine) {
+  const int k = bp.depth, item = blockIdx.y;
+  const unsigned code = bp.code[item];
+  const int sc = n >> k;
+  const long long nf = (long long)n * n;
+  const double* cin = coarse + (long long)item * sc * sc;
+  double* fout = fine + (long long)item * nf;
+  GRID_LOOP(f, nf) {
+    const int r = (int)(f / n), c = (int)(f % n);
+    double v = cin[(long long)(r >> k) * sc + (c >> k)];
+    for (int lv = k - 1; lv >= 0; --lv) {
+      double s[4];
+      band_signs((code >> (2 * lv)) & 3, s[0], s[1], s[2], s[3]);
+      v = dmul(s[(((r >> lv) & 1) << 1) | ((c >> lv) & 1)], v);
+    }
+    fout[f] = v;
+  }
+}
+
+// coarse_i = R_{b(k-1)} ... R_{b0} fine_i: the level-by-level restrictions
+// (haar_restrict_kernel, one band each) fused: each output sums its 4^k fine
+// pixels in nested 2 x 2 groups, children in CSR order, every partial sum
+// formed exactly as the per-level kernel forms it (bit-identical).
+__global__ void haar_restrict_path_kernel(int n, BandPaths bp, const double* __restrict__ fine,
+                                          double* __restrict__ coarse) {
+  const int k = bp.depth, item = blockIdx.y;
+  const unsigned code = bp.code[item];
+  const int sc = n >> k;
+  const long long nc = (long long)sc * sc;
+  const double* fin = fine + (long long)item * n * n;
+  double* cout = coarse + (long long)item * nc;
+  GRID_LOOP(q, nc) {
+    const int qi = (int)(q / sc), qk = (int)(q % sc);
+    double acc[12];
+    for (int lv = 0; lv < k; ++lv) acc[lv] = 0.0;
+    double v = 0.0;
+    const int leaves = 1 << (2 * k);
+    for (int t = 0; t < leaves; ++t) {
+      int r = qi << k, c = qk << k;
+      // digit of level lv is bits [2 lv, 2 lv + 1] of t (level 0 = finest)
+      for (int lv = 0; lv < k; ++lv) {
+        const int dg = (t >> (2 * lv)) & 3;
+        r += (dg >> 1) << lv;
+        c += (dg & 1) << lv;
+      }
+      v = fin[(long long)r * n + c];
+      for (int lv = 0; lv < k; ++lv) {
+        const int dg = (t >> (2 * lv)) & 3;
+        double s[4];
+        band_signs((code >> (2 * lv)) & 3, s[0], s[1], s[2], s[3]);
+        acc[lv] = dadd(acc[lv], dmul(s[dg], v));
+        if (dg != 3) break;
+        v = acc[lv];
+        acc[lv] = 0.0;
+      }
+    }
+    cout[q] = v;
+  }
+}
+
 // fine = (accumulate ? fine : 0) + R_b^T coarse  (one product per fine pixel)
 __global__ void haar_prolong_kernel(int side, const double* __restrict__ coarse, int band,
                                     double* __restrict__ fine, int accumulate) {
@@ -527,6 +601,50 @@ cudaError_t haar_restrict(int side, const double* fine, int band_mask, double* o
   if (nc <= 0) return cudaSuccess;
   vec::haar_restrict_kernel<<<grid_for(nc, 256), 256, 0, st>>>(side, fine, band_mask, out);
   return cudaGetLastError();
+}
+
+cudaError_t haar_prolong_path(int n, int depth, int batch, const int* bands,
+                              const double* coarse, double* fine, cudaStream_t st) {
+  const int sc = n >> depth;
+  for (int b0 = 0; b0 < batch; b0 += vec::kPathBatch) {
+    const int nb = batch - b0 < vec::kPathBatch ? batch - b0 : vec::kPathBatch;
+    vec::BandPaths bp;
+    bp.depth = depth;
+    for (int i = 0; i < nb; ++i) {
+      unsigned code = 0;
+      for (int lv = 0; lv < depth; ++lv) code |= (unsigned)(bands[(b0 + i) * depth + lv] & 3) << (2 * lv);
+      bp.code[i] = (unsigned short)code;
+    }
+    const long long nf = (long long)n * n;
+    dim3 grid(grid_for(nf, 256), nb);
+    vec::haar_prolong_path_kernel<<<grid, 256, 0, st>>>(n, bp, coarse + (long long)b0 * sc * sc,
+                                                        fine + (long long)b0 * nf);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+cudaError_t haar_restrict_path(int n, int depth, int batch, const int* bands, const double* fine,
+                               double* coarse, cudaStream_t st) {
+  const int sc = n >> depth;
+  for (int b0 = 0; b0 < batch; b0 += vec::kPathBatch) {
+    const int nb = batch - b0 < vec::kPathBatch ? batch - b0 : vec::kPathBatch;
+    vec::BandPaths bp;
+    bp.depth = depth;
+    for (int i = 0; i < nb; ++i) {
+      unsigned code = 0;
+      for (int lv = 0; lv < depth; ++lv) code |= (unsigned)(bands[(b0 + i) * depth + lv] & 3) << (2 * lv);
+      bp.code[i] = (unsigned short)code;
+    }
+    const long long nc = (long long)sc * sc;
+    dim3 grid(grid_for(nc, 128), nb);
+    vec::haar_restrict_path_kernel<<<grid, 128, 0, st>>>(n, bp, fine + (long long)b0 * n * n,
+                                                         coarse + (long long)b0 * nc);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 cudaError_t haar_prolong(int side, const double* coarse, int band, double* fine, int accumulate,

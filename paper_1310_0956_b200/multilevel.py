@@ -110,6 +110,36 @@ def prolong(side: int, coarse, band: str, fine, accumulate: bool):
     return fine
 
 
+# Node applications prolong / restrict along the whole band path in one launch
+# (wmg_haar_prolong_path / wmg_haar_restrict_path, bit-identical to the
+# level-by-level kernels); False: level by level (testing).
+FUSED_PATHS = True
+
+
+def _path_codes(paths):
+    depth = len(paths[0])
+    arr = (N.ctypes.c_int * (len(paths) * depth))(
+        *[BAND_CODE[b] for p in paths for b in p])
+    return depth, arr
+
+
+def prolong_path(n: int, paths, coarse, fine):
+    """fine[i] (n*n) = R_{paths[i]}^T coarse[i] for a batch of band paths
+    (coarse: (B, (n >> depth)^2), fine: (B, n*n), contiguous rows)."""
+    depth, arr = _path_codes(paths)
+    N.call("wmg_haar_prolong_path", n, depth, len(paths), arr, D.ptr(coarse), D.ptr(fine),
+           D.stream_handle())
+    return fine
+
+
+def restrict_path(n: int, paths, fine, coarse):
+    """coarse[i] = R_{paths[i]} fine[i] for a batch of band paths."""
+    depth, arr = _path_codes(paths)
+    N.call("wmg_haar_restrict_path", n, depth, len(paths), arr, D.ptr(fine), D.ptr(coarse),
+           D.stream_handle())
+    return coarse
+
+
 # ------------------------------------------------------------------ nodes
 @dataclass
 class WmgNode:
@@ -144,21 +174,27 @@ class WmgNode:
         t = D.torch()
         # prolong to the fine grid (coarsest factor first, as R_path^T does)
         cur = v
-        for lv in range(k - 1, -1, -1):
-            side_f = h.n >> lv
-            buf = h.buf(("pf", lv), side_f * side_f)
-            prolong(side_f, cur, self.bands[lv], buf, accumulate=False)
-            cur = buf
+        if k and FUSED_PATHS:
+            cur = prolong_path(h.n, [self.bands], v, h.buf(("pf", 0), h.n * h.n))
+        else:
+            for lv in range(k - 1, -1, -1):
+                side_f = h.n >> lv
+                buf = h.buf(("pf", lv), side_f * side_f)
+                prolong(side_f, cur, self.bands[lv], buf, accumulate=False)
+                cur = buf
         sino = h.buf(("sino",), w.shape[0])
         w.forward_(cur, sino)
         img = h.buf(("img",), w.shape[1]) if k else out
         w.backward_(sino, img)
         cur = img
-        for lv in range(k):
-            side_f = h.n >> lv
-            dst = out if lv == k - 1 else h.buf(("rs", lv), (side_f // 2) ** 2)
-            restrict(side_f, cur, (self.bands[lv],), out=dst.view(1, -1))
-            cur = dst
+        if k and FUSED_PATHS:
+            restrict_path(h.n, [self.bands], img, out)
+        else:
+            for lv in range(k):
+                side_f = h.n >> lv
+                dst = out if lv == k - 1 else h.buf(("rs", lv), (side_f // 2) ** 2)
+                restrict(side_f, cur, (self.bands[lv],), out=dst.view(1, -1))
+                cur = dst
         if self.lam != 0:
             D.add_scaled(out, out, self.lam, +1, v)
         return out
@@ -491,20 +527,26 @@ def _apply_system_batch_(nodes, V, OUT):
     n2 = h.n * h.n
     M = w.shape[0]
     F = h.buf(("bpf", B), B * n2).view(B, n2)
-    for b, nd in enumerate(nodes):
-        cur = V[b]
-        for lv in range(k - 1, -1, -1):
-            side_f = h.n >> lv
-            dst = F[b] if lv == 0 else h.buf(("bpfl", lv, b), side_f * side_f)
-            prolong(side_f, cur, nd.bands[lv], dst, accumulate=False)
-            cur = dst
+    fused = FUSED_PATHS and k > 0 and V.is_contiguous() and OUT.is_contiguous()
+    if fused:
+        prolong_path(h.n, [nd.bands for nd in nodes], V, F)
+    else:
+        for b, nd in enumerate(nodes):
+            cur = V[b]
+            for lv in range(k - 1, -1, -1):
+                side_f = h.n >> lv
+                dst = F[b] if lv == 0 else h.buf(("bpfl", lv, b), side_f * side_f)
+                prolong(side_f, cur, nd.bands[lv], dst, accumulate=False)
+                cur = dst
     sino = h.buf(("bsino", B), B * M).view(B, M)
     w.forward_batch_(F, sino)
     img = h.buf(("bimg", B), B * n2).view(B, n2)
     w.backward_batch_(sino, img)
+    if fused:
+        restrict_path(h.n, [nd.bands for nd in nodes], img, OUT)
     for b, nd in enumerate(nodes):
         cur = img[b]
-        for lv in range(k):
+        for lv in range(k if not fused else 0):
             side_f = h.n >> lv
             dst = OUT[b] if lv == k - 1 else h.buf(("brs", lv, b), (side_f // 2) ** 2)
             restrict(side_f, cur, (nd.bands[lv],), out=dst.view(1, -1))

@@ -284,3 +284,54 @@ def test_sparse_leaf_gram_bit_reproducible(gpu, golden):
     for _ in range(2):
         _, g2 = _assemble_leaf_grams(w, 160, 0.0, 3, method="sparse")
         assert bool((g1 == g2).all())
+
+
+@pytest.mark.parametrize("depth", [1, 2, 3, 4])
+def test_fused_band_path_haar_bitwise(gpu, depth):
+    """wmg_haar_prolong_path / wmg_haar_restrict_path == the per-level Haar
+    kernels applied along each node's band path, bit for bit."""
+    torch = gpu
+    from paper_1310_0956_b200.multilevel import (BAND_IDS, prolong, prolong_path, restrict,
+                                                 restrict_path)
+    n = 64
+    rng = np.random.default_rng(depth)
+    paths = [tuple(BAND_IDS[i] for i in rng.integers(0, 4, depth)) for _ in range(5)]
+    nc = (n >> depth) ** 2
+    C = torch.from_numpy(rng.standard_normal((5, nc))).cuda()
+    Fi = torch.from_numpy(rng.standard_normal((5, n * n))).cuda()
+    F = torch.empty(5, n * n, dtype=torch.float64, device="cuda")
+    prolong_path(n, paths, C, F)
+    R = torch.empty(5, nc, dtype=torch.float64, device="cuda")
+    restrict_path(n, paths, Fi, R)
+    for b, p in enumerate(paths):
+        cur = C[b]
+        for lv in range(depth - 1, -1, -1):
+            side = n >> lv
+            nxt = torch.empty(side * side, dtype=torch.float64, device="cuda")
+            prolong(side, cur, p[lv], nxt, accumulate=False)
+            cur = nxt
+        assert torch.equal(cur, F[b])
+        cur = Fi[b]
+        for lv in range(depth):
+            side = n >> lv
+            cur = restrict(side, cur, (p[lv],))[0]
+        assert torch.equal(cur, R[b])
+
+
+@pytest.mark.parametrize("levels", [3, 4])
+def test_fused_paths_vcycle_bitwise(gpu, levels):
+    """The V-cycle with fused band-path Haar launches equals the level-by-level one."""
+    torch = gpu
+    from paper_1310_0956_b200 import build_geometry, build_projector, build_wmg_hierarchy
+    from paper_1310_0956_b200 import multilevel as ML
+    w = build_projector(build_geometry(64, 91, 90))
+    h = build_wmg_hierarchy(w, 64, 0.1, levels, nu_pre=1, nu_post=1)
+    v = torch.from_numpy(np.random.default_rng(5).standard_normal(64 * 64)).cuda()
+    try:
+        ML.FUSED_PATHS = False
+        ref = ML.wmg_preconditioner(h, graph=False)(v)
+        ML.FUSED_PATHS = True
+        got = ML.wmg_preconditioner(h, graph=False)(v)
+    finally:
+        ML.FUSED_PATHS = True
+    assert torch.equal(got, ref)
