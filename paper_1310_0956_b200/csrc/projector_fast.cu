@@ -1689,12 +1689,16 @@ cudaError_t tma_forward(const GeomDev& G, float* P, float* PT, TOut* sino, int* 
 // G.sym: 0 off, 1 on when profitable, 2 forced (tests), 10 forced with the row
 // warp layout of the symmetric backprojector (A/B tests), 4 forced + TMA-staged
 // forward (experimental: slower than the L2 gather on B200)
+// G.sym: bit 0 auto, bit 1 forced, bit 2 forced + TMA forward; the higher bits
+// select testing variants
 static inline bool use_sym_bwd(const GeomDev& G) {
-  return G.sym >= 2 || (G.sym == 1 && G.n >= 1024);
+  const int base = G.sym & 7;
+  return base >= 2 || (base == 1 && G.n >= 1024);
 }
 static inline bool use_sym_fwd(const GeomDev& G) {
   const long long blocks = (long long)(((G.d + 1) / 2 + 127) / 128) * G.n_half;   // 128-ray units
-  return G.sym >= 2 || (G.sym == 1 && blocks >= 4LL * 148);
+  const int base = G.sym & 7;
+  return base >= 2 || (base == 1 && blocks >= 4LL * 148);
 }
 static inline bool use_tiled_bwd(const GeomDev& G) { return G.n >= 768; }
 // one thread per ray / pixel fills the SMs only beyond ~512 px
