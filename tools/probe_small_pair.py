@@ -30,7 +30,7 @@ o = torch.empty_like(x)
 X3 = torch.rand(3, n * n, dtype=torch.float64, device="cuda")
 S3 = torch.empty(3, m * d, dtype=torch.float64, device="cuda")
 ref = None
-for mode in ("auto", "fwdsplit64", "auto"):
+for mode in ("auto",):
     w.set_symmetry(True if mode == "auto" else mode)
     tf = ev(lambda: w.forward_(x, s))
     tb = ev(lambda: w.backward_(y, o))
