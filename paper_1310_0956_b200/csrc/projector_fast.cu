@@ -510,6 +510,85 @@ __global__ void __launch_bounds__(128) fwd_v2_kernel(GeomDev G, const float* __r
   if (j < G.d) sino[(long long)(G.rowmap ? G.rowmap[a] : a) * G.d + j] = (TOut)acc;
 }
 
+// fwd_v2_kernel with each ray's slab range split over kSplit segments
+// (threadIdx.y), partial sums reduced in shared memory in segment order: for
+// the two axis-aligned angles of a symmetric set, which alone launch too few
+// rays to fill the GPU (their walk is n slabs long).
+template <typename TOut, int ES = 1>
+__global__ void __launch_bounds__(32 * kSplit) fwd_v2_split_kernel(GeomDev G,
+                                                                   const float* __restrict__ P,
+                                                                   const float* __restrict__ PT,
+                                                                   TOut* __restrict__ sino) {
+  __shared__ float part[kSplit][33];
+  const int a = blockIdx.y, lane = threadIdx.x, seg = threadIdx.y;
+  const int j = blockIdx.x * 32 + lane;
+  const AngleParams& A = G.ang[a];
+  const int n = G.n;
+  const int pitch = n + 2 * kPadMargin;
+  const double off = (double)j - (double)(G.d - 1) * 0.5;
+  const double u0 = A.u0 + off * A.du;
+  const double slope = A.slope;
+  int r0 = 0, r1 = n - 1;
+  if (j >= G.d) {
+    r0 = n; r1 = -1;
+  } else if (slope > 0.0) {
+    const double ra = floor((-1.0 - u0) / slope) - 1.0;
+    const double rb = ceil(((double)n + 1.0 - u0) / slope) + 1.0;
+    r0 = (int)fmin(fmax(ra, 0.0), (double)n);
+    r1 = (int)fmax(fmin(rb, (double)(n - 1)), -1.0);
+  } else if (u0 < -1.0 || u0 > (double)n + 1.0) {
+    r0 = n; r1 = -1;
+  }
+  const int rw0 = __reduce_min_sync(0xffffffffu, r0);
+  const int rw1 = __reduce_max_sync(0xffffffffu, r1);
+  float acc = 0.0f;
+  if (rw0 <= rw1) {
+    const int len = rw1 - rw0 + 1;
+    const int rs = rw0 + (len * seg) / kSplit;
+    const int re = rw0 + (len * (seg + 1)) / kSplit - 1;
+    const float* __restrict__ src = (A.major ? PT : P) + ES * kPadMargin;
+    const long long S = llrint(slope * kQ32);
+    long long U = llrint(u0 * kQ32) + (long long)rs * S;
+    const float L = A.Lf, Ls = A.Lsf;
+    long long rowoff = (long long)rs * pitch;
+    if (!A.mirror) {
+#pragma unroll 4
+      for (int r = rs; r <= re; ++r) {
+        U += S;
+        const int k = hi32(U);
+        const float f = frac1((unsigned)U);
+        const float wh = fminf(fmaf(f, Ls, -Ls), L);    // NaN (axis: inf-inf) -> L
+        const float* p = src + ES * (rowoff + k);
+        const float v1 = __ldg(p), v0 = __ldg(p - ES);
+        acc = fmaf(L, v0, acc);
+        acc = fmaf(wh, v1 - v0, acc);
+        rowoff += pitch;
+      }
+    } else {
+#pragma unroll 4
+      for (int r = rs; r <= re; ++r) {
+        U += S;
+        const int k = hi32(U);
+        const float f = frac1((unsigned)U);
+        const float wh = fminf(fmaf(f, Ls, -Ls), L);
+        const float* p = src + ES * (rowoff + (n - 1 - k));
+        const float v1 = __ldg(p), v0 = __ldg(p + ES);
+        acc = fmaf(L, v0, acc);
+        acc = fmaf(wh, v1 - v0, acc);
+        rowoff += pitch;
+      }
+    }
+  }
+  part[seg][lane] = acc;
+  __syncthreads();
+  if (seg == 0 && j < G.d) {
+    float sum = part[0][lane];
+#pragma unroll
+    for (int q = 1; q < kSplit; ++q) sum += part[q][lane];
+    sino[(long long)(G.rowmap ? G.rowmap[a] : a) * G.d + j] = (TOut)sum;
+  }
+}
+
 // Backward: 32 x 32 pixel tile per block (128 threads; warp w owns rows
 // 8w..8w+7, lane = column).  Angles are processed in chunks of 32: the
 // detector window of every angle is staged in shared memory as pairs
@@ -1747,9 +1826,10 @@ static cudaError_t fwd_v2_impl(const GeomDev& G, const void* x, void* ws, void* 
         G, (const float*)PM, (const float*)PMT, (TOut*)y);
     e = cudaGetLastError();
     if (e != cudaSuccess || Gx->m == 0) return e;
-    dim3 xgrid((G.d + 127) / 128, Gx->m);   // the axis-aligned angles of the set
-    fast::fwd_v2_kernel<TOut, 2><<<xgrid, 128, 0, st>>>(*Gx, (const float*)PM,
-                                                         (const float*)PMT, (TOut*)y);
+    // the axis-aligned angles of the set: slab segments over threadIdx.y
+    dim3 xgrid((G.d + 31) / 32, Gx->m), xblock(32, fast::kSplit);
+    fast::fwd_v2_split_kernel<TOut, 2><<<xgrid, xblock, 0, st>>>(*Gx, (const float*)PM,
+                                                                 (const float*)PMT, (TOut*)y);
     return cudaGetLastError();
   }
   fast::pad_transpose_kernel<TIn><<<tg, tb, 0, st>>>((const TIn*)x, P, PT, G.n);
