@@ -175,11 +175,22 @@ __global__ void __launch_bounds__(256) leaf_gram_kernel(GeomDev G, LeafPath path
     }
   }
   __syncthreads();
-  // pass 3: lower-triangle pairs of local blocks that share a ray
-  const long long QQ = (long long)Q * Q;
-  for (long long t = tid; t < QQ; t += blockDim.x) {
-    const int i = (int)(t / Q), jj = (int)(t % Q);
-    if (jj > i) continue;
+  // pass 3: pairs of crossed local blocks that share a ray.  The crossed blocks
+  // are compacted first (their order does not matter: the fixed-point atomics
+  // are associative), so the pair loop skips the empty ones.
+  int* act = chi + sc;                                // [Q]
+  __shared__ int nact_s;
+  if (tid == 0) nact_s = 0;
+  __syncthreads();
+  for (int i = tid; i < Q; i += blockDim.x)
+    if (mask[i]) act[atomicAdd(&nact_s, 1)] = i;
+  __syncthreads();
+  const int nact = nact_s;
+  const long long npairs = (long long)nact * (nact + 1) / 2;
+  for (long long t = tid; t < npairs; t += blockDim.x) {
+    int u, v;
+    tri_unrank((int)t, u, v);
+    const int i = act[u], jj = act[v];
     unsigned mm = mask[i] & mask[jj];
     if (!mm) continue;
     double sum = 0.0;
@@ -210,7 +221,8 @@ __global__ void fixed_to_double_kernel(double* __restrict__ g, long long count, 
 size_t leaf_gram_smem(int n, int depth, int nb) {
   const int sc = n >> depth;
   const int Q = sc * ml::kWc;
-  return (size_t)Q * nb * sizeof(double) + (size_t)Q * sizeof(unsigned) + 2 * sc * sizeof(int);
+  return (size_t)Q * nb * sizeof(double) + (size_t)Q * sizeof(unsigned) + 2 * sc * sizeof(int) +
+         (size_t)Q * sizeof(int);
 }
 
 cudaError_t leaf_gram(const GeomDev& G, int depth, const int* bands, double* gram, int* overflow,
