@@ -44,3 +44,30 @@ def test_invalid_arguments_map_to_errors():
     assert b"positive" in lib.wmg_last_error()
     rc = lib.wmg_haar_restrict(3, ctypes.c_void_p(8), 1, ctypes.c_void_p(8), None)
     assert rc == _native.WMG_EINVAL
+
+
+def test_new_entry_points_validate_without_a_gpu():
+    """Argument checks of the WMG coarse-solve and band-path entry points run
+    before any CUDA call (no device needed)."""
+    from paper_1310_0956_b200 import _native
+    lib = _native.load()
+    dp = ctypes.c_void_p(8)
+    nbytes = ctypes.c_size_t()
+    assert lib.wmg_spd_inverse_workspace(2, 256, ctypes.byref(nbytes)) == _native.WMG_OK
+    assert nbytes.value == 2 * 2 * (128 * 128 + 2 * 256 * 128) * 8   # two buffer sets
+    assert lib.wmg_spd_inverse(1, 100, dp, 100 * 100, dp, dp, None) == _native.WMG_EINVAL
+    assert b"multiple of 128" in lib.wmg_last_error()
+    assert lib.wmg_spd_inverse(2, 128, dp, 10, dp, dp, None) == _native.WMG_EDIM
+    elems = ctypes.c_longlong()
+    assert lib.wmg_packed_sym_sizes(3, 384, ctypes.byref(elems), None) == _native.WMG_OK
+    assert elems.value == 6 * 128 * 128
+    assert lib.wmg_packed_sym_sizes(1, 100, ctypes.byref(elems), None) == _native.WMG_EINVAL
+    assert lib.wmg_sym_pack(1, 130, dp, 130 * 130, dp, 1, None) == _native.WMG_EINVAL
+    assert lib.wmg_packed_symv(1, 64, dp, 1, dp, 64, dp, 64, dp, None) == _native.WMG_EINVAL
+    bands = (ctypes.c_int * 2)(0, 5)
+    assert lib.wmg_haar_prolong_path(64, 2, 1, bands, dp, dp, None) == _native.WMG_EINVAL
+    assert b"bad band" in lib.wmg_last_error()
+    bands = (ctypes.c_int * 2)(0, 3)
+    assert lib.wmg_haar_restrict_path(66, 2, 1, bands, dp, dp, None) == _native.WMG_EINVAL
+    assert lib.wmg_haar_restrict_path(64, 8, 1, bands, dp, dp, None) == _native.WMG_EINVAL
+    assert lib.wmg_haar_prolong_path(64, 2, 0, bands, dp, dp, None) == _native.WMG_OK
