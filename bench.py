@@ -580,6 +580,10 @@ def run_ours(args):
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     t_e2e = float(te.item())
     e2e_value = rays_total * args.steps / t_e2e / 1e9
+    # the pipelined host round trips returned exactly the device-resident results
+    # (deterministic kernels, same inputs): the overlap hides nothing
+    last = args.steps & 1                  # buffer set of the last timed step (warm-up = 0)
+    e2e_ok = bool(torch.equal(out_s2[last], sino.cpu()) and torch.equal(out_i2[last], img.cpu()))
 
     # ---- roofline ---------------------------------------------------------
     peaks, peak_src = measured_peaks()
@@ -605,7 +609,8 @@ def run_ours(args):
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": config_dict(n, d, m, world),
-        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 4 * (Npix + M_loc),
+        "e2e": {"value": e2e_value, "unit": UNIT, "verified_against_device": e2e_ok,
+                "h2d_bytes_per_step": 4 * (Npix + M_loc),
                 "d2h_bytes_per_step": 4 * (Npix + M_loc)},
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm,
                      "unit": "GB/s", "frac": achieved / hbm, "traffic": traffic,
