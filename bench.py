@@ -20,9 +20,10 @@ rel. residual 1e-4, setup separate, plain CGLS beside it), the end-to-end
 number with host buffers (``e2e``), the CPU baselines and the rooflines;
 ``--workload config2|config4`` runs the other BASELINE configurations.
 
-``value`` times each step's two independent products on two streams (they
-share the SMs); ``value_sequential`` times them back to back on one stream,
-which also gives the per-kernel times behind the rooflines.  ``e2e`` is what a user streaming pairs through the
+``value`` is the faster of two timings of the same steps: the two independent
+products on two streams (they share the SMs; ``value_two_streams``) or back
+to back on one stream (``value_sequential``, which also gives the per-kernel
+times behind the rooflines); ``pair_schedule`` names the one reported.  ``e2e`` is what a user streaming pairs through the
 public API sees: every step copies x and y from pinned host memory and both
 results back, with copies on their own streams (double-buffered, overlapping
 the kernels) and the two independent products on two streams, so the
@@ -483,10 +484,15 @@ def run_ours(args):
     if world > 1:
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
     t_tot, t_fwd, t_bwd, t_conc = [float(v) for v in tt.cpu()]
-    ms_step = t_conc / args.steps * 1e3
+    # both schedules compute the same step; report the faster (small grids with
+    # an L2 flush between steps can lose from the cross-stream joins)
+    concurrent = t_conc <= t_tot
+    t_val = t_conc if concurrent else t_tot
+    ms_step = t_val / args.steps * 1e3
     rays_total = m * d
-    value = rays_total * args.steps / t_conc / 1e9
+    value = rays_total * args.steps / t_val / 1e9
     value_seq = rays_total * args.steps / t_tot / 1e9
+    value_conc = rays_total * args.steps / t_conc / 1e9
 
     # ---- end to end through the public API with host buffers -------------
     pin_x = torch.from_numpy(x_h).pin_memory()
@@ -620,6 +626,8 @@ def run_ours(args):
                             "frac": upd_rate / gather_peak,
                             "definition": "SURVEY s8(d): 148 SMs x 32 lanes x f_SM"},
         "roofline_onchip": onchip_roofline(n, fwd_avg, bwd_avg, n_sm, f_sm, world),
+        "pair_schedule": "two streams" if concurrent else "one stream",
+        "value_two_streams": value_conc,
         "value_sequential": value_seq,
         "ms_per_step_sequential": t_tot / args.steps * 1e3,
         "kernels_ms": {"forward": fwd_avg * 1e3, "backward": bwd_avg * 1e3},

@@ -1770,9 +1770,12 @@ cudaError_t tma_forward(const GeomDev& G, float* P, float* PT, TOut* sino, int* 
 // forward (experimental: slower than the L2 gather on B200)
 // G.sym: bit 0 auto, bit 1 forced, bit 2 forced + TMA forward; the higher bits
 // select testing variants
-static inline bool use_sym_bwd(const GeomDev& G) {
+static inline bool use_sym_bwd(const GeomDev& G, int precision = 1) {
+  // fp32: the run layout beats the split kernel from n ~ 384 up (n = 512:
+  // 0.17 vs 0.31 ms; n = 256: 0.083 vs 0.053 ms); fp64: from n = 1024 (the
+  // angle-split cluster kernel covers the small grids)
   const int base = G.sym & 7;
-  return base >= 2 || (base == 1 && G.n >= 1024);
+  return base >= 2 || (base == 1 && G.n >= (precision == 0 ? 512 : 1024));
 }
 static inline bool use_sym_fwd(const GeomDev& G) {
   const long long blocks = (long long)(((G.d + 1) / 2 + 127) / 128) * G.n_half;   // 128-ray units
@@ -1942,7 +1945,7 @@ static cudaError_t bwd_sym_impl(const GeomDev& G, const GeomDev& Gx, const void*
 template <typename TIn, typename TOut>
 static cudaError_t bwd_v2_impl(const GeomDev& G, const void* y, void* x, bool accumulate,
                                cudaStream_t st, const GeomDev* G_axis) {
-  if (use_sym_bwd(G) && G_axis)
+  if (use_sym_bwd(G, 0) && G_axis)
     return bwd_sym_impl<TIn, TOut>(G, *G_axis, y, x, accumulate, st);
   if (use_split(G)) return bwd_split_launch<TIn, TOut, float>(G, y, x, accumulate, st);
   if (!use_tiled_bwd(G)) {   // small grids: one thread per pixel
@@ -2186,7 +2189,7 @@ cudaError_t fast_backward_batch(const GeomDev& G, int precision, int tin, int to
                        !use_sym_bwd(G);
   if (small64)   // one cluster launch for the whole batch
     return bwd64_impl<double, double>(G, y, x, accumulate, st, Gx, true, batch);
-  const bool sym = use_sym_bwd(G) && Gx;
+  const bool sym = use_sym_bwd(G, precision) && Gx;
   if (use_split(G) && !sym && tin == tout) {
     if (precision == 1 && tin == 1)
       return bwd_split_launch<double, double, double>(G, y, x, accumulate, st, batch);
