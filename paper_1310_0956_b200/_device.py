@@ -77,7 +77,9 @@ def capture_graph(fn, device):
     side.wait_stream(cur)
     g = t.cuda.CUDAGraph()
     with t.cuda.stream(side):
-        g.capture_begin()
+        # thread-local capture: solves running concurrently in other host threads
+        # (their own streams) may keep launching while this thread captures
+        g.capture_begin(capture_error_mode="thread_local")
         try:
             out = fn()
         finally:
@@ -87,10 +89,14 @@ def capture_graph(fn, device):
 
 
 def scratch(n: int, K: int, device):
-    """Cached device scratch for wmg_det_reduce (+ K result slots)."""
+    """Cached device scratch for wmg_det_reduce (+ K result slots), per stream.
+    Inside a graph capture a fresh buffer comes from the graph's private pool,
+    so two captured graphs never share scratch (they may replay concurrently)."""
     t = torch()
     L = N.load()
     need = int(L.wmg_det_scratch_len(int(n), int(K))) + 16
+    if t.cuda.is_current_stream_capturing():
+        return t.empty(max(need, 4096), dtype=t.float64, device=device)
     key = (str(device), t.cuda.current_stream(device).cuda_stream)
     buf = _scratch.get(key)
     if buf is None or buf.numel() < need:

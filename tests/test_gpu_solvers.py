@@ -228,3 +228,35 @@ def test_zero_and_degenerate_inputs(gpu, golden):
     assert (rows == 0).any()                  # empty rows exist
     x, rec = sirt_solve(w, b, None, SolverConfig(max_iterations=50))
     assert np.all(np.isfinite(x)) and rec.rel_residual[-1] < rec.rel_residual[0]
+
+
+def test_concurrent_cgls_solves_on_two_streams_match_sequential(gpu):
+    """Independent slices solved concurrently (host thread + CUDA stream each, a
+    projector instance each -- config 4's bench) give bit-identical results."""
+    import threading
+    torch = gpu
+    from paper_1310_0956_b200 import (SolverConfig, build_geometry, build_projector,
+                                      cgls_solve, random_ellipses)
+    g = build_geometry(256, 363, 180)
+    ws = [build_projector(g, precision="float32") for _ in range(2)]
+    bs = [torch.from_numpy(ws[0] @ random_ellipses(256, 10, seed=k)).cuda() for k in range(4)]
+    cfg = SolverConfig(max_iterations=40, residual_tolerance=1e-6)
+    ref = [cgls_solve(ws[0], b, cfg=cfg) for b in bs]
+    streams = [torch.cuda.Stream() for _ in range(2)]
+    out = [None] * 4
+
+    def worker(i):
+        with torch.cuda.stream(streams[i]):
+            for k in range(i, 4, 2):
+                out[k] = cgls_solve(ws[i], bs[k], cfg=cfg)
+        streams[i].synchronize()
+
+    th = [threading.Thread(target=worker, args=(i,)) for i in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    torch.cuda.synchronize()
+    for k in range(4):
+        assert torch.equal(out[k][0], ref[k][0])
+        assert out[k][1].rel_residual == ref[k][1].rel_residual
