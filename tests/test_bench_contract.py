@@ -1,0 +1,51 @@
+"""The bench JSON contract, checked on the committed B200 results (no GPU).
+
+bench.py prints one JSON line that the round driver parses; this pins its keys,
+units and internal consistency on `results/r1_bench.json` (the last measured
+line) so a refactor of bench.py cannot silently drop a field.
+"""
+import json
+import os
+
+import pytest
+
+ROOT = os.path.abspath(os.path.join(os.path.dirname(__file__), ".."))
+
+
+def _line(name):
+    path = os.path.join(ROOT, "results", name)
+    if not os.path.exists(path):
+        pytest.skip(f"{name} not committed")
+    with open(path) as fh:
+        return json.loads(fh.read().strip().splitlines()[-1])
+
+
+def test_bench_line_keys_and_consistency():
+    d = _line("r1_bench.json")
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
+              "higher_is_better", "scaling", "vs_baseline", "dtype", "data", "config", "e2e",
+              "roofline", "cpu_baseline", "gpu_launches", "clocks"):
+        assert k in d, k
+    assert d["unit"] == "GRays/s" and d["higher_is_better"] is True and d["warmup"] >= 3
+    assert d["config"]["workload"].startswith("config3_pair")
+    n, m, dd = d["config"]["n"], d["config"]["n_angles"], d["config"]["n_detectors"]
+    # value = rays per step / step time
+    assert abs(m * dd / (d["ms_per_step"] * 1e-3) / 1e9 - d["value"]) <= 1e-6 * d["value"]
+    e = d["e2e"]
+    assert e["unit"] == d["unit"] and e["h2d_bytes_per_step"] == 4 * (n * n + m * dd)
+    assert e["verified_against_device"] is True
+    r = d["roofline"]
+    assert r["bound"] in ("hbm", "tensor") and abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-9
+    cb = d["cpu_baseline"]
+    assert cb["kind"] in ("reference", "port") and cb["cores"] >= 1 and cb["sample"]
+    assert d["gpu_launches"] > 0
+    assert not set(d["clocks"]["reasons"]) & {"hw_slowdown", "hw_thermal_slowdown",
+                                              "sw_thermal_slowdown"}
+    w = d["wmg_cgls"]
+    assert w["status"] == "converged" and w["final_rel_residual"] < 1e-4
+
+
+def test_reference_arm_line():
+    d = _line("r1_bench_reference.json")
+    assert d["impl"] == "reference" and d["unit"] == "GRays/s"
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["cpu_baseline"]["value"] == d["value"]
