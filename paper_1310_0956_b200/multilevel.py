@@ -455,13 +455,14 @@ def _setup_smoothers(h: WmgHierarchy, power_iterations: int = 10):
         nd.smooth_c = c.contiguous()
         v = t.rand(nd.dim, dtype=t.float64, device=w.device, generator=gen)
         out = t.empty_like(v)
-        lam_max = 1.0
+        lam = None
         for _ in range(power_iterations):
             v = v / v.norm()
             nd.apply_system_(v, out)
             out.mul_(c)
-            lam_max = float(v.dot(out))
+            lam = v.dot(out)                 # stays on the device: one read at the end
             v = out.clone()
+        lam_max = float(lam) if lam is not None else 1.0
         nd.smooth_omega = 0.95 / lam_max if lam_max > 0 else 0.0
 
 
