@@ -479,6 +479,7 @@ def run_ours(args):
                 t_conc += c0.elapsed_time(c1) / 1e3
     if world > 1:
         dist.barrier()
+    step_ms = sorted(a.elapsed_time(dd) for a, _, _, dd in ev)   # per-step, back to back
     t_fwd = sum(a.elapsed_time(b) for a, b, _, _ in ev) / 1e3
     t_bwd = sum(b.elapsed_time(c) for _, b, c, _ in ev) / 1e3
     t_tot = sum(a.elapsed_time(dd) for a, _, _, dd in ev) / 1e3
@@ -631,6 +632,7 @@ def run_ours(args):
         "pair_schedule": "two streams" if concurrent else "one stream",
         "value_two_streams": value_conc,
         "value_sequential": value_seq,
+        "step_ms_sequential": {"median": step_ms[len(step_ms) // 2], "best": step_ms[0]},
         "ms_per_step_sequential": t_tot / args.steps * 1e3,
         "kernels_ms": {"forward": fwd_avg * 1e3, "backward": bwd_avg * 1e3},
         "gpu_launches": launches,
