@@ -71,19 +71,29 @@ def capture_graph(fn, device):
     and return (graph, fn's result).  Unlike ``torch.cuda.graph`` this does not
     empty the caching allocator first: a capture right after a hierarchy build
     would otherwise pay ~10 ms of cudaFree for the released setup buffers."""
+    import gc
     t = torch()
     cur = t.cuda.current_stream(device)
     side = t.cuda.Stream(device=device)
     side.wait_stream(cur)
     g = t.cuda.CUDAGraph()
-    with t.cuda.stream(side):
-        # thread-local capture: solves running concurrently in other host threads
-        # (their own streams) may keep launching while this thread captures
-        g.capture_begin(capture_error_mode="thread_local")
-        try:
-            out = fn()
-        finally:
-            g.capture_end()
+    # no cyclic garbage collection while capturing: collecting an unreachable
+    # earlier preconditioner would destroy its CUDA graph mid-capture, which
+    # invalidates the capture
+    gc_was_enabled = gc.isenabled()
+    gc.disable()
+    try:
+        with t.cuda.stream(side):
+            # thread-local capture: solves running concurrently in other host
+            # threads (their own streams) may keep launching while this one captures
+            g.capture_begin(capture_error_mode="thread_local")
+            try:
+                out = fn()
+            finally:
+                g.capture_end()
+    finally:
+        if gc_was_enabled:
+            gc.enable()
     cur.wait_stream(side)
     return g, out
 
