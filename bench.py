@@ -67,7 +67,8 @@ def parse():
     ap.add_argument("--cpu-angles", type=int, default=4)
     ap.add_argument("--no-wmg", action="store_true",
                     help="skip the config-1 WMG-CGLS time-to-tolerance measurement")
-    ap.add_argument("--workload", choices=["pair", "config2", "config4"], default="pair",
+    ap.add_argument("--workload", choices=["pair", "config2", "config4", "launch-check"],
+                    default="pair",
                     help="pair: config-3 projector pair (the default bench line); "
                          "config2: CGLS vs WMG-GMRES on config 2; config4: slice-stack "
                          "throughput (separate JSON lines)")
@@ -198,6 +199,29 @@ def ncu_traffic():
         return {}
 
 
+def host_info():
+    """CPU model, logical cores and BLAS threading of the box."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for ln in fh:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    blas = None
+    try:
+        from threadpoolctl import threadpool_info
+        blas = [{"api": i.get("internal_api"), "threads": i.get("num_threads")}
+                for i in threadpool_info()]
+    except Exception:
+        pass
+    return {"cpu_model": model, "logical_cpus": os.cpu_count(),
+            "OPENBLAS_NUM_THREADS": os.environ.get("OPENBLAS_NUM_THREADS"),
+            "blas_threadpools": blas}
+
+
 # ------------------------------------------------------------ CPU baseline
 def cpu_pair_rate(n, d, m, k_angles, target_seconds=10.0, max_reps=50):
     """Reference algorithm on the host: exact CSR of W for k evenly spaced
@@ -222,7 +246,7 @@ def cpu_pair_rate(n, d, m, k_angles, target_seconds=10.0, max_reps=50):
     t_pair = t_tot / reps
     rays = w.shape[0]
     return {"value": rays / t_pair / 1e9, "unit": UNIT, "cores": cproj.num_threads(),
-            "kind": "port",
+            "kind": "port", "host": host_info(),
             "sample": f"{k_angles} of {m} angles (exact reference CSR rows), {reps} pairs, "
                       f"{t_pair * 1e3:.1f} ms/pair, nnz={w.nnz}; rate scales linearly in angles"}
 
@@ -254,7 +278,7 @@ def run_reference(args):
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": config_dict(n, d, m, 1, {"sample_angles": int(args.cpu_angles)}),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cproj.num_threads(),
-                             "kind": "port",
+                             "kind": "port", "host": host_info(),
                              "sample": f"{args.cpu_angles} of {m} angles per step, exact "
                                        f"reference CSR (nnz={w.nnz}), CSR SpMV pair"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
@@ -365,7 +389,7 @@ def cpu_wmg_cgls(b):
     t3 = time.perf_counter()
     return {"seconds": t2 - t1, "setup_seconds": t1 - t0, "iterations": rec.iterations[-1],
             "cgls_seconds": t3 - t2, "cgls_iterations": rec_c.iterations[-1],
-            "cores": cproj.num_threads(), "kind": "port",
+            "cores": cproj.num_threads(), "kind": "port", "host": host_info(),
             "sample": "full config-1 problem, reference smoother-free V-cycle (nu = 0)"}
 
 
@@ -487,17 +511,51 @@ def run_ours(args):
     if world > 1:
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
     t_tot, t_fwd, t_bwd, t_conc = [float(v) for v in tt.cpu()]
-    # both schedules compute the same step; report the faster (small grids with
-    # an L2 flush between steps can lose from the cross-stream joins)
-    concurrent = t_conc <= t_tot
-    t_val = t_conc if concurrent else t_tot
+    # ``value`` is the DEPENDENT schedule a Krylov iteration uses (A x, then
+    # A^T y, back to back on one stream); the two-stream schedule of the two
+    # independent config-3 products is reported beside it
+    t_val = t_tot
     ms_step = t_val / args.steps * 1e3
     rays_total = m * d
     value = rays_total * args.steps / t_val / 1e9
-    value_seq = rays_total * args.steps / t_tot / 1e9
+    value_seq = value
     value_conc = rays_total * args.steps / t_conc / 1e9
 
-    # ---- end to end through the public API with host buffers -------------
+    # ---- end to end through the drop-in call -----------------------------
+    # What a reference-style caller does (geometry.py:200-215 semantics): numpy
+    # vectors in, numpy vectors out, ``w @ x`` then ``w.T @ y``; every call
+    # copies its operand to HBM, runs the kernel and copies the result back
+    # before returning.  (Single rank: the sharded projector has no numpy path.)
+    e2e_dropin = None
+    if world == 1:
+        x_np = x_h.copy()
+        y_np = y_h.copy()
+        for _ in range(2):
+            sino_np = w @ x_np
+            img_np = w.T @ y_np
+        torch.cuda.synchronize(dev)
+        d0 = torch.cuda.Event(enable_timing=True)
+        d1 = torch.cuda.Event(enable_timing=True)
+        t0w = time.perf_counter()
+        d0.record(stream)
+        for _ in range(args.steps):
+            sino_np = w @ x_np
+            img_np = w.T @ y_np
+        d1.record(stream)
+        d1.synchronize()
+        t_dropin = d0.elapsed_time(d1) / 1e3
+        t_dropin_wall = time.perf_counter() - t0w
+        dropin_ok = bool(np.array_equal(sino_np, sino.cpu().numpy())
+                         and np.array_equal(img_np, img.cpu().numpy()))
+        e2e_dropin = {"value": rays_total * args.steps / t_dropin / 1e9, "unit": UNIT,
+                      "h2d_bytes_per_step": int(x_np.nbytes + y_np.nbytes),
+                      "d2h_bytes_per_step": int(sino_np.nbytes + img_np.nbytes),
+                      "ms_per_step": t_dropin / args.steps * 1e3,
+                      "wall_ms_per_step": t_dropin_wall / args.steps * 1e3,
+                      "call": "sino = w @ x; img = w.T @ y (float32 numpy in and out)",
+                      "verified_against_device": dropin_ok}
+
+    # ---- pipelined end to end (pinned host buffers, copies overlapped) ----
     pin_x = torch.from_numpy(x_h).pin_memory()
     pin_y = torch.from_numpy(y_h).pin_memory()
     out_s = torch.empty(M_loc, dtype=torch.float32).pin_memory()
@@ -594,48 +652,75 @@ def run_ours(args):
     last = args.steps & 1                  # buffer set of the last timed step (warm-up = 0)
     e2e_ok = bool(torch.equal(out_s2[last], sino.cpu()) and torch.equal(out_i2[last], img.cpu()))
 
-    # ---- roofline ---------------------------------------------------------
+    # ---- roofline ------------------------------------------
+    # Unit = one intersection update (one gathered operand + FMA + crossing
+    # arithmetic); a launch of either product does nnz(W_local) of them, nnz
+    # from an exact GPU counting pass of the reference walker.  Peak gather
+    # rate = SMs x 32 lanes x f_SM (fp32 operands).  The compulsory HBM bytes
+    # 4 (N + M) per launch are reported beside it (orders of magnitude below).
     peaks, peak_src = measured_peaks()
     hbm = float(peaks.get("hbm_gbs", 6650.0))
     clk = clocks.summary()
     f_sm = (clk["sm_mhz"] or peaks.get("sm_max_mhz", 1965.0)) * 1e6
     n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
-    nnz_total = int(round(4.0 / math.pi * m * n * n))    # (4/pi) m n^2, SURVEY A.1
+    wl = getattr(w, "local", w)
+    nnz_local = wl.nnz()
+    nnz_formula = 4.0 / math.pi * M_loc / d * n * n        # (4/pi) m n^2, SURVEY A.1
     fwd_avg, bwd_avg = t_fwd / args.steps, t_bwd / args.steps
     dom = "backward" if bwd_avg >= fwd_avg else "forward"
     t_dom = max(fwd_avg, bwd_avg)
-    bytes_dom = 4 * (Npix + M_loc)                       # read one operand, write the other
-    achieved = bytes_dom / t_dom / 1e9
-    upd_rate = (nnz_total / world) / t_dom               # intersection updates per second
     gather_peak = n_sm * 32 * f_sm
+    upd_rate = nnz_local / t_dom
+    bytes_launch = 4 * (Npix + M_loc)                    # read one operand, write the other
     traffic = ncu_traffic().get(f"{dom}_n{n}")
-    # per step: pad/transpose + forward (+ the axis-angle forward) + backward
-    # (+ the axis-angle backward) on symmetric grids (profiles/r1b_launches_*)
-    sym = bool(getattr(getattr(w, "local", w), "symmetric", False)) and n >= 1024
-    launches = args.steps * (5 if sym else 3)
+    pair_rate = 2 * nnz_local / (t_tot / args.steps)
+    # kernels launched per step, counted from one profiled step (outside the
+    # timed region)
+    from torch.profiler import ProfilerActivity, profile
+    torch.cuda.synchronize(dev)
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        step()
+        torch.cuda.synchronize(dev)
+    step_kernels = [e.name for e in prof.events() if e.device_type.name == "CUDA"
+                    and "nccl" not in e.name.lower() and "Memcpy" not in e.name
+                    and "Memset" not in e.name]
+    launches = args.steps * len(step_kernels)
+    e2e_pipe = {"value": e2e_value, "unit": UNIT, "verified_against_device": e2e_ok,
+                "h2d_bytes_per_step": 4 * (Npix + M_loc),
+                "d2h_bytes_per_step": 4 * (Npix + M_loc),
+                "schedule": "pinned host buffers, copies on their own streams (double-"
+                            "buffered), the two independent products on two streams"}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": config_dict(n, d, m, world),
-        "e2e": {"value": e2e_value, "unit": UNIT, "verified_against_device": e2e_ok,
-                "h2d_bytes_per_step": 4 * (Npix + M_loc),
-                "d2h_bytes_per_step": 4 * (Npix + M_loc)},
-        "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm,
-                     "unit": "GB/s", "frac": achieved / hbm, "traffic": traffic,
-                     "peak_source": peak_src},
-        "roofline_gather": {"kernel": dom, "achieved": upd_rate / 1e9,
-                            "peak": gather_peak / 1e9, "unit": "Gupdates/s",
-                            "frac": upd_rate / gather_peak,
-                            "definition": "SURVEY s8(d): 148 SMs x 32 lanes x f_SM"},
+        "e2e": e2e_dropin if e2e_dropin is not None else e2e_pipe,
+        "e2e_pipelined": e2e_pipe,
+        "roofline": {"bound": "gather", "kernel": dom, "achieved": upd_rate / 1e9,
+                     "peak": gather_peak / 1e9, "unit": "Gupdates/s",
+                     "frac": upd_rate / gather_peak,
+                     "traffic": traffic, "algorithmic_bytes": bytes_launch,
+                     "updates_per_launch": nnz_local,
+                     "definition": "SURVEY s8(d): exact nnz(W) intersection updates per "
+                                   "launch / launch time / (SMs x 32 lanes x f_SM)",
+                     "f_sm_mhz": f_sm / 1e6, "n_sm": n_sm},
+        "roofline_pair": {"achieved": pair_rate / 1e9, "peak": gather_peak / 1e9,
+                          "unit": "Gupdates/s", "frac": pair_rate / gather_peak,
+                          "definition": "2 nnz(W) per dependent pair / pair time"},
+        "roofline_hbm": {"kernel": dom, "achieved": bytes_launch / t_dom / 1e9, "peak": hbm,
+                         "unit": "GB/s", "frac": bytes_launch / t_dom / 1e9 / hbm,
+                         "peak_source": peak_src},
         "roofline_onchip": onchip_roofline(n, fwd_avg, bwd_avg, n_sm, f_sm, world),
-        "pair_schedule": "two streams" if concurrent else "one stream",
+        "nnz": {"exact_local": nnz_local, "formula_local": nnz_formula},
+        "pair_schedule": "one stream, dependent (A x then A^T y)",
         "value_two_streams": value_conc,
         "value_sequential": value_seq,
         "step_ms_sequential": {"median": step_ms[len(step_ms) // 2], "best": step_ms[0]},
-        "ms_per_step_sequential": t_tot / args.steps * 1e3,
+        "ms_per_step_two_streams": t_conc / args.steps * 1e3,
         "kernels_ms": {"forward": fwd_avg * 1e3, "backward": bwd_avg * 1e3},
         "gpu_launches": launches,
+        "kernels_per_step": sorted(set(step_kernels)),
         "clocks": clk,
     }
     if not args.no_wmg:
@@ -864,8 +949,60 @@ def run_config4(args):
     return 0
 
 
+def _relaunch_under_torchrun(args):
+    """``--gpus N`` (N > 1) without torchrun: re-run this command as N ranks,
+    one process per GPU (torch.distributed.run, NCCL, rendezvous on
+    127.0.0.1); rank 0 prints the JSON line.  Returns the launcher's exit code."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")       # NCCL init lines show the rank count
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    env.setdefault("OMP_NUM_THREADS", "1")
+    print(f"[bench] --gpus {args.gpus}: launching {args.gpus} ranks: {' '.join(cmd)}",
+          file=sys.stderr, flush=True)
+    return subprocess.run(cmd, env=env).returncode
+
+
+def _check_world(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+    return world
+
+
+def run_launch_check(args):
+    """``--workload launch-check``: rendezvous only (CPU-testable with
+    WMG_BENCH_BACKEND=gloo): every rank joins the process group, rank 0 prints
+    the world size the bench would time."""
+    import torch.distributed as dist
+    world = _check_world(args)
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1:
+        dist.init_process_group(os.environ.get("WMG_BENCH_BACKEND", "nccl"))
+        ranks = [None] * world
+        dist.all_gather_object(ranks, rank)
+        dist.destroy_process_group()
+    else:
+        ranks = [0]
+    if rank == 0:
+        print(json.dumps({"workload": "launch-check", "n_gpus": world, "ranks": ranks}),
+              flush=True)
+    return 0
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return _relaunch_under_torchrun(args)
+    _check_world(args)
+    if args.workload == "launch-check":
+        return run_launch_check(args)
     if args.impl == "reference":
         return run_reference(args)
     if args.workload == "config2":

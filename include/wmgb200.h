@@ -236,7 +236,10 @@ int wmg_spd_inverse_workspace(int batch, int p, size_t *bytes);
  * matrix.  info (device int[batch], written) = 0, or the order of the first
  * leading minor that is not positive definite (potrf's convention; G_b is then
  * garbage).  Replaces the reference's per-leaf potrf (sparse_kernels.py:53-65,
- * called at multilevel.py:125-137) plus the inverse the V-cycle's GEMV needs. */
+ * called at multilevel.py:125-137) plus the inverse the V-cycle's GEMV needs.
+ * Thread safety: calls are serialised by an internal lock (they share one
+ * per-device look-ahead stream and its events); callers on different streams
+ * are safe, their device work may overlap. */
 int wmg_spd_inverse(int batch, int p, double *G, long long strideG, int *info, void *work,
                     void *stream);
 

@@ -9,6 +9,7 @@ resident).
 from __future__ import annotations
 
 import ctypes
+import threading
 
 import numpy as np
 
@@ -57,13 +58,99 @@ def to_device(v, dtype=None, device=None):
             return out.contiguous(), False
         return v.to(device=device or "cuda", dtype=dtype).contiguous(), True
     a = np.ascontiguousarray(np.asarray(v), dtype=np.float64 if dtype == t.float64 else np.float32)
-    return t.from_numpy(a).to(device or "cuda", non_blocking=False), True
+    dev = t.device(device) if device is not None else t.device("cuda", t.cuda.current_device())
+    if a.nbytes >= _STAGE_MIN_BYTES:
+        return _h2d_staged(a, dtype, dev), True
+    return t.from_numpy(a).to(dev, non_blocking=False), True
+
+
+# Host <-> device copies of large numpy vectors (the reference-style call
+# ``w @ x`` with numpy in and out).  Measured on the B200 box (64-95 MB):
+# pageable H2D 10.9 GB/s, ``.cpu()`` D2H 2.1 GB/s; pinned copies 47-57 GB/s.
+# H2D: the array is copied into a cached pinned staging buffer by a few host
+# threads (numpy releases the GIL) and each slice's DMA is issued as soon as
+# it is staged.  D2H: into a block of torch's caching pinned-host allocator,
+# returned as a numpy view that keeps the block alive.
+_STAGE_MIN_BYTES = 4 << 20
+_STAGE_THREADS = 4
+_stage = {}
+_stage_lock = threading.Lock()
+_pool = None
+
+
+def _copy_pool():
+    global _pool
+    if _pool is None:
+        from concurrent.futures import ThreadPoolExecutor
+        _pool = ThreadPoolExecutor(_STAGE_THREADS, thread_name_prefix="wmg-stage")
+    return _pool
+
+
+def _h2d_staged(a, dtype, dev):
+    t = torch()
+    key = (str(dev), threading.get_ident())
+    with _stage_lock:
+        ent = _stage.get(key)
+    if ent is None or ent[0].numel() < a.nbytes:
+        buf = t.empty(max(a.nbytes, 1), dtype=t.uint8).pin_memory()
+        ent = (buf, t.cuda.Event())
+        with _stage_lock:
+            _stage[key] = ent
+    buf, done = ent
+    done.synchronize()                       # the previous DMA out of this buffer
+    host = buf[:a.nbytes].view(dtype)
+    hn = host.numpy()
+    out = t.empty(a.size, dtype=dtype, device=dev)
+    n = a.size
+    k = _STAGE_THREADS
+    bounds = [(i * n) // k for i in range(k + 1)]
+    futs = [_copy_pool().submit(np.copyto, hn[bounds[i]:bounds[i + 1]],
+                                a.reshape(-1)[bounds[i]:bounds[i + 1]]) for i in range(k)]
+    stream = t.cuda.current_stream(dev)
+    for i, f in enumerate(futs):
+        f.result()
+        out[bounds[i]:bounds[i + 1]].copy_(host[bounds[i]:bounds[i + 1]], non_blocking=True)
+    done.record(stream)
+    return out
 
 
 def to_caller(tensor, was_numpy):
     if was_numpy:
-        return tensor.detach().cpu().numpy()
+        tt = tensor.detach()
+        if tt.is_cuda and tt.numel() * tt.element_size() >= _STAGE_MIN_BYTES:
+            t = torch()
+            host = t.empty(tt.shape, dtype=tt.dtype, pin_memory=True)
+            host.copy_(tt, non_blocking=True)
+            t.cuda.current_stream(tt.device).synchronize()
+            return host.numpy()
+        return tt.cpu().numpy()
     return tensor
+
+
+_gc_lock = threading.Lock()
+_gc_depth = 0
+_gc_was_enabled = False
+
+
+def _gc_pause():
+    """Disable the cyclic GC while any thread captures (reference-counted:
+    concurrent captures from several host threads nest)."""
+    import gc
+    global _gc_depth, _gc_was_enabled
+    with _gc_lock:
+        if _gc_depth == 0:
+            _gc_was_enabled = gc.isenabled()
+            gc.disable()
+        _gc_depth += 1
+
+
+def _gc_resume():
+    import gc
+    global _gc_depth
+    with _gc_lock:
+        _gc_depth -= 1
+        if _gc_depth == 0 and _gc_was_enabled:
+            gc.enable()
 
 
 def capture_graph(fn, device):
@@ -71,7 +158,6 @@ def capture_graph(fn, device):
     and return (graph, fn's result).  Unlike ``torch.cuda.graph`` this does not
     empty the caching allocator first: a capture right after a hierarchy build
     would otherwise pay ~10 ms of cudaFree for the released setup buffers."""
-    import gc
     t = torch()
     cur = t.cuda.current_stream(device)
     side = t.cuda.Stream(device=device)
@@ -80,8 +166,7 @@ def capture_graph(fn, device):
     # no cyclic garbage collection while capturing: collecting an unreachable
     # earlier preconditioner would destroy its CUDA graph mid-capture, which
     # invalidates the capture
-    gc_was_enabled = gc.isenabled()
-    gc.disable()
+    _gc_pause()
     try:
         with t.cuda.stream(side):
             # thread-local capture: solves running concurrently in other host
@@ -92,8 +177,7 @@ def capture_graph(fn, device):
             finally:
                 g.capture_end()
     finally:
-        if gc_was_enabled:
-            gc.enable()
+        _gc_resume()
     cur.wait_stream(side)
     return g, out
 

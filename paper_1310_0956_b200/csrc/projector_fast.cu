@@ -1412,6 +1412,24 @@ __global__ void pad_transpose64_kernel(const T* __restrict__ in, double* __restr
     const int c = bx + i, r = by + threadIdx.x;
     if (r < n && c < n) PT[(long long)c * pitch + kPadMargin + r] = tile[threadIdx.x][i];
   }
+  // margins: rewritten every call (the workspace is shared with the generic
+  // path, which stores an unpadded transposed copy over them)
+  if (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1) {
+    for (int i = threadIdx.y; i < 32; i += 8) {
+      const int r = by + i;
+      if (r >= n) continue;
+      for (int k = threadIdx.x; k < kPadMargin; k += 32) {
+        if (blockIdx.x == 0) {
+          P[(long long)r * pitch + k] = 0.0;
+          PT[(long long)r * pitch + k] = 0.0;
+        }
+        if (blockIdx.x == gridDim.x - 1) {
+          P[(long long)r * pitch + kPadMargin + n + k] = 0.0;
+          PT[(long long)r * pitch + kPadMargin + n + k] = 0.0;
+        }
+      }
+    }
+  }
 }
 
 // Small-grid float64 forward on the padded planes: one ray per lane, kSplit

@@ -19,6 +19,7 @@
 // first non-positive one names the same leading minor as potrf's info.
 // Flops: p^3 per leaf (lower-triangle tiles only), all of it in 128x128x128
 // DMMA tile products; HBM: the lower triangle read and written once per step.
+#include <mutex>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -439,6 +440,14 @@ size_t spd_inverse_workspace(int batch, int p) {
 }
 
 namespace {
+// Serialises spd_inverse's host-side enqueue: the lazily created per-device
+// auxiliary stream, its fork/join events and the kernel attributes are shared
+// by every caller, so two threads (or two caller streams) enqueueing at once
+// would re-record each other's events between a record and the matching wait.
+// Under the lock each call enqueues its whole fork/join chain before the next
+// starts; the GPU work of concurrent calls may still overlap (a later call's
+// auxiliary items queue behind the earlier call's on the in-order aux stream).
+std::mutex g_spd_mutex;
 // per-device auxiliary stream + fork/join events of the look-ahead (created once)
 struct AuxStreams {
   cudaStream_t s = nullptr;
@@ -470,6 +479,7 @@ cudaError_t spd_inverse(int batch, int p, double* G, long long sG, int* info, do
                         cudaStream_t st) {
   using namespace spd;
   if (batch <= 0 || p <= 0) return cudaSuccess;
+  std::lock_guard<std::mutex> lock(g_spd_mutex);
   cudaError_t e;
   static bool attrs = false;
   if (!attrs) {

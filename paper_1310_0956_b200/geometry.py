@@ -232,9 +232,15 @@ class LineProjector:
         raise TypeError(f"unsupported dtype {tensor.dtype}")
 
     def _io_dtype(self, v):
+        """Vector dtype of a call: float64 (the reference's convention), except
+        that a float32 projector keeps float32 vectors float32 (CUDA tensors or
+        numpy arrays) -- half the bytes over PCIe and in HBM."""
         t = D.torch()
-        if D.is_torch(v) and v.is_cuda and v.dtype == t.float32 and self.precision == N.F32:
-            return t.float32
+        if self.precision == N.F32:
+            if D.is_torch(v) and v.dtype == t.float32:
+                return t.float32
+            if isinstance(v, np.ndarray) and v.dtype == np.float32:
+                return t.float32
         return t.float64 if (self.precision == N.F64 or not D.is_torch(v)) else v.dtype
 
     # ------------------------------------------------------------ operators
@@ -379,6 +385,15 @@ class LineProjector:
         indptr, cols, vals, _ = self.csr_device()
         return sp.csr_matrix((vals.cpu().numpy(), cols.cpu().numpy(), indptr.cpu().numpy()),
                              shape=self.shape)
+
+    def nnz(self) -> int:
+        """Exact number of stored entries of W (the reference CSR's nnz), from a
+        GPU counting pass of the exact walker (no CSR is formed)."""
+        t = D.torch()
+        counts = t.empty(self.shape[0], dtype=t.int64, device=self.device)
+        anomaly = t.zeros(1, dtype=t.int32, device=self.device)
+        N.call("wmg_csr_counts", self._h, D.ptr(counts), D.ptr(anomaly), D.stream_handle())
+        return int(counts.sum().item())
 
     def anomaly_count(self):
         """Parity-walk consistency counter over one forward + backward pass."""

@@ -441,6 +441,9 @@ def _cgls_graphed(w, bd, x, lam, precond, cfg, errs, was_np, record, t0):
         if cache is not None:
             cache[key] = ctx
     r, q, s, s_old, S, S_host = (ctx[k] for k in ("r", "q", "s", "s_old", "S", "S_host"))
+    # every solve starts from clean scalars: S[8] is the sticky breakdown flag
+    # wmg_cgls_scalars sets, and a cached context must not carry it over
+    S.zero_()
     # A preconditioner that already holds its own captured graph (captured at
     # construction, i.e. in the setup) is replayed between two captured halves
     # of the iteration instead of being re-captured inside it.

@@ -1,0 +1,91 @@
+"""Parity of the fp32 projector pair at the sizes the bench measures.
+
+The bench line (``bench.py``) times BASELINE config 3 at n = 4096 (4096 angles,
+5793 detectors, float32) through the DEFAULT dispatch: the mirror-packed
+symmetric forward ``fwd_sym_kernel`` and the eight-image backprojector
+``bwd_sym8_kernel``.  These tests run exactly that dispatch (asserted from the
+CUDA kernel names the profiler records) on the bench's own inputs and compare:
+
+* forward rows of >= 8 angles (0, pi/4, pi/2, 3pi/4, ... and the mirror /
+  transposition partners) against the pinned CPU oracle
+  (``oracle.cproj.forward``, bit-identical to the reference ``W @ x`` of
+  /root/reference/pkg/src/wmgtomo/geometry.py:200-206 on exact angle subsets),
+  within 1e-5 relative per angle and over the set;
+* the full sinogram against the float64 PARITY forward (bit-identical to the
+  reference on every golden case), within 1e-5;
+* the full backprojection against the float64 parity backprojector
+  (geometry.py:209-215), within 1e-5;
+* the adjoint identity <W x, y> = <x, W^T y> of the fp32 pair, within 1e-6.
+
+Repeated at n = 2048 (2048 angles, 2897 detectors), the next config-3 size,
+which takes the same kernels.
+"""
+import math
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _kernel_names(torch, fn):
+    from torch.profiler import ProfilerActivity, profile
+    torch.cuda.synchronize()
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        fn()
+        torch.cuda.synchronize()
+    return {e.name for e in prof.events() if e.device_type.name == "CUDA"}
+
+
+def _angle_sample(m):
+    q = m // 8
+    idx = {0, q, 2 * q, 3 * q, 4 * q, 5 * q, 6 * q, 7 * q,     # 0, pi/8, ..., 7pi/8
+           1, m - 1, m // 2 - 1, m // 2 + 1, 1025 % m, 3069 % m}
+    return np.array(sorted(idx))
+
+
+@pytest.mark.parametrize("n", [4096, 2048])
+def test_default_dispatch_pair_vs_oracle(gpu, oracle_proj, n):
+    torch = gpu
+    from paper_1310_0956_b200.geometry import build_geometry, build_projector
+    m, d = n, int(math.ceil(n * math.sqrt(2.0)))
+    g = build_geometry(n, d, m)
+    w = build_projector(g, precision="float32")
+    assert w.symmetric and w.transposition_closed
+    x = np.random.default_rng(3000).uniform(0.0, 1.0, n * n).astype(np.float32)
+    y = np.random.default_rng(3001).uniform(0.0, 1.0, m * d).astype(np.float32)
+    xd = torch.from_numpy(x).cuda()
+    yd = torch.from_numpy(y).cuda()
+    sino = torch.empty(m * d, dtype=torch.float32, device="cuda")
+    img = torch.empty(n * n, dtype=torch.float32, device="cuda")
+
+    names_f = _kernel_names(torch, lambda: w.forward_(xd, sino))
+    names_b = _kernel_names(torch, lambda: w.backward_(yd, img))
+    assert any("fwd_sym_kernel" in k for k in names_f), sorted(names_f)
+    assert any("bwd_sym8_kernel" in k for k in names_b), sorted(names_b)
+
+    got_f = sino.double().cpu().numpy().reshape(m, d)
+    got_b = img.double().cpu().numpy()
+    x64, y64 = x.astype(np.float64), y.astype(np.float64)
+
+    # (1) forward rows of sampled angles vs the oracle (exact reference rows)
+    idx = _angle_sample(m)
+    assert {0, m // 4, m // 2, 3 * m // 4} <= set(idx.tolist())
+    ref_rows = oracle_proj.forward(n, d, g.angles[idx], x64).reshape(idx.size, d)
+    for k, a in enumerate(idx):
+        r = ref_rows[k]
+        assert np.linalg.norm(got_f[a] - r) <= 1e-5 * np.linalg.norm(r), int(a)
+    assert np.linalg.norm(got_f[idx] - ref_rows) <= 1e-5 * np.linalg.norm(ref_rows)
+
+    # (2) full sinogram and (3) full backprojection vs the float64 parity kernels
+    wp = build_projector(g)
+    ref_f = wp.forward(torch.from_numpy(x64).cuda()).cpu().numpy().reshape(m, d)
+    assert np.array_equal(ref_f[idx], ref_rows)          # parity kernel == oracle rows
+    assert np.linalg.norm(got_f - ref_f) <= 1e-5 * np.linalg.norm(ref_f)
+    ref_b = wp.backward(torch.from_numpy(y64).cuda()).cpu().numpy()
+    assert np.linalg.norm(got_b - ref_b) <= 1e-5 * np.linalg.norm(ref_b)
+
+    # (4) adjoint identity of the fp32 pair
+    lhs = float(np.dot(got_f.ravel(), y64))
+    rhs = float(np.dot(x64, got_b))
+    assert abs(lhs - rhs) <= 1e-6 * abs(lhs)
