@@ -6,6 +6,16 @@ Follows /root/reference/pkg/src/wmgtomo/multilevel.py:
   node factors P_child = P R_band^T with the 1e-15 drop     (:123-148, sparse_kernels.py:30-39)
   leaf Gram P^T P + lam I, lower Cholesky                    (:125-130, sparse_kernels.py:53-65)
   wtg_apply hybrid / multiplicative                          (:175-198)
+  + the SIRT-type node smoother of the WMG-CGLS configurations (BASELINE
+    configs 1/2/4 "2+2 SIRT sweeps per level"; NOT defined by the reference,
+    whose only sweep is the TG smoother at :241-242 -- SURVEY.md s8 a16
+    option (ii)), restating paper_1310_0956_b200/multilevel.py's definition:
+      C_p = 1 / (2^-k * block sums of W's column sums)   (zero -> 0)
+      omega_p = 0.95 / lambda_max(C_p A_p), 10 power iterations from the fixed
+                start vector v_i = 1 + ((7919 i) mod 1013) / 1013, DET_SUM
+                norms / dots (oracle/solvers.py)
+      node solve: nu_pre sweeps z += omega_p C_p (r - A_p z) from z = 0, the
+                wavelet two-grid correction of the residual, nu_post sweeps.
 Leaf factors are kept Fortran-ordered so cho_solve does not copy them (the
 reference's C-ordered factors make each solve ~20x slower; the
 arithmetic is identical).
@@ -41,7 +51,11 @@ def _spgemm(a, b):
 class Node:
     def __init__(self, p, side, level, levels, lam, path):
         self.side, self.path, self.lam = side, path, lam
+        self.depth = level - 1
         self.children = {}
+        self.c = None
+        self.omega = 0.0
+        self.nu_pre = self.nu_post = 0
         if level == levels:
             gram = (p.T @ p).toarray()
             if lam != 0:
@@ -65,14 +79,64 @@ class Node:
         return out
 
 
-def build_hierarchy(w, n, lam, levels):
-    return Node(w.tocsr(), n, 1, levels, lam, "")
+def start_vector(dim):
+    i = np.arange(dim, dtype=np.int64)
+    return 1.0 + ((i * 7919) % 1013).astype(np.float64) / 1013.0
+
+
+def _nodes(node):
+    yield node
+    for b in BANDS:
+        if b in node.children:
+            yield from _nodes(node.children[b])
+
+
+def setup_smoothers(root, w, n, nu_pre, nu_post, power_iterations=10):
+    from .solvers import det_dot, det_sq
+    colsum = w.T @ np.ones(w.shape[0])            # bitwise the reference's W^T 1
+    for nd in _nodes(root):
+        if nd.lower is not None:
+            continue
+        k = nd.depth
+        B = 1 << k
+        blk = colsum.reshape(n // B, B, n // B, B).sum(axis=(1, 3)).reshape(-1)
+        blk = blk * (0.5 ** k)
+        with np.errstate(divide="ignore"):
+            nd.c = np.where(blk > 0, 1.0 / blk, 0.0)
+        v = start_vector(nd.side * nd.side)
+        lam = None
+        for _ in range(power_iterations):
+            v = v / np.sqrt(det_sq(v))
+            out = nd.apply_system(v) * nd.c
+            lam = det_dot(v, out)
+            v = out
+        nd.omega = 0.95 / lam if lam > 0 else 0.0
+        nd.nu_pre, nd.nu_post = nu_pre, nu_post
+
+
+def build_hierarchy(w, n, lam, levels, nu_pre=0, nu_post=0):
+    root = Node(w.tocsr(), n, 1, levels, lam, "")
+    if nu_pre or nu_post:
+        setup_smoothers(root, w, n, nu_pre, nu_post)
+    return root
 
 
 def _solve(node, r, mult):
     if node.lower is not None:
         return scipy.linalg.cho_solve((node.lower, True), r, check_finite=False)
-    return wtg_apply(node, r, mult)
+    if node.nu_pre == 0 and node.nu_post == 0:
+        return wtg_apply(node, r, mult)
+    z = np.zeros_like(r)
+    for _ in range(node.nu_pre):
+        z = z + node.omega * (node.c * (r - node.apply_system(z)))
+    if node.nu_pre:
+        e = wtg_apply(node, r - node.apply_system(z), mult)
+        z = z + e
+    else:
+        z = wtg_apply(node, r, mult)
+    for _ in range(node.nu_post):
+        z = z + node.omega * (node.c * (r - node.apply_system(z)))
+    return z
 
 
 def wtg_apply(node, r, multiplicative=False):
@@ -87,4 +151,5 @@ def wtg_apply(node, r, multiplicative=False):
 
 
 def preconditioner(root, multiplicative=False):
-    return lambda v: wtg_apply(root, np.asarray(v, dtype=np.float64), multiplicative)
+    # the root is an internal node: with nu = 0 this is exactly wtg_apply(root, v)
+    return lambda v: _solve(root, np.asarray(v, dtype=np.float64), multiplicative)

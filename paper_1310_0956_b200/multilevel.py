@@ -437,32 +437,52 @@ class _LazyIntergrid:
         return self._set[band]
 
 
+def smoother_start_vector(dim: int) -> np.ndarray:
+    """Fixed, positive start vector of the smoother's power iteration:
+    v_i = 1 + ((7919 i) mod 1013) / 1013 (integer arithmetic and one IEEE
+    division -- identical on every host)."""
+    i = np.arange(dim, dtype=np.int64)
+    return 1.0 + ((i * 7919) % 1013).astype(np.float64) / 1013.0
+
+
+def smoother_scaling(colsum_host: np.ndarray, n: int, depth: int) -> np.ndarray:
+    """C_p of a node at band-path depth k: 1 / (2^-k * the sum of W's column
+    sums over each 2^k x 2^k block of fine pixels), zero sums -> 0 (the SIRT
+    convention of solvers.py:84-85).  Host numpy, so the result is bitwise the
+    same wherever it is evaluated."""
+    B = 1 << depth
+    blk = colsum_host.reshape(n // B, B, n // B, B).sum(axis=(1, 3)).reshape(-1)
+    blk = blk * (0.5 ** depth)
+    with np.errstate(divide="ignore"):
+        return np.where(blk > 0, 1.0 / blk, 0.0)
+
+
 def _setup_smoothers(h: WmgHierarchy, power_iterations: int = 10):
-    """C_p and omega_p for the SIRT-type node smoother (see module docstring)."""
+    """C_p and omega_p = 0.95 / lambda_max(C_p A_p) for the SIRT-type node
+    smoother (module docstring).  Deterministic: C_p from the column sums (bit-
+    identical to the reference's W^T 1) summed on the host, lambda_max from
+    ``power_iterations`` steps from ``smoother_start_vector`` with DET_SUM norms
+    and dots (oracle/multilevel.py restates the same procedure)."""
     t = D.torch()
     w = h.projector
-    colsum = w.col_sums_dev().view(h.n, h.n)
-    gen = t.Generator(device=w.device)
-    gen.manual_seed(1234)
+    colsum = w.col_sums_dev().cpu().numpy()
     for nd in h.nodes():
         if nd.is_coarsest:
             continue
         k = len(nd.bands)
-        B = 1 << k
-        blk = colsum.view(h.n // B, B, h.n // B, B).sum(dim=(1, 3)).reshape(-1)
-        blk = blk * (0.5 ** k)
-        c = t.where(blk > 0, 1.0 / blk, t.zeros_like(blk))
+        c = t.from_numpy(smoother_scaling(colsum, h.n, k)).to(w.device)
         nd.smooth_c = c.contiguous()
-        v = t.rand(nd.dim, dtype=t.float64, device=w.device, generator=gen)
+        v = t.from_numpy(smoother_start_vector(nd.dim)).to(w.device)
         out = t.empty_like(v)
         lam = None
         for _ in range(power_iterations):
-            v = v / v.norm()
+            nrm = D.det_norm_sq(v).sqrt_()
+            v = v / nrm
             nd.apply_system_(v, out)
             out.mul_(c)
-            lam = v.dot(out)                 # stays on the device: one read at the end
+            lam = D.det_dot(v, out)            # stays on the device: one read at the end
             v = out.clone()
-        lam_max = float(lam) if lam is not None else 1.0
+        lam_max = float(lam.item()) if lam is not None else 1.0
         nd.smooth_omega = 0.95 / lam_max if lam_max > 0 else 0.0
 
 

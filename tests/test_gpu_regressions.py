@@ -17,7 +17,7 @@ def test_graphed_cgls_recovers_after_breakdown(gpu):
     cfg = SolverConfig(max_iterations=30)
     _, rec_ok = cgls_solve(w, b, cfg=cfg)
     bad = b.copy()
-    bad[bad.size // 2] = np.nan        # a central ray (edge rays miss the grid)
+    bad[45 * 91 + 45] = np.nan          # the central ray of angle 45 (edge rays miss the grid)
     _, rec_bad = cgls_solve(w, bad, cfg=cfg)
     assert rec_bad.status == "breakdown"
     _, rec = cgls_solve(w, b, cfg=cfg)
