@@ -243,6 +243,28 @@ int wmg_spd_inverse_workspace(int batch, int p, size_t *bytes);
 int wmg_spd_inverse(int batch, int p, double *G, long long strideG, int *info, void *work,
                     void *stream);
 
+/* Dense Cholesky factorization (LAPACK potrf, lower) of `batch` SPD matrices
+ * G_b (p x p row-major float64 at G + b * strideG; p % 128 == 0 -- pad with an
+ * identity block otherwise; only the lower triangle is read), in place: on
+ * return G_b = L_b with zeros above the diagonal.  Right-looking, 128-blocks,
+ * panel and trailing update on the fp64 tensor cores (DMMA).  dinv (device,
+ * batch * wmg_cholesky_dinv_elems(p) doubles, written) receives the inverses
+ * of the 128 x 128 diagonal blocks of L_b for wmg_cholesky_solve.  info
+ * (device int[batch], written) = 0 or the order of the first leading minor
+ * that is not positive definite (potrf's info).  Replaces scipy.linalg.
+ * cholesky(lower=True) in cholesky_factor (sparse_kernels.py:53-65). */
+int wmg_cholesky_dinv_elems(int p, long long *elems);
+int wmg_cholesky_factor(int batch, int p, double *G, long long strideG, double *dinv, int *info,
+                        void *stream);
+
+/* Solve L_b L_b^T Z = B_b in place (LAPACK potrs): B_b is p x nrhs row-major
+ * at B + b * strideB; L, dinv from wmg_cholesky_factor; p <= 12800.  One CTA
+ * per (right-hand side, matrix), blocked forward / backward substitution in a
+ * fixed summation order (bit-reproducible).  Replaces cho_solve in
+ * cholesky_solve (sparse_kernels.py:68-75). */
+int wmg_cholesky_solve(int batch, int p, const double *L, long long strideL, const double *dinv,
+                       double *B, long long strideB, int nrhs, void *stream);
+
 /* Packed symmetric storage (p % 128 == 0): the lower 128 x 128 tiles of a
  * symmetric matrix, tile (I, J), I >= J, at index I (I + 1) / 2 + J, each
  * row-major, diagonal tiles full.  *elems_per_matrix = doubles per packed

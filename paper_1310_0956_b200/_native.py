@@ -78,6 +78,9 @@ _SIGS = {
     "wmg_leaf_gram": (_i, [_vp, _i, ctypes.POINTER(_i), _dp, _dp, _vp]),
     "wmg_spd_inverse_workspace": (_i, [_i, _i, ctypes.POINTER(ctypes.c_size_t)]),
     "wmg_spd_inverse": (_i, [_i, _i, _dp, _ll, _dp, _dp, _vp]),
+    "wmg_cholesky_dinv_elems": (_i, [_i, ctypes.POINTER(_ll)]),
+    "wmg_cholesky_factor": (_i, [_i, _i, _dp, _ll, _dp, _dp, _vp]),
+    "wmg_cholesky_solve": (_i, [_i, _i, _dp, _ll, _dp, _dp, _ll, _i, _vp]),
     "wmg_packed_sym_sizes": (_i, [_i, _i, ctypes.POINTER(_ll), ctypes.POINTER(ctypes.c_size_t)]),
     "wmg_sym_pack": (_i, [_i, _i, _dp, _ll, _dp, _ll, _vp]),
     "wmg_packed_symv": (_i, [_i, _i, _dp, _ll, _dp, _ll, _dp, _ll, _dp, _vp]),

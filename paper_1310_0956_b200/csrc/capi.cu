@@ -67,6 +67,10 @@ cudaError_t leaf_factor(const GeomDev&, int, const int*, long long, long long, d
 cudaError_t leaf_gram(const GeomDev&, int, const int*, double*, int*, cudaStream_t);
 size_t spd_inverse_workspace(int, int);
 cudaError_t spd_inverse(int, int, double*, long long, int*, double*, cudaStream_t);
+size_t cholesky_dinv_elems(int);
+cudaError_t cholesky_factor(int, int, double*, long long, double*, int*, cudaStream_t);
+cudaError_t cholesky_solve(int, int, const double*, long long, const double*, double*, long long,
+                           int, cudaStream_t);
 size_t packed_sym_elems(int);
 size_t packed_symv_scratch(int, int);
 cudaError_t sym_pack(int, int, const double*, long long, double*, long long, cudaStream_t);
@@ -709,6 +713,37 @@ int wmg_spd_inverse(int batch, int p, double* G, long long strideG, int* info, v
   if (batch > 65535) return fail(WMG_EINVAL, "batch > 65535");
   return cuda_rc(wmg::spd_inverse(batch, p, G, strideG, info, static_cast<double*>(work),
                                   STREAM(stream)));
+}
+
+int wmg_cholesky_dinv_elems(int p, long long* elems) {
+  REQ(elems);
+  if (p < 0) return fail(WMG_EINVAL, "negative size");
+  if (p % 128) return fail(WMG_EINVAL, "p must be a multiple of 128 (pad with identity)");
+  *elems = (long long)wmg::cholesky_dinv_elems(p);
+  return WMG_OK;
+}
+
+int wmg_cholesky_factor(int batch, int p, double* G, long long strideG, double* dinv, int* info,
+                        void* stream) {
+  REQ(G && dinv && info);
+  if (batch < 0 || p < 0) return fail(WMG_EINVAL, "negative size");
+  if (p % 128) return fail(WMG_EINVAL, "p must be a multiple of 128 (pad with identity)");
+  if (batch > 1 && strideG < (long long)p * p) return fail(WMG_EDIM, "batch stride < p*p");
+  if (batch > 65535) return fail(WMG_EINVAL, "batch > 65535");
+  return cuda_rc(wmg::cholesky_factor(batch, p, G, strideG, dinv, info, STREAM(stream)));
+}
+
+int wmg_cholesky_solve(int batch, int p, const double* L, long long strideL, const double* dinv,
+                       double* B, long long strideB, int nrhs, void* stream) {
+  REQ(L && dinv && B);
+  if (batch < 0 || p < 0 || nrhs < 0) return fail(WMG_EINVAL, "negative size");
+  if (p % 128) return fail(WMG_EINVAL, "p must be a multiple of 128 (pad with identity)");
+  if (p > 12800) return fail(WMG_EINVAL, "p > 12800 (solve keeps two p-vectors in shared memory)");
+  if (batch > 1 && (strideL < (long long)p * p || strideB < (long long)p * nrhs))
+    return fail(WMG_EDIM, "batch stride too small");
+  if (batch > 65535 || nrhs > 65535) return fail(WMG_EINVAL, "batch or nrhs > 65535");
+  return cuda_rc(wmg::cholesky_solve(batch, p, L, strideL, dinv, B, strideB, nrhs,
+                                     STREAM(stream)));
 }
 
 int wmg_packed_sym_sizes(int batch, int p, long long* elems_per_matrix, size_t* scratch_bytes) {

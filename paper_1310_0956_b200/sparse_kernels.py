@@ -3,8 +3,9 @@
 Mirrors /root/reference/pkg/src/wmgtomo/sparse_kernels.py:
   * ``DimensionMismatchError`` / ``NotPositiveDefiniteError`` (:22-27),
   * ``DenseFactorization`` / ``cholesky_factor`` / ``cholesky_solve`` (:42-75),
-    here holding a float64 lower factor in HBM (cuSOLVER potrf through torch)
-    and solving with two triangular solves on the device,
+    here holding a float64 lower factor in HBM, factored and solved by the
+    hand-written ``wmg_cholesky_factor`` / ``wmg_cholesky_solve`` kernels
+    (csrc/cholesky.cu: blocked potrf with DMMA panel/update, blocked potrs),
   * ``spd_inverse_``: the WMG leaves' batched SPD inverse on the fp64 tensor
     cores (hand-written DMMA sweep, ``wmg_spd_inverse``).
 ``spgemm`` / ``seeded_uniform`` are not on the B200 path (the hierarchy is
@@ -35,13 +36,17 @@ class DenseFactorization:
     Immutable like the reference's frozen dataclass.
     """
 
-    __slots__ = ("dimension", "_lower", "_inv", "_gram")
+    __slots__ = ("dimension", "_lower", "_inv", "_gram", "_padded", "_np")
 
-    def __init__(self, dimension: int, lower=None, inverse=None, gram=None):
+    def __init__(self, dimension: int, lower=None, inverse=None, gram=None, padded=None,
+                 was_numpy=False):
         object.__setattr__(self, "dimension", dimension)
         object.__setattr__(self, "_lower", lower)
         object.__setattr__(self, "_inv", inverse)   # dense tensor or PackedSymmetric
         object.__setattr__(self, "_gram", gram)
+        # (padded factor (b, q, q), diagonal-block inverses, q) of wmg_cholesky_factor
+        object.__setattr__(self, "_padded", padded)
+        object.__setattr__(self, "_np", bool(was_numpy))
 
     @property
     def inverse(self):
@@ -57,13 +62,28 @@ class DenseFactorization:
     def __repr__(self):
         return f"DenseFactorization(dimension={self.dimension})"
 
+    def _ensure_factor(self):
+        """Factor the kept Gram on first use (leaves built by spd_inverse_)."""
+        if self._padded is None and self._gram is not None:
+            g = self._gram
+            gl = g.tril()
+            full = gl + gl.tril(-1).transpose(-1, -2)
+            f = cholesky_factor(full)
+            object.__setattr__(self, "_lower", f._lower)
+            object.__setattr__(self, "_padded", f._padded)
+        if self._padded is None and self._lower is not None:
+            raise ValueError("factorization has no device factor")
+
     @property
     def lower(self):
-        if self._lower is None and self._gram is not None:
-            import torch
-            low, _ = torch.linalg.cholesky_ex(self._gram)
-            object.__setattr__(self, "_lower", low)
-        return self._lower
+        """The lower Cholesky factor (zeros above the diagonal), in the caller's
+        array type (numpy when the factored matrix was numpy)."""
+        if self._lower is None:
+            self._ensure_factor()
+        low = self._lower
+        if low is not None and self._np:
+            return low.cpu().numpy()
+        return low
 
     def solve(self, rhs):
         return cholesky_solve(self, rhs)
@@ -220,48 +240,109 @@ def batched_gemv(A, x, out=None):
     return y if x.dim() == 2 else y.view(p)
 
 
+def _pad_order(p: int) -> int:
+    return -(-p // 128) * 128
+
+
 def cholesky_factor(g, sym_tol: float = 1e-10) -> DenseFactorization:
-    """Factor dense SPD matrices (torch CUDA tensor, (d,d) or (b,d,d)).
+    """Factor dense SPD matrices: numpy or torch, (d, d) or (b, d, d).
 
     Same contract as the reference (sparse_kernels.py:53-65): non-square ->
     DimensionMismatchError; asymmetric beyond sym_tol * max|G| or not positive
-    definite -> NotPositiveDefiniteError.
+    definite -> NotPositiveDefiniteError.  The factorization runs on the GPU
+    (``wmg_cholesky_factor``: blocked potrf, DMMA panel and trailing update);
+    orders that are not a multiple of 128 are factored through an identity-
+    padded copy.  ``lower`` is returned in the caller's array type.
     """
+    import ctypes
+
     import torch
 
-    g = torch.as_tensor(g)
-    if g.dim() not in (2, 3) or g.shape[-1] != g.shape[-2]:
-        raise DimensionMismatchError(f"cholesky_factor: matrix is not square {tuple(g.shape)}")
-    if not g.is_cuda:
-        raise RuntimeError("cholesky_factor: expects a CUDA tensor (no CPU fallback)")
-    g = g.to(torch.float64)
+    from . import _device as D
+    from . import _native as N
+    was_np = not isinstance(g, torch.Tensor)
+    if was_np:
+        import numpy as np
+        ga = np.asarray(g, dtype=np.float64)
+        if ga.ndim not in (2, 3) or ga.shape[-1] != ga.shape[-2]:
+            raise DimensionMismatchError(f"cholesky_factor: matrix is not square {ga.shape}")
+        D.require_cuda()
+        g = torch.from_numpy(np.ascontiguousarray(ga)).cuda()
+    else:
+        if g.dim() not in (2, 3) or g.shape[-1] != g.shape[-2]:
+            raise DimensionMismatchError(
+                f"cholesky_factor: matrix is not square {tuple(g.shape)}")
+        D.require_cuda()
+        g = g.to(device="cuda" if not g.is_cuda else g.device, dtype=torch.float64)
     if g.numel():
         scale = g.abs().amax()
         asym = (g - g.transpose(-1, -2)).abs().amax()
         if float(scale) and float(asym) > sym_tol * float(scale):
             raise NotPositiveDefiniteError("matrix is not symmetric")
-    lower, info = torch.linalg.cholesky_ex(g)
-    bad = int(info.max()) if info.numel() else 0
-    if bad > 0:
+    g3 = g if g.dim() == 3 else g.unsqueeze(0)
+    b, p = g3.shape[0], g3.shape[-1]
+    if p == 0 or b == 0:
+        return DenseFactorization(dimension=p, lower=g.clone(), was_numpy=was_np)
+    q = _pad_order(p)
+    work = torch.zeros((b, q, q), dtype=torch.float64, device=g.device)
+    work[:, :p, :p].copy_(g3)
+    if q != p:
+        work.diagonal(dim1=1, dim2=2)[:, p:].fill_(1.0)
+    elems = ctypes.c_longlong()
+    N.call("wmg_cholesky_dinv_elems", q, ctypes.byref(elems))
+    dinv = torch.empty((b, elems.value), dtype=torch.float64, device=g.device)
+    info = torch.empty(b, dtype=torch.int32, device=g.device)
+    N.call("wmg_cholesky_factor", b, q, D.ptr(work), q * q, D.ptr(dinv), D.ptr(info),
+           D.stream_handle())
+    bad = info.cpu()
+    if int(bad.max()) > 0:
+        i = int(bad.argmax())
+        where = f"matrix {i}: " if b > 1 else ""
         raise NotPositiveDefiniteError(
-            f"leading minor of order {bad} is not positive definite")
-    return DenseFactorization(dimension=int(g.shape[-1]), lower=lower)
+            f"{where}leading minor of order {int(bad[i])} is not positive definite")
+    lower = work[:, :p, :p] if q != p else work
+    if g.dim() == 2:
+        lower = lower[0]
+    return DenseFactorization(dimension=p, lower=lower, padded=(work, dinv, q),
+                              was_numpy=was_np)
 
 
 def cholesky_solve(f: DenseFactorization, rhs):
-    """Solve L L^T z = rhs on the device; rhs (d,), (d,k), (b,d) or (b,d,k)."""
+    """Solve L L^T z = rhs on the device (``wmg_cholesky_solve``: blocked
+    forward / backward substitution, fixed summation order); rhs (d,), (d, k)
+    -- the reference's shapes (sparse_kernels.py:68-75) -- or, for batched
+    factors, (b, d) / (b, d, k).  Returns the caller's array type."""
     import torch
 
-    rhs = torch.as_tensor(rhs)
-    if rhs.shape[-1] != f.dimension and (rhs.dim() < 2 or rhs.shape[-2] != f.dimension):
+    from . import _device as D
+    from . import _native as N
+    was_np = not isinstance(rhs, torch.Tensor)
+    r = torch.as_tensor(rhs, dtype=torch.float64) if was_np else rhs.to(torch.float64)
+    p = f.dimension
+    pk = f._padded
+    batched = pk is not None and pk[0].shape[0] > 1 or (f._lower is not None and
+                                                          f._lower.dim() == 3)
+    if batched:
+        ok = r.dim() in (2, 3) and r.shape[1] == p
+    else:
+        ok = r.dim() in (1, 2) and r.shape[0] == p
+    if not ok:
         raise DimensionMismatchError(
-            f"cholesky_solve: rhs length {rhs.shape[-1]} != dimension {f.dimension}")
-    L = f.lower
-    if L.dim() == 2:
-        if rhs.dim() == 1:
-            return torch.cholesky_solve(rhs.unsqueeze(1), L).squeeze(1)
-        return torch.cholesky_solve(rhs, L)
-    # batched factors: rhs (b, d) or (b, d, k)
-    if rhs.dim() == 2:
-        return torch.cholesky_solve(rhs.unsqueeze(2), L).squeeze(2)
-    return torch.cholesky_solve(rhs, L)
+            f"cholesky_solve: rhs shape {tuple(r.shape)} does not match dimension {p}")
+    if pk is None:
+        f._ensure_factor()
+        pk = f._padded
+    work, dinv, q = pk
+    b = work.shape[0]
+    dev = work.device
+    r3 = r.reshape(b, p, -1) if batched else r.reshape(1, p, -1)
+    k = r3.shape[-1]
+    B = torch.zeros((b, q, k), dtype=torch.float64, device=dev)
+    B[:, :p, :].copy_(r3)
+    if k and p:
+        N.call("wmg_cholesky_solve", b, q, D.ptr(work), q * q, D.ptr(dinv), D.ptr(B), q * k, k,
+               D.stream_handle())
+    out = B[:, :p, :].reshape(r.shape)
+    if was_np:
+        return out.cpu().numpy()
+    return out.to(r.device) if r.device != dev else out
