@@ -361,10 +361,12 @@ int wmg_geometry_symmetry(wmg_geometry* g, int set, int* enabled) {
   // forced mode: +8 row-layout backprojector, +16 one-angle forward blocks,
   // +256 the 8x4-block float4-window backprojector, +512 / +1024 run layout with
   // R = 4 / R = 8 rows per thread at any size, +8192 / +16384 the eight-image
-  // backprojector forced at any size / disabled
+  // backprojector forced at any size / disabled, +32768 (with +16384) the run
+  // layout without the small-grid angle-split cluster, +65536 the symmetric
+  // forward without the small-grid row-segment split
   if (set == 0 || set == 1 || set == 2 || set == 4 || set == 10 || set == 18 || set == 26 || set == 34 || set == 66 || set == 130 ||
       set == 258 || set == 514 || set == 1026 || set == 8194 ||
-      set == 16386)
+      set == 16386 || set == 49154 || set == 65538)
     g->dev.sym = (set && g->sym_capable) ? set : 0;
   if (enabled) *enabled = g->dev.sym;
   return WMG_OK;

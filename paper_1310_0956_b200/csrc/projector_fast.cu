@@ -819,11 +819,18 @@ __global__ void __launch_bounds__(256, 5) bwd_sym_kernel(GeomDev G, const TIn* _
 // wavefronts of the float4 windows.  A half-warp is 16 consecutive columns of
 // one row: its detector indices span <= 16 consecutive entries, so the LDS.64
 // are conflict-free (2 wavefronts each).  Tile: 32 columns x 8R rows.
-template <typename TIn, typename TOut, bool kAccumulate, int R>
+//
+// kCluster (small grids, where the quadrant has too few tiles to fill the
+// SMs): the nsplit CTAs of a tile form a thread-block cluster along z, each
+// walking a contiguous slice of the primary angles; the partial tiles are then
+// summed over the cluster ranks in rank order through DSMEM (each CTA reduces
+// and stores a 1/nsplit share of the tile) -- deterministic, no global scratch.
+template <typename TIn, typename TOut, bool kAccumulate, int R, bool kCluster = false>
 __global__ void __launch_bounds__(256, R == 4 ? 5 : (sizeof(TOut) == 4 ? 4 : 3))
 bwd_symrun_kernel(GeomDev G,
                                                             const TIn* __restrict__ sino,
-                                                            TOut* __restrict__ img) {
+                                                            TOut* __restrict__ img,
+                                                            int nsplit = 1) {
   constexpr int TR = 8 * R;                  // tile rows
   constexpr int WIN = R == 4 ? 64 : 96;      // window entries (>= span + 3)
   constexpr int OFF = kSymChunk * WIN;       // winB - winA (float2 entries)
@@ -850,8 +857,16 @@ bwd_symrun_kernel(GeomDev G,
     accA[i] = make_float2(0.0f, 0.0f);
     accB[i] = make_float2(0.0f, 0.0f);
   }
-  for (int c0 = 0; c0 < G.n_prim; c0 += kSymChunk) {
-    const int na = min(kSymChunk, G.n_prim - c0);
+  const int rank = kCluster ? (int)(blockIdx.z % nsplit) : 0;
+  if (kCluster) {
+    const long long item = blockIdx.z / nsplit;
+    sino += item * G.m * d;
+    img += item * n * n;
+  }
+  const int q_begin = kCluster ? (int)((long long)G.n_prim * rank / nsplit) : 0;
+  const int q_end = kCluster ? (int)((long long)G.n_prim * (rank + 1) / nsplit) : G.n_prim;
+  for (int c0 = q_begin; c0 < q_end; c0 += kSymChunk) {
+    const int na = min(kSymChunk, q_end - c0);
     __syncthreads();
     if (tid < na) {
       const int q = c0 + tid;
@@ -921,24 +936,66 @@ bwd_symrun_kernel(GeomDev G,
       }
     }
   }
-  const int col = col0 + lane;
+  if constexpr (kCluster) {
+    // partial tile -> shared memory as [slot = 2 i + (A|B)][thread]; rank r
+    // sums elements [E r / nsplit, E (r + 1) / nsplit) over the ranks in order
+    namespace cg = cooperative_groups;
+    constexpr int E = 2 * R * 256;
+    __shared__ float2 part[E];
 #pragma unroll
-  for (int i = 0; i < R; ++i) {
-    const int row = row0 + trow + i;
-    const long long p1 = (long long)row * n + col;                       // (p, a)
-    const long long p2 = (long long)row * n + (n - 1 - col);             // x-mirror, m-a
-    const long long p3 = (long long)(n - 1 - row) * n + (n - 1 - col);   // rotation, a rev
-    const long long p4 = (long long)(n - 1 - row) * n + col;             // y-mirror, m-a rev
-    if (kAccumulate) {
-      img[p1] = (TOut)((float)img[p1] + accA[i].x);
-      img[p2] = (TOut)((float)img[p2] + accA[i].y);
-      img[p3] = (TOut)((float)img[p3] + accB[i].x);
-      img[p4] = (TOut)((float)img[p4] + accB[i].y);
-    } else {
-      img[p1] = (TOut)accA[i].x;
-      img[p2] = (TOut)accA[i].y;
-      img[p3] = (TOut)accB[i].x;
-      img[p4] = (TOut)accB[i].y;
+    for (int i = 0; i < R; ++i) {
+      part[(2 * i) * 256 + tid] = accA[i];
+      part[(2 * i + 1) * 256 + tid] = accB[i];
+    }
+    cg::cluster_group cl = cg::this_cluster();
+    cl.sync();
+    const int e0 = E * rank / nsplit, e1 = E * (rank + 1) / nsplit;
+    for (int e = e0 + tid; e < e1; e += 256) {
+      float2 v = cl.map_shared_rank(part, 0)[e];
+      for (int z = 1; z < nsplit; ++z) {
+        const float2 u = cl.map_shared_rank(part, z)[e];
+        v.x += u.x;
+        v.y += u.y;
+      }
+      const int slot = e >> 8, src = e & 255;
+      const int row = row0 + (src >> 5) * R + (slot >> 1), col = col0 + (src & 31);
+      long long pa, pb;
+      if ((slot & 1) == 0) {
+        pa = (long long)row * n + col;                          // (p, a)
+        pb = (long long)row * n + (n - 1 - col);                // x-mirror, m-a
+      } else {
+        pa = (long long)(n - 1 - row) * n + (n - 1 - col);      // rotation, a rev
+        pb = (long long)(n - 1 - row) * n + col;                // y-mirror, m-a rev
+      }
+      if (kAccumulate) {
+        img[pa] = (TOut)((float)img[pa] + v.x);
+        img[pb] = (TOut)((float)img[pb] + v.y);
+      } else {
+        img[pa] = (TOut)v.x;
+        img[pb] = (TOut)v.y;
+      }
+    }
+    cl.sync();   // peers' shared memory must outlive the remote reads
+  } else {
+    const int col = col0 + lane;
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const int row = row0 + trow + i;
+      const long long p1 = (long long)row * n + col;                       // (p, a)
+      const long long p2 = (long long)row * n + (n - 1 - col);             // x-mirror, m-a
+      const long long p3 = (long long)(n - 1 - row) * n + (n - 1 - col);   // rotation, a rev
+      const long long p4 = (long long)(n - 1 - row) * n + col;             // y-mirror, m-a rev
+      if (kAccumulate) {
+        img[p1] = (TOut)((float)img[p1] + accA[i].x);
+        img[p2] = (TOut)((float)img[p2] + accA[i].y);
+        img[p3] = (TOut)((float)img[p3] + accB[i].x);
+        img[p4] = (TOut)((float)img[p4] + accB[i].y);
+      } else {
+        img[p1] = (TOut)accA[i].x;
+        img[p2] = (TOut)accA[i].y;
+        img[p3] = (TOut)accB[i].x;
+        img[p4] = (TOut)accB[i].y;
+      }
     }
   }
 }
@@ -1200,8 +1257,13 @@ __global__ void __launch_bounds__(256, 4) bwd_sym8_kernel(GeomDev G,
 // forward is bound by L1 sector throughput, and this cuts the sector requests
 // 2.3x (profiles/r1b_fwd_variants_ncu.txt).  Without kMix the 4 angles are 4
 // warps that share L1 lines (2.4x less L2 traffic, little time gained).
-template <typename TOut, int kAG, bool kLock = false, bool kMix = false, bool kPM = false>
-__global__ void __launch_bounds__(kAG == 1 ? 128 : 32 * kAG) fwd_sym_kernel(GeomDev G, const float* __restrict__ P,
+// kSeg > 1 (small grids, where the ray groups alone do not fill the SMs):
+// blockDim.y = kSeg warps-groups split the warp's slab range into kSeg
+// contiguous row segments; partial sums are combined in segment order through
+// shared memory (deterministic).
+template <typename TOut, int kAG, bool kLock = false, bool kMix = false, bool kPM = false,
+          int kSeg = 1>
+__global__ void __launch_bounds__(kAG == 1 ? 128 : 32 * kAG * kSeg) fwd_sym_kernel(GeomDev G, const float* __restrict__ P,
                                                       const float* __restrict__ PT,
                                                       TOut* __restrict__ sino) {
   int hidx, j;
@@ -1244,6 +1306,12 @@ __global__ void __launch_bounds__(kAG == 1 ? 128 : 32 * kAG) fwd_sym_kernel(Geom
   }
   int rw0 = __reduce_min_sync(0xffffffffu, r0);
   int rw1 = __reduce_max_sync(0xffffffffu, r1);
+  if (kSeg > 1 && rw0 <= rw1) {   // this segment's share of the warp's slab range
+    const int len = rw1 - rw0 + 1, sg = threadIdx.y;
+    const int rs = rw0 + (len * sg) / kSeg;
+    rw1 = rw0 + (len * (sg + 1)) / kSeg - 1;
+    rw0 = rs;
+  }
   if (kLock) {
     // lockstep: the block's warps (adjacent angles) walk the union slab range
     // together, so each image line is fetched into L1 once for all of them;
@@ -1368,6 +1436,20 @@ __global__ void __launch_bounds__(kAG == 1 ? 128 : 32 * kAG) fwd_sym_kernel(Geom
       walk(std::true_type{});
     else
       walk(std::false_type{});
+  }
+  if constexpr (kSeg > 1) {
+    __shared__ float4 red[kSeg][32 * kAG];
+    red[threadIdx.y][threadIdx.x] = make_float4(accA.x, accA.y, accB.x, accB.y);
+    __syncthreads();
+    if (threadIdx.y != 0) return;
+#pragma unroll
+    for (int sg = 1; sg < kSeg; ++sg) {
+      const float4 v = red[sg][threadIdx.x];
+      accA.x += v.x;
+      accA.y += v.y;
+      accB.x += v.z;
+      accB.y += v.w;
+    }
   }
   if (j < jh && hvalid) {
     // slab-coordinate images -> rays; x-major swaps which image is the x-mirror
@@ -1789,13 +1871,19 @@ cudaError_t tma_forward(const GeomDev& G, float* P, float* PT, TOut* sino, int* 
 // G.sym: bit 0 auto, bit 1 forced, bit 2 forced + TMA forward; the higher bits
 // select testing variants
 static inline bool use_sym_bwd(const GeomDev& G, int precision = 1) {
-  // fp32: the run layout beats the split kernel from n ~ 384 up (n = 512:
-  // 0.17 vs 0.31 ms; n = 256: 0.083 vs 0.053 ms); fp64: from n = 1024 (the
-  // angle-split cluster kernel covers the small grids)
+  // fp32: the run layout (angle-split over a cluster on small quadrants) beats
+  // the split kernel from n = 256 up (n = 256, 180 angles: 18.6 vs 33.8 us;
+  // n = 512: 63.5 vs 303 us); fp64: from n = 1024 (the angle-split cluster
+  // kernel covers the small grids)
   const int base = G.sym & 7;
-  return base >= 2 || (base == 1 && G.n >= (precision == 0 ? 512 : 1024));
+  return base >= 2 || (base == 1 && G.n >= (precision == 0 ? 256 : 1024));
 }
-static inline bool use_sym_fwd(const GeomDev& G) {
+static inline bool use_sym_fwd(const GeomDev& G, int precision = 0) {
+  // fp32: the row-segment split keeps the symmetric forward ahead down to n = 256
+  if (precision == 0) {
+    const int base = G.sym & 7;
+    return base >= 2 || (base == 1 && G.n >= 256);
+  }
   const long long blocks = (long long)(((G.d + 1) / 2 + 127) / 128) * G.n_half;   // 128-ray units
   const int base = G.sym & 7;
   return base >= 2 || (base == 1 && blocks >= 4LL * 148);
@@ -1843,8 +1931,19 @@ static cudaError_t fwd_v2_impl(const GeomDev& G, const void* x, void* ws, void* 
     if (e != cudaSuccess) return e;
     constexpr int ag = fast::kFwdAG;
     dim3 mgrid(((G.d + 1) / 2 + 8 * ag - 1) / (8 * ag), (G.n_half + 3) / 4);
-    fast::fwd_sym_kernel<TOut, ag, false, true, true><<<mgrid, 32 * ag, 0, st>>>(
-        G, (const float*)PM, (const float*)PMT, (TOut*)y);
+    const long long blocks = (long long)mgrid.x * mgrid.y;
+    // small grids: split each warp's slab range over 8 / 4 row segments
+    // (sym & 65536: testing, unsplit)
+    const int seg = (G.sym & 65536) ? 1 : blocks < 2LL * 148 ? 8 : blocks < 6LL * 148 ? 4 : 1;
+    if (seg == 8)
+      fast::fwd_sym_kernel<TOut, ag, false, true, true, 8><<<mgrid, dim3(32 * ag, 8), 0, st>>>(
+          G, (const float*)PM, (const float*)PMT, (TOut*)y);
+    else if (seg == 4)
+      fast::fwd_sym_kernel<TOut, ag, false, true, true, 4><<<mgrid, dim3(32 * ag, 4), 0, st>>>(
+          G, (const float*)PM, (const float*)PMT, (TOut*)y);
+    else
+      fast::fwd_sym_kernel<TOut, ag, false, true, true><<<mgrid, 32 * ag, 0, st>>>(
+          G, (const float*)PM, (const float*)PMT, (TOut*)y);
     e = cudaGetLastError();
     if (e != cudaSuccess || Gx->m == 0) return e;
     // the axis-aligned angles of the set: slab segments over threadIdx.y
@@ -1896,6 +1995,37 @@ template <typename TIn, typename TOut>
 static cudaError_t bwd_v2_impl(const GeomDev& G, const void* y, void* x, bool accumulate,
                                cudaStream_t st, const GeomDev* G_axis = nullptr);
 
+// small quadrants: the run layout with the angles split over a cluster of
+// nsplit CTAs per tile (~4 CTAs per SM, >= 4 primary angles per CTA)
+static inline int symrun_nsplit(const GeomDev& G) {
+  const int tiles = (G.n / 64) * (G.n / 64);
+  return max(1, min(16, min((4 * 148 + tiles - 1) / tiles, G.n_prim / 4)));
+}
+
+template <typename TIn, typename TOut, bool kAcc>
+static cudaError_t bwd_symrun_cluster(const GeomDev& G, const void* y, void* x, int nsplit,
+                                      int batch, cudaStream_t st) {
+  auto kern = fast::bwd_symrun_kernel<TIn, TOut, kAcc, 4, true>;
+  static bool attr = false;   // per instantiation
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(G.n / 64, G.n / 64, nsplit * batch);
+  cfg.blockDim = dim3(256);
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 1;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = nsplit;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, G, (const TIn*)y, (TOut*)x, nsplit);
+}
+
 template <typename TIn, typename TOut, int R>
 static void bwd_symrun_launch(const GeomDev& G, const void* y, void* x, bool accumulate,
                               cudaStream_t st) {
@@ -1933,7 +2063,15 @@ static cudaError_t bwd_sym_impl(const GeomDev& G, const GeomDev& Gx, const void*
   } else if (!rowlayout && !blocks8x4) {
     // run layout: 64-row tiles (fewer window loads per pixel) when the quadrant
     // allows and the grid still fills the SMs (n >= ~3400), else 32-row tiles
-    // (sym & 1024: testing, 64-row tiles at any size; sym & 512: 32-row tiles)
+    // (sym & 1024: testing, 64-row tiles at any size; sym & 512: 32-row tiles);
+    // small quadrants split the angles over a cluster (sym & 32768: testing, off)
+    const int nsplit = symrun_nsplit(G);
+    if (nsplit > 1 && !(G.sym & (512 | 1024 | 32768))) {
+      cudaError_t e = accumulate ? bwd_symrun_cluster<TIn, TOut, true>(G, y, x, nsplit, 1, st)
+                                 : bwd_symrun_cluster<TIn, TOut, false>(G, y, x, nsplit, 1, st);
+      if (e != cudaSuccess || Gx.m == 0) return e;
+      return bwd_v2_impl<TIn, TOut>(Gx, y, x, true, st);   // axis angles, accumulate
+    }
     if ((G.n / 2) % 64 == 0 &&
         ((long long)(G.n / 64) * (G.n / 128) >= 12LL * 148 || (G.sym & 1024)) &&
         !(G.sym & 512))
@@ -2129,7 +2267,7 @@ cudaError_t fast_forward(const GeomDev& G, int precision, int tin, int tout, con
     if (tin == 1 && tout == 0) return fwd_v2_impl<double, float>(G, x, xT_ws, y, st, Gx);
     if (tin == 0 && tout == 1) return fwd_v2_impl<float, double>(G, x, xT_ws, y, st, Gx);
   } else {
-    if (use_sym_fwd(G) && Gx && tin == 1 && tout == 1)
+    if (use_sym_fwd(G, 1) && Gx && tin == 1 && tout == 1)
       return fwd64_impl<double, double>(G, x, xT_ws, y, st, Gx);
     if (tin == 1 && tout == 1) return fwd_impl<double, double, double>(G, x, xT_ws, y, st);
     if (tin == 0 && tout == 0) return fwd_impl<float, float, double>(G, x, xT_ws, y, st);
@@ -2176,7 +2314,7 @@ cudaError_t fast_forward_batch(const GeomDev& G, int precision, int tin, int tou
   const long long N = (long long)G.n * G.n, M = (long long)G.m * G.d;
   const size_t si = tin == 1 ? 8 : 4, so = tout == 1 ? 8 : 4;
   const bool split64 = precision == 1 && tin == 1 && tout == 1 && use_split(G) &&
-                       !(use_sym_fwd(G) && Gx);
+                       !(use_sym_fwd(G, 1) && Gx);
   if (split64 && G.m > 0 && G.d > 0) {
     // batch * (P, PT) padded planes; ws_item = 2 * n * (n + 2 margin) doubles
     double* P = (double*)ws;

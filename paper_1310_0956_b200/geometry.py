@@ -200,7 +200,7 @@ class LineProjector:
         forced with the experimental TMA-staged forward) or disable (False) the
         mirror-symmetry kernels; no-op if the angle set is not symmetric.
         Returns whether it is enabled."""
-        code = {"force": 2, "tma": 4, "rowlayout": 10, "fwd1": 18, "lockstep": 34, "fwdrows": 66, "plainplanes": 130, "bwd8x4": 258, "bwdrun32": 514, "bwdrun64": 1026, "bwdsym8": 8194, "bwdrun": 16386}.get(enable, None)
+        code = {"force": 2, "tma": 4, "rowlayout": 10, "fwd1": 18, "lockstep": 34, "fwdrows": 66, "plainplanes": 130, "bwd8x4": 258, "bwdrun32": 514, "bwdrun64": 1026, "bwdsym8": 8194, "bwdrun": 16386, "bwdrunflat": 49154, "fwdflat": 65538}.get(enable, None)
         if code is None:
             code = int(bool(enable))
         st = N.ctypes.c_int()
