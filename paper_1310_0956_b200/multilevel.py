@@ -344,39 +344,65 @@ def build_wmg_hierarchy(w, n: int, lam: float, levels: int, nu_pre: int = 0,
         # Joseph weights exist in parity mode only: exact leaf factors + DGEMM
         # and the parity projector for the node systems
         gram, node_mode = "dense", "parity"
-    if sharded:
-        # angle-sharded W: every rank accumulates its angles' share of each leaf
-        # Gram (the Gram is a sum over rays), one NCCL allreduce sums them, and
-        # every rank factors all leaves (the V-cycle's coarse solves are local)
-        paths, grams = _assemble_leaf_grams(base, n, 0.0, levels, method=gram, full=False)
-        w.dist.all_reduce(grams, group=w.group)
-        if lam != 0:
-            grams.diagonal(dim1=1, dim2=2).add_(lam)
-    else:
-        paths, grams = _assemble_leaf_grams(w, n, lam, levels, method=gram, full=False)
-    n_leaf, p = grams.shape[0], grams.shape[-1]
+    depth = levels - 1
+    p = (n >> depth) ** 2
+    all_paths = _leaf_paths(levels)
+    n_leaf = len(all_paths)
+    names = ["/".join(q) or "root" for q in all_paths]
+    # Leaves are assembled, inverted and (optionally) packed in chunks of at
+    # most ~8 GB of Grams, so the full dense Grams never coexist (config 4 at
+    # 6 levels: 1024 leaves of 4096^2 = 137 GB dense, 69 GB packed inverses).
+    chunk = max(1, min(n_leaf, (8 << 30) // max(1, p * p * 8)))
+    use_packed = packed and p % 128 == 0
     # keep a copy of the Grams (API: coarse_solve.lower, a Cholesky factor
     # computed on first access) only when they are small; the V-cycle itself
     # only needs the inverses
-    keep_gram = grams.numel() * 8 <= (8 << 30)
-    gram_copy = grams.clone() if keep_gram else None
-    names = ["/".join(q) or "root" for q in paths]
-    batch = max(1, min(n_leaf, (4 << 30) // max(1, p * p * 8)))
-    for b0 in range(0, n_leaf, batch):
-        try:
-            # hand-written batched SPD inverse on the fp64 tensor cores (in place)
-            spd_inverse_(grams[b0:b0 + batch], names=names[b0:b0 + batch])
-        except NotPositiveDefiniteError as exc:
-            name, _, why = str(exc).partition(": ")
-            raise NotPositiveDefiniteError(
-                f"coarsest subproblem '{name}' is singular (lambda={lam}): {why}") from None
-    if packed and p % 128 == 0:
-        # packed symmetric storage: the V-cycle's coarse solves stream half the bytes
-        from .sparse_kernels import PackedSymmetric
-        packed = PackedSymmetric.pack(grams)
+    keep_gram = n_leaf * p * p * 8 <= (8 << 30)
+    gram_copy = None
+    inverses = None
+    from .sparse_kernels import PackedSymmetric
+    for c0 in range(0, n_leaf, chunk):
+        cpaths = all_paths[c0:c0 + chunk]
+        if sharded:
+            # angle-sharded W: every rank accumulates its angles' share of each
+            # leaf Gram (the Gram is a sum over rays), one NCCL allreduce sums
+            # them, and every rank inverts all leaves (coarse solves are local)
+            _, grams = _assemble_leaf_grams(base, n, 0.0, levels, paths=cpaths, method=gram,
+                                            full=False)
+            w.dist.all_reduce(grams, group=w.group)
+            if lam != 0:
+                grams.diagonal(dim1=1, dim2=2).add_(lam)
+        else:
+            _, grams = _assemble_leaf_grams(w, n, lam, levels, paths=cpaths, method=gram,
+                                            full=False)
+        if keep_gram:
+            if gram_copy is None:
+                gram_copy = t.empty((n_leaf, p, p), dtype=t.float64, device=grams.device)
+            gram_copy[c0:c0 + len(cpaths)].copy_(grams)
+        sub = 4 << 30
+        batch = max(1, min(len(cpaths), sub // max(1, p * p * 8)))
+        for b0 in range(0, len(cpaths), batch):
+            try:
+                # hand-written batched SPD inverse on the fp64 tensor cores (in place)
+                spd_inverse_(grams[b0:b0 + batch], names=names[c0 + b0:c0 + b0 + batch])
+            except NotPositiveDefiniteError as exc:
+                name, _, why = str(exc).partition(": ")
+                raise NotPositiveDefiniteError(
+                    f"coarsest subproblem '{name}' is singular (lambda={lam}): {why}") from None
+        if use_packed:
+            # packed symmetric storage: the V-cycle's coarse solves stream half the bytes
+            pk = PackedSymmetric.pack(grams)
+            if inverses is None:
+                inverses = PackedSymmetric(
+                    t.empty((n_leaf, pk.data.shape[1]), dtype=t.float64, device=grams.device), p)
+            inverses.data[c0:c0 + len(cpaths)].copy_(pk.data)
+            del pk
+        else:
+            if inverses is None:
+                inverses = t.empty((n_leaf, p, p), dtype=t.float64, device=grams.device)
+            inverses[c0:c0 + len(cpaths)].copy_(grams)
         del grams
-        grams = packed
-    inverses = grams
+    paths = all_paths
     leaf_index = {path: i for i, path in enumerate(paths)}
     if node_mode not in ("fast", "fast32", "parity"):
         raise ValueError(f"unknown node_mode '{node_mode}'")
