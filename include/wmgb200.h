@@ -119,6 +119,19 @@ int wmg_forward(const wmg_geometry *g, int mode, int precision, int dtype_in, in
 int wmg_backward(const wmg_geometry *g, int mode, int precision, int dtype_in, int dtype_out,
                  const void *y, void *x, int accumulate, int *anomaly, void *stream);
 
+/* Banded fast backprojection (fp32 arithmetic, eight-image kernels; for
+ * angle-sharded solves that overlap the allreduce of W^T y with the rest of
+ * the backprojection).  *bands = number of quadrant row-blocks qt = n / 64 when
+ * the geometry takes the banded path in this precision, else 0.
+ * wmg_backward_band writes bands [band0, band1): image rows [32 band0,
+ * 32 band1) and [n - 32 band1, n - 32 band0) receive their complete W^T y
+ * (bit-identical to wmg_backward); calls must cover 0..qt in increasing
+ * order on one stream.  Same reference function as wmg_backward
+ * (geometry.py:209-215). */
+int wmg_backward_bands(const wmg_geometry *g, int precision, int *bands);
+int wmg_backward_band(const wmg_geometry *g, int precision, int dtype_in, int dtype_out,
+                      const void *y, void *x, int band0, int band1, void *stream);
+
 /* Batched W x / W^T y over `batch` contiguous images (n*n apart) and sinograms
  * (n_angles*n_detectors apart), each item computed exactly as by wmg_forward /
  * wmg_backward (the WMG cycle applies sibling node systems together; on small

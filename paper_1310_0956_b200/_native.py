@@ -44,6 +44,8 @@ _SIGS = {
     "wmg_forward_workspace": (_i, [_vp, _i, _i, ctypes.POINTER(ctypes.c_size_t)]),
     "wmg_forward": (_i, [_vp, _i, _i, _i, _i, _dp, _dp, _dp, _dp, _vp]),
     "wmg_backward": (_i, [_vp, _i, _i, _i, _i, _dp, _dp, _i, _dp, _vp]),
+    "wmg_backward_bands": (_i, [_vp, _i, ctypes.POINTER(_i)]),
+    "wmg_backward_band": (_i, [_vp, _i, _i, _i, _dp, _dp, _i, _i, _vp]),
     "wmg_forward_batch": (_i, [_vp, _i, _i, _i, _i, _dp, _dp, _i, _dp, _vp]),
     "wmg_backward_batch": (_i, [_vp, _i, _i, _i, _i, _dp, _dp, _i, _i, _vp]),
     "wmg_row_sums": (_i, [_vp, _dp, _vp]),

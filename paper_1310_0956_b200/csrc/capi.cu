@@ -24,6 +24,9 @@ cudaError_t fast_backward(const GeomDev&, int, int, int, const void*, void*, boo
                           const GeomDev*);
 cudaError_t fast_forward_batch(const GeomDev&, int, int, int, const void*, void*, size_t, void*,
                                int, cudaStream_t, const GeomDev*);
+int fast_backward_bands(const GeomDev&, int, const GeomDev*);
+cudaError_t fast_backward_band(const GeomDev&, int, int, int, const void*, void*, int, int,
+                               cudaStream_t, const GeomDev*);
 cudaError_t fast_backward_batch(const GeomDev&, int, int, int, const void*, void*, bool, int,
                                 cudaStream_t, const GeomDev*);
 size_t fast_forward_workspace_bytes(int, int, int);
@@ -445,6 +448,24 @@ int wmg_backward(const wmg_geometry* g, int mode, int precision, int dtype_in, i
   return cuda_rc(wmg::fast_backward(g->dev, precision, dtype_in, dtype_out, y, x,
                                     accumulate != 0, STREAM(stream),
                                     g->dev.sym ? &g->axis : nullptr));
+}
+
+int wmg_backward_bands(const wmg_geometry* g, int precision, int* bands) {
+  if (!g || !bands) return fail(WMG_EINVAL, "NULL argument");
+  *bands = g->dev.sym ? wmg::fast_backward_bands(g->dev, precision, &g->axis) : 0;
+  return WMG_OK;
+}
+
+int wmg_backward_band(const wmg_geometry* g, int precision, int dtype_in, int dtype_out,
+                      const void* y, void* x, int band0, int band1, void* stream) {
+  if (!g || !x || !y) return fail(WMG_EINVAL, "NULL argument");
+  int rc = check_types(WMG_MODE_FAST, precision, dtype_in, dtype_out);
+  if (rc) return rc;
+  const int nb = g->dev.sym ? wmg::fast_backward_bands(g->dev, precision, &g->axis) : 0;
+  if (nb == 0) return fail(WMG_EINVAL, "no banded backprojection for this geometry / mode");
+  if (band0 < 0 || band1 > nb || band0 > band1) return fail(WMG_EINVAL, "band range");
+  return cuda_rc(wmg::fast_backward_band(g->dev, precision, dtype_in, dtype_out, y, x, band0,
+                                         band1, STREAM(stream), &g->axis));
 }
 
 int wmg_forward_batch(const wmg_geometry* g, int mode, int precision, int dtype_in,

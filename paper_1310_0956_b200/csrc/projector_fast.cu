@@ -601,14 +601,15 @@ constexpr int kBwdWin = 64;
 
 template <typename TIn, typename TOut, bool kAccumulate>
 __global__ void __launch_bounds__(128) bwd_v2_kernel(GeomDev G, const TIn* __restrict__ sino,
-                                                     TOut* __restrict__ img) {
+                                                     TOut* __restrict__ img,
+                                                     int row_tile0 = 0) {
   __shared__ float2 win[kBwdChunk][kBwdWin];
   __shared__ long long qx[kBwdChunk][kBwdTile];
   __shared__ long long qhead[kBwdChunk];
   __shared__ int jlo_s[kBwdChunk];
   const int n = G.n;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int col0 = blockIdx.x * kBwdTile, row0 = blockIdx.y * kBwdTile;
+  const int col0 = blockIdx.x * kBwdTile, row0 = (blockIdx.y + row_tile0) * kBwdTile;
   const double half = (double)n * 0.5, dc = (double)(G.d - 1) * 0.5;
   const double xc0 = (double)col0 - half + 0.5;           // pixel-centre x of the tile origin
   const double yc0 = half - (double)row0 - 0.5;           // pixel-centre y
@@ -1015,10 +1016,26 @@ bwd_symrun_kernel(GeomDev G,
 // has one writer per step) and each output pixel is written once -- no
 // atomics, deterministic.  Diagonal tiles (tau = tau^T) take phase 1 only.
 constexpr int kS8Win = 64;
+// Banded launches (pair0 >= 0): tile pairs enumerated by their smaller
+// quadrant index s = min(i, j) (s = 0: qt pairs, s = 1: qt - 1, ...) and
+// blockIdx.x offset by pair0.  After the pairs of s < S have run, quadrant
+// row-blocks 0..S-1 -- image rows [0, 32 S) and [n - 32 S, n) -- are final,
+// so a sharded backprojection can allreduce them while the rest runs.
+__device__ __forceinline__ void minmajor_unrank(int lin, int qt, int& I, int& J) {
+  int s = 0;
+  while (lin >= qt - s) {
+    lin -= qt - s;
+    ++s;
+  }
+  I = s + lin;
+  J = s;
+}
+
 template <typename TIn, typename TOut, bool kAccumulate>
 __global__ void __launch_bounds__(256, 4) bwd_sym8_kernel(GeomDev G,
                                                           const TIn* __restrict__ sino,
-                                                          TOut* __restrict__ img) {
+                                                          TOut* __restrict__ img,
+                                                          int pair0 = -1) {
   constexpr int R = 4;
   constexpr int OFF = kSymChunk * kS8Win;      // window stride (float2 entries)
   __shared__ float2 win[4][kSymChunk][kS8Win]; // A (a, mir a), B reversed, C, D (u1, u2)
@@ -1036,7 +1053,10 @@ __global__ void __launch_bounds__(256, 4) bwd_sym8_kernel(GeomDev G,
   const int n = G.n, d = G.d;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   int ti, tj;
-  tri_unrank(blockIdx.x, ti, tj);
+  if (pair0 < 0)
+    tri_unrank(blockIdx.x, ti, tj);
+  else
+    minmajor_unrank(pair0 + (int)blockIdx.x, n / 64, ti, tj);
   const bool diag = ti == tj;
   const int trow = warp * R;
   const double half = (double)n * 0.5, dc = (double)(d - 1) * 0.5;
@@ -2059,7 +2079,7 @@ static cudaError_t bwd_sym_impl(const GeomDev& G, const GeomDev& Gx, const void*
       if (ea != cudaSuccess) return ea;
       attr[accumulate] = true;
     }
-    k8<<<grid8, 256, smem8, st>>>(G, (const TIn*)y, (TOut*)x);
+    k8<<<grid8, 256, smem8, st>>>(G, (const TIn*)y, (TOut*)x, -1);
   } else if (!rowlayout && !blocks8x4) {
     // run layout: 64-row tiles (fewer window loads per pixel) when the quadrant
     // allows and the grid still fills the SMs (n >= ~3400), else 32-row tiles
@@ -2272,6 +2292,59 @@ cudaError_t fast_forward(const GeomDev& G, int precision, int tin, int tout, con
     if (tin == 1 && tout == 1) return fwd_impl<double, double, double>(G, x, xT_ws, y, st);
     if (tin == 0 && tout == 0) return fwd_impl<float, float, double>(G, x, xT_ws, y, st);
   }
+  return cudaErrorInvalidValue;
+}
+
+// Banded fp32 backprojection (the eight-image path): quadrant row-blocks
+// [s0, s1), i.e. image rows [32 s0, 32 s1) and [n - 32 s1, n - 32 s0), are
+// written complete (all angles, axis angles included) -- every pixel gets the
+// same sums as the unbanded launch.  Bands must be run in order (s0 = 0 first)
+// because a tile pair (i, j) writes row-blocks i and j >= s0.
+int fast_backward_bands(const GeomDev& G, int precision, const GeomDev* Gx) {
+  if (precision != 0 || !Gx || !use_sym_bwd(G, 0) || !G.tsym || G.n % 64) return 0;
+  const int qt = G.n / 64;
+  if (G.sym & (8 | 256 | 512 | 1024 | 16384)) return 0;
+  if (!((long long)qt * (qt + 1) / 2 >= 3LL * 148 || (G.sym & 8192))) return 0;
+  return qt;
+}
+
+template <typename TIn, typename TOut>
+static cudaError_t bwd_band_impl(const GeomDev& G, const GeomDev& Gx, const void* y, void* x,
+                                 int s0, int s1, cudaStream_t st) {
+  const int qt = G.n / 64;
+  auto off = [&](int s) { return s * qt - s * (s - 1) / 2; };
+  const int p0 = off(s0), np = off(s1) - p0;
+  if (np > 0) {
+    constexpr int smem8 = 2 * 4 * fast::kBwdTile * (fast::kBwdTile + 1) * (int)sizeof(float);
+    static bool attr = false;
+    auto k8 = fast::bwd_sym8_kernel<TIn, TOut, false>;
+    if (!attr) {
+      cudaError_t ea = cudaFuncSetAttribute(k8, cudaFuncAttributeMaxDynamicSharedMemorySize, smem8);
+      if (ea != cudaSuccess) return ea;
+      attr = true;
+    }
+    k8<<<np, 256, smem8, st>>>(G, (const TIn*)y, (TOut*)x, p0);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  if (Gx.m == 0 || s1 <= s0) return cudaSuccess;
+  // the axis-aligned angles of the set on the band's two row ranges
+  const int tiles = G.n / fast::kBwdTile;
+  dim3 g1(tiles, s1 - s0);
+  fast::bwd_v2_kernel<TIn, TOut, true><<<g1, 128, 0, st>>>(Gx, (const TIn*)y, (TOut*)x, s0);
+  fast::bwd_v2_kernel<TIn, TOut, true><<<g1, 128, 0, st>>>(Gx, (const TIn*)y, (TOut*)x,
+                                                           tiles - s1);
+  return cudaGetLastError();
+}
+
+cudaError_t fast_backward_band(const GeomDev& G, int precision, int tin, int tout, const void* y,
+                               void* x, int s0, int s1, cudaStream_t st, const GeomDev* Gx) {
+  const int qt = fast_backward_bands(G, precision, Gx);
+  if (qt == 0 || s0 < 0 || s1 > qt || s0 > s1) return cudaErrorInvalidValue;
+  if (tin == 0 && tout == 0) return bwd_band_impl<float, float>(G, *Gx, y, x, s0, s1, st);
+  if (tin == 1 && tout == 1) return bwd_band_impl<double, double>(G, *Gx, y, x, s0, s1, st);
+  if (tin == 1 && tout == 0) return bwd_band_impl<double, float>(G, *Gx, y, x, s0, s1, st);
+  if (tin == 0 && tout == 1) return bwd_band_impl<float, double>(G, *Gx, y, x, s0, s1, st);
   return cudaErrorInvalidValue;
 }
 

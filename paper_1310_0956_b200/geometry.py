@@ -300,6 +300,23 @@ class LineProjector:
                D.ptr(out), int(bool(accumulate)), D.ptr(anomaly), D.stream_handle())
         return out
 
+    def backward_bands(self) -> int:
+        """Number of row bands of the banded backprojection (0: not available
+        for this geometry / precision; see wmg_backward_band)."""
+        nb = N.ctypes.c_int()
+        N.call("wmg_backward_bands", self._h, self.precision, N.ctypes.byref(nb))
+        return nb.value if self._mode_code == N.MODE_FAST else 0
+
+    def backward_band_(self, y, out, band0: int, band1: int):
+        """Bands [band0, band1) of out = W^T y: image rows [32 band0, 32 band1)
+        and [n - 32 band1, n - 32 band0) complete (bit-identical to backward_).
+        Bands must be issued in increasing order on one stream."""
+        if y.numel() != self.shape[0] or out.numel() != self.shape[1]:
+            raise DimensionMismatchError("backward_band_: length mismatch")
+        N.call("wmg_backward_band", self._h, self.precision, self._code(y), self._code(out),
+               D.ptr(y), D.ptr(out), int(band0), int(band1), D.stream_handle())
+        return out
+
     def forward(self, x):
         t = D.torch()
         dt = self._io_dtype(x)

@@ -130,12 +130,52 @@ class AngleShardedProjector:
     def forward_(self, x, out):
         return self.local.forward_(x, out)
 
+    # W^T y is summed over the ranks band by band while the backprojection of
+    # the later bands still runs (``overlap_groups`` groups of quadrant row-
+    # blocks of equal work; the eight-image fp32 path only, else one allreduce
+    # after the whole backprojection)
+    overlap_groups = 4
+
+    def _band_groups(self, qt):
+        total = qt * (qt + 1) // 2
+        bounds, s, done = [0], 0, 0
+        for k in range(1, self.overlap_groups + 1):
+            target = total * k // self.overlap_groups
+            while s < qt and done < target:
+                done += qt - s
+                s += 1
+            if s > bounds[-1]:
+                bounds.append(s)
+        return list(zip(bounds[:-1], bounds[1:]))
+
     def backward_(self, y, out, accumulate=False):
         if accumulate:
             raise ValueError("accumulate is not supported on a sharded backprojection")
-        self.local.backward_(y, out)
-        if self.world > 1:
-            self.dist.all_reduce(out, group=self.group)
+        qt = self.local.backward_bands() if (self.world > 1 and self.overlap_groups > 1 and
+                                             hasattr(self.local, "backward_bands")) else 0
+        if qt == 0:
+            self.local.backward_(y, out)
+            if self.world > 1:
+                self.dist.all_reduce(out, group=self.group)
+            return out
+        import torch
+        n = self.geometry.n_pixels_per_side
+        cur = torch.cuda.current_stream(out.device)
+        comm = getattr(self, "_comm", None)
+        if comm is None:
+            comm = self._comm = torch.cuda.Stream(device=out.device)
+        for s0, s1 in self._band_groups(qt):
+            self.local.backward_band_(y, out, s0, s1)
+            comm.wait_stream(cur)
+            with torch.cuda.stream(comm):
+                top = out[32 * s0 * n:32 * s1 * n]
+                bot = out[(n - 32 * s1) * n:(n - 32 * s0) * n]
+                if (n - 32 * s1) == 32 * s1:            # the two bands meet at the centre
+                    self.dist.all_reduce(out[32 * s0 * n:(n - 32 * s0) * n], group=self.group)
+                else:
+                    self.dist.all_reduce(top, group=self.group)
+                    self.dist.all_reduce(bot, group=self.group)
+        cur.wait_stream(comm)
         return out
 
     def row_sums_dev(self):

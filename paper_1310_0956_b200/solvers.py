@@ -680,8 +680,10 @@ def gmres_solve(op, f, precond=None, x0=None, cfg: SolverConfig = None, x_ex=Non
                 restart: int = 100):
     """Right-preconditioned restarted GMRES on op x = f (op = normal operator).
 
-    Arnoldi with classical Gram-Schmidt applied twice (CGS2); Givens rotations
-    on the host (O(restart^2) scalars).  Logged residual: the GMRES residual
+    Arnoldi with classical Gram-Schmidt applied twice (CGS2): the projections
+    stay on the device (DET_SUM, 8 per launch) and each Arnoldi step reads back
+    its Hessenberg column and ||w|| once; Givens rotations on the host
+    (O(restart^2) scalars).  Logged residual: the GMRES residual
     estimate |g_{j+1}| / ||f - op x0||, i.e. the normal-equations residual.
     """
     t = D.require_cuda()
@@ -716,6 +718,7 @@ def gmres_solve(op, f, precond=None, x0=None, cfg: SolverConfig = None, x_ex=Non
     k = 0
     beta = beta0
     hbuf = t.empty(m + 1, dtype=t.float64, device=dev)
+    hacc = t.zeros(m + 2, dtype=t.float64, device=dev)
     while True:
         D.scale(V[0], 1.0 / beta, r)
         H = np.zeros((m + 1, m))
@@ -732,18 +735,22 @@ def gmres_solve(op, f, precond=None, x0=None, cfg: SolverConfig = None, x_ex=Non
                 Z[j].copy_(zj)
             wv = A(zj)
             wv = wv.clone() if wv.data_ptr() == zj.data_ptr() else wv
-            hcol = np.zeros(j + 2)
-            for _ in range(2):                        # CGS2
+            # CGS2 with the projections kept on the device: both passes, their
+            # sum (the oracle's hcol += hh, same order) and ||w||^2 come back to
+            # the host in ONE read per Arnoldi step
+            hacc.zero_()
+            for _ in range(2):
                 specs = [(N.RED_DOT, V[i], wv, None) for i in range(j + 1)]
-                hh = []
                 for c0 in range(0, len(specs), 8):
-                    hh.append(_readback(D.det_reduce(specs[c0:c0 + 8])))
-                hh = np.concatenate(hh)
-                hbuf[: j + 1].copy_(t.as_tensor(hh, device=dev))
+                    D.det_reduce(specs[c0:c0 + 8], out=hbuf[c0:min(c0 + 8, j + 1)])
                 N.call("wmg_cgs_update", n, j + 1, D.ptr(wv), D.ptr(V), n, D.ptr(hbuf),
                        D.stream_handle())
-                hcol[: j + 1] += hh
-            hn = float(np.sqrt(_readback(D.det_norm_sq(wv))[0]))
+                hacc[: j + 1].add_(hbuf[: j + 1])
+            D.det_reduce([(N.RED_SQ, wv, None, None)], out=hacc[m + 1:m + 2])
+            hv = _readback(hacc[: j + 1], hacc[m + 1:m + 2])
+            hcol = np.zeros(j + 2)
+            hcol[: j + 1] = hv[: j + 1]
+            hn = float(np.sqrt(hv[j + 1]))
             hcol[j + 1] = hn
             # apply previous rotations
             for i in range(j):

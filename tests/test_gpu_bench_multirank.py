@@ -43,6 +43,6 @@ def test_bench_pair_and_wmg_two_ranks(gpu):
 
 
 def test_bench_config2_two_ranks(gpu):
-    d = _torchrun(["--workload", "config2", "--grid", "256", "--levels", "3"])
+    d = _torchrun(["--gpus", "2", "--workload", "config2", "--grid", "256", "--levels", "3"])
     assert d["n_gpus"] == 2 and d["cgls"]["status"] == "converged"
     assert d["wmg_gmres"]["status"] == "converged"
