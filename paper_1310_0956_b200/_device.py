@@ -71,7 +71,7 @@ def to_device(v, dtype=None, device=None):
 # threads (numpy releases the GIL) and each slice's DMA is issued as soon as
 # it is staged.  D2H: into a block of torch's caching pinned-host allocator,
 # returned as a numpy view that keeps the block alive.
-_STAGE_MIN_BYTES = 4 << 20
+_STAGE_MIN_BYTES = 64 << 10         # below: plain pageable copies (latency bound anyway)
 _STAGE_THREADS = 4
 _stage = {}
 _stage_lock = threading.Lock()
@@ -102,7 +102,7 @@ def _h2d_staged(a, dtype, dev):
     hn = host.numpy()
     out = t.empty(a.size, dtype=dtype, device=dev)
     n = a.size
-    k = _STAGE_THREADS
+    k = max(1, min(_STAGE_THREADS, a.nbytes >> 20))     # ~1 MB or more per host thread
     bounds = [(i * n) // k for i in range(k + 1)]
     futs = [_copy_pool().submit(np.copyto, hn[bounds[i]:bounds[i + 1]],
                                 a.reshape(-1)[bounds[i]:bounds[i + 1]]) for i in range(k)]

@@ -1,8 +1,8 @@
 """The bench JSON contract, checked on the committed B200 results (no GPU).
 
 bench.py prints one JSON line that the round driver parses; this pins its keys,
-units and internal consistency on `results/r1_bench.json` (the last measured
-line) so a refactor of bench.py cannot silently drop a field.
+units and internal consistency on `results/r2_bench.json` (the last measured
+line of round 2) so a refactor of bench.py cannot silently drop a field.
 """
 import json
 import os
@@ -21,7 +21,7 @@ def _line(name):
 
 
 def test_bench_line_keys_and_consistency():
-    d = _line("r1_bench.json")
+    d = _line("r2_bench.json")
     for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
               "higher_is_better", "scaling", "vs_baseline", "dtype", "data", "config", "e2e",
               "roofline", "cpu_baseline", "gpu_launches", "clocks"):
@@ -34,8 +34,21 @@ def test_bench_line_keys_and_consistency():
     e = d["e2e"]
     assert e["unit"] == d["unit"] and e["h2d_bytes_per_step"] == 4 * (n * n + m * dd)
     assert e["verified_against_device"] is True
+    # the drop-in call (numpy in / out through w @ x, w.T @ y) is the headline e2e;
+    # the pipelined pinned-buffer schedule is reported beside it
+    assert "w @ x" in e["call"] and d["e2e_pipelined"]["verified_against_device"] is True
     r = d["roofline"]
-    assert r["bound"] in ("hbm", "tensor") and abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-9
+    assert r["bound"] == "gather" and abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-9
+    # exact nnz per launch over the dominant kernel's time
+    t_dom = max(d["kernels_ms"].values()) * 1e-3
+    assert abs(r["updates_per_launch"] / t_dom / 1e9 - r["achieved"]) <= 1e-3 * r["achieved"]
+    assert r["peak"] == pytest.approx(r["n_sm"] * 32 * r["f_sm_mhz"] * 1e-3)
+    # formula (4/pi) m n^2 within 1e-5 of the exact count
+    nz = d["nnz"]
+    assert abs(nz["formula_local"] - nz["exact_local"]) <= 1e-5 * nz["exact_local"]
+    # value is the dependent (one-stream) pair
+    assert d["value"] == d["value_sequential"] and d["value_two_streams"] >= d["value"] * 0.9
+    assert "host" in d["cpu_baseline"] and d["cpu_baseline"]["host"]["cpu_model"]
     cb = d["cpu_baseline"]
     assert cb["kind"] in ("reference", "port") and cb["cores"] >= 1 and cb["sample"]
     assert d["gpu_launches"] > 0
@@ -46,6 +59,6 @@ def test_bench_line_keys_and_consistency():
 
 
 def test_reference_arm_line():
-    d = _line("r1_bench_reference.json")
+    d = _line("r2_bench_reference.json")
     assert d["impl"] == "reference" and d["unit"] == "GRays/s"
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["cpu_baseline"]["value"] == d["value"]
