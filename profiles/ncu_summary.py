@@ -13,8 +13,14 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "lts__t_bytes.sum", "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
         "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
         "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active",
+        "l1tex__data_pipe_lsu_wavefronts.sum",
+        "l1tex__data_pipe_lsu_wavefronts.sum.pct_of_peak_sustained_elapsed",
+        "l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum",
         "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum",
         "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum"]
+
+
+N_SM = 148
 
 
 def main(path):
@@ -28,6 +34,13 @@ def main(path):
         for k in KEYS:
             if k in d:
                 print(f"   {k:65s} {d[k]:>18s} {units[hdr.index(k)]}")
+        # the L1 data-pipe wavefronts are reported per SM (SM_A.TriageCompute ...avg):
+        # total per launch = average x SM count
+        kk = "SM_A.TriageCompute.l1tex__data_pipe_lsu_wavefronts.avg"
+        if kk in d and d[kk]:
+            tot = float(d[kk].replace(",", "")) * N_SM
+            print(f"   {'l1tex__data_pipe_lsu_wavefronts (per-SM avg x ' + str(N_SM) + ')':65s} "
+                  f"{tot:18.0f}")
         stalls = [(k, d[k]) for k in hdr if k.startswith("smsp__average_warp_latency_issue_stalled")
                   or k.startswith("smsp__warp_issue_stalled_") and k.endswith("_per_warp_active.pct")]
         vals = []
