@@ -1282,7 +1282,7 @@ __global__ void __launch_bounds__(256, 4) bwd_sym8_kernel(GeomDev G,
 // contiguous row segments; partial sums are combined in segment order through
 // shared memory (deterministic).
 template <typename TOut, int kAG, bool kLock = false, bool kMix = false, bool kPM = false,
-          int kSeg = 1>
+          int kSeg = 1, int kStride = 1>
 __global__ void __launch_bounds__(kAG == 1 ? 128 : 32 * kAG * kSeg) fwd_sym_kernel(GeomDev G, const float* __restrict__ P,
                                                       const float* __restrict__ PT,
                                                       TOut* __restrict__ sino) {
@@ -1293,10 +1293,16 @@ __global__ void __launch_bounds__(kAG == 1 ? 128 : 32 * kAG * kSeg) fwd_sym_kern
   } else if (kMix) {
     // lanes = 8 rays x 4 adjacent angles: the warp's addresses span ~8 rays
     // (2-3 sectors per load instead of 6-7 for 32 rays of one angle); the warp
-    // walks the union of its lanes' slab ranges (see clampk below)
+    // walks the union of its lanes' slab ranges (see clampk below).
+    // kStride > 1: the block's kAG ray octets are kStride octets apart (kStride
+    // consecutive blocks interleave over kAG * kStride octets), so no two warps
+    // of a block load the same L1 lines: warps of one block that shared lines
+    // at octet boundaries cost extra L1 data-pipe wavefronts (2.34 instead of
+    // 2.09 per LDG.64; n = 4096 forward 16.8 -> 15.5 ms, profiles/r2s_*)
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     hidx = blockIdx.y * 4 + (lane >> 3);
-    j = blockIdx.x * 8 * (kAG) + warp * 8 + (lane & 7);
+    j = ((blockIdx.x / kStride) * kAG * kStride + (blockIdx.x % kStride) + warp * kStride) * 8 +
+        (lane & 7);
   } else {
     hidx = blockIdx.y * kAG + (threadIdx.x >> 5);
     j = blockIdx.x * 32 + (threadIdx.x & 31);
@@ -1961,9 +1967,20 @@ static cudaError_t fwd_v2_impl(const GeomDev& G, const void* x, void* ws, void* 
     else if (seg == 4)
       fast::fwd_sym_kernel<TOut, ag, false, true, true, 4><<<mgrid, dim3(32 * ag, 4), 0, st>>>(
           G, (const float*)PM, (const float*)PMT, (TOut*)y);
-    else
-      fast::fwd_sym_kernel<TOut, ag, false, true, true><<<mgrid, 32 * ag, 0, st>>>(
-          G, (const float*)PM, (const float*)PMT, (TOut*)y);
+    else {
+      // ray octets kStride apart inside each block (see fwd_sym_kernel)
+      constexpr int kStride = 4;
+      dim3 sgrid(((G.d + 1) / 2 + 8 * ag * kStride - 1) / (8 * ag * kStride) * kStride,
+                 (G.n_half + 3) / 4);
+      // (below n ~ 1280 the planes are L2-resident and the octets' shared L1
+      // lines are worth more: n = 1024 0.36 ms adjacent vs 0.39 strided)
+      if (G.n >= 1280)
+        fast::fwd_sym_kernel<TOut, ag, false, true, true, 1, kStride><<<sgrid, 32 * ag, 0, st>>>(
+            G, (const float*)PM, (const float*)PMT, (TOut*)y);
+      else
+        fast::fwd_sym_kernel<TOut, ag, false, true, true><<<mgrid, 32 * ag, 0, st>>>(
+            G, (const float*)PM, (const float*)PMT, (TOut*)y);
+    }
     e = cudaGetLastError();
     if (e != cudaSuccess || Gx->m == 0) return e;
     // the axis-aligned angles of the set: slab segments over threadIdx.y
