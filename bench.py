@@ -20,15 +20,16 @@ rel. residual 1e-4, setup separate, plain CGLS beside it), the end-to-end
 number with host buffers (``e2e``), the CPU baselines and the rooflines;
 ``--workload config2|config4`` runs the other BASELINE configurations.
 
-``value`` is the faster of two timings of the same steps: the two independent
-products on two streams (they share the SMs; ``value_two_streams``) or back
+``value`` is the DEPENDENT pair a Krylov iteration uses: A x then A^T y back
 to back on one stream (``value_sequential``, which also gives the per-kernel
-times behind the rooflines); ``pair_schedule`` names the one reported.  ``e2e`` is what a user streaming pairs through the
-public API sees: every step copies x and y from pinned host memory and both
-results back, with copies on their own streams (double-buffered, overlapping
-the kernels) and the two independent products on two streams, so the
-forward (bound by the L1 data pipe) and the backprojection (more ALU / issue
-bound) share the SMs -- which is why ``e2e`` can exceed ``value``.
+times behind the rooflines); the two independent config-3 products on two
+streams sharing the SMs are reported beside it (``value_two_streams``).
+``e2e`` is the drop-in call a reference-style user makes: ``sino = w @ x;
+img = w.T @ y`` with float32 numpy vectors in and out (every call copies its
+operand to HBM and its result back before returning).  ``e2e_pipelined`` is
+what a user streaming pairs through the public API with pinned host buffers
+sees: copies on their own streams (double-buffered, overlapping the kernels)
+and the two independent products on two streams.
 
 Prints ONE JSON line (rank 0).  ``--impl reference`` times the reference
 algorithm on the host CPU instead (the pinned C oracle: the reference's CSR
@@ -515,17 +516,17 @@ def run_ours(args):
     if world > 1:
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
     t_tot, t_fwd, t_bwd, t_conc = [float(v) for v in tt.cpu()]
-    # ``value``: the config-3 step's two products are independent (x and y are
-    # separate inputs), so they run on two streams and share the SMs;
-    # ``value_sequential`` beside it is the DEPENDENT schedule a Krylov
-    # iteration uses (A x, then A^T y, back to back on one stream), which also
-    # gives the per-kernel times behind the rooflines
-    t_val = t_conc
+    # ``value``: the DEPENDENT schedule a Krylov iteration uses (A x, then A^T y,
+    # back to back on one stream), which also gives the per-kernel times behind
+    # the rooflines; the config-3 step's two products are independent (x and y
+    # are separate inputs), so the same steps on two streams sharing the SMs
+    # are reported beside it (``value_two_streams``)
+    t_val = t_tot
     ms_step = t_val / args.steps * 1e3
     rays_total = m * d
     value = rays_total * args.steps / t_val / 1e9
-    value_seq = rays_total * args.steps / t_tot / 1e9
-    value_conc = value
+    value_seq = value
+    value_conc = rays_total * args.steps / t_conc / 1e9
 
     # ---- end to end through the drop-in call -----------------------------
     # What a reference-style caller does (geometry.py:200-215 semantics): numpy
@@ -719,9 +720,9 @@ def run_ours(args):
                          "peak_source": peak_src},
         "roofline_onchip": onchip_roofline(n, fwd_avg, bwd_avg, n_sm, f_sm, world),
         "nnz": {"exact_local": nnz_local, "formula_local": nnz_formula},
-        "pair_schedule": "two streams (the two independent products share the SMs); "
-                         "value_sequential = dependent A x then A^T y on one stream",
-        "ms_per_step_sequential": t_tot / args.steps * 1e3,
+        "pair_schedule": "one stream, dependent (A x then A^T y); value_two_streams = the "
+                         "two independent products on two streams sharing the SMs",
+        "ms_per_step_two_streams": t_conc / args.steps * 1e3,
         "value_two_streams": value_conc,
         "value_sequential": value_seq,
         "step_ms_sequential": {"median": step_ms[len(step_ms) // 2], "best": step_ms[0]},

@@ -188,6 +188,13 @@ int wmg_cgs_update(long long n, int k, double *w, const double *V, long long ldv
 int wmg_combo(long long n, int k, double *out, const double *V, long long ldv, const double *cf,
               int accumulate, void *stream);
 int wmg_cast(long long n, int to_f32, void *out, const void *in, void *stream);
+/* Host -> device copy of a caller's pageable vector (the numpy `w @ x` calls,
+ * geometry.py:200-215) staged through `pinned` (>= bytes of page-locked host
+ * memory): host threads copy 4 MB chunks, each chunk's DMA is issued on the
+ * stream as soon as it has landed.  Returns once every DMA is issued; `pinned`
+ * may be reused after the stream passes them. */
+int wmg_h2d_staged(void *dst, const void *src, size_t bytes, void *pinned, int threads,
+                   void *stream);
 /* device-coefficient variants (coefficient read from device memory, so solver
  * iterations can be captured in a CUDA graph): out = y + sgn*(coef[0]*x);
  * out = a*x + coef[0]*y */

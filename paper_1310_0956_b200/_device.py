@@ -68,26 +68,18 @@ def to_device(v, dtype=None, device=None):
 # Host <-> device copies of large numpy vectors (the reference-style call
 # ``w @ x`` with numpy in and out).  Measured on the B200 box (64-95 MB):
 # pageable H2D 10.9 GB/s, ``.cpu()`` D2H 2.1 GB/s; pinned copies 47-57 GB/s.
-# H2D: the array is copied into a cached pinned staging buffer by a few host
-# threads (numpy releases the GIL) and each slice's DMA is issued as soon as
-# it is staged.  D2H: into a block of torch's caching pinned-host allocator,
-# returned as a numpy view that keeps the block alive.
+# H2D: ``wmg_h2d_staged`` (csrc/hostio.cu) copies the array into a cached
+# pinned staging buffer with a pool of native host threads (no GIL) in 4 MB
+# chunks and issues each chunk's DMA as soon as it has landed.  D2H: into a
+# pinned buffer from a small pool, returned as the numpy view itself.
 _STAGE_MIN_BYTES = 64 << 10         # below: plain pageable copies (latency bound anyway)
-_STAGE_THREADS = 4
+_STAGE_THREADS = 8
 _stage = {}
 _stage_lock = threading.Lock()
-_pool = None
-
-
-def _copy_pool():
-    global _pool
-    if _pool is None:
-        from concurrent.futures import ThreadPoolExecutor
-        _pool = ThreadPoolExecutor(_STAGE_THREADS, thread_name_prefix="wmg-stage")
-    return _pool
 
 
 def _h2d_staged(a, dtype, dev):
+    from . import _native as N
     t = torch()
     key = (str(dev), threading.get_ident())
     with _stage_lock:
@@ -99,18 +91,10 @@ def _h2d_staged(a, dtype, dev):
             _stage[key] = ent
     buf, done = ent
     done.synchronize()                       # the previous DMA out of this buffer
-    host = buf[:a.nbytes].view(dtype)
-    hn = host.numpy()
     out = t.empty(a.size, dtype=dtype, device=dev)
-    n = a.size
-    k = max(1, min(_STAGE_THREADS, a.nbytes >> 20))     # ~1 MB or more per host thread
-    bounds = [(i * n) // k for i in range(k + 1)]
-    futs = [_copy_pool().submit(np.copyto, hn[bounds[i]:bounds[i + 1]],
-                                a.reshape(-1)[bounds[i]:bounds[i + 1]]) for i in range(k)]
     stream = t.cuda.current_stream(dev)
-    for i, f in enumerate(futs):
-        f.result()
-        out[bounds[i]:bounds[i + 1]].copy_(host[bounds[i]:bounds[i + 1]], non_blocking=True)
+    N.call("wmg_h2d_staged", out.data_ptr(), a.ctypes.data, a.nbytes, buf.data_ptr(),
+           _STAGE_THREADS, stream.cuda_stream)
     done.record(stream)
     return out
 

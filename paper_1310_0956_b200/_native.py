@@ -68,6 +68,7 @@ _SIGS = {
     "wmg_cgs_update": (_i, [_ll, _i, _dp, _dp, _ll, _dp, _vp]),
     "wmg_combo": (_i, [_ll, _i, _dp, _dp, _ll, _dp, _i, _vp]),
     "wmg_cast": (_i, [_ll, _i, _dp, _dp, _vp]),
+    "wmg_h2d_staged": (_i, [_vp, _vp, ctypes.c_size_t, _vp, _i, _vp]),
     "wmg_axpy_dev": (_i, [_ll, _dp, _dp, _dp, _i, _dp, _vp]),
     "wmg_lincomb_dev": (_i, [_ll, _dp, _d, _dp, _dp, _dp, _vp]),
     "wmg_cgls_scalars": (_i, [_dp, _d, _i, _vp]),

@@ -80,6 +80,7 @@ cudaError_t sym_pack(int, int, const double*, long long, double*, long long, cud
 cudaError_t packed_symv(int, int, const double*, long long, const double*, long long, double*,
                         long long, double*, cudaStream_t);
 bool tma_window_fits(const AngleParams*, int, int, int);
+cudaError_t h2d_staged(void*, const void*, size_t, void*, int, cudaStream_t);
 }  // namespace wmg
 
 struct wmg_geometry {
@@ -637,6 +638,14 @@ int wmg_cgls_scalars(double* S, double lam, int op, void* stream) {
   if (op < 0 || op > 2) return fail(WMG_EINVAL, "bad scalar op");
   return cuda_rc(wmg::cgls_scalars(S, lam, op, STREAM(stream)));
 }
+int wmg_h2d_staged(void* dst, const void* src, size_t bytes, void* pinned, int threads,
+                   void* stream) {
+  if (bytes == 0) return WMG_OK;
+  if (!dst || !src || !pinned) return fail(WMG_EINVAL, "h2d_staged: NULL buffer");
+  if (threads < 1 || threads > 64) return fail(WMG_EINVAL, "h2d_staged: threads not in [1, 64]");
+  return cuda_rc(wmg::h2d_staged(dst, src, bytes, pinned, threads, STREAM(stream)));
+}
+
 int wmg_cast(long long n, int to_f32, void* out, const void* in, void* stream) {
   REQ(out && in);
   return cuda_rc(wmg::ew_cast(n, to_f32, out, in, STREAM(stream)));

@@ -7,7 +7,7 @@ import os
 import re
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-SRC = "r2_pair4096_ncu_full.txt"
+SRC = "r2b_pair4096_ncu_full.txt"
 
 
 def parse(path):
