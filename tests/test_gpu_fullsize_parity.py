@@ -98,3 +98,30 @@ def test_default_dispatch_pair_vs_oracle(gpu, oracle_proj, n):
     lhs = float(np.dot(got_f.ravel(), y64))
     rhs = float(np.dot(x64, got_b))
     assert abs(lhs - rhs) <= 1e-6 * abs(lhs)
+
+
+@pytest.mark.parametrize("n,m,stride", [(1280, 720, 4), (1536, 1000, 4), (1024, 1024, 1)])
+def test_forward_block_layouts_vs_parity(gpu, n, m, stride):
+    """The symmetric forward's block layouts around their switch (ray octets 4
+    apart inside a block from n = 1280, adjacent below), on angle counts that are
+    not multiples of the 4-angle groups' super-blocks: the full sinogram within
+    1e-5 of the float64 parity forward (reference geometry.py:200-206), every row
+    within 1e-5, the layout asserted from the launched kernel's template."""
+    torch = gpu
+    from paper_1310_0956_b200.geometry import build_geometry, build_projector
+    d = int(math.ceil(n * math.sqrt(2.0)))
+    g = build_geometry(n, d, m)
+    w = build_projector(g, precision="float32")
+    x = np.random.default_rng(n + m).uniform(0.0, 1.0, n * n).astype(np.float32)
+    xd = torch.from_numpy(x).cuda()
+    sino = torch.empty(m * d, dtype=torch.float32, device="cuda")
+    names = _kernel_names(torch, lambda: w.forward_(xd, sino), "fwd_sym_kernel")
+    k = [s for s in names if "fwd_sym_kernel" in s]
+    assert k and all(s.split("(")[0].replace(" ", "").endswith(f",1,{stride}>") for s in k), k
+    got = sino.double().cpu().numpy().reshape(m, d)
+    ref = build_projector(g).forward(torch.from_numpy(x.astype(np.float64)).cuda())
+    ref = ref.cpu().numpy().reshape(m, d)
+    assert np.linalg.norm(got - ref) <= 1e-5 * np.linalg.norm(ref)
+    err = np.linalg.norm(got - ref, axis=1)
+    nrm = np.linalg.norm(ref, axis=1)
+    assert np.all(err <= 1e-5 * np.maximum(nrm, 1e-30)), int(np.argmax(err / np.maximum(nrm, 1e-30)))
