@@ -61,6 +61,14 @@ def to_device(v, dtype=None, device=None):
     a = np.ascontiguousarray(np.asarray(v), dtype=np.float64 if dtype == t.float64 else np.float32)
     dev = t.device(device) if device is not None else t.device("cuda", t.cuda.current_device())
     if a.nbytes >= _STAGE_MIN_BYTES:
+        h = t.from_numpy(a)
+        if h.is_pinned():
+            # already page-locked (e.g. a previous result handed out from the
+            # pinned pool, as in the reference's ``w.T @ (w @ v)``): one DMA
+            out = t.empty(a.size, dtype=dtype, device=dev)
+            out.copy_(h, non_blocking=True)
+            t.cuda.current_stream(dev).synchronize()   # the caller may reuse the array
+            return out, True
         return _h2d_staged(a, dtype, dev), True
     return t.from_numpy(a).to(dev, non_blocking=False), True
 

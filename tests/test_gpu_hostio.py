@@ -71,3 +71,18 @@ def test_concurrent_numpy_calls_from_threads():
         t.join()
     assert not errs, errs
     assert outs == {0: (True, True), 1: (True, True)}
+
+
+def test_pinned_numpy_result_fed_back():
+    """A result of `w @ x` is handed out from the pinned pool; feeding it straight
+    into `w.T @ ...` (the reference's normal_operator, solvers.py:140-156) takes
+    the direct DMA path and gives the same image as a pageable copy."""
+    from paper_1310_0956_b200 import build_geometry, build_projector
+    n = 512
+    w = build_projector(build_geometry(n, 725, 128), precision="float32")
+    x = np.random.default_rng(5).random(n * n, dtype=np.float32)
+    s = w @ x
+    assert torch.from_numpy(s).is_pinned()
+    a = w.T @ s
+    b = w.T @ s.copy()
+    assert np.array_equal(a, b)
