@@ -1285,7 +1285,8 @@ template <typename TOut, int kAG, bool kLock = false, bool kMix = false, bool kP
           int kSeg = 1, int kStride = 1>
 __global__ void __launch_bounds__(kAG == 1 ? 128 : 32 * kAG * kSeg) fwd_sym_kernel(GeomDev G, const float* __restrict__ P,
                                                       const float* __restrict__ PT,
-                                                      TOut* __restrict__ sino) {
+                                                      TOut* __restrict__ sino, int band_lo = 0,
+                                                      int band_hi = 1 << 30, int band_acc = 0) {
   int hidx, j;
   if (kAG == 1) {
     hidx = blockIdx.y;
@@ -1332,6 +1333,10 @@ __global__ void __launch_bounds__(kAG == 1 ? 128 : 32 * kAG * kSeg) fwd_sym_kern
   }
   int rw0 = __reduce_min_sync(0xffffffffu, r0);
   int rw1 = __reduce_max_sync(0xffffffffu, r1);
+  // slab band [band_lo, band_hi) of a banded pass (the planes' working set of
+  // one pass stays L2-resident); band_acc: add to the partial sums in sino
+  rw0 = max(rw0, band_lo);
+  rw1 = min(rw1, band_hi - 1);
   if (kSeg > 1 && rw0 <= rw1) {   // this segment's share of the warp's slab range
     const int len = rw1 - rw0 + 1, sg = threadIdx.y;
     const int rs = rw0 + (len * sg) / kSeg;
@@ -1481,11 +1486,24 @@ __global__ void __launch_bounds__(kAG == 1 ? 128 : 32 * kAG * kSeg) fwd_sym_kern
     // slab-coordinate images -> rays; x-major swaps which image is the x-mirror
     const float r_m = A.major ? accB.y : accA.y;    // (m-a, j)
     const float r_mr = A.major ? accA.y : accB.y;   // (m-a, d-1-j)
+    if (band_acc) {
+      TOut* p0 = sino + (long long)a * d + j;
+      TOut* p1 = sino + (long long)b * d + j;
+      *p0 = (TOut)((float)*p0 + accA.x);
+      *p1 = (TOut)((float)*p1 + r_m);
+      if (d - 1 - j != j) {
+        TOut* p2 = sino + (long long)a * d + (d - 1 - j);
+        TOut* p3 = sino + (long long)b * d + (d - 1 - j);
+        *p2 = (TOut)((float)*p2 + accB.x);
+        *p3 = (TOut)((float)*p3 + r_mr);
+      }
+    } else {
     __stcs(sino + (long long)a * d + j, (TOut)accA.x);   // streaming: keep L2 for the planes
     __stcs(sino + (long long)b * d + j, (TOut)r_m);
     if (d - 1 - j != j) {
       __stcs(sino + (long long)a * d + (d - 1 - j), (TOut)accB.x);
       __stcs(sino + (long long)b * d + (d - 1 - j), (TOut)r_mr);
+    }
     }
   }
 }
@@ -1974,7 +1992,20 @@ static cudaError_t fwd_v2_impl(const GeomDev& G, const void* x, void* ws, void* 
                  (G.n_half + 3) / 4);
       // (below n ~ 1280 the planes are L2-resident and the octets' shared L1
       // lines are worth more: n = 1024 0.36 ms adjacent vs 0.39 strided)
-      if (G.n >= 1280)
+      // Banded passes over the slab index when the two padded planes exceed the
+      // L2 (n = 4096: 277 MB -> 4 passes): the blocks of one pass walk only
+      // slabs [lo, hi) (rows lo..hi-1 and their mirrors n-hi..n-lo-1 of both
+      // planes), so the planes are read from DRAM about once instead of ~30x
+      // (9.5 -> 0.9 GB per launch, 15.6 -> 15.1 ms); later passes add their
+      // partial ray sums to the sinogram (fixed order: deterministic)
+      const double plane_mb = 2.0 * G.n * (G.n + 2.0 * kPadMargin) * 8.0 / 1e6;
+      const int nb = plane_mb > 128.0 ? (int)ceil(plane_mb / 70.0) : 1;
+      if (G.n >= 1280 && nb > 1) {
+        for (int bi = 0; bi < nb; ++bi)
+          fast::fwd_sym_kernel<TOut, ag, false, true, true, 1, kStride><<<sgrid, 32 * ag, 0, st>>>(
+              G, (const float*)PM, (const float*)PMT, (TOut*)y, G.n * bi / nb,
+              G.n * (bi + 1) / nb, bi > 0);
+      } else if (G.n >= 1280)
         fast::fwd_sym_kernel<TOut, ag, false, true, true, 1, kStride><<<sgrid, 32 * ag, 0, st>>>(
             G, (const float*)PM, (const float*)PMT, (TOut*)y);
       else

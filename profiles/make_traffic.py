@@ -7,24 +7,42 @@ import os
 import re
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-SRC = "r2b_pair4096_ncu_full.txt"
+SRC = "r2c_pair4096_ncu_full.txt"
+FWD_PASSES = 4          # banded passes of the n = 4096 forward (projector_fast.cu)
 
 
 def parse(path):
-    out, cur = {}, None
+    """Per-product counters: the forward of one product is FWD_PASSES banded
+    launches of fwd_sym_kernel (summed), the backward one bwd_sym8 launch."""
+    launches = {"forward": [], "backward": []}
+    cur = None
     for ln in open(path):
         if ln.startswith("=="):
             cur = "forward" if "fwd_sym_kernel" in ln else "backward" if "bwd_sym8" in ln else None
-            if cur in out:          # first launch of each kernel only
-                cur = None
-            elif cur:
-                out[cur] = {}
+            if cur:
+                launches[cur].append({})
             continue
         if cur is None:
             continue
         m = re.match(r"\s+(\S.*?)\s{2,}([-0-9.eE+]+)\s*(\S*)\s*$", ln)
         if m:
-            out[cur][m.group(1).strip()] = (float(m.group(2)), m.group(3))
+            v, u = float(m.group(2)), m.group(3)
+            scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9,
+                     "ns": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3}
+            if u in scale:      # common units so the banded launches can be summed
+                v, u = v * scale[u], ("byte" if "byte" in u else "us")
+            launches[cur][-1][m.group(1).strip()] = (v, u)
+    out = {}
+    for kern, want in (("forward", FWD_PASSES), ("backward", 1)):
+        ls = launches[kern][:want]
+        assert len(ls) == want, (kern, len(ls))
+        agg = {}
+        for d in ls:
+            for k, (v, u) in d.items():
+                if k.endswith(".pct") or "pct_of_peak" in k or k.startswith("launch__"):
+                    continue
+                agg[k] = (agg.get(k, (0.0, u))[0] + v, u)
+        out[kern] = agg
     return out
 
 
@@ -32,7 +50,7 @@ def main():
     k = parse(os.path.join(HERE, SRC))
     unit = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
     res = {"_source": f"profiles/{SRC} (ncu --set full --clock-control none, n = 4096 config-3 "
-                      "pair, default dispatch); bytes = dram__bytes_read.sum + "
+                      "pair, default dispatch; the forward = its 4 banded launches summed); bytes = dram__bytes_read.sum + "
                       "dram__bytes_write.sum; L1 data-pipe wavefronts = per-SM average x 148"}
     for kern in ("forward", "backward"):
         d = k[kern]
