@@ -1731,18 +1731,10 @@ __global__ void __launch_bounds__(128) fwd_sym64_kernel(GeomDev G, const double*
 // symmetric backprojector in float64: 52-fractional-bit fixed point
 constexpr double kQ52 = 4503599627370496.0;   // 2^52
 constexpr int kSym64Chunk = 8;
-constexpr int kSym64MaxCluster = 16;   // small-grid angle splits = cluster size (non-portable)
 
-// kCluster (small grids): the nsplit CTAs of one tile form a thread-block
-// cluster along z, each taking a slice of the primary angles.  After the angle
-// loop every CTA parks its four partial tiles in shared memory; CTA r then sums
-// its 1/nsplit share of the tile over the peers in rank order through DSMEM,
-// adds the axis-aligned angles of Gx and stores -- deterministic, no global
-// scratch, no second launch.  blockIdx.z = batch item * nsplit + rank.
-template <typename TIn, typename TOut, bool kAccumulate, bool kCluster = false>
-__global__ void __launch_bounds__(256, kCluster ? 3 : 4) bwd_sym64_kernel(GeomDev G, const TIn* __restrict__ sino,
-                                                        TOut* __restrict__ img, int nsplit,
-                                                        GeomDev Gx) {
+template <typename TIn, typename TOut, bool kAccumulate>
+__global__ void __launch_bounds__(256, 4) bwd_sym64_kernel(GeomDev G, const TIn* __restrict__ sino,
+                                                        TOut* __restrict__ img) {
   // winA = win[0] (y_a[t], y_b[t], y_a[t+1], y_b[t+1]), winB = win[1] reversed
   // detectors; in cluster mode the same 32 KB hold the partial tile at the end
   __shared__ double4 win[2][kSym64Chunk][kBwdWin];
@@ -1761,19 +1753,12 @@ __global__ void __launch_bounds__(256, kCluster ? 3 : 4) bwd_sym64_kernel(GeomDe
   const double half = (double)n * 0.5, dc = (double)(d - 1) * 0.5;
   const double xc0 = (double)col0 - half + 0.5;
   const double yc0 = half - (double)row0 - 0.5;
-  const int rank = kCluster ? (int)(blockIdx.z % nsplit) : 0;
-  if (kCluster) {
-    const long long item = blockIdx.z / nsplit;
-    sino += item * G.m * d;
-    img += item * n * n;
-  }
   double acc[4][4];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int q = 0; q < 4; ++q) acc[i][q] = 0.0;
-  const int q_begin = (int)((long long)G.n_prim * rank / nsplit);
-  const int q_end = (int)((long long)G.n_prim * (rank + 1) / nsplit);
+  const int q_begin = 0, q_end = G.n_prim;
   for (int c0 = q_begin; c0 < q_end; c0 += kSym64Chunk) {
     const int na = min(kSym64Chunk, q_end - c0);
     __syncthreads();
@@ -1843,57 +1828,125 @@ __global__ void __launch_bounds__(256, kCluster ? 3 : 4) bwd_sym64_kernel(GeomDe
     const int c = (q == 0 || q == 3) ? col : n - 1 - col;
     return (long long)r * n + c;
   };
-  if constexpr (!kCluster) {
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < 4; ++i)
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const long long p = pixel(i, q, warp, lane);
-        if (kAccumulate)
-          img[p] = (TOut)((double)img[p] + acc[i][q]);
-        else
-          img[p] = (TOut)acc[i][q];
-      }
-  } else {
-    namespace cg = cooperative_groups;
-    cg::cluster_group cl = cg::this_cluster();
-    double* part = reinterpret_cast<double*>(&win[0][0][0]);   // [16][256]
-    __syncthreads();
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int q = 0; q < 4; ++q) part[(i * 4 + q) * 256 + tid] = acc[i][q];
-    cl.sync();
-    const int k0 = 16 * rank / nsplit, k1 = 16 * (rank + 1) / nsplit;
-    const double dcx = (double)(Gx.d - 1) * 0.5;
-    for (int k = k0; k < k1; ++k) {
-      double s = 0.0;   // rank order; loads issued four at a time
-      for (int z0 = 0; z0 < nsplit; z0 += 4) {
-        double v[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-          v[u] = (z0 + u < nsplit) ? cl.map_shared_rank(part, z0 + u)[k * 256 + tid] : 0.0;
-        s = (z0 == 0) ? v[0] : s + v[0];
-#pragma unroll
-        for (int u = 1; u < 4; ++u)
-          if (z0 + u < nsplit) s += v[u];
-      }
-      const long long p = pixel(k >> 2, k & 3, warp, lane);
-      const int prow = (int)(p / n), pix = (int)(p % n);
-      const double xc = (double)pix - half + 0.5, yc = half - (double)prow - 0.5;
-      for (int a = 0; a < Gx.m; ++a) {   // axis-aligned angles (Gx: the tie rule)
-        const AngleParams& P = Gx.ang[a];
-        const int j = (int)ceil(xc * P.c + yc * P.s + dcx - 0.5);
-        if (j >= 0 && j < Gx.d)
-          s += (double)__ldg(sino + (long long)(Gx.rowmap ? Gx.rowmap[a] : a) * Gx.d + j);
-      }
+    for (int q = 0; q < 4; ++q) {
+      const long long p = pixel(i, q, warp, lane);
       if (kAccumulate)
-        img[p] = (TOut)((double)img[p] + s);
+        img[p] = (TOut)((double)img[p] + acc[i][q]);
       else
-        img[p] = (TOut)s;
+        img[p] = (TOut)acc[i][q];
     }
-    cl.sync();   // peers' shared memory must outlive the remote reads
+
+}
+
+
+// Small-grid float64 symmetric backprojector without staging or clusters
+// (config 1 and the WMG node systems, n <= 512).  At these sizes the whole
+// sinogram is L2-resident and the angle-split cluster kernel was latency bound
+// (18 % of the warps active, a third of its stall samples at the cluster
+// barrier).  Here a CTA owns 32 pixels of one quadrant row (and their three
+// mirror / rotation images) and its kSlices warps split the primary angles;
+// every (pixel, angle) reads its two detectors of the four sinogram rows
+// directly (L1 / L2), so a warp has no barrier until the end, where the slice
+// partials are summed in slice order through shared memory and the axis-
+// aligned angles are added (deterministic; same weights as bwd_sym64_kernel).
+// blockIdx = (column block of 32, quadrant row, batch item).
+constexpr int kSmall64Slices = 16;
+template <typename TIn, typename TOut, bool kAccumulate>
+__global__ void __launch_bounds__(32 * kSmall64Slices, 2) bwd_small64_kernel(GeomDev G,
+                                                                              const TIn* __restrict__ sino,
+                                                                              TOut* __restrict__ img,
+                                                                              GeomDev Gx) {
+  __shared__ double part[kSmall64Slices][4][32];
+  // per warp: the constants of up to 32 angles of its slice (lane l loads angle
+  // l of the chunk), read back as broadcasts -- no dependent global loads in
+  // the angle loop
+  __shared__ double2 angc[kSmall64Slices][32][3];   // (c, s), (dc - hw, ic), (hw ic, w1c)
+  __shared__ double angL[kSmall64Slices][32];
+  __shared__ int2 angab[kSmall64Slices][32];
+  const int n = G.n, d = G.d;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int row = blockIdx.y, col = blockIdx.x * 32 + lane;   // top-left quadrant pixel
+  {
+    const long long item = blockIdx.z;
+    sino += item * G.m * d;
+    img += item * (long long)n * n;
   }
+  const double half = (double)n * 0.5, dc = (double)(d - 1) * 0.5;
+  const double xc = (double)col - half + 0.5, yc = half - (double)row - 0.5;
+  double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
+  const int q0 = (int)((long long)G.n_prim * warp / kSmall64Slices);
+  const int q1 = (int)((long long)G.n_prim * (warp + 1) / kSmall64Slices);
+  for (int qc = q0; qc < q1; qc += 32) {
+    const int cnt = min(32, q1 - qc);
+    if (lane < cnt) {
+      const int a = G.prim[qc + lane];
+      const AngleParams& A = G.ang[a];
+      const double hw = A.hw, ic = A.inv_cs;
+      angc[warp][lane][0] = make_double2(A.c, A.s);
+      angc[warp][lane][1] = make_double2(dc - hw, ic);
+      angc[warp][lane][2] = make_double2(hw * ic, (2.0 * hw - 3.0) * ic);
+      angL[warp][lane] = A.L;
+      angab[warp][lane] = make_int2(a, G.mir[a]);
+    }
+    __syncwarp();
+#pragma unroll 4
+    for (int t = 0; t < cnt; ++t) {
+      const double2 cs = angc[warp][t][0], dh = angc[warp][t][1], hv = angc[warp][t][2];
+      const double L = angL[warp][t];
+      const int2 ab = angab[warp][t];
+      const double P = fma(xc, cs.x, fma(yc, cs.y, dh.x));
+      const double fl = floor(P);
+      const double f = 1.0 + (P - fl);               // in [1, 2), as the fixed-point kernel
+      const double d0 = (2.0 - (dc - dh.x)) - f;      // 2 - hw - f
+      const double w0 = dmin_to(fma(-fabs(d0), dh.y, hv.x), L);
+      const double w1 = dmax_0(fma(f, dh.y, hv.y));
+      const int jA = (int)fl + 1, jB = jA + 1;
+      const int rA = d - 1 - jA, rB = d - 1 - jB;
+      const TIn* ya = sino + (long long)ab.x * d;
+      const TIn* yb = sino + (long long)ab.y * d;
+      auto ld = [&](const TIn* y, int j) -> double {
+        return (j >= 0 && j < d) ? (double)__ldg(y + j) : 0.0;
+      };
+      const double a0 = ld(ya, jA), a1 = ld(ya, jB), b0 = ld(yb, jA), b1 = ld(yb, jB);
+      const double c0 = ld(ya, rA), c1 = ld(ya, rB), e0 = ld(yb, rA), e1 = ld(yb, rB);
+      acc0 = fma(w0, a0, fma(w1, a1, acc0));   // (r, c) at a
+      acc1 = fma(w0, b0, fma(w1, b1, acc1));   // (r, n-1-c) at mir a
+      acc2 = fma(w0, c0, fma(w1, c1, acc2));   // (n-1-r, n-1-c) at a, detectors reversed
+      acc3 = fma(w0, e0, fma(w1, e1, acc3));   // (n-1-r, c) at mir a, reversed
+    }
+    __syncwarp();
+  }
+  part[warp][0][lane] = acc0;
+  part[warp][1][lane] = acc1;
+  part[warp][2][lane] = acc2;
+  part[warp][3][lane] = acc3;
+  __syncthreads();
+  if (warp >= 4) return;
+  // warp k finishes image k of the 32 pixels: slices in order, then the axis angles
+  const int k = warp;
+  double sacc = part[0][k][lane];
+#pragma unroll
+  for (int w = 1; w < kSmall64Slices; ++w) sacc += part[w][k][lane];
+  const int r = (k < 2) ? row : n - 1 - row;
+  const int cc = (k == 0 || k == 3) ? col : n - 1 - col;
+  const long long p = (long long)r * n + cc;
+  {
+    const double xcp = (double)cc - half + 0.5, ycp = half - (double)r - 0.5;
+    const double dcx = (double)(Gx.d - 1) * 0.5;
+    for (int ax = 0; ax < Gx.m; ++ax) {   // axis-aligned angles (Gx: the tie rule)
+      const AngleParams& Px = Gx.ang[ax];
+      const int j = (int)ceil(xcp * Px.c + ycp * Px.s + dcx - 0.5);
+      if (j >= 0 && j < Gx.d)
+        sacc += (double)__ldg(sino + (long long)(Gx.rowmap ? Gx.rowmap[ax] : ax) * Gx.d + j);
+    }
+  }
+  if (kAccumulate)
+    img[p] = (TOut)((double)img[p] + sacc);
+  else
+    img[p] = (TOut)sacc;
 }
 
 }  // namespace fast
@@ -2225,58 +2278,26 @@ static cudaError_t fwd64_impl(const GeomDev& G, const void* x, void* ws, void* y
   return cudaGetLastError();
 }
 
-// cluster launch of the small-grid symmetric backprojector (nsplit CTAs per
-// tile along z; > 8 needs the non-portable cluster-size attribute)
-template <typename TIn, typename TOut, bool kAcc>
-static cudaError_t bwd_sym64_cluster(const GeomDev& G, const GeomDev& Gx, const void* y, void* x,
-                                     int nsplit, int batch, cudaStream_t st) {
-  auto kern = fast::bwd_sym64_kernel<TIn, TOut, kAcc, true>;
-  static bool attr = false;   // per instantiation
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(G.n / 64, G.n / 64, nsplit * batch);
-  cfg.blockDim = dim3(256);
-  cfg.stream = st;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = 1;
-  at[0].val.clusterDim.y = 1;
-  at[0].val.clusterDim.z = nsplit;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, G, (const TIn*)y, (TOut*)x, nsplit, Gx);
-}
-
-// angle splits for the small-grid path: ~192 CTAs (1.3 per SM; the sweep at
-// 256^2 / 180 angles: 4 -> 44 us, 8 -> 37, 12 -> 29, 16 -> 31), at most one
-// cluster of kSym64MaxCluster, at least 4 primary angles per CTA.  Independent
-// of the batch: every item is summed exactly like a single call.
-static inline int sym64_nsplit(const GeomDev& G) {
-  const int tiles = (G.n / 64) * (G.n / 64);
-  return max(1, min(fast::kSym64MaxCluster, min((192 + tiles - 1) / tiles, G.n_prim / 4)));
-}
-
 template <typename TIn, typename TOut>
 static cudaError_t bwd64_impl(const GeomDev& G, const void* y, void* x, bool accumulate,
                               cudaStream_t st, const GeomDev* Gx, bool small = false,
                               int batch = 1) {
   if (!(G.sym && Gx)) return cudaErrorNotSupported;
-  if (small) {   // small grids: angle splits over a cluster, reduced through DSMEM
-    const int nsplit = sym64_nsplit(G);
-    return accumulate ? bwd_sym64_cluster<TIn, TOut, true>(G, *Gx, y, x, nsplit, batch, st)
-                      : bwd_sym64_cluster<TIn, TOut, false>(G, *Gx, y, x, nsplit, batch, st);
+  if (small) {   // small grids: stage-free angle-sliced kernel (bwd_small64_kernel)
+    dim3 grid(G.n / 64, G.n / 2, batch);
+    if (accumulate)
+      fast::bwd_small64_kernel<TIn, TOut, true><<<grid, 32 * fast::kSmall64Slices, 0, st>>>(
+          G, (const TIn*)y, (TOut*)x, *Gx);
+    else
+      fast::bwd_small64_kernel<TIn, TOut, false><<<grid, 32 * fast::kSmall64Slices, 0, st>>>(
+          G, (const TIn*)y, (TOut*)x, *Gx);
+    return cudaGetLastError();
   }
   dim3 grid(G.n / 64, G.n / 64, 1);
   if (accumulate)
-    fast::bwd_sym64_kernel<TIn, TOut, true><<<grid, 256, 0, st>>>(G, (const TIn*)y, (TOut*)x, 1,
-                                                                  *Gx);
+    fast::bwd_sym64_kernel<TIn, TOut, true><<<grid, 256, 0, st>>>(G, (const TIn*)y, (TOut*)x);
   else
-    fast::bwd_sym64_kernel<TIn, TOut, false><<<grid, 256, 0, st>>>(G, (const TIn*)y, (TOut*)x, 1,
-                                                                   *Gx);
+    fast::bwd_sym64_kernel<TIn, TOut, false><<<grid, 256, 0, st>>>(G, (const TIn*)y, (TOut*)x);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess || Gx->m == 0) return e;
   dim3 g2((G.n + 31) / 32, (G.n + 7) / 8);
