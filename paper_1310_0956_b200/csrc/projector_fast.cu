@@ -181,7 +181,7 @@ __global__ void __launch_bounds__(256) bwd_kernel(GeomDev G, const TIn* __restri
 // kSplit threads -- consecutive slab (angle) segments -- and reduce the
 // partial sums in shared memory in segment order (deterministic).
 constexpr int kSplit = 8;
-constexpr int kSplitF = 8;   // slab segments per ray of the padded-plane fp64 forward
+constexpr int kSplitF = 4;   // slab segments per ray of the padded-plane fp64 forward (8: same single-image time, 10 % slower sibling batches)
 constexpr int kFwdAG = 4;    // adjacent angles per symmetric-forward block
 
 // block (32 rays, kSplit slab segments); grid (ceil(d/32), m)
@@ -1560,11 +1560,12 @@ __global__ void pad_transpose64_kernel(const T* __restrict__ in, double* __restr
 
 // Small-grid float64 forward on the padded planes: one ray per lane, kSplit
 // slab segments per ray (threadIdx.y) reduced in shared memory in segment
-// order; u is evaluated directly at every slab end (fma), the two straddling
+// order; u is walked in 12.52 fixed point (see below), the two straddling
 // pixels are read without bounds checks (zero margins) and blended as
 // L v0 + wh (v1 - v0).  blockIdx.z = batch item.
-// kMix: lanes = 8 rays x 4 adjacent angles (fewer sectors per warp load)
-template <typename TOut, bool kMix = false>
+// kA: lanes = (32 / kA) rays x kA adjacent angles (kA = 4 default; 1, 2 and 8 measured
+// within 10 %: an LDG.64 of 32 lanes spans >= 8 sectors at any layout)
+template <typename TOut, int kA = 1>
 __global__ void __launch_bounds__(32 * kSplitF) fwd_split64_kernel(GeomDev G,
                                                                   const double* __restrict__ P,
                                                                   const double* __restrict__ PT,
@@ -1572,8 +1573,10 @@ __global__ void __launch_bounds__(32 * kSplitF) fwd_split64_kernel(GeomDev G,
                                                                   long long bs_sino) {
   __shared__ double part[kSplitF][33];
   const int lane = threadIdx.x, seg = threadIdx.y;
-  const int a = kMix ? blockIdx.y * 4 + (lane >> 3) : blockIdx.y;
-  const int j = kMix ? blockIdx.x * 8 + (lane & 7) : blockIdx.x * 32 + lane;
+  // lanes = (32 / kA) rays x kA adjacent angles
+  constexpr int kR = 32 / kA;
+  const int a = blockIdx.y * kA + lane / kR;
+  const int j = blockIdx.x * kR + lane % kR;
   const bool live = j < G.d && a < G.m;
   const int n = G.n;
   const int pitch = n + 2 * kPadMargin;
@@ -1590,8 +1593,11 @@ __global__ void __launch_bounds__(32 * kSplitF) fwd_split64_kernel(GeomDev G,
     const double slope = A.slope;
     int r0 = 0, r1 = n - 1;
     if (slope > 0.0) {
-      const double ra = floor((-1.0 - u0) / slope) - 1.0;
-      const double rb = ceil(((double)n + 1.0 - u0) / slope) + 1.0;
+      // one reciprocal instead of two divisions: the +-1 slab margins absorb
+      // the last-bit difference
+      const double is = __drcp_rn(slope);
+      const double ra = floor((-1.0 - u0) * is) - 1.0;
+      const double rb = ceil(((double)n + 1.0 - u0) * is) + 1.0;
       r0 = (int)fmax(ra, 0.0);
       r1 = (int)fmin(rb, (double)(n - 1));
     } else if (u0 < -1.0 || u0 > (double)n + 1.0) {
@@ -1603,28 +1609,25 @@ __global__ void __launch_bounds__(32 * kSplitF) fwd_split64_kernel(GeomDev G,
     const double* __restrict__ src = (A.major ? PT : P) + kPadMargin;
     const double L = A.L, Ls = A.Ls;
     const double* row = src + (long long)rs * pitch;
-    if (!A.mirror) {
-      for (int r = rs; r <= re; ++r) {
-        const double uh = fma((double)(r + 1), slope, u0);
-        const double fk = floor(uh);
-        const double wh = dmin_to((uh - fk) * Ls, L);     // NaN (0 * inf) -> L
-        const double* p = row + (int)fk;
-        const double v1 = __ldg(p), v0 = __ldg(p - 1);
-        acc = fma(L, v0, acc);
-        acc = fma(wh, v1 - v0, acc);
-        row += pitch;
-      }
-    } else {
-      for (int r = rs; r <= re; ++r) {
-        const double uh = fma((double)(r + 1), slope, u0);
-        const double fk = floor(uh);
-        const double wh = dmin_to((uh - fk) * Ls, L);
-        const double* p = row + (n - 1 - (int)fk);
-        const double v1 = __ldg(p), v0 = __ldg(p + 1);
-        acc = fma(L, v0, acc);
-        acc = fma(wh, v1 - v0, acc);
-        row += pitch;
-      }
+    // u in 12.52 fixed point (offset by the margin so it stays >= 0): the slab
+    // walk is integer adds, the straddled pixel the high bits and the fraction
+    // an exact bit move -- no floor / conversions in the loop; error <= (r + 1)
+    // 2^-53 px, as small as the direct fp64 evaluation's
+    constexpr double kQ52d = 4503599627370496.0;   // 2^52
+    const long long S = llrint(slope * kQ52d);
+    long long U = llrint((u0 + (double)kPadMargin) * kQ52d) + (long long)rs * S;
+    const int kofs = A.mirror ? (n - 1 + kPadMargin) : -kPadMargin;   // pixel = +-k + kofs
+    const int ksgn = A.mirror ? -1 : 1;
+    for (int r = rs; r <= re; ++r) {
+      U += S;
+      const int k = (int)(U >> 52);
+      const double f = __longlong_as_double(0x3FF0000000000000LL | (U & 0xFFFFFFFFFFFFFLL)) - 1.0;
+      const double wh = dmin_to(f * Ls, L);        // NaN (0 * inf) -> L
+      const double* p = row + (ksgn * k + kofs);
+      const double v1 = __ldg(p), v0 = __ldg(p - ksgn);
+      acc = fma(L, v0, acc);
+      acc = fma(wh, v1 - v0, acc);
+      row += pitch;
     }
   }
   part[seg][lane] = acc;
@@ -2319,7 +2322,7 @@ static cudaError_t fwd_impl(const GeomDev& G, const void* x, void* xT_ws, void* 
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     dim3 sg((G.d + 7) / 8, (G.m + 3) / 4), sb(32, fast::kSplitF);
-    fast::fwd_split64_kernel<TOut, true><<<sg, sb, 0, st>>>(G, P, PT, (TOut*)y, 0);
+    fast::fwd_split64_kernel<TOut, 4><<<sg, sb, 0, st>>>(G, P, PT, (TOut*)y, 0);
     return cudaGetLastError();
   }
   cudaError_t e = launch_transpose<TIn>(img, imgT, G.n, st);
@@ -2466,7 +2469,7 @@ cudaError_t fast_forward_batch(const GeomDev& G, int precision, int tin, int tou
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     dim3 sg((G.d + 7) / 8, (G.m + 3) / 4, batch), sb(32, fast::kSplitF);
-    fast::fwd_split64_kernel<double, true><<<sg, sb, 0, st>>>(G, P, PT, (double*)y, M);
+    fast::fwd_split64_kernel<double, 4><<<sg, sb, 0, st>>>(G, P, PT, (double*)y, M);
     return cudaGetLastError();
   }
   for (int b = 0; b < batch; ++b) {
