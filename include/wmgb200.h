@@ -210,6 +210,21 @@ int wmg_cgls_scalars(double *S, double lam, int op, void *stream);
  * restrict: out holds one (side/2)^2 block per band set in band_mask, in band
  * order.  prolong: fine = (accumulate ? fine : 0) + R_band^T coarse. */
 int wmg_haar_restrict(int side, const double *fine, int band_mask, double *out, void *stream);
+/* Batched forms for the sibling batches of the hybrid cycle (wtg_apply,
+ * multilevel.py:175-198), bit-identical to one wmg_haar_restrict /
+ * wmg_haar_prolong / wmg_smooth_update call per item: items contiguous (fine
+ * side^2 apart, coarse nbands * (side/2)^2 apart, smoother vectors n apart).
+ * wmg_haar_prolong_batch applies the nbands bands in the order given, each
+ * added to the running fine value (the first one overwrites when !accumulate);
+ * wmg_smooth_update_batch takes host arrays of per-item omegas and scaling
+ * pointers (device memory). */
+int wmg_haar_restrict_batch(int side, int batch, const double *fine, int band_mask, double *out,
+                            void *stream);
+int wmg_haar_prolong_batch(int side, int batch, int nbands, const int *bands,
+                           const double *coarse, double *fine, int accumulate, void *stream);
+int wmg_smooth_update_batch(long long n, int batch, double *z, const double *omegas,
+                            const double *const *c, const double *r, const double *az,
+                            void *stream);
 int wmg_haar_prolong(int side, const double *coarse, int band, double *fine, int accumulate,
                      void *stream);
 

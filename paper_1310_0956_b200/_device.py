@@ -297,6 +297,18 @@ def smooth_update(z, omega, c, r, az=None):
     return z
 
 
+def smooth_update_batch(Z, omegas, scalings, R, AZ=None):
+    """Z[b] += omegas[b] * (scalings[b] .* (R[b] - AZ[b])) for a batch of node
+    smoothers in one launch (rows of Z, R, AZ contiguous; bit-identical to
+    ``smooth_update`` per row)."""
+    B = Z.shape[0]
+    om = (ctypes.c_double * B)(*[float(o) for o in omegas])
+    cs = (ctypes.c_void_p * B)(*[c.data_ptr() for c in scalings])
+    N.call("wmg_smooth_update_batch", int(Z.shape[1]), B, ptr(Z), om, cs, ptr(R),
+           ptr(AZ) if AZ is not None else None, stream_handle())
+    return Z
+
+
 def hadamard(out, x, y):
     N.call("wmg_scale", out.numel(), ptr(out), 1.0, ptr(x), ptr(y), stream_handle())
     return out

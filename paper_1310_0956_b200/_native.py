@@ -75,6 +75,10 @@ _SIGS = {
     "wmg_batched_gemv": (_i, [_i, _i, _dp, _ll, _dp, _ll, _dp, _ll, _vp]),
     "wmg_haar_restrict": (_i, [_i, _dp, _i, _dp, _vp]),
     "wmg_haar_prolong": (_i, [_i, _dp, _i, _dp, _i, _vp]),
+    "wmg_haar_restrict_batch": (_i, [_i, _i, _dp, _i, _dp, _vp]),
+    "wmg_haar_prolong_batch": (_i, [_i, _i, _i, ctypes.POINTER(_i), _dp, _dp, _i, _vp]),
+    "wmg_smooth_update_batch": (_i, [_ll, _i, _dp, ctypes.POINTER(_d), ctypes.POINTER(_vp), _dp,
+                                     _dp, _vp]),
     "wmg_haar_prolong_path": (_i, [_i, _i, _i, ctypes.POINTER(_i), _dp, _dp, _vp]),
     "wmg_haar_restrict_path": (_i, [_i, _i, _i, ctypes.POINTER(_i), _dp, _dp, _vp]),
     "wmg_leaf_factor": (_i, [_vp, _i, ctypes.POINTER(_i), _ll, _ll, _dp, _vp]),

@@ -81,6 +81,11 @@ cudaError_t packed_symv(int, int, const double*, long long, const double*, long 
                         long long, double*, cudaStream_t);
 bool tma_window_fits(const AngleParams*, int, int, int);
 cudaError_t h2d_staged(void*, const void*, size_t, void*, int, cudaStream_t);
+cudaError_t haar_restrict_batch(int, int, const double*, int, double*, cudaStream_t);
+cudaError_t haar_prolong_batch(int, int, int, const int*, const double*, double*, int,
+                               cudaStream_t);
+cudaError_t ew_smooth_update_batch(long long, int, double*, const double*, const double* const*,
+                                   const double*, const double*, cudaStream_t);
 }  // namespace wmg
 
 struct wmg_geometry {
@@ -672,6 +677,40 @@ int wmg_haar_prolong(int side, const double* coarse, int band, double* fine, int
   if (side < 2 || side % 2) return fail(WMG_EINVAL, "grid side must be even and >= 2");
   if (band < 0 || band > 3) return fail(WMG_EINVAL, "bad band");
   return cuda_rc(wmg::haar_prolong(side, coarse, band, fine, accumulate, STREAM(stream)));
+}
+
+int wmg_haar_restrict_batch(int side, int batch, const double* fine, int band_mask, double* out,
+                            void* stream) {
+  if (batch == 0) return WMG_OK;
+  REQ(fine && out);
+  if (batch < 0) return fail(WMG_EINVAL, "negative batch");
+  if (side < 2 || side % 2) return fail(WMG_EINVAL, "grid side must be even and >= 2");
+  if (band_mask < 1 || band_mask > 15) return fail(WMG_EINVAL, "bad band mask");
+  return cuda_rc(wmg::haar_restrict_batch(side, batch, fine, band_mask, out, STREAM(stream)));
+}
+
+int wmg_haar_prolong_batch(int side, int batch, int nbands, const int* bands,
+                           const double* coarse, double* fine, int accumulate, void* stream) {
+  if (batch == 0) return WMG_OK;
+  REQ(bands && coarse && fine);
+  if (batch < 0) return fail(WMG_EINVAL, "negative batch");
+  if (side < 2 || side % 2) return fail(WMG_EINVAL, "grid side must be even and >= 2");
+  if (nbands < 1 || nbands > 4) return fail(WMG_EINVAL, "nbands must be in [1, 4]");
+  for (int i = 0; i < nbands; ++i)
+    if (bands[i] < 0 || bands[i] > 3) return fail(WMG_EINVAL, "bad band");
+  return cuda_rc(wmg::haar_prolong_batch(side, batch, nbands, bands, coarse, fine, accumulate,
+                                         STREAM(stream)));
+}
+
+int wmg_smooth_update_batch(long long n, int batch, double* z, const double* omegas,
+                            const double* const* c, const double* r, const double* az,
+                            void* stream) {
+  if (batch == 0) return WMG_OK;
+  REQ(z && omegas && c && r);
+  if (batch < 0) return fail(WMG_EINVAL, "negative batch");
+  for (int i = 0; i < batch; ++i)
+    if (!c[i]) return fail(WMG_EINVAL, "NULL smoother scaling");
+  return cuda_rc(wmg::ew_smooth_update_batch(n, batch, z, omegas, c, r, az, STREAM(stream)));
 }
 
 static int check_path(int n, int depth, int batch, const int* bands) {

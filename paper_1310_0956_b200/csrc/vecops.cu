@@ -388,6 +388,87 @@ __global__ void haar_prolong_kernel(int side, const double* __restrict__ coarse,
 }
 
 
+// Batched forms for the sibling batches of the hybrid cycle (one launch per
+// batch instead of one per node; every element computed exactly as by the
+// single-item kernels above).  blockIdx.y = batch item.
+__global__ void haar_restrict_batch_kernel(int side, const double* __restrict__ fine,
+                                           int band_mask, double* __restrict__ out) {
+  const int item = blockIdx.y;
+  const int hs = side / 2;
+  const long long nc = (long long)hs * hs;
+  const int nb = __popc(band_mask & 15);
+  fine += (long long)item * side * side;
+  out += (long long)item * nb * nc;
+  GRID_LOOP(q, nc) {
+    const int i = (int)(q / hs), k = (int)(q % hs);
+    const long long f0 = (long long)(2 * i) * side + 2 * k;
+    const double x00 = fine[f0], x01 = fine[f0 + 1];
+    const double x10 = fine[f0 + side], x11 = fine[f0 + side + 1];
+    int slot = 0;
+    for (int b = 0; b < 4; ++b) {
+      if (!((band_mask >> b) & 1)) continue;
+      double s00, s01, s10, s11;
+      band_signs(b, s00, s01, s10, s11);
+      double acc = 0.0;
+      acc = dadd(acc, dmul(s00, x00));
+      acc = dadd(acc, dmul(s01, x01));
+      acc = dadd(acc, dmul(s10, x10));
+      acc = dadd(acc, dmul(s11, x11));
+      out[(long long)slot * nc + q] = acc;
+      ++slot;
+    }
+  }
+}
+
+// fine_b = (accumulate ? fine_b : first product) + R_{band 1}^T c_b1 + ... in band
+// order, one dadd per band exactly as successive haar_prolong_kernel calls
+struct BandList {
+  int n;
+  int code[4];
+};
+__global__ void haar_prolong_batch_kernel(int side, BandList bl, const double* __restrict__ coarse,
+                                          double* __restrict__ fine, int accumulate) {
+  const int item = blockIdx.y;
+  const long long nf = (long long)side * side;
+  const int hs = side / 2;
+  const long long nc = (long long)hs * hs;
+  coarse += (long long)item * bl.n * nc;
+  fine += (long long)item * nf;
+  GRID_LOOP(f, nf) {
+    const int r = (int)(f / side), col = (int)(f % side);
+    const long long q = (long long)(r >> 1) * hs + (col >> 1);
+    const int sl = ((r & 1) << 1) | (col & 1);
+    double x = 0.0;
+    for (int i = 0; i < bl.n; ++i) {
+      double s[4];
+      band_signs(bl.code[i], s[0], s[1], s[2], s[3]);
+      const double v = dmul(s[sl], coarse[(long long)i * nc + q]);
+      x = (i == 0 && !accumulate) ? v : dadd(i == 0 ? fine[f] : x, v);
+    }
+    fine[f] = x;
+  }
+}
+
+// z_b += omega_b * (c_b .* (r_b - az_b)) for a batch of node smoothers
+constexpr int kSmoothBatch = 64;
+struct SmoothArgs {
+  double omega[kSmoothBatch];
+  const double* c[kSmoothBatch];
+};
+__global__ void smooth_update_batch_kernel(long long n, double* z, SmoothArgs A, const double* r,
+                                           const double* az) {
+  const int item = blockIdx.y;
+  const double omega = A.omega[item];
+  const double* __restrict__ c = A.c[item];
+  z += item * n;
+  r += item * n;
+  if (az) az += item * n;
+  GRID_LOOP(i, n) {
+    const double res = az ? dsub(r[i], az[i]) : r[i];
+    z[i] = dadd(z[i], dmul(omega, dmul(c[i], res)));
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Batched dense float64 GEMV for the WMG coarse solves: y_b = A_b x_b with the
 // stored SPD inverse A_b (p x p, row-major).  HBM-bound: every element of A is
@@ -675,6 +756,49 @@ cudaError_t haar_prolong(int side, const double* coarse, int band, double* fine,
   vec::haar_prolong_kernel<<<grid_for(nf, 256), 256, 0, st>>>(side, coarse, band, fine,
                                                               accumulate);
   return cudaGetLastError();
+}
+
+cudaError_t haar_restrict_batch(int side, int batch, const double* fine, int band_mask,
+                                double* out, cudaStream_t st) {
+  const long long nc = (long long)(side / 2) * (side / 2);
+  if (nc <= 0 || batch <= 0) return cudaSuccess;
+  dim3 grid(grid_for(nc, 256), batch);
+  vec::haar_restrict_batch_kernel<<<grid, 256, 0, st>>>(side, fine, band_mask, out);
+  return cudaGetLastError();
+}
+
+cudaError_t haar_prolong_batch(int side, int batch, int nbands, const int* bands,
+                               const double* coarse, double* fine, int accumulate,
+                               cudaStream_t st) {
+  const long long nf = (long long)side * side;
+  if (nf <= 0 || batch <= 0 || nbands <= 0) return cudaSuccess;
+  vec::BandList bl;
+  bl.n = nbands;
+  for (int i = 0; i < 4; ++i) bl.code[i] = i < nbands ? (bands[i] & 3) : 0;
+  dim3 grid(grid_for(nf, 256), batch);
+  vec::haar_prolong_batch_kernel<<<grid, 256, 0, st>>>(side, bl, coarse, fine, accumulate);
+  return cudaGetLastError();
+}
+
+cudaError_t ew_smooth_update_batch(long long n, int batch, double* z, const double* omegas,
+                                   const double* const* cs, const double* r, const double* az,
+                                   cudaStream_t st) {
+  if (n <= 0 || batch <= 0) return cudaSuccess;
+  for (int b0 = 0; b0 < batch; b0 += vec::kSmoothBatch) {
+    const int nb = batch - b0 < vec::kSmoothBatch ? batch - b0 : vec::kSmoothBatch;
+    vec::SmoothArgs A;
+    for (int i = 0; i < nb; ++i) {
+      A.omega[i] = omegas[b0 + i];
+      A.c[i] = cs[b0 + i];
+    }
+    dim3 grid(grid_for(n, 256), nb);
+    vec::smooth_update_batch_kernel<<<grid, 256, 0, st>>>(n, z + (long long)b0 * n, A,
+                                                          r + (long long)b0 * n,
+                                                          az ? az + (long long)b0 * n : nullptr);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 }  // namespace wmg

@@ -110,6 +110,29 @@ def prolong(side: int, coarse, band: str, fine, accumulate: bool):
     return fine
 
 
+def restrict_batch(side: int, fine, bands, out):
+    """out[b] = R_band fine[b] for each band, a batch of contiguous items in one
+    launch (bit-identical to ``restrict`` per item); out: (B, len(bands), nc)."""
+    mask = 0
+    for b in bands:
+        mask |= 1 << BAND_CODE[b]
+    if [b for b in BAND_IDS if (mask >> BAND_CODE[b]) & 1] != list(bands):
+        raise ValueError("bands must be given in LL, LH, HL, HH order")
+    N.call("wmg_haar_restrict_batch", side, fine.shape[0], D.ptr(fine), mask, D.ptr(out),
+           D.stream_handle())
+    return out
+
+
+def prolong_batch(side: int, coarse, bands, fine, accumulate: bool):
+    """fine[b] (+)= R_{bands[0]}^T coarse[b, 0] + ... in band order, one launch
+    for the batch (bit-identical to successive ``prolong`` calls per item);
+    coarse: (B, len(bands), (side/2)^2), fine: (B, side^2)."""
+    codes = (N.ctypes.c_int * len(bands))(*[BAND_CODE[b] for b in bands])
+    N.call("wmg_haar_prolong_batch", side, fine.shape[0], len(bands), codes, D.ptr(coarse),
+           D.ptr(fine), int(bool(accumulate)), D.stream_handle())
+    return fine
+
+
 # Node applications prolong / restrict along the whole band path in one launch
 # (wmg_haar_prolong_path / wmg_haar_restrict_path, bit-identical to the
 # level-by-level kernels); False: level by level (testing).
@@ -632,16 +655,17 @@ def _node_solve_batch_(nodes, R):
                         for b, nd in enumerate(nodes)])
     if h.nu_pre == 0 and h.nu_post == 0:
         return _wtg_batch_(nodes, R)
+    R = R.contiguous()
     Z = t.zeros_like(R)
     AZ = t.empty_like(R)
     RES = t.empty_like(R)
+    omegas = [nd.smooth_omega for nd in nodes]
+    scalings = [nd.smooth_c for nd in nodes]
 
     def sweep(z_is_zero):
         if not z_is_zero:
             _apply_system_batch_(nodes, Z, AZ)
-        for b, nd in enumerate(nodes):
-            D.smooth_update(Z[b], nd.smooth_omega, nd.smooth_c, R[b],
-                            None if z_is_zero else AZ[b])
+        D.smooth_update_batch(Z, omegas, scalings, R, None if z_is_zero else AZ)
 
     zero = True
     for _ in range(h.nu_pre):
@@ -665,25 +689,21 @@ def _wtg_batch_(nodes, R):
     B = len(nodes)
     side = nodes[0].side
     nc = (side // 2) ** 2
+    R = R.contiguous()
     RLL = t.empty((B, nc), dtype=R.dtype, device=R.device)
-    for b in range(B):
-        restrict(side, R[b], ("LL",), out=RLL[b].view(1, -1))
-    ZLL = _node_solve_batch_([nd.children["LL"] for nd in nodes], RLL)
+    restrict_batch(side, R, ("LL",), RLL)
+    ZLL = _node_solve_batch_([nd.children["LL"] for nd in nodes], RLL).contiguous()
     E = t.empty_like(R)
-    for b in range(B):
-        prolong(side, ZLL[b], "LL", E[b], accumulate=False)
+    prolong_batch(side, ZLL, ("LL",), E, accumulate=False)
     AE = t.empty_like(R)
     _apply_system_batch_(nodes, E, AE)
     RW = t.empty_like(R)
     D.axpy(RW.view(-1), R.view(-1), 1.0, -1, AE.view(-1))
     RB = t.empty((B, 3, nc), dtype=R.dtype, device=R.device)
-    for b in range(B):
-        restrict(side, RW[b], ("LH", "HL", "HH"), out=RB[b])
+    restrict_batch(side, RW, ("LH", "HL", "HH"), RB)
     kids = [nd.children[band] for nd in nodes for band in ("LH", "HL", "HH")]
-    ZK = _node_solve_batch_(kids, RB.view(3 * B, nc))
-    for b in range(B):
-        for i, band in enumerate(("LH", "HL", "HH")):
-            prolong(side, ZK[3 * b + i], band, E[b], accumulate=True)
+    ZK = _node_solve_batch_(kids, RB.view(3 * B, nc)).contiguous()
+    prolong_batch(side, ZK, ("LH", "HL", "HH"), E, accumulate=True)
     return E
 
 
