@@ -129,6 +129,16 @@ int wmg_backward(const wmg_geometry *g, int mode, int precision, int dtype_in, i
  * order on one stream.  Same reference function as wmg_backward
  * (geometry.py:209-215). */
 int wmg_backward_bands(const wmg_geometry *g, int precision, int *bands);
+/* W R_path^T for a batch of WMG node vectors (the prolongation of the node
+ * systems, multilevel.py:109-113, fused into the float64 fast forward): item b
+ * = coarse + b (n >> depth)^2, bands[b depth + lv] = its band at level lv (lv 0
+ * the finest; 0 LL, 1 LH, 2 HL, 3 HH), sinograms n_angles * n_detectors apart;
+ * workspace = batch * wmg_forward_workspace(FLOAT64, FLOAT64) bytes.  Bit-
+ * identical to wmg_haar_prolong_path + wmg_forward_batch (FAST, float64);
+ * available when wmg_forward_path_supported (small grids) reports 1. */
+int wmg_forward_path_supported(const wmg_geometry *g, int precision, int *ok);
+int wmg_forward_path(const wmg_geometry *g, const double *coarse, int depth, int batch,
+                     const int *bands, double *y, void *workspace, void *stream);
 int wmg_backward_band(const wmg_geometry *g, int precision, int dtype_in, int dtype_out,
                       const void *y, void *x, int band0, int band1, void *stream);
 

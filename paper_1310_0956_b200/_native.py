@@ -76,6 +76,8 @@ _SIGS = {
     "wmg_haar_restrict": (_i, [_i, _dp, _i, _dp, _vp]),
     "wmg_haar_prolong": (_i, [_i, _dp, _i, _dp, _i, _vp]),
     "wmg_haar_restrict_batch": (_i, [_i, _i, _dp, _i, _dp, _vp]),
+    "wmg_forward_path_supported": (_i, [_vp, _i, ctypes.POINTER(_i)]),
+    "wmg_forward_path": (_i, [_vp, _dp, _i, _i, ctypes.POINTER(_i), _dp, _dp, _vp]),
     "wmg_haar_prolong_batch": (_i, [_i, _i, _i, ctypes.POINTER(_i), _dp, _dp, _i, _vp]),
     "wmg_smooth_update_batch": (_i, [_ll, _i, _dp, ctypes.POINTER(_d), ctypes.POINTER(_vp), _dp,
                                      _dp, _vp]),

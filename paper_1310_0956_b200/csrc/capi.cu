@@ -81,6 +81,9 @@ cudaError_t packed_symv(int, int, const double*, long long, const double*, long 
                         long long, double*, cudaStream_t);
 bool tma_window_fits(const AngleParams*, int, int, int);
 cudaError_t h2d_staged(void*, const void*, size_t, void*, int, cudaStream_t);
+bool fast_forward_path_supported(const GeomDev&, int, const GeomDev*);
+cudaError_t fast_forward_path(const GeomDev&, int, int, const int*, const double*, void*, double*,
+                              cudaStream_t, const GeomDev*);
 cudaError_t haar_restrict_batch(int, int, const double*, int, double*, cudaStream_t);
 cudaError_t haar_prolong_batch(int, int, int, const int*, const double*, double*, int,
                                cudaStream_t);
@@ -472,6 +475,32 @@ int wmg_backward_band(const wmg_geometry* g, int precision, int dtype_in, int dt
   if (band0 < 0 || band1 > nb || band0 > band1) return fail(WMG_EINVAL, "band range");
   return cuda_rc(wmg::fast_backward_band(g->dev, precision, dtype_in, dtype_out, y, x, band0,
                                          band1, STREAM(stream), &g->axis));
+}
+
+int wmg_forward_path_supported(const wmg_geometry* g, int precision, int* ok) {
+  if (!g || !ok) return fail(WMG_EINVAL, "NULL argument");
+  *ok = (!g->dev.joseph &&
+         wmg::fast_forward_path_supported(g->dev, precision, g->dev.sym ? &g->axis : nullptr))
+            ? 1
+            : 0;
+  return WMG_OK;
+}
+
+int wmg_forward_path(const wmg_geometry* g, const double* coarse, int depth, int batch,
+                     const int* bands, double* y, void* workspace, void* stream) {
+  if (batch == 0 && g) return WMG_OK;
+  if (!g || !coarse || !bands || !y || !workspace) return fail(WMG_EINVAL, "NULL argument");
+  if (batch < 0) return fail(WMG_EINVAL, "negative batch");
+  if (depth < 1 || depth > 7) return fail(WMG_EINVAL, "depth must be in [1, 7]");
+  for (long long i = 0; i < (long long)batch * depth; ++i)
+    if (bands[i] < 0 || bands[i] > 3) return fail(WMG_EINVAL, "bad band");
+  if ((g->dev.n >> depth) << depth != g->dev.n)
+    return fail(WMG_EINVAL, "2^depth must divide n");
+  int ok = 0;
+  wmg_forward_path_supported(g, 1, &ok);
+  if (!ok) return fail(WMG_EINVAL, "no fused path forward for this geometry");
+  return cuda_rc(wmg::fast_forward_path(g->dev, depth, batch, bands, coarse, workspace, y,
+                                        STREAM(stream), g->dev.sym ? &g->axis : nullptr));
 }
 
 int wmg_forward_batch(const wmg_geometry* g, int mode, int precision, int dtype_in,

@@ -87,4 +87,43 @@ __device__ __forceinline__ void tri_unrank(int lin, int& I, int& J) {
   J = lin - i * (i + 1) / 2;
 }
 
+// Haar band coefficient signs of the 2 x 2 block (2i,2k), (2i,2k+1), (2i+1,2k),
+// (2i+1,2k+1) times h = fl(fl(1/sqrt 2)^2) (multilevel.py:36-53): band 0 LL,
+// 1 LH (wavelet along rows), 2 HL (along columns), 3 HH
+__device__ __forceinline__ void haar_band_signs(int band, double& s00, double& s01, double& s10,
+                                                double& s11) {
+  const double h = 0.4999999999999999;
+  const bool wy = (band == 1 || band == 3);
+  const bool wx = (band == 2 || band == 3);
+  s00 = h;
+  s01 = wx ? -h : h;
+  s10 = wy ? -h : h;
+  s11 = (wx != wy) ? -h : h;
+}
+
+// band paths of a batch of WMG nodes: depth and, per item, the bands of levels
+// 0..depth-1 in 2-bit fields (level 0 = the finest), passed by value so the
+// launches stay graph-capturable
+constexpr int kPathBatch = 128;
+struct BandPaths {
+  int depth;
+  unsigned short code[kPathBatch];
+};
+
+// fine pixel (r, c) of R_path^T coarse, coarsest level first: the same chain
+// of sign * h products as the level-by-level prolongations (bit-identical)
+__device__ __forceinline__ double haar_path_value(const BandPaths& bp, int item,
+                                                  const double* __restrict__ coarse, int sc,
+                                                  int r, int c) {
+  const int k = bp.depth;
+  const unsigned code = bp.code[item];
+  double v = coarse[(long long)(r >> k) * sc + (c >> k)];
+  for (int lv = k - 1; lv >= 0; --lv) {
+    double s[4];
+    haar_band_signs((code >> (2 * lv)) & 3, s[0], s[1], s[2], s[3]);
+    v = __dmul_rn(s[(((r >> lv) & 1) << 1) | ((c >> lv) & 1)], v);
+  }
+  return v;
+}
+
 }  // namespace wmg

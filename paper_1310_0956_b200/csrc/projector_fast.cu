@@ -1512,14 +1512,17 @@ __global__ void __launch_bounds__((kAG == 1 && !kMix) ? 128 : 32 * kAG * kSeg) f
 // ===========================================================================
 // float64 fast kernels (same algorithms, float64 arithmetic; <= 1e-12)
 // ===========================================================================
-template <typename T>
-__global__ void pad_transpose64_kernel(const T* __restrict__ in, double* __restrict__ P,
-                                       double* __restrict__ PT, int n) {
+template <typename T, bool kPath>
+__device__ __forceinline__ void pad_transpose64_body(const T* __restrict__ in,
+                                                     double* __restrict__ P,
+                                                     double* __restrict__ PT, int n,
+                                                     const BandPaths* bp) {
   __shared__ double tile[32][33];
   const int pitch = n + 2 * kPadMargin;
-  {   // batch: images n*n apart, plane pairs 2 * n * pitch apart
+  const int sc = kPath ? (n >> bp->depth) : 0;
+  {   // batch: images n*n (coarse items sc*sc) apart, plane pairs 2 * n * pitch apart
     const long long z = blockIdx.z;
-    in += z * n * n;
+    in += kPath ? z * sc * sc : z * n * n;
     P += z * 2LL * n * pitch;
     PT += z * 2LL * n * pitch;
   }
@@ -1528,7 +1531,10 @@ __global__ void pad_transpose64_kernel(const T* __restrict__ in, double* __restr
     const int r = by + i, c = bx + threadIdx.x;
     double v = 0.0;
     if (r < n && c < n) {
-      v = (double)in[(long long)r * n + c];
+      if constexpr (kPath)
+        v = haar_path_value(*bp, (int)blockIdx.z, (const double*)in, sc, r, c);
+      else
+        v = (double)in[(long long)r * n + c];
       P[(long long)r * pitch + kPadMargin + c] = v;
     }
     tile[i][threadIdx.x] = v;
@@ -1556,6 +1562,20 @@ __global__ void pad_transpose64_kernel(const T* __restrict__ in, double* __restr
       }
     }
   }
+}
+
+template <typename T>
+__global__ void pad_transpose64_kernel(const T* __restrict__ in, double* __restrict__ P,
+                                       double* __restrict__ PT, int n) {
+  pad_transpose64_body<T, false>(in, P, PT, n, nullptr);
+}
+
+// WMG node applications: the image is R_path^T coarse (the prolongation along
+// each item's band path, wmg_forward_path), evaluated while padding -- the
+// same values haar_prolong_path_kernel writes, without the intermediate image
+__global__ void prolong_pad64_kernel(BandPaths bp, const double* __restrict__ coarse,
+                                     double* __restrict__ P, double* __restrict__ PT, int n) {
+  pad_transpose64_body<double, true>(coarse, P, PT, n, &bp);
 }
 
 // Small-grid float64 forward on the padded planes: one ray per lane, kSplit
@@ -2481,6 +2501,47 @@ cudaError_t fast_forward_batch(const GeomDev& G, int precision, int tin, int tou
   for (int b = 0; b < batch; ++b) {
     cudaError_t e = fast_forward(G, precision, tin, tout, (const char*)x + b * N * si,
                                  (char*)ws + b * ws_item, (char*)y + b * M * so, st, Gx);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+// W R_path^T for a batch of WMG node vectors (float64 fast, small grids): the
+// prolongation along each item's band path is evaluated inside the padding
+// kernel, then the same batched fwd_split64 launch as fast_forward_batch --
+// bit-identical to haar_prolong_path followed by fast_forward_batch.
+bool fast_forward_path_supported(const GeomDev& G, int precision, const GeomDev* Gx) {
+  return precision == 1 && use_split(G) && !(use_sym_fwd(G, 1) && Gx) && G.m > 0 && G.d > 0;
+}
+
+cudaError_t fast_forward_path(const GeomDev& G, int depth, int batch, const int* bands,
+                              const double* coarse, void* ws, double* y, cudaStream_t st,
+                              const GeomDev* Gx) {
+  if (!fast_forward_path_supported(G, 1, Gx) || depth < 1 || depth > 7 || (G.n >> depth) < 1)
+    return cudaErrorInvalidValue;
+  const long long M = (long long)G.m * G.d;
+  const long long plane = (long long)G.n * (G.n + 2 * kPadMargin);
+  const int sc = G.n >> depth;
+  for (int b0 = 0; b0 < batch; b0 += kPathBatch) {
+    const int nb = batch - b0 < kPathBatch ? batch - b0 : kPathBatch;
+    BandPaths bp;
+    bp.depth = depth;
+    for (int i = 0; i < nb; ++i) {
+      unsigned code = 0;
+      for (int lv = 0; lv < depth; ++lv)
+        code |= (unsigned)(bands[(b0 + i) * depth + lv] & 3) << (2 * lv);
+      bp.code[i] = (unsigned short)code;
+    }
+    double* P = (double*)ws + (long long)b0 * 2 * plane;
+    double* PT = P + plane;
+    dim3 tg((G.n + 31) / 32, (G.n + 31) / 32, nb), tb(32, 8);
+    fast::prolong_pad64_kernel<<<tg, tb, 0, st>>>(bp, coarse + (long long)b0 * sc * sc, P, PT,
+                                                  G.n);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    dim3 sg((G.d + 7) / 8, (G.m + 3) / 4, nb), sb(32, fast::kSplitF);
+    fast::fwd_split64_kernel<double, 4><<<sg, sb, 0, st>>>(G, P, PT, y + (long long)b0 * M, M);
+    e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;

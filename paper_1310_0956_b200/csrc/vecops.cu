@@ -262,13 +262,7 @@ __global__ void cast_f32_f64(long long n, double* out, const float* in) {
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ void band_signs(int band, double& s00, double& s01, double& s10,
                                            double& s11) {
-  const double h = 0.4999999999999999;   // fl(fl(1/sqrt(2))^2), multilevel.py:43,53
-  const bool wy = (band == 1 || band == 3);   // wavelet along rows (y)
-  const bool wx = (band == 2 || band == 3);   // wavelet along columns (x)
-  s00 = h;
-  s01 = wx ? -h : h;
-  s10 = wy ? -h : h;
-  s11 = (wx != wy) ? -h : h;
+  haar_band_signs(band, s00, s01, s10, s11);
 }
 
 // coarse[b][(i,k)] = R_b fine, for the bands in mask (bit b); out laid out as
@@ -298,15 +292,7 @@ __global__ void haar_restrict_kernel(int side, const double* __restrict__ fine, 
   }
 }
 
-// Band paths of a batch of WMG nodes (item i: bands of levels 0..depth-1 in
-// 2-bit fields, level 0 = the finest restriction) -- kernel parameters, so the
-// launches stay graph-capturable.
-constexpr int kPathBatch = 128;
-struct BandPaths {
-  int depth;
-  unsigned short code[kPathBatch];
-};
-
+// Band paths of a batch of WMG nodes: wmg::BandPaths (common.cuh).
 // fine_i (n x n) = R_{b0}^T ... R_{b(k-1)}^T coarse_i, coarsest level first:
 // the level-by-level prolongations (haar_prolong_kernel) fused into one pass,
 // the same sequence of sign * h products per fine pixel (bit-identical).
@@ -314,20 +300,13 @@ struct BandPaths {
 __global__ void haar_prolong_path_kernel(int n, BandPaths bp, const double* __restrict__ coarse,
                                          double* __restrict__ fine) {
   const int k = bp.depth, item = blockIdx.y;
-  const unsigned code = bp.code[item];
   const int sc = n >> k;
   const long long nf = (long long)n * n;
   const double* cin = coarse + (long long)item * sc * sc;
   double* fout = fine + (long long)item * nf;
   GRID_LOOP(f, nf) {
     const int r = (int)(f / n), c = (int)(f % n);
-    double v = cin[(long long)(r >> k) * sc + (c >> k)];
-    for (int lv = k - 1; lv >= 0; --lv) {
-      double s[4];
-      band_signs((code >> (2 * lv)) & 3, s[0], s[1], s[2], s[3]);
-      v = dmul(s[(((r >> lv) & 1) << 1) | ((c >> lv) & 1)], v);
-    }
-    fout[f] = v;
+    fout[f] = haar_path_value(bp, item, cin, sc, r, c);
   }
 }
 
@@ -708,9 +687,9 @@ cudaError_t haar_restrict(int side, const double* fine, int band_mask, double* o
 cudaError_t haar_prolong_path(int n, int depth, int batch, const int* bands,
                               const double* coarse, double* fine, cudaStream_t st) {
   const int sc = n >> depth;
-  for (int b0 = 0; b0 < batch; b0 += vec::kPathBatch) {
-    const int nb = batch - b0 < vec::kPathBatch ? batch - b0 : vec::kPathBatch;
-    vec::BandPaths bp;
+  for (int b0 = 0; b0 < batch; b0 += kPathBatch) {
+    const int nb = batch - b0 < kPathBatch ? batch - b0 : kPathBatch;
+    BandPaths bp;
     bp.depth = depth;
     for (int i = 0; i < nb; ++i) {
       unsigned code = 0;
@@ -730,9 +709,9 @@ cudaError_t haar_prolong_path(int n, int depth, int batch, const int* bands,
 cudaError_t haar_restrict_path(int n, int depth, int batch, const int* bands, const double* fine,
                                double* coarse, cudaStream_t st) {
   const int sc = n >> depth;
-  for (int b0 = 0; b0 < batch; b0 += vec::kPathBatch) {
-    const int nb = batch - b0 < vec::kPathBatch ? batch - b0 : vec::kPathBatch;
-    vec::BandPaths bp;
+  for (int b0 = 0; b0 < batch; b0 += kPathBatch) {
+    const int nb = batch - b0 < kPathBatch ? batch - b0 : kPathBatch;
+    BandPaths bp;
     bp.depth = depth;
     for (int i = 0; i < nb; ++i) {
       unsigned code = 0;

@@ -205,6 +205,7 @@ class LineProjector:
             code = int(bool(enable))
         st = N.ctypes.c_int()
         N.call("wmg_geometry_symmetry", self._h, code, N.ctypes.byref(st))
+        self._ws.pop("path_ok", None)         # the fused path forward follows the dispatch
         return bool(st.value)
 
     def tocsr(self):
@@ -276,6 +277,35 @@ class LineProjector:
                 self._ws[key] = ws
         N.call("wmg_forward_batch", self._h, self._mode_code, self.precision, tin, tout,
                D.ptr(X), D.ptr(OUT), B, D.ptr(ws), D.stream_handle())
+        return OUT
+
+    @property
+    def supports_forward_path(self) -> bool:
+        """Whether forward_path_ (prolongation fused into the forward) is available."""
+        v = self._ws.get("path_ok")
+        if v is None:
+            ok = N.ctypes.c_int()
+            N.call("wmg_forward_path_supported", self._h, self.precision, N.ctypes.byref(ok))
+            v = self._ws["path_ok"] = bool(ok.value) and self._mode_code == N.MODE_FAST
+        return v
+
+    def forward_path_(self, C, paths, OUT):
+        """OUT[b] = W R_{paths[b]}^T C[b] (float64 fast mode, small grids): the
+        WMG node prolongation (multilevel.py:109-113) evaluated inside the forward's
+        padding pass, bit-identical to prolong_path + forward_batch_."""
+        t = D.torch()
+        B = C.shape[0]
+        depth = len(paths[0])
+        ws = self._ws.get(("batch", N.F64, B))
+        if ws is None:
+            nbytes = N.ctypes.c_size_t()
+            N.call("wmg_forward_workspace", self._h, self.precision, N.F64, N.ctypes.byref(nbytes))
+            ws = t.zeros((B * nbytes.value + 7) // 8, dtype=t.float64, device=self.device)
+            self._ws[("batch", N.F64, B)] = ws
+        from .multilevel import BAND_CODE
+        codes = (N.ctypes.c_int * (B * depth))(*[BAND_CODE[b] for p in paths for b in p])
+        N.call("wmg_forward_path", self._h, D.ptr(C), depth, B, codes, D.ptr(OUT), D.ptr(ws),
+               D.stream_handle())
         return OUT
 
     def backward_batch_(self, Y, OUT, accumulate=False):

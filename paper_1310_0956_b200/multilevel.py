@@ -196,17 +196,21 @@ class WmgNode:
         k = len(self.bands)
         t = D.torch()
         # prolong to the fine grid (coarsest factor first, as R_path^T does)
-        cur = v
-        if k and FUSED_PATHS:
-            cur = prolong_path(h.n, [self.bands], v, h.buf(("pf", 0), h.n * h.n))
-        else:
-            for lv in range(k - 1, -1, -1):
-                side_f = h.n >> lv
-                buf = h.buf(("pf", lv), side_f * side_f)
-                prolong(side_f, cur, self.bands[lv], buf, accumulate=False)
-                cur = buf
         sino = h.buf(("sino",), w.shape[0])
-        w.forward_(cur, sino)
+        if k and FUSED_PATHS and getattr(w, "supports_forward_path", False):
+            # prolongation evaluated inside the forward's padding pass
+            w.forward_path_(v.view(1, -1), [self.bands], sino.view(1, -1))
+        else:
+            cur = v
+            if k and FUSED_PATHS:
+                cur = prolong_path(h.n, [self.bands], v, h.buf(("pf", 0), h.n * h.n))
+            else:
+                for lv in range(k - 1, -1, -1):
+                    side_f = h.n >> lv
+                    buf = h.buf(("pf", lv), side_f * side_f)
+                    prolong(side_f, cur, self.bands[lv], buf, accumulate=False)
+                    cur = buf
+            w.forward_(cur, sino)
         img = h.buf(("img",), w.shape[1]) if k else out
         w.backward_(sino, img)
         cur = img
@@ -596,20 +600,24 @@ def _apply_system_batch_(nodes, V, OUT):
     k = len(nodes[0].bands)
     n2 = h.n * h.n
     M = w.shape[0]
-    F = h.buf(("bpf", B), B * n2).view(B, n2)
     fused = FUSED_PATHS and k > 0 and V.is_contiguous() and OUT.is_contiguous()
-    if fused:
-        prolong_path(h.n, [nd.bands for nd in nodes], V, F)
-    else:
-        for b, nd in enumerate(nodes):
-            cur = V[b]
-            for lv in range(k - 1, -1, -1):
-                side_f = h.n >> lv
-                dst = F[b] if lv == 0 else h.buf(("bpfl", lv, b), side_f * side_f)
-                prolong(side_f, cur, nd.bands[lv], dst, accumulate=False)
-                cur = dst
     sino = h.buf(("bsino", B), B * M).view(B, M)
-    w.forward_batch_(F, sino)
+    if fused and getattr(w, "supports_forward_path", False):
+        # prolongation evaluated inside the forward's padding pass
+        w.forward_path_(V, [nd.bands for nd in nodes], sino)
+    else:
+        F = h.buf(("bpf", B), B * n2).view(B, n2)
+        if fused:
+            prolong_path(h.n, [nd.bands for nd in nodes], V, F)
+        else:
+            for b, nd in enumerate(nodes):
+                cur = V[b]
+                for lv in range(k - 1, -1, -1):
+                    side_f = h.n >> lv
+                    dst = F[b] if lv == 0 else h.buf(("bpfl", lv, b), side_f * side_f)
+                    prolong(side_f, cur, nd.bands[lv], dst, accumulate=False)
+                    cur = dst
+        w.forward_batch_(F, sino)
     img = h.buf(("bimg", B), B * n2).view(B, n2)
     w.backward_batch_(sino, img)
     if fused:

@@ -335,3 +335,27 @@ def test_fused_paths_vcycle_bitwise(gpu, levels):
     finally:
         ML.FUSED_PATHS = True
     assert torch.equal(got, ref)
+
+
+def test_fused_path_forward_bitwise(gpu):
+    """wmg_forward_path (the node prolongation evaluated inside the float64 fast
+    forward's padding pass) == haar_prolong_path + forward_batch_, bit for bit,
+    for depths 1..3, every band and a batch that spans two path tables."""
+    torch = gpu
+    from paper_1310_0956_b200 import build_geometry, build_projector
+    from paper_1310_0956_b200.multilevel import BAND_IDS, prolong_path
+    n, d, m = 256, 363, 180
+    w = build_projector(build_geometry(n, d, m), precision="float64", mode="fast")
+    assert w.supports_forward_path
+    rng = np.random.default_rng(7)
+    for depth, B in ((1, 3), (2, 5), (3, 130)):
+        paths = [tuple(BAND_IDS[(i * 7 + lv * 3) % 4] for lv in range(depth)) for i in range(B)]
+        nc = (n >> depth) ** 2
+        C = torch.from_numpy(rng.standard_normal((B, nc))).cuda()
+        got = torch.empty(B, w.shape[0], dtype=torch.float64, device="cuda")
+        w.forward_path_(C, paths, got)
+        F = torch.empty(B, n * n, dtype=torch.float64, device="cuda")
+        prolong_path(n, paths, C, F)
+        ref = torch.empty_like(got)
+        w.forward_batch_(F, ref)
+        assert torch.equal(got, ref), (depth, B)
