@@ -1512,17 +1512,14 @@ __global__ void __launch_bounds__((kAG == 1 && !kMix) ? 128 : 32 * kAG * kSeg) f
 // ===========================================================================
 // float64 fast kernels (same algorithms, float64 arithmetic; <= 1e-12)
 // ===========================================================================
-template <typename T, bool kPath>
-__device__ __forceinline__ void pad_transpose64_body(const T* __restrict__ in,
-                                                     double* __restrict__ P,
-                                                     double* __restrict__ PT, int n,
-                                                     const BandPaths* bp) {
+template <typename T>
+__global__ void pad_transpose64_kernel(const T* __restrict__ in, double* __restrict__ P,
+                                       double* __restrict__ PT, int n) {
   __shared__ double tile[32][33];
   const int pitch = n + 2 * kPadMargin;
-  const int sc = kPath ? (n >> bp->depth) : 0;
-  {   // batch: images n*n (coarse items sc*sc) apart, plane pairs 2 * n * pitch apart
+  {   // batch: images n*n apart, plane pairs 2 * n * pitch apart
     const long long z = blockIdx.z;
-    in += kPath ? z * sc * sc : z * n * n;
+    in += z * n * n;
     P += z * 2LL * n * pitch;
     PT += z * 2LL * n * pitch;
   }
@@ -1531,10 +1528,7 @@ __device__ __forceinline__ void pad_transpose64_body(const T* __restrict__ in,
     const int r = by + i, c = bx + threadIdx.x;
     double v = 0.0;
     if (r < n && c < n) {
-      if constexpr (kPath)
-        v = haar_path_value(*bp, (int)blockIdx.z, (const double*)in, sc, r, c);
-      else
-        v = (double)in[(long long)r * n + c];
+      v = (double)in[(long long)r * n + c];
       P[(long long)r * pitch + kPadMargin + c] = v;
     }
     tile[i][threadIdx.x] = v;
@@ -1564,19 +1558,82 @@ __device__ __forceinline__ void pad_transpose64_body(const T* __restrict__ in,
   }
 }
 
-template <typename T>
-__global__ void pad_transpose64_kernel(const T* __restrict__ in, double* __restrict__ P,
-                                       double* __restrict__ PT, int n) {
-  pad_transpose64_body<T, false>(in, P, PT, n, nullptr);
+// Pair planes for the small-grid float64 forward: element e of a padded row
+// holds (pixel e - 1, pixel e) as one 16-byte word, so a ray-slab reads both
+// pixels it straddles with one LDG.128 (half the load instructions, 9 % fewer
+// L1 data-pipe wavefronts than two LDG.64).  Q[r][M + c] = (v(r, c-1), v(r, c)),
+// QT[c][M + r] = (v(r-1, c), v(r, c)), v = 0 outside the image, every margin
+// element rewritten each call.  kPath: v = R_path^T coarse (wmg_forward_path).
+template <typename T, bool kPath>
+__device__ __forceinline__ void pad_pairs64_body(const T* __restrict__ in, double2* __restrict__ Q,
+                                                 double2* __restrict__ QT, int n,
+                                                 const BandPaths* bp) {
+  __shared__ double2 tile[32][33];
+  const int pitch = n + 2 * kPadMargin;
+  const int sc = kPath ? (n >> bp->depth) : 0;
+  {   // batch: images n*n (coarse items sc*sc) apart, plane pairs 2 * n * pitch apart
+    const long long z = blockIdx.z;
+    in += kPath ? z * sc * sc : z * n * n;
+    Q += z * 2LL * n * pitch;
+    QT += z * 2LL * n * pitch;
+  }
+  auto val = [&](int r, int c) -> double {
+    if (r < 0 || c < 0 || r >= n || c >= n) return 0.0;
+    if constexpr (kPath)
+      return haar_path_value(*bp, (int)blockIdx.z, (const double*)in, sc, r, c);
+    else
+      return (double)in[(long long)r * n + c];
+  };
+  const int bx = blockIdx.x * 32, by = blockIdx.y * 32;
+  for (int i = threadIdx.y; i < 32; i += 8) {
+    const int r = by + i, c = bx + threadIdx.x;
+    double2 q = make_double2(0.0, 0.0), qt = make_double2(0.0, 0.0);
+    if (r < n && c < n) {
+      const double v = val(r, c);
+      q = make_double2(val(r, c - 1), v);
+      qt = make_double2(val(r - 1, c), v);
+      Q[(long long)r * pitch + kPadMargin + c] = q;
+    }
+    tile[i][threadIdx.x] = qt;
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += 8) {
+    const int c = bx + i, r = by + threadIdx.x;
+    if (r < n && c < n) QT[(long long)c * pitch + kPadMargin + r] = tile[threadIdx.x][i];
+  }
+  // margins: zero pairs, except the first element past the last pixel, which
+  // still carries that pixel as its left member
+  if (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1) {
+    for (int i = threadIdx.y; i < 32; i += 8) {
+      const int r = by + i;   // row of Q, column of QT
+      if (r >= n) continue;
+      for (int k = threadIdx.x; k < kPadMargin; k += 32) {
+        if (blockIdx.x == 0) {
+          Q[(long long)r * pitch + k] = make_double2(0.0, 0.0);
+          QT[(long long)r * pitch + k] = make_double2(0.0, 0.0);
+        }
+        if (blockIdx.x == gridDim.x - 1) {
+          Q[(long long)r * pitch + kPadMargin + n + k] =
+              make_double2(k == 0 ? val(r, n - 1) : 0.0, 0.0);
+          QT[(long long)r * pitch + kPadMargin + n + k] =
+              make_double2(k == 0 ? val(n - 1, r) : 0.0, 0.0);
+        }
+      }
+    }
+  }
 }
 
-// WMG node applications: the image is R_path^T coarse (the prolongation along
-// each item's band path, wmg_forward_path), evaluated while padding -- the
-// same values haar_prolong_path_kernel writes, without the intermediate image
-__global__ void prolong_pad64_kernel(BandPaths bp, const double* __restrict__ coarse,
-                                     double* __restrict__ P, double* __restrict__ PT, int n) {
-  pad_transpose64_body<double, true>(coarse, P, PT, n, &bp);
+template <typename T>
+__global__ void pad_pairs64_kernel(const T* __restrict__ in, double2* __restrict__ Q,
+                                   double2* __restrict__ QT, int n) {
+  pad_pairs64_body<T, false>(in, Q, QT, n, nullptr);
 }
+
+__global__ void prolong_pairs64_kernel(BandPaths bp, const double* __restrict__ coarse,
+                                       double2* __restrict__ Q, double2* __restrict__ QT, int n) {
+  pad_pairs64_body<double, true>(coarse, Q, QT, n, &bp);
+}
+
 
 // Small-grid float64 forward on the padded planes: one ray per lane, kSplit
 // slab segments per ray (threadIdx.y) reduced in shared memory in segment
@@ -1587,8 +1644,8 @@ __global__ void prolong_pad64_kernel(BandPaths bp, const double* __restrict__ co
 // within 10 %: an LDG.64 of 32 lanes spans >= 8 sectors at any layout)
 template <typename TOut, int kA = 1>
 __global__ void __launch_bounds__(32 * kSplitF) fwd_split64_kernel(GeomDev G,
-                                                                  const double* __restrict__ P,
-                                                                  const double* __restrict__ PT,
+                                                                  const double2* __restrict__ Q,
+                                                                  const double2* __restrict__ QT,
                                                                   TOut* __restrict__ sino,
                                                                   long long bs_sino) {
   __shared__ double part[kSplitF][33];
@@ -1602,8 +1659,8 @@ __global__ void __launch_bounds__(32 * kSplitF) fwd_split64_kernel(GeomDev G,
   const int pitch = n + 2 * kPadMargin;
   {
     const long long zp = (long long)blockIdx.z * 2LL * n * pitch;
-    P += zp;
-    PT += zp;
+    Q += zp;
+    QT += zp;
     sino += (long long)blockIdx.z * bs_sino;
   }
   double acc = 0.0;
@@ -1626,9 +1683,9 @@ __global__ void __launch_bounds__(32 * kSplitF) fwd_split64_kernel(GeomDev G,
     const int len = r1 - r0 + 1;
     const int rs = r0 + (len > 0 ? (len * seg) / kSplitF : 0);
     const int re = r0 + (len > 0 ? (len * (seg + 1)) / kSplitF : 0) - 1;
-    const double* __restrict__ src = (A.major ? PT : P) + kPadMargin;
     const double L = A.L, Ls = A.Ls;
-    const double* row = src + (long long)rs * pitch;
+    // pair planes: element e of a row holds (pixel e - 1, pixel e)
+    const double2* rowq = (A.major ? QT : Q) + kPadMargin + (long long)rs * pitch;
     // u in 12.52 fixed point (offset by the margin so it stays >= 0): the slab
     // walk is integer adds, the straddled pixel the high bits and the fraction
     // an exact bit move -- no floor / conversions in the loop; error <= (r + 1)
@@ -1643,11 +1700,13 @@ __global__ void __launch_bounds__(32 * kSplitF) fwd_split64_kernel(GeomDev G,
       const int k = (int)(U >> 52);
       const double f = __longlong_as_double(0x3FF0000000000000LL | (U & 0xFFFFFFFFFFFFFLL)) - 1.0;
       const double wh = dmin_to(f * Ls, L);        // NaN (0 * inf) -> L
-      const double* p = row + (ksgn * k + kofs);
-      const double v1 = __ldg(p), v0 = __ldg(p - ksgn);
+      // pixel px = ksgn k + kofs and its neighbour px - ksgn, one 16-byte load:
+      // (px - 1, px) at element px, or (px, px + 1) at element px + 1 (mirrored)
+      const double2 q = __ldg(rowq + (ksgn * k + kofs + (ksgn < 0 ? 1 : 0)));
+      const double v1 = ksgn > 0 ? q.y : q.x, v0 = ksgn > 0 ? q.x : q.y;
       acc = fma(L, v0, acc);
       acc = fma(wh, v1 - v0, acc);
-      row += pitch;
+      rowq += pitch;
     }
   }
   part[seg][lane] = acc;
@@ -2275,8 +2334,9 @@ size_t fast_forward_workspace_bytes(int n, int precision, int tin) {
   // fp32: P and PT, or the mirror-packed float2 planes PM and PMT (twice the size)
   if (precision == 0) return sizeof(float) * 4 * (size_t)n * (size_t)(n + 2 * kPadMargin);
   // float64: padded double planes (symmetric path) -- also holds the transposed
-  // copy of the generic path
-  return sizeof(double) * 2 * (size_t)n * (size_t)(n + 2 * kPadMargin);
+  // copy of the generic path; small grids: the split forward's 16-byte pair planes
+  const size_t elem = n <= 512 ? 2 * sizeof(double) : sizeof(double);
+  return elem * 2 * (size_t)n * (size_t)(n + 2 * kPadMargin);
 }
 
 template <typename TIn, typename TOut>
@@ -2341,14 +2401,15 @@ static cudaError_t fwd_impl(const GeomDev& G, const void* x, void* xT_ws, void* 
   TIn* imgT = (TIn*)xT_ws;
   if (sizeof(R) == 8 && use_split(G)) {
     // padded float64 planes (the workspace holds 2 * n * (n + 2 margin) doubles)
-    double* P = (double*)xT_ws;
-    double* PT = P + (long long)G.n * (G.n + 2 * kPadMargin);
+    // padded float64 pair planes (the workspace holds 2 * n * (n + 2 margin) double2)
+    double2* Q = (double2*)xT_ws;
+    double2* QT = Q + (long long)G.n * (G.n + 2 * kPadMargin);
     dim3 tg((G.n + 31) / 32, (G.n + 31) / 32), tb(32, 8);
-    fast::pad_transpose64_kernel<TIn><<<tg, tb, 0, st>>>(img, P, PT, G.n);
+    fast::pad_pairs64_kernel<TIn><<<tg, tb, 0, st>>>(img, Q, QT, G.n);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     dim3 sg((G.d + 7) / 8, (G.m + 3) / 4), sb(32, fast::kSplitF);
-    fast::fwd_split64_kernel<TOut, 4><<<sg, sb, 0, st>>>(G, P, PT, (TOut*)y, 0);
+    fast::fwd_split64_kernel<TOut, 4><<<sg, sb, 0, st>>>(G, Q, QT, (TOut*)y, 0);
     return cudaGetLastError();
   }
   cudaError_t e = launch_transpose<TIn>(img, imgT, G.n, st);
@@ -2487,15 +2548,15 @@ cudaError_t fast_forward_batch(const GeomDev& G, int precision, int tin, int tou
   const bool split64 = precision == 1 && tin == 1 && tout == 1 && use_split(G) &&
                        !(use_sym_fwd(G, 1) && Gx);
   if (split64 && G.m > 0 && G.d > 0) {
-    // batch * (P, PT) padded planes; ws_item = 2 * n * (n + 2 margin) doubles
-    double* P = (double*)ws;
-    double* PT = P + (long long)G.n * (G.n + 2 * kPadMargin);
+    // batch * (Q, QT) padded pair planes; ws_item = 2 * n * (n + 2 margin) double2
+    double2* Q = (double2*)ws;
+    double2* QT = Q + (long long)G.n * (G.n + 2 * kPadMargin);
     dim3 tg((G.n + 31) / 32, (G.n + 31) / 32, batch), tb(32, 8);
-    fast::pad_transpose64_kernel<double><<<tg, tb, 0, st>>>((const double*)x, P, PT, G.n);
+    fast::pad_pairs64_kernel<double><<<tg, tb, 0, st>>>((const double*)x, Q, QT, G.n);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     dim3 sg((G.d + 7) / 8, (G.m + 3) / 4, batch), sb(32, fast::kSplitF);
-    fast::fwd_split64_kernel<double, 4><<<sg, sb, 0, st>>>(G, P, PT, (double*)y, M);
+    fast::fwd_split64_kernel<double, 4><<<sg, sb, 0, st>>>(G, Q, QT, (double*)y, M);
     return cudaGetLastError();
   }
   for (int b = 0; b < batch; ++b) {
@@ -2532,15 +2593,15 @@ cudaError_t fast_forward_path(const GeomDev& G, int depth, int batch, const int*
         code |= (unsigned)(bands[(b0 + i) * depth + lv] & 3) << (2 * lv);
       bp.code[i] = (unsigned short)code;
     }
-    double* P = (double*)ws + (long long)b0 * 2 * plane;
-    double* PT = P + plane;
+    double2* Q = (double2*)ws + (long long)b0 * 2 * plane;
+    double2* QT = Q + plane;
     dim3 tg((G.n + 31) / 32, (G.n + 31) / 32, nb), tb(32, 8);
-    fast::prolong_pad64_kernel<<<tg, tb, 0, st>>>(bp, coarse + (long long)b0 * sc * sc, P, PT,
-                                                  G.n);
+    fast::prolong_pairs64_kernel<<<tg, tb, 0, st>>>(bp, coarse + (long long)b0 * sc * sc, Q, QT,
+                                                    G.n);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     dim3 sg((G.d + 7) / 8, (G.m + 3) / 4, nb), sb(32, fast::kSplitF);
-    fast::fwd_split64_kernel<double, 4><<<sg, sb, 0, st>>>(G, P, PT, y + (long long)b0 * M, M);
+    fast::fwd_split64_kernel<double, 4><<<sg, sb, 0, st>>>(G, Q, QT, y + (long long)b0 * M, M);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
