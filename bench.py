@@ -293,7 +293,7 @@ def run_reference(args):
 
 
 # ----------------------------------------------------- WMG-CGLS (config 1)
-def run_wmg_cgls(dev, reps=3, world=1):
+def run_wmg_cgls(dev, reps=5, world=1):
     """BASELINE config 1: 256^2, 180 angles, 363 detectors, float64, seeded
     20-ellipse phantom (seed 1000), 1 % Gaussian noise (seed 1500); WMG-CGLS
     (flexible PCG on the normal equations, 3 levels, 2 pre + 2 post SIRT-type
