@@ -334,7 +334,8 @@ def _assemble_leaf_grams(w, n, lam, levels, ray_chunk=None, paths=None, method="
 
 def _is_sharded(w) -> bool:
     """An AngleShardedProjector (sharding.py) spanning more than one rank."""
-    return hasattr(w, "local") and hasattr(w, "reduce_sino_") and getattr(w, "world", 1) > 1
+    return (hasattr(w, "local") and hasattr(w, "reduce_sino_")
+            and getattr(w, "collectives", getattr(w, "world", 1) > 1))
 
 
 def build_wmg_hierarchy(w, n: int, lam: float, levels: int, nu_pre: int = 0,
@@ -442,7 +443,7 @@ def build_wmg_hierarchy(w, n: int, lam: float, levels: int, nu_pre: int = 0,
         from .sharding import AngleShardedProjector
         node_w = AngleShardedProjector(
             w.geometry, group=w.group, precision="float64" if node_mode == "fast" else "float32",
-            mode="fast", scheme=w.scheme, device=w.device)
+            mode="fast", scheme=w.scheme, device=w.device, always_reduce=w.collectives)
     elif node_mode == "fast":
         node_w = LineProjector(w.geometry, precision="float64", mode="fast", device=w.device)
     else:
@@ -800,7 +801,7 @@ class _GraphedOperator:
             t = D.torch()
             z = t.zeros(self.dim, dtype=t.float64, device=self._device())
             out = t.empty_like(z)
-            while self._graph is None:
+            while self._graph is None and self.use_graph:
                 self.apply_(z, out)
         return self
 
@@ -819,7 +820,18 @@ class _GraphedOperator:
                 return out
             self._gin = t.empty_like(v)
             self._gin.copy_(v)
-            g, self._gout = D.capture_graph(lambda: self._eager(self._gin), v.device)
+            try:
+                g, self._gout = D.capture_graph(lambda: self._eager(self._gin), v.device)
+            except RuntimeError as exc:
+                if not getattr(self, "_sharded", False):
+                    raise
+                # a collective the communicator cannot capture: keep this rank's
+                # cycle eager (the sequence of collectives is unchanged)
+                import warnings
+                warnings.warn(f"sharded V-cycle not captured, running eagerly: {exc}")
+                self.use_graph = False
+                out.copy_(self._eager(v))
+                return out
             self._graph = g
         self._gin.copy_(v)
         self._graph.replay()
@@ -844,8 +856,11 @@ class WmgPreconditioner(_GraphedOperator):
         self.h = h
         self.multiplicative = multiplicative
         self.dim = h.root.dim
-        # an angle-sharded cycle runs collectives between its kernels: eager
-        self._init_graph(graph and not _is_sharded(h.node_projector))
+        # an angle-sharded cycle runs collectives between its kernels: captured
+        # with them when they are NCCL's (stream-ordered), eager over gloo
+        self._sharded = _is_sharded(h.node_projector)
+        self._init_graph(graph and (not self._sharded or
+                                    getattr(h.node_projector, "graph_capturable", False)))
 
     def _eager(self, v):
         return _node_solve_(self.h.root, v, self.multiplicative)

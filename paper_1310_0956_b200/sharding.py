@@ -78,12 +78,24 @@ class AngleShardedProjector:
     """W restricted to this rank's angles, with a summed backprojection."""
 
     def __init__(self, g, group=None, precision: str = "float32", mode=None,
-                 scheme: str = "quad", local=None, device=None):
+                 scheme: str = "quad", local=None, device=None, always_reduce=None):
+        import os
         import torch.distributed as dist
         self.dist = dist
         self.group = group
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        backend = dist.get_backend(group) if dist.is_initialized() else None
+        # ``always_reduce`` issues the collectives at world size 1 too (they are
+        # in-place no-ops there): the one-GPU test boxes exercise the NCCL calls,
+        # their stream ordering and their CUDA-graph capture this way
+        if always_reduce is None:
+            always_reduce = os.environ.get("WMG_ALWAYS_REDUCE", "0") == "1"
+        self.collectives = dist.is_initialized() and (self.world > 1 or bool(always_reduce))
+        # NCCL collectives are stream-ordered device work and can be captured in
+        # a CUDA graph; gloo's are host-side, so loops over gloo stay eager
+        self.graph_capturable = (not self.collectives) or (
+            backend == "nccl" and os.environ.get("WMG_SHARDED_GRAPHS", "1") == "1")
         self.geometry = g
         self.scheme = scheme
         self.index = shard_angles(g.n_angles, self.world, self.rank, scheme)
@@ -151,11 +163,11 @@ class AngleShardedProjector:
     def backward_(self, y, out, accumulate=False):
         if accumulate:
             raise ValueError("accumulate is not supported on a sharded backprojection")
-        qt = self.local.backward_bands() if (self.world > 1 and self.overlap_groups > 1 and
+        qt = self.local.backward_bands() if (self.collectives and self.overlap_groups > 1 and
                                              hasattr(self.local, "backward_bands")) else 0
         if qt == 0:
             self.local.backward_(y, out)
-            if self.world > 1:
+            if self.collectives:
                 self.dist.all_reduce(out, group=self.group)
             return out
         import torch
@@ -183,7 +195,7 @@ class AngleShardedProjector:
 
     def col_sums_dev(self):
         c = self.local.col_sums_dev().clone()       # column sums = sum over angles
-        if self.world > 1:
+        if self.collectives:
             self.dist.all_reduce(c, group=self.group)
         return c
 
@@ -207,7 +219,7 @@ class AngleShardedProjector:
 
     def reduce_sino_(self, t):
         """Sum rank-local sinogram-space partial reductions (in place)."""
-        if self.world > 1:
+        if self.collectives:
             self.dist.all_reduce(t, group=self.group)
         return t
 

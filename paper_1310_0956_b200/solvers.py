@@ -386,24 +386,39 @@ class _GraphedLoop:
     """Runs a device-only loop body: eagerly once (warm-up), then captured once
     as a CUDA graph and replayed for every further iteration."""
 
-    def __init__(self, body):
+    def __init__(self, body, tolerate_capture_failure=False):
         self.body = body
         self.calls = 0
         self.graph = None
+        self.eager = False
+        self.tolerant = tolerate_capture_failure
 
     def step(self):
         t = D.torch()
         self.calls += 1
-        if self.calls == 1:
+        if self.calls == 1 or self.eager:
             self.body()
             return
         if self.graph is None:
-            self.graph, _ = D.capture_graph(self.body, t.cuda.current_device())
+            try:
+                self.graph, _ = D.capture_graph(self.body, t.cuda.current_device())
+            except RuntimeError as exc:
+                if not self.tolerant:
+                    raise
+                # sharded loop whose collectives could not be captured: this rank
+                # keeps issuing the same sequence eagerly
+                import warnings
+                warnings.warn(f"sharded iteration not captured, running eagerly: {exc}")
+                self.eager = True
+                self.body()
+                return
         self.graph.replay()
 
 
 def _graphable(w, precond):
-    if getattr(w, "world", 1) > 1:        # sharded: NCCL inside the loop, stay eager
+    # sharded: the loop holds collectives; NCCL's are stream-ordered and are
+    # captured with the kernels, host-side ones (gloo) keep the loop eager
+    if not getattr(w, "graph_capturable", getattr(w, "world", 1) == 1):
         return False
     if not (hasattr(w, "forward_") and hasattr(w, "backward_")):
         return False
@@ -493,6 +508,7 @@ def _cgls_graphed(w, bd, x, lam, precond, cfg, errs, was_np, record, t0):
         precond = pref() if pref is not None else None
         w.forward_(p, q)
         D.det_reduce([(N.RED_SQ, q, None, None)], out=S[1:2])
+        _sino(w, S[1:2])                  # angle shards: sum of the ranks' partials
         if lam != 0:
             D.det_reduce([(N.RED_SQ, p, None, None)], out=S[2:3])
         N.call("wmg_cgls_scalars", D.ptr(S), float(lam), 0, st())
@@ -526,10 +542,11 @@ def _cgls_graphed(w, bd, x, lam, precond, cfg, errs, was_np, record, t0):
     zbuf = ctx["z"]
     loop = ctx["loop"]
     if loop is None:
-        loop = ctx["loop"] = _GraphedLoop(body)
+        loop = ctx["loop"] = _GraphedLoop(body, bool(getattr(w, "collectives", False)))
     loop_b = ctx["loopB"]
     if split and loop_b is None:
-        loop_b = ctx["loopB"] = _GraphedLoop(lambda: tail(zbuf))
+        loop_b = ctx["loopB"] = _GraphedLoop(lambda: tail(zbuf),
+                                             bool(getattr(w, "collectives", False)))
     for k in range(1, cfg.max_iterations + 1):
         loop.step()
         if split:
