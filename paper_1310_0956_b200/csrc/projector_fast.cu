@@ -136,13 +136,15 @@ __global__ void __launch_bounds__(128) fwd_kernel(GeomDev G, const TIn* __restri
 }
 
 // One thread per pixel; all threads walk the angles in the same order.
+// (row_lo, row_hi: the image rows this launch covers, default all)
 template <typename TIn, typename TOut, typename R, bool kAccumulate>
 __global__ void __launch_bounds__(256) bwd_kernel(GeomDev G, const TIn* __restrict__ sino,
-                                                  TOut* __restrict__ img) {
+                                                  TOut* __restrict__ img, int row_lo = 0,
+                                                  int row_hi = 0x7fffffff) {
   const int n = G.n;
   const int ix = blockIdx.x * 32 + (threadIdx.x & 31);
-  const int row = blockIdx.y * 8 + (threadIdx.x >> 5);
-  if (ix >= n || row >= n) return;
+  const int row = row_lo + blockIdx.y * 8 + (threadIdx.x >> 5);
+  if (ix >= n || row >= n || row >= row_hi) return;
   const double xc = (double)ix - (double)n * 0.5 + 0.5;
   const double yc = (double)n * 0.5 - (double)row - 0.5;
   const double dc = (double)(G.d - 1) * 0.5;
@@ -181,6 +183,7 @@ __global__ void __launch_bounds__(256) bwd_kernel(GeomDev G, const TIn* __restri
 // kSplit threads -- consecutive slab (angle) segments -- and reduce the
 // partial sums in shared memory in segment order (deterministic).
 constexpr int kSplit = 8;
+constexpr int kSplitAxis = 32;   // slab segments per ray of the two axis-aligned angles
 constexpr int kSplitF = 4;   // slab segments per ray of the padded-plane fp64 forward (8: same single-image time, 10 % slower sibling batches)
 constexpr int kFwdAG = 4;    // adjacent angles per symmetric-forward block
 
@@ -514,12 +517,12 @@ __global__ void __launch_bounds__(128) fwd_v2_kernel(GeomDev G, const float* __r
 // (threadIdx.y), partial sums reduced in shared memory in segment order: for
 // the two axis-aligned angles of a symmetric set, which alone launch too few
 // rays to fill the GPU (their walk is n slabs long).
-template <typename TOut, int ES = 1>
-__global__ void __launch_bounds__(32 * kSplit) fwd_v2_split_kernel(GeomDev G,
+template <typename TOut, int ES = 1, int KS = kSplit>
+__global__ void __launch_bounds__(32 * KS) fwd_v2_split_kernel(GeomDev G,
                                                                    const float* __restrict__ P,
                                                                    const float* __restrict__ PT,
                                                                    TOut* __restrict__ sino) {
-  __shared__ float part[kSplit][33];
+  __shared__ float part[KS][33];
   const int a = blockIdx.y, lane = threadIdx.x, seg = threadIdx.y;
   const int j = blockIdx.x * 32 + lane;
   const AngleParams& A = G.ang[a];
@@ -544,8 +547,8 @@ __global__ void __launch_bounds__(32 * kSplit) fwd_v2_split_kernel(GeomDev G,
   float acc = 0.0f;
   if (rw0 <= rw1) {
     const int len = rw1 - rw0 + 1;
-    const int rs = rw0 + (len * seg) / kSplit;
-    const int re = rw0 + (len * (seg + 1)) / kSplit - 1;
+    const int rs = rw0 + (len * seg) / KS;
+    const int re = rw0 + (len * (seg + 1)) / KS - 1;
     const float* __restrict__ src = (A.major ? PT : P) + ES * kPadMargin;
     const long long S = llrint(slope * kQ32);
     long long U = llrint(u0 * kQ32) + (long long)rs * S;
@@ -584,7 +587,7 @@ __global__ void __launch_bounds__(32 * kSplit) fwd_v2_split_kernel(GeomDev G,
   if (seg == 0 && j < G.d) {
     float sum = part[0][lane];
 #pragma unroll
-    for (int q = 1; q < kSplit; ++q) sum += part[q][lane];
+    for (int q = 1; q < KS; ++q) sum += part[q][lane];
     sino[(long long)(G.rowmap ? G.rowmap[a] : a) * G.d + j] = (TOut)sum;
   }
 }
@@ -2155,10 +2158,12 @@ static cudaError_t fwd_v2_impl(const GeomDev& G, const void* x, void* ws, void* 
     }
     e = cudaGetLastError();
     if (e != cudaSuccess || Gx->m == 0) return e;
-    // the axis-aligned angles of the set: slab segments over threadIdx.y
-    dim3 xgrid((G.d + 31) / 32, Gx->m), xblock(32, fast::kSplit);
-    fast::fwd_v2_split_kernel<TOut, 2><<<xgrid, xblock, 0, st>>>(*Gx, (const float*)PM,
-                                                                 (const float*)PMT, (TOut*)y);
+    // the axis-aligned angles of the set: 32 slab segments over threadIdx.y (two
+    // angles launch only 2 d / 32 blocks, each walking n slabs: with 8 segments
+    // this serial tail took 15 / 25 / 46 us at n = 512 / 1024 / 2048)
+    dim3 xgrid((G.d + 31) / 32, Gx->m), xblock(32, fast::kSplitAxis);
+    fast::fwd_v2_split_kernel<TOut, 2, fast::kSplitAxis><<<xgrid, xblock, 0, st>>>(
+        *Gx, (const float*)PM, (const float*)PMT, (TOut*)y);
     return cudaGetLastError();
   }
   fast::pad_transpose_kernel<TIn><<<tg, tb, 0, st>>>((const TIn*)x, P, PT, G.n);
@@ -2247,6 +2252,21 @@ static void bwd_symrun_launch(const GeomDev& G, const void* y, void* x, bool acc
                                                                       (TOut*)x);
 }
 
+// The axis-aligned angles of a symmetric set, added to image rows [row_lo,
+// row_hi): one thread per pixel (per angle one detector load of weight 1 and
+// the pixel's read-modify-write; the tiled kernel's window staging for two
+// angles took 11 / 26 us at n = 1024 / 2048, the angle-split one 13 us at 512)
+template <typename TIn, typename TOut>
+static cudaError_t bwd_axis_launch(const GeomDev& Gx, const void* y, void* x, cudaStream_t st,
+                                   int row_lo = 0, int row_hi = -1) {
+  if (row_hi < 0) row_hi = Gx.n;
+  if (Gx.m == 0 || row_hi <= row_lo) return cudaSuccess;
+  dim3 g1((Gx.n + 31) / 32, (row_hi - row_lo + 7) / 8);
+  fast::bwd_kernel<TIn, TOut, float, true><<<g1, 256, 0, st>>>(Gx, (const TIn*)y, (TOut*)x,
+                                                                row_lo, row_hi);
+  return cudaGetLastError();
+}
+
 template <typename TIn, typename TOut>
 static cudaError_t bwd_sym_impl(const GeomDev& G, const GeomDev& Gx, const void* y, void* x,
                                 bool accumulate, cudaStream_t st) {
@@ -2279,7 +2299,7 @@ static cudaError_t bwd_sym_impl(const GeomDev& G, const GeomDev& Gx, const void*
       cudaError_t e = accumulate ? bwd_symrun_cluster<TIn, TOut, true>(G, y, x, nsplit, 1, st)
                                  : bwd_symrun_cluster<TIn, TOut, false>(G, y, x, nsplit, 1, st);
       if (e != cudaSuccess || Gx.m == 0) return e;
-      return bwd_v2_impl<TIn, TOut>(Gx, y, x, true, st);   // axis angles, accumulate
+      return bwd_axis_launch<TIn, TOut>(Gx, y, x, st);   // axis angles, accumulate
     }
     if ((G.n / 2) % 64 == 0 &&
         ((long long)(G.n / 64) * (G.n / 128) >= 12LL * 148 || (G.sym & 1024)) &&
@@ -2304,7 +2324,7 @@ static cudaError_t bwd_sym_impl(const GeomDev& G, const GeomDev& Gx, const void*
   }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess || Gx.m == 0) return e;
-  return bwd_v2_impl<TIn, TOut>(Gx, y, x, true, st);   // axis angles, accumulate
+  return bwd_axis_launch<TIn, TOut>(Gx, y, x, st);   // axis angles, accumulate
 }
 
 template <typename TIn, typename TOut>
@@ -2488,12 +2508,10 @@ static cudaError_t bwd_band_impl(const GeomDev& G, const GeomDev& Gx, const void
   }
   if (Gx.m == 0 || s1 <= s0) return cudaSuccess;
   // the axis-aligned angles of the set on the band's two row ranges
-  const int tiles = G.n / fast::kBwdTile;
-  dim3 g1(tiles, s1 - s0);
-  fast::bwd_v2_kernel<TIn, TOut, true><<<g1, 128, 0, st>>>(Gx, (const TIn*)y, (TOut*)x, s0);
-  fast::bwd_v2_kernel<TIn, TOut, true><<<g1, 128, 0, st>>>(Gx, (const TIn*)y, (TOut*)x,
-                                                           tiles - s1);
-  return cudaGetLastError();
+  const int T = fast::kBwdTile;
+  cudaError_t e = bwd_axis_launch<TIn, TOut>(Gx, y, x, st, T * s0, T * s1);
+  if (e != cudaSuccess) return e;
+  return bwd_axis_launch<TIn, TOut>(Gx, y, x, st, G.n - T * s1, G.n - T * s0);
 }
 
 cudaError_t fast_backward_band(const GeomDev& G, int precision, int tin, int tout, const void* y,
