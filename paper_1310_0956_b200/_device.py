@@ -257,6 +257,27 @@ def det_reduce(specs, n=None, out=None):
     return out
 
 
+def det_partials(specs):
+    """Level 1 of ``det_reduce`` only: returns the scratch tensor holding the
+    chunk sums (reduction k at offset k * ceil(n / 1024)), for the fused CGLS
+    kernels that finish the reduction themselves."""
+    K = len(specs)
+    a0 = specs[0][1]
+    n = a0.numel()
+    for sp_ in specs:
+        for v in sp_[1:]:
+            if v is not None and v.numel() != n:
+                raise ValueError("det_partials operands must have equal lengths")
+    sc = scratch(n, K, a0.device)
+    ops = (ctypes.c_int * K)(*[int(s[0]) for s in specs])
+    A = (ctypes.c_void_p * K)(*[s[1].data_ptr() for s in specs])
+    B = (ctypes.c_void_p * K)(*[(s[2].data_ptr() if s[2] is not None else 0) for s in specs])
+    C = (ctypes.c_void_p * K)(*[(s[3].data_ptr() if len(s) > 3 and s[3] is not None else 0)
+                                for s in specs])
+    N.call("wmg_det_partials", int(n), K, ops, A, B, C, ptr(sc), stream_handle())
+    return sc
+
+
 def det_dot(a, b):
     return det_reduce([(N.RED_DOT, a, b, None)])
 

@@ -62,6 +62,10 @@ cudaError_t ew_axpy_dev(long long, double*, const double*, const double*, int, c
 cudaError_t ew_lincomb_dev(long long, double*, double, const double*, const double*,
                            const double*, cudaStream_t);
 cudaError_t cgls_scalars(double*, double, int, cudaStream_t);
+cudaError_t cgls_update(long long, long long, double*, const double*, double*, const double*,
+                        const double*, double*, cudaStream_t);
+cudaError_t cgls_direction(long long, double*, const double*, const double*, int, double*,
+                           cudaStream_t);
 cudaError_t batched_gemv(int, int, const double*, long long, const double*, long long, double*,
                          long long, cudaStream_t);
 cudaError_t haar_prolong(int, const double*, int, double*, int, cudaStream_t);
@@ -576,10 +580,9 @@ int wmg_csr_fill(const wmg_geometry* g, const long long* indptr, long long* cols
 
 long long wmg_det_scratch_len(long long n, int K) { return wmg::det_scratch_len(n, K); }
 
-int wmg_det_reduce(long long n, int K, const int* ops, const double* const* a,
-                   const double* const* b, const double* const* c, double* scratch, double* out,
-                   void* stream) {
-  if (K < 1 || K > 8 || !ops || !a || !scratch || !out)
+static int det_args_check(long long n, int K, const int* ops, const double* const* a,
+                          const double* const* b, const double* const* c, const double* scratch) {
+  if (K < 1 || K > 8 || !ops || !a || !scratch)
     return fail(WMG_EINVAL, "bad det_reduce arguments");
   if (n > 1024LL * 1024LL * 1024LL) return fail(WMG_EINVAL, "vector longer than 2^30");
   for (int k = 0; k < K; ++k) {
@@ -590,7 +593,25 @@ int wmg_det_reduce(long long n, int K, const int* ops, const double* const* a,
       return fail(WMG_EINVAL, "NULL operand");
     if (ops[k] == WMG_RED_DOTDIFF && (!c || !c[k])) return fail(WMG_EINVAL, "NULL operand");
   }
+  return WMG_OK;
+}
+
+int wmg_det_reduce(long long n, int K, const int* ops, const double* const* a,
+                   const double* const* b, const double* const* c, double* scratch, double* out,
+                   void* stream) {
+  if (!out) return fail(WMG_EINVAL, "bad det_reduce arguments");
+  const int rc = det_args_check(n, K, ops, a, b, c, scratch);
+  if (rc) return rc;
   return cuda_rc(wmg::det_reduce(n, K, ops, a, b, c, scratch, out, STREAM(stream)));
+}
+
+int wmg_det_partials(long long n, int K, const int* ops, const double* const* a,
+                     const double* const* b, const double* const* c, double* partials,
+                     void* stream) {
+  const int rc = det_args_check(n, K, ops, a, b, c, partials);
+  if (rc) return rc;
+  if (n < 1) return fail(WMG_EINVAL, "det_partials: empty vector");
+  return cuda_rc(wmg::det_reduce(n, K, ops, a, b, c, partials, nullptr, STREAM(stream)));
 }
 
 int wmg_maxabs(long long n, const double* a, const double* b, double* out, void* stream) {
@@ -671,6 +692,20 @@ int wmg_cgls_scalars(double* S, double lam, int op, void* stream) {
   REQ(S);
   if (op < 0 || op > 2) return fail(WMG_EINVAL, "bad scalar op");
   return cuda_rc(wmg::cgls_scalars(S, lam, op, STREAM(stream)));
+}
+int wmg_cgls_update(long long n_img, long long n_sino, double* x, const double* p, double* r,
+                    const double* q, const double* partials, double* S, void* stream) {
+  REQ(x && p && r && q && partials && S);
+  if (n_img <= 0 || n_sino <= 0 || n_sino > (1LL << 20))
+    return fail(WMG_EINVAL, "cgls_update: lengths must be in [1, 2^20]");
+  return cuda_rc(wmg::cgls_update(n_img, n_sino, x, p, r, q, partials, S, STREAM(stream)));
+}
+int wmg_cgls_direction(long long n, double* p, const double* z, const double* partials, int mode,
+                       double* S, void* stream) {
+  REQ(p && z && partials && S);
+  if (n <= 0 || n > (1LL << 20)) return fail(WMG_EINVAL, "cgls_direction: n not in [1, 2^20]");
+  if (mode != 1 && mode != 2) return fail(WMG_EINVAL, "cgls_direction: mode must be 1 or 2");
+  return cuda_rc(wmg::cgls_direction(n, p, z, partials, mode, S, STREAM(stream)));
 }
 int wmg_h2d_staged(void* dst, const void* src, size_t bytes, void* pinned, int threads,
                    void* stream) {

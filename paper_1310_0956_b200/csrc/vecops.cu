@@ -541,6 +541,85 @@ __global__ void cgls_scalars_kernel(double* S, double lam, int op) {
   }
 }
 
+// --- fused forms (lam == 0, unsharded, vectors of at most 2^20 elements) ---
+// The reduction's last level, the scalar recurrence and the vector update in
+// one kernel: every block finishes the <= 1024 level-1 chunk sums itself (one
+// warp, the order det_finish uses, so every block holds the bit-identical
+// value), forms the coefficient and updates its share of the vectors; block 0
+// publishes the scalars.  Same arithmetic as det_finish + cgls_scalars +
+// axpy_dev / lincomb_dev, five launches fewer per iteration.  gamma lives in
+// two slots so that no block reads a slot another block writes in the same
+// launch: the update kernel reads S[11] and commits it to S[0], the direction
+// kernel reads S[0] and writes the new gamma to S[11].
+__device__ __forceinline__ double finish_small(const double* partials, long long C, int lane) {
+  if (C == 1) return partials[0];
+  return __shfl_sync(0xffffffffu, warp_chunk(partials, C, 0, lane), 0);
+}
+
+// x += alpha p, r -= alpha q with alpha = gamma / <q,q>; partials: level 1 of <q,q>
+__global__ void __launch_bounds__(256) cgls_update_kernel(long long n_img, long long n_sino,
+                                                          double* x, const double* p, double* r,
+                                                          const double* q,
+                                                          const double* partials, long long C,
+                                                          double* S) {
+  __shared__ double sh_alpha;
+  if (threadIdx.x < 32) {
+    const double qq = finish_small(partials, C, threadIdx.x);
+    if (threadIdx.x == 0) {
+      const double gamma = S[11];
+      const bool ok = qq > 0.0 && isfinite(qq);
+      const double alpha = ok ? gamma / qq : 0.0;
+      sh_alpha = alpha;
+      if (blockIdx.x == 0) {
+        S[1] = qq;
+        S[3] = alpha;
+        S[0] = gamma;
+        if (!ok) S[8] = 1.0;
+      }
+    }
+  }
+  __syncthreads();
+  const double alpha = sh_alpha;
+  GRID_LOOP(i, n_img) { x[i] = dadd(x[i], dmul(alpha, p[i])); }
+  GRID_LOOP(j, n_sino) { r[j] = dsub(r[j], dmul(alpha, q[j])); }
+}
+
+// p = z + beta p.  mode 1 (CGLS): partials of <s,s>; beta = ss / gamma, gamma' = ss.
+// mode 2 (flexible PCG-NE): partials of <s,s>, <z,s>, <z,s-s_old>; beta = pr / gamma,
+// gamma' = zs.
+__global__ void __launch_bounds__(256) cgls_direction_kernel(long long n, double* p,
+                                                             const double* z,
+                                                             const double* partials, long long C,
+                                                             int mode, double* S) {
+  __shared__ double sh_beta;
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    const double ss = finish_small(partials, C, lane);
+    double zs = 0.0, pr = 0.0;
+    if (mode == 2) {
+      zs = finish_small(partials + C, C, lane);
+      pr = finish_small(partials + 2 * C, C, lane);
+    }
+    if (lane == 0) {
+      const double gamma = S[0];
+      const double beta = (mode == 1 ? ss : pr) / gamma;
+      sh_beta = beta;
+      if (blockIdx.x == 0) {
+        S[5] = ss;
+        if (mode == 2) {
+          S[6] = zs;
+          S[7] = pr;
+        }
+        S[4] = beta;
+        S[11] = mode == 1 ? ss : zs;
+      }
+    }
+  }
+  __syncthreads();
+  const double beta = sh_beta;
+  GRID_LOOP(i, n) { p[i] = dadd(dmul(1.0, z[i]), dmul(beta, p[i])); }
+}
+
 }  // namespace vec
 
 // ---------------------------------------------------------------------------
@@ -565,15 +644,35 @@ cudaError_t det_reduce(long long n, int K, const int* ops, const double* const* 
     A.op[k] = k < K ? ops[k] : 0;
   }
   if (n <= 0) {
-    return cudaMemsetAsync(out, 0, sizeof(double) * K, st);
+    return out ? cudaMemsetAsync(out, 0, sizeof(double) * K, st) : cudaErrorInvalidValue;
   }
   const long long C = (n + 1023) / 1024;
   if (C > 1024LL * 1024LL) return cudaErrorInvalidValue;
   dim3 grid((unsigned)((C + 7) / 8), K);
   vec::det_level1<<<grid, 256, 0, st>>>(n, A, scratch, C);
   cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
+  if (e != cudaSuccess || !out) return e;   // out == nullptr: level-1 chunk sums only
   vec::det_finish<<<K, 1024, 0, st>>>(scratch, C, out);
+  return cudaGetLastError();
+}
+
+// fused CGLS steps on the level-1 chunk sums a det_reduce(..., out = nullptr) left
+// in ``partials`` (reduction k at partials + k * C, C = ceil(n / 1024) <= 1024)
+cudaError_t cgls_update(long long n_img, long long n_sino, double* x, const double* p, double* r,
+                        const double* q, const double* partials, double* S, cudaStream_t st) {
+  const long long C = (n_sino + 1023) / 1024;
+  if (n_img <= 0 || n_sino <= 0 || C > 1024) return cudaErrorInvalidValue;
+  const long long nmax = n_img > n_sino ? n_img : n_sino;
+  vec::cgls_update_kernel<<<grid_for(nmax, 256), 256, 0, st>>>(n_img, n_sino, x, p, r, q,
+                                                               partials, C, S);
+  return cudaGetLastError();
+}
+
+cudaError_t cgls_direction(long long n, double* p, const double* z, const double* partials,
+                           int mode, double* S, cudaStream_t st) {
+  const long long C = (n + 1023) / 1024;
+  if (n <= 0 || C > 1024 || (mode != 1 && mode != 2)) return cudaErrorInvalidValue;
+  vec::cgls_direction_kernel<<<grid_for(n, 256), 256, 0, st>>>(n, p, z, partials, C, mode, S);
   return cudaGetLastError();
 }
 

@@ -382,6 +382,9 @@ def bicgstab_solve(op, f, precond=None, x0=None, cfg: SolverConfig = None, x_ex=
     return D.to_caller(x, was_np), record
 
 
+FUSED_CGLS = True      # tests switch it off to compare with the unfused kernels
+
+
 class _GraphedLoop:
     """Runs a device-only loop body: eagerly once (warm-up), then captured once
     as a CUDA graph and replayed for every further iteration."""
@@ -437,7 +440,12 @@ def _cgls_graphed(w, bd, x, lam, precond, cfg, errs, was_np, record, t0):
     # so repeated solves replay it instead of re-capturing (no x_ex tracking:
     # the error terms read a per-solve buffer).
     owner = precond if precond is not None else w
-    key = (id(w), lam, str(dev))
+    # lam == 0, unsharded, vectors of <= 2^20 elements: the reductions' last
+    # level, the scalar recurrences and the vector updates run fused
+    # (wmg_cgls_update / wmg_cgls_direction: same arithmetic, 5 launches fewer)
+    fused = (FUSED_CGLS and lam == 0 and not getattr(w, "collectives", False)
+             and max(M_, Nn) <= (1 << 20))
+    key = (id(w), lam, str(dev), fused)
     cache = None if errs.active else owner.__dict__.setdefault("_cgls_graph_cache", {})
     ctx = cache.get(key) if cache is not None else None
     if ctx is not None and ctx["wref"]() is not w:
@@ -485,6 +493,7 @@ def _cgls_graphed(w, bd, x, lam, precond, cfg, errs, was_np, record, t0):
         S[0:1].copy_(S[6:7])
     p = ctx["p"]
     p.copy_(z)
+    S[11:12].copy_(S[0:1])                # gamma's second slot (fused kernels)
     if errs.active:
         S[9:11].copy_(errs.device_terms(x))
     S_host.copy_(S, non_blocking=True)
@@ -507,29 +516,45 @@ def _cgls_graphed(w, bd, x, lam, precond, cfg, errs, was_np, record, t0):
         w = wref()
         precond = pref() if pref is not None else None
         w.forward_(p, q)
-        D.det_reduce([(N.RED_SQ, q, None, None)], out=S[1:2])
-        _sino(w, S[1:2])                  # angle shards: sum of the ranks' partials
-        if lam != 0:
-            D.det_reduce([(N.RED_SQ, p, None, None)], out=S[2:3])
-        N.call("wmg_cgls_scalars", D.ptr(S), float(lam), 0, st())
-        N.call("wmg_axpy_dev", n_img, D.ptr(x), D.ptr(x), D.ptr(S[3:4]), 1, D.ptr(p), st())
-        N.call("wmg_axpy_dev", n_sino, D.ptr(r), D.ptr(r), D.ptr(S[3:4]), -1, D.ptr(q), st())
+        if fused:
+            part = D.det_partials([(N.RED_SQ, q, None, None)])
+            N.call("wmg_cgls_update", n_img, n_sino, D.ptr(x), D.ptr(p), D.ptr(r), D.ptr(q),
+                   D.ptr(part), D.ptr(S), st())
+        else:
+            D.det_reduce([(N.RED_SQ, q, None, None)], out=S[1:2])
+            _sino(w, S[1:2])              # angle shards: sum of the ranks' partials
+            if lam != 0:
+                D.det_reduce([(N.RED_SQ, p, None, None)], out=S[2:3])
+            N.call("wmg_cgls_scalars", D.ptr(S), float(lam), 0, st())
+            N.call("wmg_axpy_dev", n_img, D.ptr(x), D.ptr(x), D.ptr(S[3:4]), 1, D.ptr(p), st())
+            N.call("wmg_axpy_dev", n_sino, D.ptr(r), D.ptr(r), D.ptr(S[3:4]), -1, D.ptr(q),
+                   st())
         if precond is not None:
             s_old.copy_(s)
         w.backward_(r, s)
         if lam != 0:
             D.add_scaled(s, s, lam, -1, x)
         if precond is None:
-            D.det_reduce([(N.RED_SQ, s, None, None)], out=S[5:6])
-            N.call("wmg_cgls_scalars", D.ptr(S), float(lam), 1, st())
-            N.call("wmg_lincomb_dev", n_img, D.ptr(p), 1.0, D.ptr(s), D.ptr(S[4:5]), D.ptr(p),
-                   st())
+            if fused:
+                part = D.det_partials([(N.RED_SQ, s, None, None)])
+                N.call("wmg_cgls_direction", n_img, D.ptr(p), D.ptr(s), D.ptr(part), 1,
+                       D.ptr(S), st())
+            else:
+                D.det_reduce([(N.RED_SQ, s, None, None)], out=S[5:6])
+                N.call("wmg_cgls_scalars", D.ptr(S), float(lam), 1, st())
+                N.call("wmg_lincomb_dev", n_img, D.ptr(p), 1.0, D.ptr(s), D.ptr(S[4:5]),
+                       D.ptr(p), st())
             tail()
         elif not split:
             tail(precond._eager(s))
 
     def tail(zz=None):
-        if zz is not None:
+        if zz is not None and fused:
+            part = D.det_partials([(N.RED_SQ, s, None, None), (N.RED_DOT, zz, s, None),
+                                   (N.RED_DOTDIFF, zz, s, s_old)])
+            N.call("wmg_cgls_direction", n_img, D.ptr(p), D.ptr(zz), D.ptr(part), 2,
+                   D.ptr(S), st())
+        elif zz is not None:
             D.det_reduce([(N.RED_SQ, s, None, None), (N.RED_DOT, zz, s, None),
                           (N.RED_DOTDIFF, zz, s, s_old)], out=S[5:8])
             N.call("wmg_cgls_scalars", D.ptr(S), float(lam), 2, st())
@@ -563,7 +588,7 @@ def _cgls_graphed(w, bd, x, lam, precond, cfg, errs, was_np, record, t0):
         if cfg.residual_tolerance > 0 and rel < cfg.residual_tolerance:
             record.status = STATUS_CONVERGED
             break
-        if h[0] == 0.0:
+        if h[11 if fused else 0] == 0.0:      # gamma
             record.status = STATUS_CONVERGED
             break
     else:
