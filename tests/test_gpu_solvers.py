@@ -277,9 +277,7 @@ def test_fused_cgls_kernels_bitwise_vs_unfused(gpu, precond_kind):
     n, d, m = 64, 91, 90
     w = build_projector(build_geometry(n, d, m), precision="float64", mode="fast")
     b = torch.from_numpy(w @ random_ellipses(n, 10, seed=0)).cuda()
-    cfg = SolverConfig(max_iterations=20, residual_tolerance=0.0)
-
-    def run(fused):
+    def run(fused, cfg):
         S.FUSED_CGLS = fused
         try:
             pre = None
@@ -294,11 +292,17 @@ def test_fused_cgls_kernels_bitwise_vs_unfused(gpu, precond_kind):
         finally:
             S.FUSED_CGLS = True
 
-    xf, rf = run(True)
-    xu, ru = run(False)
-    assert torch.equal(xf, xu)
-    assert rf.rel_residual == ru.rel_residual
-    assert rf.status == ru.status and rf.iterations == ru.iterations
+    # a fixed iteration count, an early exit on the tolerance, a single iteration
+    for cfg in (SolverConfig(max_iterations=20, residual_tolerance=0.0),
+                SolverConfig(max_iterations=60, residual_tolerance=1e-3),
+                SolverConfig(max_iterations=1, residual_tolerance=0.0)):
+        xu, ru = run(False, cfg)
+        xf, rf = run(True, cfg)
+        assert torch.equal(xf, xu), cfg
+        assert rf.rel_residual == ru.rel_residual
+        assert rf.status == ru.status and rf.iterations == ru.iterations
+        if cfg.residual_tolerance > 0:
+            assert ru.status == "converged" and ru.iterations[-1] < cfg.max_iterations
 
 
 def test_fused_cgls_breakdown_flag(gpu):
