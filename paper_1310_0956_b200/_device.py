@@ -81,7 +81,8 @@ def to_device(v, dtype=None, device=None):
 # chunks and issues each chunk's DMA as soon as it has landed.  D2H: into a
 # pinned buffer from a small pool, returned as the numpy view itself.
 _STAGE_MIN_BYTES = 64 << 10         # below: plain pageable copies (latency bound anyway)
-_STAGE_THREADS = 8
+_STAGE_THREADS = 6                   # host-copy threads (tools/probe_h2d_threads.py: 4-6 saturate
+                                     # the box's ~25 GB/s pageable -> pinned copy rate; more are slower)
 _stage = {}
 _stage_lock = threading.Lock()
 
