@@ -358,7 +358,9 @@ def run_wmg_cgls(dev, reps=5, world=1):
                                                mx[3 * k:4 * k], mx[4 * k:5 * k],
                                                mx[5 * k:6 * k])
     nu0 = {"seconds": min(s0), "setup_seconds": min(u0), "iterations": rec0.iterations[-1]}
+    nu0["roofline"] = _wmg_model_roofline(n, m, 3, 0, 0, nu0["iterations"], nu0["seconds"], world)
     return {"metric": "WMG-CGLS seconds to rel. residual 1e-4", "config": "config1_256_180x363",
+            "roofline": _wmg_model_roofline(n, m, 3, 2, 2, iters, min(solves), world),
             "n_gpus": world, "seconds": min(solves), "setup_seconds": min(setups),
             "seconds_repeat_rhs": min(repeats),
             "seconds_incl_setup": min(a + c for a, c in zip(solves, setups)),
@@ -372,6 +374,34 @@ def run_wmg_cgls(dev, reps=5, world=1):
             "timing": "torch.cuda.synchronize + perf_counter, max over ranks, best of %d; "
                       "every WMG solve uses a freshly built hierarchy (graph capture "
                       "included)" % reps}
+
+
+def _wmg_model_roofline(n, m, levels, nu_pre, nu_post, iterations, seconds, world=1):
+    """SURVEY s8(d) model roofline of a WMG-CGLS solve: node pairs x t_roof_pair
+    + coarse leaf bytes / HBM bandwidth.  A pair is 2 nnz(W) intersection
+    updates at the float64 gather peak (n_SM x 32 lanes x f_SM / 2); every
+    internal node of the hierarchy applies its (matrix-free) system nu_pre +
+    nu_post + 1 times per V-cycle (once without smoother sweeps), the outer
+    iteration once, and a V-cycle streams every packed leaf inverse once."""
+    nnz = (4.0 / math.pi) * m * n * n               # within 1e-5 of the exact count
+    internal = (4 ** (levels - 1) - 1) // 3
+    apps = (nu_pre + nu_post + 1) if nu_pre > 0 else (1 + nu_post)
+    pairs = (iterations + 1) * (1 + internal * apps)
+    p = (n >> (levels - 1)) ** 2
+    leaves = 4 ** (levels - 1)
+    leaf_bytes = leaves * (p * (p + 128) // 2) * 8  # packed lower 128 x 128 tiles
+    peaks, peak_source = measured_peaks()
+    f_sm = (peaks.get("sm_max_mhz") or 1965.0) * 1e6
+    hbm = (peaks.get("hbm_gbs") or 6650.0) * 1e9
+    r64 = 148 * 32 * f_sm / 2 * world
+    t_pairs = pairs * 2 * nnz / r64
+    t_leaf = (iterations + 1) * leaf_bytes / hbm
+    model = t_pairs + t_leaf
+    return {"bound": "gather + hbm (model)", "model_seconds": model, "frac": model / seconds,
+            "node_pairs": pairs, "pair_seconds_at_peak": 2 * nnz / r64,
+            "leaf_bytes_per_cycle": leaf_bytes, "peak_source": peak_source,
+            "definition": "SURVEY s8(d): node pairs x 2 nnz / (n_SM x 32 x f_SM / 2) + "
+                          "V-cycles x packed leaf bytes / measured HBM bandwidth"}
 
 
 def cpu_wmg_cgls(b):
