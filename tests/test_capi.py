@@ -71,3 +71,29 @@ def test_new_entry_points_validate_without_a_gpu():
     assert lib.wmg_haar_restrict_path(66, 2, 1, bands, dp, dp, None) == _native.WMG_EINVAL
     assert lib.wmg_haar_restrict_path(64, 8, 1, bands, dp, dp, None) == _native.WMG_EINVAL
     assert lib.wmg_haar_prolong_path(64, 2, 0, bands, dp, dp, None) == _native.WMG_OK
+
+
+def test_fused_cgls_entry_points_validate_without_a_gpu():
+    """wmg_det_partials / wmg_cgls_update / wmg_cgls_direction reject what the
+    fused kernels cannot do (vectors longer than 2^20, unknown modes, NULL
+    buffers) before any CUDA call."""
+    from paper_1310_0956_b200 import _native
+    lib = _native.load()
+    dp = ctypes.c_void_p(8)
+    big = (1 << 20) + 1
+    assert lib.wmg_cgls_update(100, big, dp, dp, dp, dp, dp, dp, None) == _native.WMG_EINVAL
+    assert b"2^20" in lib.wmg_last_error()
+    assert lib.wmg_cgls_update(0, 100, dp, dp, dp, dp, dp, dp, None) == _native.WMG_EINVAL
+    assert lib.wmg_cgls_update(100, 100, None, dp, dp, dp, dp, dp, None) == _native.WMG_EINVAL
+    assert lib.wmg_cgls_direction(big, dp, dp, dp, 1, dp, None) == _native.WMG_EINVAL
+    assert lib.wmg_cgls_direction(100, dp, dp, dp, 3, dp, None) == _native.WMG_EINVAL
+    assert b"mode" in lib.wmg_last_error()
+    assert lib.wmg_cgls_direction(100, dp, dp, None, 1, dp, None) == _native.WMG_EINVAL
+    ops = (ctypes.c_int * 1)(4)
+    a = (ctypes.c_void_p * 1)(8)
+    assert lib.wmg_det_partials(0, 1, ops, a, None, None, dp, None) == _native.WMG_EINVAL
+    assert lib.wmg_det_partials(100, 0, ops, a, None, None, dp, None) == _native.WMG_EINVAL
+    bad = (ctypes.c_int * 1)(7)
+    assert lib.wmg_det_partials(100, 1, bad, a, None, None, dp, None) == _native.WMG_EINVAL
+    dot = (ctypes.c_int * 1)(0)                        # RED_DOT needs a second operand
+    assert lib.wmg_det_partials(100, 1, dot, a, None, None, dp, None) == _native.WMG_EINVAL
