@@ -215,14 +215,15 @@ int wmg_lincomb_dev(long long n, double *out, double a, const double *x, const d
 /* CGLS / flexible PCG-NE scalar recurrences on device slots (see vecops.cu):
  * op 0 alpha = gamma/(qq + lam pp); op 1 beta = ss/gamma; op 2 beta = pr/gamma */
 int wmg_cgls_scalars(double *S, double lam, int op, void *stream);
-/* Fused forms for lam == 0 and vectors of at most 2^20 elements (the last
+/* Fused forms for vectors of at most 2^20 elements (the last
  * reduction level, the scalar recurrence and the vector update in one launch;
  * bit-identical to wmg_det_reduce + wmg_cgls_scalars + wmg_axpy_dev /
  * wmg_lincomb_dev).  wmg_det_partials runs level 1 of wmg_det_reduce only:
  * reduction k's ceil(n/1024) chunk sums at partials + k * ceil(n/1024)
  * (wmg_det_scratch_len doubles).  gamma is read from S[11] by wmg_cgls_update
  * (which commits it to S[0]) and written to S[11] by wmg_cgls_direction.
- *   wmg_cgls_update:    partials of <q,q>;  alpha = gamma / qq;  x += alpha p;  r -= alpha q
+ *   wmg_cgls_update:    partials of <q,q> (and, when lam != 0, partials_pp of <p,p>; else
+ *                       NULL);  alpha = gamma / (qq + lam pp);  x += alpha p;  r -= alpha q
  *   wmg_cgls_direction: mode 1: partials of <s,s>; beta = ss / gamma; gamma' = ss
  *                       mode 2: partials of <s,s>, <z,s>, <z,s - s_old>; beta = pr / gamma;
  *                       gamma' = zs;   then p = z + beta p */
@@ -230,7 +231,8 @@ int wmg_det_partials(long long n, int K, const int *ops, const double *const *a,
                      const double *const *b, const double *const *c, double *partials,
                      void *stream);
 int wmg_cgls_update(long long n_img, long long n_sino, double *x, const double *p, double *r,
-                    const double *q, const double *partials, double *S, void *stream);
+                    const double *q, const double *partials, const double *partials_pp,
+                    double lam, double *S, void *stream);
 int wmg_cgls_direction(long long n, double *p, const double *z, const double *partials, int mode,
                        double *S, void *stream);
 

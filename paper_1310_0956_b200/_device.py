@@ -212,7 +212,7 @@ def capture_graph(fn, device):
     return g, out
 
 
-def scratch(n: int, K: int, device):
+def scratch(n: int, K: int, device, slot: int = 0):
     """Cached device scratch for wmg_det_reduce (+ K result slots), per stream.
     Inside a graph capture a fresh buffer comes from the graph's private pool,
     so two captured graphs never share scratch (they may replay concurrently)."""
@@ -221,7 +221,7 @@ def scratch(n: int, K: int, device):
     need = int(L.wmg_det_scratch_len(int(n), int(K))) + 16
     if t.cuda.is_current_stream_capturing():
         return t.empty(max(need, 4096), dtype=t.float64, device=device)
-    key = (str(device), t.cuda.current_stream(device).cuda_stream)
+    key = (str(device), t.cuda.current_stream(device).cuda_stream, slot)
     buf = _scratch.get(key)
     if buf is None or buf.numel() < need:
         buf = t.empty(max(need, 4096), dtype=t.float64, device=device)
@@ -258,10 +258,11 @@ def det_reduce(specs, n=None, out=None):
     return out
 
 
-def det_partials(specs):
+def det_partials(specs, slot=0):
     """Level 1 of ``det_reduce`` only: returns the scratch tensor holding the
     chunk sums (reduction k at offset k * ceil(n / 1024)), for the fused CGLS
-    kernels that finish the reduction themselves."""
+    kernels that finish the reduction themselves.  ``slot``: which of the
+    stream's scratch buffers to use (two sets of chunk sums alive at once)."""
     K = len(specs)
     a0 = specs[0][1]
     n = a0.numel()
@@ -269,7 +270,7 @@ def det_partials(specs):
         for v in sp_[1:]:
             if v is not None and v.numel() != n:
                 raise ValueError("det_partials operands must have equal lengths")
-    sc = scratch(n, K, a0.device)
+    sc = scratch(n, K, a0.device, slot)
     ops = (ctypes.c_int * K)(*[int(s[0]) for s in specs])
     A = (ctypes.c_void_p * K)(*[s[1].data_ptr() for s in specs])
     B = (ctypes.c_void_p * K)(*[(s[2].data_ptr() if s[2] is not None else 0) for s in specs])

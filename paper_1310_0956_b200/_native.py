@@ -74,7 +74,7 @@ _SIGS = {
     "wmg_cgls_scalars": (_i, [_dp, _d, _i, _vp]),
     "wmg_det_partials": (_i, [_ll, _i, ctypes.POINTER(_i), ctypes.POINTER(_vp),
                               ctypes.POINTER(_vp), ctypes.POINTER(_vp), _dp, _vp]),
-    "wmg_cgls_update": (_i, [_ll, _ll, _dp, _dp, _dp, _dp, _dp, _dp, _vp]),
+    "wmg_cgls_update": (_i, [_ll, _ll, _dp, _dp, _dp, _dp, _dp, _dp, _d, _dp, _vp]),
     "wmg_cgls_direction": (_i, [_ll, _dp, _dp, _dp, _i, _dp, _vp]),
     "wmg_batched_gemv": (_i, [_i, _i, _dp, _ll, _dp, _ll, _dp, _ll, _vp]),
     "wmg_haar_restrict": (_i, [_i, _dp, _i, _dp, _vp]),

@@ -63,7 +63,7 @@ cudaError_t ew_lincomb_dev(long long, double*, double, const double*, const doub
                            const double*, cudaStream_t);
 cudaError_t cgls_scalars(double*, double, int, cudaStream_t);
 cudaError_t cgls_update(long long, long long, double*, const double*, double*, const double*,
-                        const double*, double*, cudaStream_t);
+                        const double*, const double*, double, double*, cudaStream_t);
 cudaError_t cgls_direction(long long, double*, const double*, const double*, int, double*,
                            cudaStream_t);
 cudaError_t batched_gemv(int, int, const double*, long long, const double*, long long, double*,
@@ -694,11 +694,15 @@ int wmg_cgls_scalars(double* S, double lam, int op, void* stream) {
   return cuda_rc(wmg::cgls_scalars(S, lam, op, STREAM(stream)));
 }
 int wmg_cgls_update(long long n_img, long long n_sino, double* x, const double* p, double* r,
-                    const double* q, const double* partials, double* S, void* stream) {
+                    const double* q, const double* partials, const double* partials_pp,
+                    double lam, double* S, void* stream) {
   REQ(x && p && r && q && partials && S);
-  if (n_img <= 0 || n_sino <= 0 || n_sino > (1LL << 20))
+  if (n_img <= 0 || n_sino <= 0 || n_sino > (1LL << 20) || n_img > (1LL << 20))
     return fail(WMG_EINVAL, "cgls_update: lengths must be in [1, 2^20]");
-  return cuda_rc(wmg::cgls_update(n_img, n_sino, x, p, r, q, partials, S, STREAM(stream)));
+  if (lam != 0.0 && !partials_pp)
+    return fail(WMG_EINVAL, "cgls_update: lam != 0 needs the <p,p> chunk sums");
+  return cuda_rc(wmg::cgls_update(n_img, n_sino, x, p, r, q, partials, partials_pp, lam, S,
+                                  STREAM(stream)));
 }
 int wmg_cgls_direction(long long n, double* p, const double* z, const double* partials, int mode,
                        double* S, void* stream) {

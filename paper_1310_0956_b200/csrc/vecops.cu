@@ -541,7 +541,7 @@ __global__ void cgls_scalars_kernel(double* S, double lam, int op) {
   }
 }
 
-// --- fused forms (lam == 0, unsharded, vectors of at most 2^20 elements) ---
+// --- fused forms (unsharded, vectors of at most 2^20 elements) ---
 // The reduction's last level, the scalar recurrence and the vector update in
 // one kernel: every block finishes the <= 1024 level-1 chunk sums itself (one
 // warp, the order det_finish uses, so every block holds the bit-identical
@@ -556,22 +556,27 @@ __device__ __forceinline__ double finish_small(const double* partials, long long
   return __shfl_sync(0xffffffffu, warp_chunk(partials, C, 0, lane), 0);
 }
 
-// x += alpha p, r -= alpha q with alpha = gamma / <q,q>; partials: level 1 of <q,q>
+// x += alpha p, r -= alpha q with alpha = gamma / (<q,q> + lam <p,p>); partials:
+// level 1 of <q,q>; partials_pp (lam != 0 only): level 1 of <p,p>
 __global__ void __launch_bounds__(256) cgls_update_kernel(long long n_img, long long n_sino,
                                                           double* x, const double* p, double* r,
                                                           const double* q,
                                                           const double* partials, long long C,
-                                                          double* S) {
+                                                          const double* partials_pp,
+                                                          long long Cpp, double lam, double* S) {
   __shared__ double sh_alpha;
   if (threadIdx.x < 32) {
     const double qq = finish_small(partials, C, threadIdx.x);
+    const double pp = lam != 0.0 ? finish_small(partials_pp, Cpp, threadIdx.x) : 0.0;
     if (threadIdx.x == 0) {
       const double gamma = S[11];
-      const bool ok = qq > 0.0 && isfinite(qq);
-      const double alpha = ok ? gamma / qq : 0.0;
+      const double delta = lam != 0.0 ? dadd(qq, dmul(lam, pp)) : qq;
+      const bool ok = delta > 0.0 && isfinite(delta);
+      const double alpha = ok ? gamma / delta : 0.0;
       sh_alpha = alpha;
       if (blockIdx.x == 0) {
         S[1] = qq;
+        S[2] = pp;
         S[3] = alpha;
         S[0] = gamma;
         if (!ok) S[8] = 1.0;
@@ -659,12 +664,15 @@ cudaError_t det_reduce(long long n, int K, const int* ops, const double* const* 
 // fused CGLS steps on the level-1 chunk sums a det_reduce(..., out = nullptr) left
 // in ``partials`` (reduction k at partials + k * C, C = ceil(n / 1024) <= 1024)
 cudaError_t cgls_update(long long n_img, long long n_sino, double* x, const double* p, double* r,
-                        const double* q, const double* partials, double* S, cudaStream_t st) {
-  const long long C = (n_sino + 1023) / 1024;
-  if (n_img <= 0 || n_sino <= 0 || C > 1024) return cudaErrorInvalidValue;
+                        const double* q, const double* partials, const double* partials_pp,
+                        double lam, double* S, cudaStream_t st) {
+  const long long C = (n_sino + 1023) / 1024, Cpp = (n_img + 1023) / 1024;
+  if (n_img <= 0 || n_sino <= 0 || C > 1024 || Cpp > 1024) return cudaErrorInvalidValue;
+  if (lam != 0.0 && !partials_pp) return cudaErrorInvalidValue;
   const long long nmax = n_img > n_sino ? n_img : n_sino;
   vec::cgls_update_kernel<<<grid_for(nmax, 256), 256, 0, st>>>(n_img, n_sino, x, p, r, q,
-                                                               partials, C, S);
+                                                               partials, C, partials_pp, Cpp,
+                                                               lam, S);
   return cudaGetLastError();
 }
 

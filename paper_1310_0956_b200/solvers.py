@@ -440,10 +440,10 @@ def _cgls_graphed(w, bd, x, lam, precond, cfg, errs, was_np, record, t0):
     # so repeated solves replay it instead of re-capturing (no x_ex tracking:
     # the error terms read a per-solve buffer).
     owner = precond if precond is not None else w
-    # lam == 0, unsharded, vectors of <= 2^20 elements: the reductions' last
+    # unsharded, vectors of <= 2^20 elements: the reductions' last
     # level, the scalar recurrences and the vector updates run fused
     # (wmg_cgls_update / wmg_cgls_direction: same arithmetic, 5 launches fewer)
-    fused = (FUSED_CGLS and lam == 0 and not getattr(w, "collectives", False)
+    fused = (FUSED_CGLS and not getattr(w, "collectives", False)
              and max(M_, Nn) <= (1 << 20))
     key = (id(w), lam, str(dev), fused)
     cache = None if errs.active else owner.__dict__.setdefault("_cgls_graph_cache", {})
@@ -518,8 +518,10 @@ def _cgls_graphed(w, bd, x, lam, precond, cfg, errs, was_np, record, t0):
         w.forward_(p, q)
         if fused:
             part = D.det_partials([(N.RED_SQ, q, None, None)])
+            # (the two reductions have different lengths: separate chunk sums)
+            part_pp = D.det_partials([(N.RED_SQ, p, None, None)], slot=1) if lam != 0 else None
             N.call("wmg_cgls_update", n_img, n_sino, D.ptr(x), D.ptr(p), D.ptr(r), D.ptr(q),
-                   D.ptr(part), D.ptr(S), st())
+                   D.ptr(part), D.ptr(part_pp), float(lam), D.ptr(S), st())
         else:
             D.det_reduce([(N.RED_SQ, q, None, None)], out=S[1:2])
             _sino(w, S[1:2])              # angle shards: sum of the ranks' partials

@@ -81,10 +81,14 @@ def test_fused_cgls_entry_points_validate_without_a_gpu():
     lib = _native.load()
     dp = ctypes.c_void_p(8)
     big = (1 << 20) + 1
-    assert lib.wmg_cgls_update(100, big, dp, dp, dp, dp, dp, dp, None) == _native.WMG_EINVAL
+    upd = lib.wmg_cgls_update
+    assert upd(100, big, dp, dp, dp, dp, dp, None, 0.0, dp, None) == _native.WMG_EINVAL
     assert b"2^20" in lib.wmg_last_error()
-    assert lib.wmg_cgls_update(0, 100, dp, dp, dp, dp, dp, dp, None) == _native.WMG_EINVAL
-    assert lib.wmg_cgls_update(100, 100, None, dp, dp, dp, dp, dp, None) == _native.WMG_EINVAL
+    assert upd(big, 100, dp, dp, dp, dp, dp, None, 0.0, dp, None) == _native.WMG_EINVAL
+    assert upd(0, 100, dp, dp, dp, dp, dp, None, 0.0, dp, None) == _native.WMG_EINVAL
+    assert upd(100, 100, None, dp, dp, dp, dp, None, 0.0, dp, None) == _native.WMG_EINVAL
+    assert upd(100, 100, dp, dp, dp, dp, dp, None, 0.5, dp, None) == _native.WMG_EINVAL
+    assert b"<p,p>" in lib.wmg_last_error()
     assert lib.wmg_cgls_direction(big, dp, dp, dp, 1, dp, None) == _native.WMG_EINVAL
     assert lib.wmg_cgls_direction(100, dp, dp, dp, 3, dp, None) == _native.WMG_EINVAL
     assert b"mode" in lib.wmg_last_error()

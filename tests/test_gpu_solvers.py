@@ -293,9 +293,13 @@ def test_fused_cgls_kernels_bitwise_vs_unfused(gpu, precond_kind):
             S.FUSED_CGLS = True
 
     # a fixed iteration count, an early exit on the tolerance, a single iteration
-    for cfg in (SolverConfig(max_iterations=20, residual_tolerance=0.0),
-                SolverConfig(max_iterations=60, residual_tolerance=1e-3),
-                SolverConfig(max_iterations=1, residual_tolerance=0.0)):
+    cfgs = [SolverConfig(max_iterations=20, residual_tolerance=0.0),
+            SolverConfig(max_iterations=60, residual_tolerance=1e-3),
+            SolverConfig(max_iterations=1, residual_tolerance=0.0)]
+    if precond_kind == "none":            # regularised CGLS: delta = <q,q> + lam <p,p>
+        cfgs.append(SolverConfig(max_iterations=25, residual_tolerance=0.0,
+                                 regularization_lambda=0.1))
+    for cfg in cfgs:
         xu, ru = run(False, cfg)
         xf, rf = run(True, cfg)
         assert torch.equal(xf, xu), cfg
