@@ -2256,6 +2256,12 @@ static void bwd_symrun_launch(const GeomDev& G, const void* y, void* x, bool acc
 // row_hi): one thread per pixel (per angle one detector load of weight 1 and
 // the pixel's read-modify-write; the tiled kernel's window staging for two
 // angles took 11 / 26 us at n = 1024 / 2048, the angle-split one 13 us at 512)
+// Eight images per weight from this many quadrant tile pairs (n >= 1600): measured
+// against the four-image run layout, warm, L2 flushed (tools/probe_bwd_threshold.py):
+// n = 1536 (300 pairs) 1236 vs 1060 us, 1600 (325) 1281 vs 1345, 1728 (378) 1398 vs
+// 1449, 1792 (406) 1459 vs 1817, 1856 (435) 1494 vs 1881 us
+constexpr long long kSym8MinPairs = 320;
+
 template <typename TIn, typename TOut>
 static cudaError_t bwd_axis_launch(const GeomDev& Gx, const void* y, void* x, cudaStream_t st,
                                    int row_lo = 0, int row_hi = -1) {
@@ -2277,7 +2283,7 @@ static cudaError_t bwd_sym_impl(const GeomDev& G, const GeomDev& Gx, const void*
   // eight images per weight where the tile pairs fill the SMs (sym & 8192:
   // testing, at any size; sym & 16384: testing, the four-image run layout)
   if (G.tsym && !rowlayout && !blocks8x4 && !(G.sym & (512 | 1024 | 16384)) &&
-      ((long long)qt * (qt + 1) / 2 >= 3LL * 148 || (G.sym & 8192))) {
+      ((long long)qt * (qt + 1) / 2 >= kSym8MinPairs || (G.sym & 8192))) {
     const unsigned grid8 = (unsigned)(qt * (qt + 1) / 2);
     constexpr int smem8 = 2 * 4 * fast::kBwdTile * (fast::kBwdTile + 1) * (int)sizeof(float);
     static bool attr[2] = {false, false};   // per instantiation
@@ -2483,7 +2489,7 @@ int fast_backward_bands(const GeomDev& G, int precision, const GeomDev* Gx) {
   if (precision != 0 || !Gx || !use_sym_bwd(G, 0) || !G.tsym || G.n % 64) return 0;
   const int qt = G.n / 64;
   if (G.sym & (8 | 256 | 512 | 1024 | 16384)) return 0;
-  if (!((long long)qt * (qt + 1) / 2 >= 3LL * 148 || (G.sym & 8192))) return 0;
+  if (!((long long)qt * (qt + 1) / 2 >= kSym8MinPairs || (G.sym & 8192))) return 0;
   return qt;
 }
 

@@ -161,3 +161,35 @@ def test_banded_forward_passes_vs_parity(gpu, n, m, passes):
     err = np.linalg.norm(got - ref, axis=1)
     nrm = np.linalg.norm(ref, axis=1)
     assert np.all(err <= 1e-5 * np.maximum(nrm, 1e-30))
+
+
+@pytest.mark.parametrize("n,m,eight", [(1600, 400, True), (1536, 384, False)])
+def test_eight_image_backprojector_threshold_vs_parity(gpu, n, m, eight):
+    """The eight-image backprojector takes over from 320 quadrant tile pairs
+    (n = 1600; the four-image run layout below): on both sides of the switch
+    the backprojection (and the banded form where it exists) is within 1e-5 of
+    the float64 parity backprojector (reference geometry.py:209-215) and the
+    kernel is the expected one."""
+    torch = gpu
+    from paper_1310_0956_b200.geometry import build_geometry, build_projector
+    d = int(math.ceil(n * math.sqrt(2.0)))
+    g = build_geometry(n, d, m)
+    w = build_projector(g, precision="float32")
+    y = np.random.default_rng(n).uniform(0.0, 1.0, m * d).astype(np.float32)
+    yd = torch.from_numpy(y).cuda()
+    img = torch.empty(n * n, dtype=torch.float32, device="cuda")
+    want = "bwd_sym8_kernel" if eight else "bwd_symrun_kernel"
+    names = _kernel_names(torch, lambda: w.backward_(yd, img), want)
+    assert any(want in k for k in names), sorted(names)
+    assert (w.backward_bands() > 0) == eight
+    ref = build_projector(g).backward(torch.from_numpy(y.astype(np.float64)).cuda())
+    ref = ref.cpu().numpy()
+    got = img.double().cpu().numpy()
+    assert np.linalg.norm(got - ref) <= 1e-5 * np.linalg.norm(ref)
+    assert np.max(np.abs(got - ref)) <= 1e-4 * np.max(np.abs(ref))
+    if eight:
+        qt = w.backward_bands()
+        out = torch.full_like(img, float("nan"))
+        for s0, s1 in ((0, 7), (7, qt // 2), (qt // 2, qt)):
+            w.backward_band_(yd, out, s0, s1)
+        assert torch.equal(out, img)

@@ -9,7 +9,7 @@ sys.path.insert(0, ".")
 from paper_1310_0956_b200 import build_geometry, build_projector  # noqa: E402
 
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
-for n in (768, 1024, 1280, 1536, 1792, 1920, 2048):
+for n in [int(a) for a in sys.argv[1:]] or (768, 1024, 1280, 1536, 1792, 1920, 2048):
     d = int(-(-n * 1.4142135623730951 // 1))
     y = torch.rand(n * d, device="cuda")
     out = {}
