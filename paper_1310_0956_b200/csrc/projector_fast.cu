@@ -2134,8 +2134,10 @@ static cudaError_t fwd_v2_impl(const GeomDev& G, const void* x, void* ws, void* 
       constexpr int kStride = 4;
       dim3 sgrid(((G.d + 1) / 2 + 8 * ag * kStride - 1) / (8 * ag * kStride) * kStride,
                  (G.n_half + 3) / 4);
-      // (below n ~ 1280 the planes are L2-resident and the octets' shared L1
-      // lines are worth more: n = 1024 0.36 ms adjacent vs 0.39 strided)
+      // (up to n = 1024 the octets' shared L1 lines are worth more: n = 1024
+      // 0.35 ms adjacent vs 0.39 strided, 896 equal; from n = 1088 strided wins:
+      // 1088 0.441 vs 0.447 ms, 1152 0.480 vs 0.519, 1216 0.529 vs 0.575)
+      constexpr int kFwdStrideMinN = 1088;
       // Banded passes over the slab index when the two padded planes exceed the
       // L2 (n = 4096: 277 MB -> 4 passes): the blocks of one pass walk only
       // slabs [lo, hi) (rows lo..hi-1 and their mirrors n-hi..n-lo-1 of both
@@ -2144,12 +2146,12 @@ static cudaError_t fwd_v2_impl(const GeomDev& G, const void* x, void* ws, void* 
       // partial ray sums to the sinogram (fixed order: deterministic)
       const double plane_mb = 2.0 * G.n * (G.n + 2.0 * kPadMargin) * 8.0 / 1e6;
       const int nb = plane_mb > 128.0 ? (int)ceil(plane_mb / 70.0) : 1;
-      if (G.n >= 1280 && nb > 1) {
+      if (G.n >= kFwdStrideMinN && nb > 1) {
         for (int bi = 0; bi < nb; ++bi)
           fast::fwd_sym_kernel<TOut, ag, false, true, true, 1, kStride><<<sgrid, 32 * ag, 0, st>>>(
               G, (const float*)PM, (const float*)PMT, (TOut*)y, G.n * bi / nb,
               G.n * (bi + 1) / nb, bi > 0);
-      } else if (G.n >= 1280)
+      } else if (G.n >= kFwdStrideMinN)
         fast::fwd_sym_kernel<TOut, ag, false, true, true, 1, kStride><<<sgrid, 32 * ag, 0, st>>>(
             G, (const float*)PM, (const float*)PMT, (TOut*)y);
       else
@@ -2252,16 +2254,16 @@ static void bwd_symrun_launch(const GeomDev& G, const void* y, void* x, bool acc
                                                                       (TOut*)x);
 }
 
-// The axis-aligned angles of a symmetric set, added to image rows [row_lo,
-// row_hi): one thread per pixel (per angle one detector load of weight 1 and
-// the pixel's read-modify-write; the tiled kernel's window staging for two
-// angles took 11 / 26 us at n = 1024 / 2048, the angle-split one 13 us at 512)
 // Eight images per weight from this many quadrant tile pairs (n >= 1600): measured
 // against the four-image run layout, warm, L2 flushed (tools/probe_bwd_threshold.py):
 // n = 1536 (300 pairs) 1236 vs 1060 us, 1600 (325) 1281 vs 1345, 1728 (378) 1398 vs
 // 1449, 1792 (406) 1459 vs 1817, 1856 (435) 1494 vs 1881 us
 constexpr long long kSym8MinPairs = 320;
 
+// The axis-aligned angles of a symmetric set, added to image rows [row_lo,
+// row_hi): one thread per pixel (per angle one detector load of weight 1 and
+// the pixel's read-modify-write; the tiled kernel's window staging for two
+// angles took 11 / 26 us at n = 1024 / 2048, the angle-split one 13 us at 512)
 template <typename TIn, typename TOut>
 static cudaError_t bwd_axis_launch(const GeomDev& Gx, const void* y, void* x, cudaStream_t st,
                                    int row_lo = 0, int row_hi = -1) {

@@ -100,10 +100,11 @@ def test_default_dispatch_pair_vs_oracle(gpu, oracle_proj, n):
     assert abs(lhs - rhs) <= 1e-6 * abs(lhs)
 
 
-@pytest.mark.parametrize("n,m,stride", [(1280, 720, 4), (1536, 1000, 4), (1024, 1024, 1)])
+@pytest.mark.parametrize("n,m,stride", [(1280, 720, 4), (1536, 1000, 4), (1152, 600, 4),
+                                        (1024, 1024, 1)])
 def test_forward_block_layouts_vs_parity(gpu, n, m, stride):
     """The symmetric forward's block layouts around their switch (ray octets 4
-    apart inside a block from n = 1280, adjacent below), on angle counts that are
+    apart inside a block from n = 1088, adjacent below), on angle counts that are
     not multiples of the 4-angle groups' super-blocks: the full sinogram within
     1e-5 of the float64 parity forward (reference geometry.py:200-206), every row
     within 1e-5, the layout asserted from the launched kernel's template."""
