@@ -2212,10 +2212,17 @@ static cudaError_t bwd_v2_impl(const GeomDev& G, const void* y, void* x, bool ac
                                cudaStream_t st, const GeomDev* G_axis = nullptr);
 
 // small quadrants: the run layout with the angles split over a cluster of
-// nsplit CTAs per tile (~4 CTAs per SM, >= 4 primary angles per CTA)
+// nsplit CTAs per tile (>= ~4 CTAs per SM, >= 4 primary angles per CTA).  At
+// least 10 CTAs per tile at every size below the eight-image switch: more,
+// shorter CTAs balance the SMs better than fewer waves of long ones (sweep of
+// the cluster size, warm, L2 flushed, tools/nsplit_sweep.sh: n = 768 181 (5
+// CTAs) -> 163 us (10), n = 1024 378 (3) -> 345, n = 1280 689 (2) -> 630,
+// n = 1408 861 (2) -> 828, n = 1536 1058 (2) -> 1054, n = 512 unchanged (10);
+// 12 and 16 are slower everywhere from n = 512)
 static inline int symrun_nsplit(const GeomDev& G) {
   const int tiles = (G.n / 64) * (G.n / 64);
-  return max(1, min(16, min((4 * 148 + tiles - 1) / tiles, G.n_prim / 4)));
+  const int fill = (4 * 148 + tiles - 1) / tiles;
+  return max(1, min(16, min(max(fill, 10), G.n_prim / 4)));
 }
 
 template <typename TIn, typename TOut, bool kAcc>
