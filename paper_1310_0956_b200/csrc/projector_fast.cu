@@ -2114,9 +2114,13 @@ static cudaError_t fwd_v2_impl(const GeomDev& G, const void* x, void* ws, void* 
     constexpr int ag = fast::kFwdAG;
     dim3 mgrid(((G.d + 1) / 2 + 8 * ag - 1) / (8 * ag), (G.n_half + 3) / 4);
     const long long blocks = (long long)mgrid.x * mgrid.y;
-    // small grids: split each warp's slab range over 8 / 4 row segments
-    // (sym & 65536: testing, unsplit)
-    const int seg = (G.sym & 65536) ? 1 : blocks < 2LL * 148 ? 8 : blocks < 6LL * 148 ? 4 : 1;
+    // grids below n = 1792 (and launches of few blocks at any size): each warp's
+    // slab range split over 8 row segments, one ray octet per block (sym & 65536:
+    // testing, unsplit).  Warm, L2 flushed, against the unsplit 4-octet blocks
+    // (tools/probe_size_scan.py): n = 640 126 -> 101 us, 1024 347 -> 304, 1152 478 ->
+    // 411, 1280 591 -> 548, 1536 957 -> 904, 1792 equal, 2048 2063 vs 2069, 3072
+    // 6536 vs 6799; 4, 6, 12 and 16 segments are slower than 8 at every size
+    const int seg = (G.sym & 65536) ? 1 : (G.n < 1792 || blocks < 6LL * 148) ? 8 : 1;
     // split kernels: one ray octet (its kSeg row segments) per block, so every
     // warp of a block walks an equally long segment and the block frees its
     // slot when they finish (with 4 octets per block the short edge-ray octets

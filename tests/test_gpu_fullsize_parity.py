@@ -100,12 +100,14 @@ def test_default_dispatch_pair_vs_oracle(gpu, oracle_proj, n):
     assert abs(lhs - rhs) <= 1e-6 * abs(lhs)
 
 
-@pytest.mark.parametrize("n,m,stride", [(1280, 720, 4), (1536, 1000, 4), (1152, 600, 4),
-                                        (1024, 1024, 1)])
-def test_forward_block_layouts_vs_parity(gpu, n, m, stride):
-    """The symmetric forward's block layouts around their switch (ray octets 4
-    apart inside a block from n = 1088, adjacent below), on angle counts that are
-    not multiples of the 4-angle groups' super-blocks: the full sinogram within
+@pytest.mark.parametrize("n,m,seg,stride", [(1280, 720, 8, 1), (1536, 1000, 8, 1),
+                                            (1152, 600, 8, 1), (1024, 1024, 8, 1),
+                                            (1792, 896, 1, 4), (1920, 960, 1, 4)])
+def test_forward_block_layouts_vs_parity(gpu, n, m, seg, stride):
+    """The symmetric forward's block layouts around their switch (below n = 1792
+    one ray octet per block with the slab range in 8 row segments; from 1792 four
+    ray octets 4 apart per block, unsplit), on angle counts that are not
+    multiples of the 4-angle groups' super-blocks: the full sinogram within
     1e-5 of the float64 parity forward (reference geometry.py:200-206), every row
     within 1e-5, the layout asserted from the launched kernel's template."""
     torch = gpu
@@ -118,7 +120,7 @@ def test_forward_block_layouts_vs_parity(gpu, n, m, stride):
     sino = torch.empty(m * d, dtype=torch.float32, device="cuda")
     names = _kernel_names(torch, lambda: w.forward_(xd, sino), "fwd_sym_kernel")
     k = [s for s in names if "fwd_sym_kernel" in s]
-    assert k and all(s.split("(")[0].replace(" ", "").endswith(f",1,{stride}>") for s in k), k
+    assert k and all(s.split("(")[0].replace(" ", "").endswith(f",{seg},{stride}>") for s in k), k
     got = sino.double().cpu().numpy().reshape(m, d)
     ref = build_projector(g).forward(torch.from_numpy(x.astype(np.float64)).cuda())
     ref = ref.cpu().numpy().reshape(m, d)
