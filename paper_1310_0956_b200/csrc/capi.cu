@@ -213,6 +213,31 @@ int wmg_geometry_create(int n, int n_detectors, int n_angles, const double* cos_
       for (int a = 0; a < n_angles; ++a)
         if (mir[(size_t)a] >= 0) prim.push_back(a);
       halfv = lo;
+      // The symmetric forward puts 4 consecutive entries of this list into one
+      // warp (8 rays x 4 angles), which pays off when the 4 angles are adjacent
+      // (their rays read the same words slab after slab).  Runs of adjacent
+      // angles (gap <= 1.5 x the smallest gap of the set) are cut into groups of
+      // 4; what is left of each run goes to the end of the list.  An equiangular
+      // set is one run (order unchanged); a per-rank shard dealt in chunks of 4
+      // adjacent angles (sharding.shard_angles "quad") keeps every chunk in one warp.
+      if (halfv.size() > 4) {
+        std::vector<double> th(halfv.size());
+        for (size_t i = 0; i < halfv.size(); ++i)
+          th[i] = std::atan2(sin_h[halfv[i]], cos_h[halfv[i]]);
+        double gmin = 1e300;
+        for (size_t i = 1; i < th.size(); ++i) gmin = std::min(gmin, th[i] - th[i - 1]);
+        std::vector<int> grouped, rest;
+        for (size_t i = 0; i < halfv.size();) {
+          size_t j = i + 1;
+          while (j < halfv.size() && th[j] - th[j - 1] <= 1.5 * gmin) ++j;
+          const size_t full = (j - i) / 4 * 4;
+          grouped.insert(grouped.end(), halfv.begin() + i, halfv.begin() + i + full);
+          rest.insert(rest.end(), halfv.begin() + i + full, halfv.begin() + j);
+          i = j;
+        }
+        grouped.insert(grouped.end(), rest.begin(), rest.end());
+        halfv.swap(grouped);
+      }
     }
   }
   // Transposition symmetry (theta -> pi/2 - theta, to 1e-12): every primary with

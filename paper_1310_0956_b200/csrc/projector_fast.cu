@@ -2120,20 +2120,34 @@ static cudaError_t fwd_v2_impl(const GeomDev& G, const void* x, void* ws, void* 
     // (tools/probe_size_scan.py): n = 640 126 -> 101 us, 1024 347 -> 304, 1152 478 ->
     // 411, 1280 591 -> 548, 1536 957 -> 904, 1792 equal, 2048 2063 vs 2069, 3072
     // 6536 vs 6799; 4, 6, 12 and 16 segments are slower than 8 at every size
-    const int seg = (G.sym & 65536) ? 1 : (G.n < 1792 || blocks < 6LL * 148) ? 8 : 1;
+    // Launches of fewer than 8000 4-octet blocks (the per-rank angle shards of
+    // the multi-GPU pair) take the same form: their 3-6 waves of long blocks
+    // left the L1 data pipe at 70 % (n = 4096, 514 of 4096 angles: forward 2.80
+    // -> 2.59 ms; n = 3072, 386 angles: 1.42 -> 1.09; n = 2048, 258 angles: 0.54
+    // -> 0.38 ms, tools/probe_shard_eff.py)
+    const int seg = (G.sym & 65536) ? 1 : (G.n < 1792 || blocks < 8000) ? 8 : 1;
+    // Banded passes over the slab index when the two padded planes exceed the
+    // L2 (n = 4096: 277 MB -> 4 passes): the blocks of one pass walk only
+    // slabs [lo, hi) (rows lo..hi-1 and their mirrors n-hi..n-lo-1 of both
+    // planes), so the planes are read from DRAM about once instead of ~30x
+    // (9.5 -> 0.9 GB per launch, 15.6 -> 15.1 ms); later passes add their
+    // partial ray sums to the sinogram (fixed order: deterministic)
+    const double plane_mb = 2.0 * G.n * (G.n + 2.0 * kPadMargin) * 8.0 / 1e6;
+    // (the 8-segment form is banded only from 200 MB: at n = 3072, 154 MB, its
+    // unbanded launch is faster: 386 angles 1.09 vs 1.18 ms, 770 angles 1.94 vs 2.11)
+    const int nb = plane_mb > (seg == 8 ? 200.0 : 128.0) ? (int)ceil(plane_mb / 70.0) : 1;
     // split kernels: one ray octet (its kSeg row segments) per block, so every
     // warp of a block walks an equally long segment and the block frees its
     // slot when they finish (with 4 octets per block the short edge-ray octets
     // held their slots until the block's longest walk ended)
     // (n = 512: 90 -> 82 us, n = 256: 40 -> 37 us)
     const dim3 ograd(((G.d + 1) / 2 + 7) / 8, (G.n_half + 3) / 4);
-    if (seg == 8)
-      fast::fwd_sym_kernel<TOut, 1, false, true, true, 8><<<ograd, dim3(32, 8), 0, st>>>(
-          G, (const float*)PM, (const float*)PMT, (TOut*)y);
-    else if (seg == 4)
-      fast::fwd_sym_kernel<TOut, 1, false, true, true, 4><<<ograd, dim3(32, 4), 0, st>>>(
-          G, (const float*)PM, (const float*)PMT, (TOut*)y);
-    else {
+    if (seg == 8) {
+      for (int bi = 0; bi < nb; ++bi)
+        fast::fwd_sym_kernel<TOut, 1, false, true, true, 8><<<ograd, dim3(32, 8), 0, st>>>(
+            G, (const float*)PM, (const float*)PMT, (TOut*)y, nb > 1 ? G.n * bi / nb : 0,
+            nb > 1 ? G.n * (bi + 1) / nb : 1 << 30, bi > 0);
+    } else {
       // ray octets kStride apart inside each block (see fwd_sym_kernel)
       constexpr int kStride = 4;
       dim3 sgrid(((G.d + 1) / 2 + 8 * ag * kStride - 1) / (8 * ag * kStride) * kStride,
@@ -2142,14 +2156,6 @@ static cudaError_t fwd_v2_impl(const GeomDev& G, const void* x, void* ws, void* 
       // 0.35 ms adjacent vs 0.39 strided, 896 equal; from n = 1088 strided wins:
       // 1088 0.441 vs 0.447 ms, 1152 0.480 vs 0.519, 1216 0.529 vs 0.575)
       constexpr int kFwdStrideMinN = 1088;
-      // Banded passes over the slab index when the two padded planes exceed the
-      // L2 (n = 4096: 277 MB -> 4 passes): the blocks of one pass walk only
-      // slabs [lo, hi) (rows lo..hi-1 and their mirrors n-hi..n-lo-1 of both
-      // planes), so the planes are read from DRAM about once instead of ~30x
-      // (9.5 -> 0.9 GB per launch, 15.6 -> 15.1 ms); later passes add their
-      // partial ray sums to the sinogram (fixed order: deterministic)
-      const double plane_mb = 2.0 * G.n * (G.n + 2.0 * kPadMargin) * 8.0 / 1e6;
-      const int nb = plane_mb > 128.0 ? (int)ceil(plane_mb / 70.0) : 1;
       if (G.n >= kFwdStrideMinN && nb > 1) {
         for (int bi = 0; bi < nb; ++bi)
           fast::fwd_sym_kernel<TOut, ag, false, true, true, 1, kStride><<<sgrid, 32 * ag, 0, st>>>(

@@ -44,10 +44,29 @@ def shard_angles(n_angles: int, world: int, rank: int, scheme: str = "round_robi
         m = n_angles
         if m % 4 or m < 4:
             return shard_angles(n_angles, world, rank, "mirror")
-        units = [[0, m // 2], [m // 4, 3 * m // 4]]
-        units += [[k, m - k, m // 2 - k, m // 2 + k] for k in range(1, m // 4)]
-        mine = [a for u in units[rank::world] for a in u]
-        return np.array(sorted(mine), dtype=np.int64)
+        # Quads of 4 adjacent angles stay on one rank: the symmetric forward packs 4
+        # adjacent angles into a warp, whose rays then read the same words -- with
+        # single quads dealt round-robin a rank's angles are `world` steps apart
+        # and its forward ran at 0.56 of the unsharded efficiency at world = 8,
+        # n = 4096 (tools/probe_shard_eff.py).  Whole rounds of such chunks are
+        # dealt round-robin; what is left (fewer than 4 world + 3 quads, the
+        # diagonal pair and the axis pair) goes, heaviest first, to the lightest rank.
+        def quad(k):
+            return [k, m - k, m // 2 - k, m // 2 + k]
+
+        ks = list(range(1, m // 4))
+        nround = (len(ks) // 4 // world) * world          # chunks dealt in whole rounds
+        shards = [[] for _ in range(world)]
+        for c in range(nround):
+            shards[c % world] += [a for k in ks[4 * c:4 * c + 4] for a in quad(k)]
+        left = [quad(k) for k in ks[4 * nround:]] + [[m // 4, 3 * m // 4], [0, m // 2]]
+        wt = lambda u: float(np.sum(angle_weights(np.asarray(u) * (np.pi / m))))  # noqa: E731
+        load = [wt(sh) if sh else 0.0 for sh in shards]
+        for u in sorted(left, key=lambda u: (-wt(u), u[0])):
+            r = min(range(world), key=lambda i: (load[i], i))
+            shards[r] += u
+            load[r] += wt(u)
+        return np.array(sorted(shards[rank]), dtype=np.int64)
     if scheme == "mirror":
         m = n_angles
         units = [[0] + ([m // 2] if m % 2 == 0 and m > 1 else [])]

@@ -102,11 +102,12 @@ def test_default_dispatch_pair_vs_oracle(gpu, oracle_proj, n):
 
 @pytest.mark.parametrize("n,m,seg,stride", [(1280, 720, 8, 1), (1536, 1000, 8, 1),
                                             (1152, 600, 8, 1), (1024, 1024, 8, 1),
-                                            (1792, 896, 1, 4), (1920, 960, 1, 4)])
+                                            (1792, 896, 8, 1), (1920, 1920, 1, 4)])
 def test_forward_block_layouts_vs_parity(gpu, n, m, seg, stride):
-    """The symmetric forward's block layouts around their switch (below n = 1792
-    one ray octet per block with the slab range in 8 row segments; from 1792 four
-    ray octets 4 apart per block, unsplit), on angle counts that are not
+    """The symmetric forward's block layouts around their switch (below n = 1792,
+    and for launches of fewer than 8000 four-octet blocks, one ray octet per block
+    with the slab range in 8 row segments; else four ray octets 4 apart per
+    block, unsplit), on angle counts that are not
     multiples of the 4-angle groups' super-blocks: the full sinogram within
     1e-5 of the float64 parity forward (reference geometry.py:200-206), every row
     within 1e-5, the layout asserted from the launched kernel's template."""
@@ -130,13 +131,15 @@ def test_forward_block_layouts_vs_parity(gpu, n, m, seg, stride):
     assert np.all(err <= 1e-5 * np.maximum(nrm, 1e-30)), int(np.argmax(err / np.maximum(nrm, 1e-30)))
 
 
-@pytest.mark.parametrize("n,m,passes", [(3072, 128, 3), (4096, 128, 4), (3072, 64, 1)])
+@pytest.mark.parametrize("n,m,passes", [(3072, 1024, 3), (4096, 128, 4), (3072, 128, 1)])
 def test_banded_forward_passes_vs_parity(gpu, n, m, passes):
-    """When the padded planes exceed the L2 the (unsplit) forward runs as slab-band
-    passes that add their partial ray sums (projector_fast.cu, fwd_v2_impl); few
-    angles take the row-segment split kernel in one launch instead.  The pass
-    count is asserted from the launches, the sinogram checked against the
-    float64 parity forward (reference geometry.py:200-206) within 1e-5 per row."""
+    """When the padded planes exceed the L2 the forward runs as slab-band passes
+    that add their partial ray sums (projector_fast.cu, fwd_v2_impl): the
+    unsplit form from 128 MB of planes (n = 3072: 3 passes), the 8-segment form
+    that few angles (a rank's shard) take from 200 MB (n = 4096: 4 passes; one
+    launch at n = 3072).  The pass count is asserted from the launches, the
+    sinogram checked against the float64 parity forward (reference
+    geometry.py:200-206) within 1e-5 per row."""
     torch = gpu
     from torch.profiler import ProfilerActivity, profile
     from paper_1310_0956_b200.geometry import build_geometry, build_projector
