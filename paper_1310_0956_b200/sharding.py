@@ -161,11 +161,16 @@ class AngleShardedProjector:
     def forward_(self, x, out):
         return self.local.forward_(x, out)
 
-    # W^T y is summed over the ranks band by band while the backprojection of
+    # W^T y can be summed over the ranks band by band while the backprojection of
     # the later bands still runs (``overlap_groups`` groups of quadrant row-
-    # blocks of equal work; the eight-image fp32 path only, else one allreduce
-    # after the whole backprojection)
-    overlap_groups = 4
+    # blocks of equal work; the eight-image fp32 path only).  Default 1: one
+    # allreduce after the whole backprojection.  Running a rank's backprojection
+    # in band groups has a price -- at n = 4096 a rank's 1.82 ms (world = 8)
+    # becomes 1.98 ms in 2 groups and 2.12 ms in 4 (world = 2: 7.2 -> 7.9 -> 8.4 ms;
+    # tools/probe_shard_bands.py) -- which is as much as the 64 MB NVLink
+    # allreduce it would hide (~0.2-0.3 ms over NVSwitch at world = 8), and the
+    # last group's allreduce stays exposed.  Set > 1 where the exchange is slower.
+    overlap_groups = int(__import__("os").environ.get("WMG_OVERLAP_GROUPS", "1"))
 
     def _band_groups(self, qt):
         total = qt * (qt + 1) // 2

@@ -82,6 +82,7 @@ WORKER = textwrap.dedent(r"""
     n, d, m = 2048, 2897, 64          # banded (eight-image) path: n >= 1600
     g = build_geometry(n, d, m)
     wf = AngleShardedProjector(g, precision="float32", device="cuda:0", always_reduce=True)
+    wf.overlap_groups = 4                             # the banded overlap path
     assert wf.local.backward_bands() > 0, "expected the banded eight-image path"
     y = torch.rand(m * d, device="cuda", dtype=torch.float32,
                    generator=torch.Generator("cuda").manual_seed(5))

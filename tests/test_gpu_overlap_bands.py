@@ -60,6 +60,7 @@ def _worker(rank, world, port, q):
     yf = torch.from_numpy(np.random.default_rng(5).uniform(0, 1, m * d).astype(np.float32))
     y = w.scatter_sinogram(yf.cuda())
     a = torch.empty(n * n, device="cuda")
+    w.overlap_groups = 4
     w.backward_(y, a)                       # overlapped (banded) path
     w.overlap_groups = 1
     b = torch.empty(n * n, device="cuda")
