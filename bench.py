@@ -939,6 +939,9 @@ def run_config4(args):
     S = max(1, min(args.streams, len(data)))
     ws_ = [w] + [build_projector(g, precision="float32", device=dev) for _ in range(S - 1)]
     streams = [torch.cuda.Stream(device=dev) for _ in range(S)]
+    if S > 1:                       # concurrent solves: the forward's throughput dispatch
+        for wi in ws_:
+            wi.prefer_concurrent(True)
     for i in range(S):                                                  # warm-up / capture
         with torch.cuda.stream(streams[i]):
             cgls_solve(ws_[i], data[i], cfg=SolverConfig(max_iterations=3))

@@ -208,6 +208,16 @@ class LineProjector:
         self._ws.pop("path_ok", None)         # the fused path forward follows the dispatch
         return bool(st.value)
 
+    def prefer_concurrent(self, on: bool = True) -> bool:
+        """Throughput dispatch for callers that run several products concurrently
+        on different streams (slice stacks): keeps the forward in its unsplit
+        four-octet blocks.  Launches of few blocks (n >= 1792 with few angles)
+        otherwise take the 8-segment form, which is faster alone (its blocks drain
+        evenly) but slower when another stream's kernels fill the tails anyway
+        (config-4 geometry: 2.15 vs 2.23 ms per pair alone, 1.94 vs 1.88 ms per
+        pair with two streams, tools/probe_cfg4_pair.py)."""
+        return self.set_symmetry("fwdflat" if on else True)
+
     def tocsr(self):
         return self
 

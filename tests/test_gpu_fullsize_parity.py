@@ -199,3 +199,26 @@ def test_eight_image_backprojector_threshold_vs_parity(gpu, n, m, eight):
         for s0, s1 in ((0, 7), (7, qt // 2), (qt // 2, qt)):
             w.backward_band_(yd, out, s0, s1)
         assert torch.equal(out, img)
+
+
+def test_prefer_concurrent_forward_form(gpu):
+    """``prefer_concurrent`` keeps a few-block forward launch (here n = 2048 with
+    128 angles) in the unsplit four-octet form instead of the 8-segment form:
+    different kernels, the same sinogram to fp32 rounding."""
+    torch = gpu
+    from paper_1310_0956_b200.geometry import build_geometry, build_projector
+    n, m = 2048, 128
+    d = int(math.ceil(n * math.sqrt(2.0)))
+    g = build_geometry(n, d, m)
+    x = torch.rand(n * n, device="cuda", generator=torch.Generator("cuda").manual_seed(7))
+    out = {}
+    for conc in (False, True):
+        w = build_projector(g, precision="float32")
+        assert w.prefer_concurrent(conc)
+        s = torch.empty(m * d, device="cuda")
+        names = _kernel_names(torch, lambda: w.forward_(x, s), "fwd_sym_kernel")
+        k = [q.split("(")[0].replace(" ", "") for q in names if "fwd_sym_kernel" in q]
+        assert k and all(q.endswith(",1,4>" if conc else ",8,1>") for q in k), k
+        out[conc] = s
+    rel = float((out[True] - out[False]).norm() / out[False].norm())
+    assert rel <= 1e-6, rel
