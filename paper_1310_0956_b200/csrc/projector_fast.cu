@@ -1290,6 +1290,13 @@ __global__ void __launch_bounds__((kAG == 1 && !kMix) ? 128 : 32 * kAG * kSeg) f
                                                       const float* __restrict__ PT,
                                                       TOut* __restrict__ sino, int band_lo = 0,
                                                       int band_hi = 1 << 30, int band_acc = 0) {
+  // Banded passes are chained with programmatic dependent launches: every block
+  // releases the next pass at once, so that pass's blocks fill the SMs this
+  // pass's last wave leaves idle; the next pass walks its own slab band (it
+  // reads only the planes) and waits for this pass to be complete just before
+  // it adds its partial sums to the sinogram (griddepcontrol.wait below).  Both
+  // instructions are no-ops for launches without the attribute.
+  asm volatile("griddepcontrol.launch_dependents;");
   int hidx, j;
   if (kAG == 1 && !kMix) {
     hidx = blockIdx.y;
@@ -1490,6 +1497,7 @@ __global__ void __launch_bounds__((kAG == 1 && !kMix) ? 128 : 32 * kAG * kSeg) f
     const float r_m = A.major ? accB.y : accA.y;    // (m-a, j)
     const float r_mr = A.major ? accA.y : accB.y;   // (m-a, d-1-j)
     if (band_acc) {
+      asm volatile("griddepcontrol.wait;" ::: "memory");   // the previous pass's sums
       TOut* p0 = sino + (long long)a * d + j;
       TOut* p1 = sino + (long long)b * d + j;
       *p0 = (TOut)((float)*p0 + accA.x);
@@ -2142,11 +2150,27 @@ static cudaError_t fwd_v2_impl(const GeomDev& G, const void* x, void* ws, void* 
     // held their slots until the block's longest walk ended)
     // (n = 512: 90 -> 82 us, n = 256: 40 -> 37 us)
     const dim3 ograd(((G.d + 1) / 2 + 7) / 8, (G.n_half + 3) / 4);
+    // passes bi >= 1: programmatic dependent launch behind pass bi - 1
+    auto launch_pass = [&](auto kern, dim3 grid, dim3 block, int bi) -> cudaError_t {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = grid;
+      cfg.blockDim = block;
+      cfg.stream = st;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      at[0].val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = bi > 0 ? 1 : 0;
+      return cudaLaunchKernelEx(&cfg, kern, G, (const float*)PM, (const float*)PMT, (TOut*)y,
+                                nb > 1 ? G.n * bi / nb : 0,
+                                nb > 1 ? G.n * (bi + 1) / nb : 1 << 30, (int)(bi > 0));
+    };
     if (seg == 8) {
-      for (int bi = 0; bi < nb; ++bi)
-        fast::fwd_sym_kernel<TOut, 1, false, true, true, 8><<<ograd, dim3(32, 8), 0, st>>>(
-            G, (const float*)PM, (const float*)PMT, (TOut*)y, nb > 1 ? G.n * bi / nb : 0,
-            nb > 1 ? G.n * (bi + 1) / nb : 1 << 30, bi > 0);
+      for (int bi = 0; bi < nb; ++bi) {
+        cudaError_t el = launch_pass(fast::fwd_sym_kernel<TOut, 1, false, true, true, 8>, ograd,
+                                     dim3(32, 8), bi);
+        if (el != cudaSuccess) return el;
+      }
     } else {
       // ray octets kStride apart inside each block (see fwd_sym_kernel)
       constexpr int kStride = 4;
@@ -2157,10 +2181,12 @@ static cudaError_t fwd_v2_impl(const GeomDev& G, const void* x, void* ws, void* 
       // 1088 0.441 vs 0.447 ms, 1152 0.480 vs 0.519, 1216 0.529 vs 0.575)
       constexpr int kFwdStrideMinN = 1088;
       if (G.n >= kFwdStrideMinN && nb > 1) {
-        for (int bi = 0; bi < nb; ++bi)
-          fast::fwd_sym_kernel<TOut, ag, false, true, true, 1, kStride><<<sgrid, 32 * ag, 0, st>>>(
-              G, (const float*)PM, (const float*)PMT, (TOut*)y, G.n * bi / nb,
-              G.n * (bi + 1) / nb, bi > 0);
+        for (int bi = 0; bi < nb; ++bi) {
+          cudaError_t el = launch_pass(
+              fast::fwd_sym_kernel<TOut, ag, false, true, true, 1, kStride>, sgrid,
+              dim3(32 * ag), bi);
+          if (el != cudaSuccess) return el;
+        }
       } else if (G.n >= kFwdStrideMinN)
         fast::fwd_sym_kernel<TOut, ag, false, true, true, 1, kStride><<<sgrid, 32 * ag, 0, st>>>(
             G, (const float*)PM, (const float*)PMT, (TOut*)y);
