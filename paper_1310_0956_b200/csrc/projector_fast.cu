@@ -2143,7 +2143,15 @@ static cudaError_t fwd_v2_impl(const GeomDev& G, const void* x, void* ws, void* 
     const double plane_mb = 2.0 * G.n * (G.n + 2.0 * kPadMargin) * 8.0 / 1e6;
     // (the 8-segment form is banded only from 200 MB: at n = 3072, 154 MB, its
     // unbanded launch is faster: 386 angles 1.09 vs 1.18 ms, 770 angles 1.94 vs 2.11)
-    const int nb = plane_mb > (seg == 8 ? 200.0 : 128.0) ? (int)ceil(plane_mb / 70.0) : 1;
+    // The unsplit form always runs in >= 3 passes: chained (below), shorter blocks
+    // balance the SMs better even where the planes fit the L2 (n = 1920 1.72 ->
+    // 1.63 ms, 2048 2.07 -> 1.98, 2304 2.84 -> 2.81; neutral from 2560)
+    // (sym & 65536, LineProjector.prefer_concurrent: one pass while the planes fit
+    // the L2 -- with a second stream's kernels on the GPU the chained passes lose:
+    // config-4 geometry, two streams, 1.88 vs 1.96 ms per pair)
+    const int nb = seg == 8 ? (plane_mb > 200.0 ? (int)ceil(plane_mb / 70.0) : 1)
+                            : (plane_mb > 128.0 ? (int)ceil(plane_mb / 70.0)
+                                                : (G.sym & 65536) ? 1 : 3);
     // split kernels: one ray octet (its kSeg row segments) per block, so every
     // warp of a block walks an equally long segment and the block frees its
     // slot when they finish (with 4 octets per block the short edge-ray octets
