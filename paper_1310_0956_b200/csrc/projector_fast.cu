@@ -2305,11 +2305,12 @@ static void bwd_symrun_launch(const GeomDev& G, const void* y, void* x, bool acc
                                                                       (TOut*)x);
 }
 
-// Eight images per weight from this many quadrant tile pairs (n >= 1600): measured
-// against the four-image run layout, warm, L2 flushed (tools/probe_bwd_threshold.py):
-// n = 1536 (300 pairs) 1236 vs 1060 us, 1600 (325) 1281 vs 1345, 1728 (378) 1398 vs
-// 1449, 1792 (406) 1459 vs 1817, 1856 (435) 1494 vs 1881 us
-constexpr long long kSym8MinPairs = 320;
+// Eight images per weight from this many quadrant tile pairs (n >= 1728): measured
+// against the four-image run layout (10 cluster CTAs per tile), warm, L2 flushed
+// (tools/probe_bwd_threshold.py): n = 1536 (300 pairs) 1228 vs 1055 us, 1600 (325)
+// 1281 vs 1193, 1664 (351) 1348 vs 1326, 1728 (378) 1402 vs 1486, 1792 (406) 1457 vs
+// 1652, 2048 (528) 2108 vs 2444 us
+constexpr long long kSym8MinPairs = 370;
 
 // The axis-aligned angles of a symmetric set, added to image rows [row_lo,
 // row_hi): one thread per pixel (per angle one detector load of weight 1 and

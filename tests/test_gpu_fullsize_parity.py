@@ -169,10 +169,10 @@ def test_banded_forward_passes_vs_parity(gpu, n, m, passes):
     assert np.all(err <= 1e-5 * np.maximum(nrm, 1e-30))
 
 
-@pytest.mark.parametrize("n,m,eight", [(1600, 400, True), (1536, 384, False)])
+@pytest.mark.parametrize("n,m,eight", [(1728, 432, True), (1664, 416, False)])
 def test_eight_image_backprojector_threshold_vs_parity(gpu, n, m, eight):
-    """The eight-image backprojector takes over from 320 quadrant tile pairs
-    (n = 1600; the four-image run layout below): on both sides of the switch
+    """The eight-image backprojector takes over from 370 quadrant tile pairs
+    (n = 1728; the four-image run layout below): on both sides of the switch
     the backprojection (and the banded form where it exists) is within 1e-5 of
     the float64 parity backprojector (reference geometry.py:209-215) and the
     kernel is the expected one."""

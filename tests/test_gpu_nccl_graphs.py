@@ -79,7 +79,7 @@ WORKER = textwrap.dedent(r"""
 
     # 3. fp32 eight-image backprojection in bands with the allreduces on the comm
     #    stream (the overlap path), captured and replayed
-    n, d, m = 2048, 2897, 64          # banded (eight-image) path: n >= 1600
+    n, d, m = 2048, 2897, 64          # banded (eight-image) path: n >= 1728
     g = build_geometry(n, d, m)
     wf = AngleShardedProjector(g, precision="float32", device="cuda:0", always_reduce=True)
     wf.overlap_groups = 4                             # the banded overlap path
